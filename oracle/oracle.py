@@ -1,0 +1,125 @@
+"""ctypes wrapper of the CPU oracle (oracle.c).  TEST INFRASTRUCTURE ONLY.
+
+`run(instance)` executes one launch of an `instances.Instance` with the
+reference's lockstep semantics and returns `(outputs, trap)`: outputs maps
+every buffer name to its final numpy array; trap is None or (kind, block).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "liboracle.so"
+
+_NP = {"i32": np.int32, "i64": np.int64, "f32": np.float32, "f64": np.float64}
+TRAP_NAMES = {1: "OutOfBounds", 2: "DivByZero", 3: "TypeFault", 4: "NonUniformTrip"}
+
+
+class Geom(C.Structure):
+    _fields_ = [("gx", C.c_int), ("gy", C.c_int), ("gz", C.c_int),
+                ("bx", C.c_int), ("by", C.c_int), ("bz", C.c_int)]
+
+
+class OTrap(C.Structure):
+    _fields_ = [("kind", C.c_int), ("pad", C.c_int), ("block", C.c_longlong)]
+
+
+def build() -> Path:
+    """Compile liboracle.so (make; gcc with -ffp-contract=off)."""
+    src = HERE / "oracle.c"
+    if not LIB.exists() or LIB.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(str(LIB))
+    return _lib
+
+
+def _arr(b) -> np.ndarray:
+    a = np.array(b.values, dtype=_NP[b.scalar]).reshape(-1)
+    if a.size < b.length:  # fill semantics: unspecified tail stays zero
+        a = np.concatenate([a, np.zeros(b.length - a.size, a.dtype)])
+    return np.ascontiguousarray(a[: b.length])
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def run(inst, nthreads: int = 1):
+    L = lib()
+    bufs = {b.name: _arr(b) for b in inst.buffers}
+    g = Geom(inst.grid.x, inst.grid.y, inst.grid.z, inst.block.x, inst.block.y, inst.block.z)
+    t = OTrap()
+    # positional values: buffers -> (ptr, len); scalars -> python values
+    argv = []
+    for a in inst.args:
+        if a[0] == "buf":
+            arr = bufs[a[1]]
+            argv.append(_ptr(arr))
+            argv.append(C.c_longlong(arr.size))
+        elif a[0] in ("i32",):
+            argv.append(C.c_int(int(a[1])))
+        elif a[0] == "i64":
+            argv.append(C.c_longlong(int(a[1])))
+        else:
+            argv.append(C.c_double(float(a[1])))
+    k = inst.kernel
+    fn = getattr(L, "or_" + k)
+    extra = []
+    if k == "reverse":
+        extra = [C.c_longlong(inst.shmem)]
+    elif k == "wreduce":
+        extra = [C.c_int(inst.warp_size)]
+    elif k in ("hotspot", "nn"):
+        extra = [C.c_int(nthreads)]
+    fn(g, *argv, *extra, C.byref(t))
+    trap = None if t.kind == 0 else (TRAP_NAMES.get(t.kind, "?"), t.block)
+    return bufs, trap
+
+
+def bfs_full(row: np.ndarray, col: np.ndarray, nv: int, source: int = 0) -> tuple[np.ndarray, int]:
+    L = lib()
+    lvl = np.empty(nv, np.int32)
+    r = np.ascontiguousarray(row, np.int32)
+    c = np.ascontiguousarray(col, np.int32)
+    levels = L.or_bfs_full(_ptr(r), _ptr(c), C.c_longlong(c.size), C.c_int(nv), C.c_int(source), _ptr(lvl))
+    return lvl, levels
+
+
+def hotspot_iterate(temp: np.ndarray, power: np.ndarray, rows: int, cols: int, params: dict,
+                    iterations: int, bx: int = 16, by: int = 16, nthreads: int = 1) -> np.ndarray:
+    """`iterations` ping-pong launches of hotspot.kn; returns the final grid."""
+    L = lib()
+    a = np.ascontiguousarray(temp, np.float32).copy()
+    b = np.zeros_like(a)
+    p = np.ascontiguousarray(power, np.float32)
+    g = Geom(-(-cols // bx), -(-rows // by), 1, bx, by, 1)
+    t = OTrap()
+    for _ in range(iterations):
+        L.or_hotspot(g, _ptr(a), C.c_longlong(a.size), _ptr(p), C.c_longlong(p.size), _ptr(b),
+                     C.c_longlong(b.size), C.c_int(rows), C.c_int(cols), C.c_double(params["sdc"]),
+                     C.c_double(params["rx1"]), C.c_double(params["ry1"]), C.c_double(params["rz1"]),
+                     C.c_double(params["amb"]), C.c_int(nthreads), C.byref(t))
+        if t.kind:
+            raise RuntimeError(f"oracle hotspot trapped: {t.kind} at block {t.block}")
+        a, b = b, a
+    return a
+
+
+def cpu_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)

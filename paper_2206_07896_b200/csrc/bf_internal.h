@@ -1,0 +1,112 @@
+// Host-side internals of libbfgpu.so shared by the runtime and the kernel
+// launchers.  Nothing here crosses the C ABI (include/bfgpu.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bfgpu.h"
+
+namespace bf {
+
+struct DevFault;
+struct KDesc;
+
+// One resolved kernel argument (an ArgSlot after unpack_args, executor.py:48-75).
+struct ArgVal {
+  int32_t kind;     // bf_slot_kind
+  int32_t scalar;   // element type for handles
+  void* ptr;        // device pointer for handles
+  int64_t len;      // element count for handles
+  uint32_t handle;
+  int32_t i32;
+  int64_t i64;
+  double f64;       // f32 and f64 slots
+};
+
+// Host-detected trap, raised at the next synchronize (runtime.py:335-343).
+struct HostTrap {
+  int kind = BF_TRAP_NONE;
+  long long block = 0;
+  std::string message;
+};
+
+// Everything a launcher needs to issue one fetched block range.
+struct LaunchCtx {
+  const char* name;
+  int grid[3];
+  int block[3];
+  long long first, count;    // logical block range of this fetch
+  int64_t shmem;             // dynamic shared bytes (Runtime.launch shmem_bytes)
+  int warp_size;             // MpmdKernel.warp_size (0 if not warp mode)
+  const ArgVal* args;
+  int nargs;
+  cudaStream_t stream;
+  int num_sms;
+  int* executed;             // device, per task (nullable)
+  DevFault* fault;           // device fault word of the runtime
+  unsigned long long task;
+  HostTrap* trap;            // host-side trap sink (first wins)
+  std::string* error;        // BF_E_UNSUPPORTED / BF_E_CUDA message sink
+
+  KDesc desc() const;
+  // Record a trap detected on the host before launching (e.g. an affine
+  // index range that leaves a buffer); first one wins.
+  void host_trap(int kind, long long blk, const std::string& msg) const;
+  // Lowest linear block id in [first, first+count) whose x coordinate is x.
+  long long first_block_with_x(long long x) const;
+  // Distinct blockIdx.x values of the fetch range as half-open intervals
+  // (at most two; y/z copies of the same x are folded together).
+  std::vector<std::pair<long long, long long>> x_intervals() const;
+  // The fetch range as rectangles of (blockIdx.x, blockIdx.y) in block
+  // units, z copies folded: {x0, x1, y0, y1} half-open.
+  struct Rect { long long x0, x1, y0, y1; };
+  std::vector<Rect> xy_rects() const;
+};
+
+typedef int (*LauncherFn)(LaunchCtx& ctx);
+
+struct ParamSpec {
+  int32_t kind;    // bf_slot_kind
+  int32_t scalar;  // element bf_scalar for handles
+  const char* name;
+};
+
+struct KernelEntry {
+  const char* name;
+  std::vector<ParamSpec> params;
+  LauncherFn launch;
+};
+
+// Registry (populated by static registrars in each k_*.cu file).
+std::vector<KernelEntry>& registry();
+const KernelEntry* find_kernel(const char* name);
+
+struct Registrar {
+  Registrar(const char* name, std::vector<ParamSpec> params, LauncherFn fn) {
+    registry().push_back(KernelEntry{name, std::move(params), fn});
+  }
+};
+
+// Grid sizing for streaming kernels: a multiple of the SM count, capped by
+// the work available.
+inline int stream_grid(long long work_items, int items_per_cta, int num_sms,
+                       int ctas_per_sm) {
+  long long need = (work_items + items_per_cta - 1) / items_per_cta;
+  long long cap = (long long)num_sms * ctas_per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+#define BF_CUDA_LAUNCH_CHECK(ctx)                                   \
+  do {                                                              \
+    cudaError_t e_ = cudaGetLastError();                            \
+    if (e_ != cudaSuccess) {                                        \
+      *(ctx).error = std::string("launch failed: ") + cudaGetErrorString(e_); \
+      return BF_E_CUDA;                                             \
+    }                                                               \
+  } while (0)
+
+}  // namespace bf

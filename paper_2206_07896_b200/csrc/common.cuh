@@ -1,0 +1,65 @@
+// Device-side helpers shared by every sm_100a kernel of the launch runtime.
+//
+// A launch of the reference runtime hands a worker a contiguous range of
+// *logical* blocks [first, first+count) of a (grid, block) geometry
+// (runtime.py:175-201, 323-350).  On the GPU that range is executed by a
+// physical grid sized for the B200 (148 SMs); the logical geometry is carried
+// in KDesc and decoded exactly as the reference does (syntax.py:61-71).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bf_internal.h"
+
+namespace bf {
+
+// Device fault word; first fault wins (runtime.py:340-341).
+struct DevFault {
+  int kind;
+  int pad;
+  long long block;
+  unsigned long long task;
+};
+
+// Logical launch descriptor passed by value to every kernel.
+struct KDesc {
+  int gx, gy, gz;          // logical gridDim
+  int bx, by, bz;          // logical blockDim
+  long long first, count;  // logical block range of this fetch
+  int* executed;           // per-task run counts (BF_FLAG_INSTRUMENT), nullable
+  DevFault* fault;
+  unsigned long long task;
+};
+
+__device__ __forceinline__ void record_fault(const KDesc& d, int kind, long long block) {
+  if (atomicCAS(&d.fault->kind, 0, kind) == 0) {
+    d.fault->block = block;
+    d.fault->task = d.task;
+  }
+}
+
+// KernelTask.executed[b] += 1 for every block of the fetch (runtime.py:345).
+// Called by every CTA of the kernel that executed the range; the counts are
+// only observable after the stream drained, so the placement in the kernel
+// does not matter.
+__device__ __forceinline__ void mark_executed(const KDesc& d) {
+  if (d.executed == nullptr) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b = d.first + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       b < d.first + d.count; b += stride)
+    atomicAdd(d.executed + b, 1);
+}
+
+// i32 wrapping multiply-add, as `blockIdx.x * blockDim.x + threadIdx.x` is
+// evaluated with wrap_int after every operator (interp.py:89-90, arena.py:39-41).
+__device__ __forceinline__ int wrap_mad(int a, int b, int c) {
+  return (int)((unsigned)a * (unsigned)b + (unsigned)c);
+}
+
+// f64 arithmetic that must never be contracted into an FMA: the reference
+// rounds every binary operator result to double (Python float arithmetic).
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+}  // namespace bf

@@ -1,0 +1,175 @@
+// hotspot — paper_2206_07896_b200/kernels/hotspot.kn (Rodinia-style 5-point
+// thermal stencil, one iteration per launch, clamped borders).
+//
+// Semantics (bit-exact with the reference interpreter): temperatures and
+// power are f32 in memory; every operator is evaluated in f64 in source order
+// (interp.py:58-91) and the result is rounded to f32 once at the store
+// (arena.py:111-116).  The f32 scalar params carry doubles (hostprog.py:
+// 390-414).  No FMA contraction: dadd/dsub/dmul are the _rn intrinsics.
+//
+// B200 mapping (fast path): a warp owns a 128-column x RS-row strip; each lane
+// holds a float4 of the north/centre/south rows in registers and slides down
+// the strip, so every row of `src` is loaded once per strip (+2 halo rows
+// per RS rows, served by L2).  West/east neighbours come from warp shuffles;
+// lanes at the strip edge load one scalar.  Algorithmic traffic per cell and
+// iteration: 12 B (read src + power, write dst).
+#include <climits>
+
+#include "bf_internal.h"
+#include "common.cuh"
+
+namespace bf {
+
+struct HsConst {
+  double sdc, rx1, ry1, rz1, amb;
+};
+
+__device__ __forceinline__ float hs_cell(float tcf, float tnf, float tsf, float twf, float tef,
+                                         float pf, const HsConst& k) {
+  const double tc = tcf, tn = tnf, ts = tsf, tw = twf, te = tef, p = pf;
+  const double two_tc = dmul(2.0, tc);
+  const double a = dsub(dadd(ts, tn), two_tc);  // (ts + tn - 2.0*tc)
+  const double b = dsub(dadd(te, tw), two_tc);  // (te + tw - 2.0*tc)
+  const double c = dsub(k.amb, tc);             // (amb - tc)
+  double acc = dadd(p, dmul(a, k.ry1));
+  acc = dadd(acc, dmul(b, k.rx1));
+  acc = dadd(acc, dmul(c, k.rz1));
+  const double delta = dmul(k.sdc, acc);
+  return __double2float_rn(dadd(tc, delta));
+}
+
+constexpr int kHsRows = 16;  // rows per warp strip
+
+// blockDim = (32, 4): warp w of CTA (X, Y) owns columns
+// [c_lo + X*128, +128) and rows [r_lo + (Y*4 + w)*RS, +RS).
+__global__ void __launch_bounds__(128) hotspot_strip(const float* __restrict__ src,
+                                                     const float* __restrict__ power,
+                                                     float* __restrict__ dst, int rows, int cols,
+                                                     int r_lo, int r_hi, int c_lo, int c_hi,
+                                                     HsConst k) {
+  const int lane = threadIdx.x;
+  const int c0 = c_lo + blockIdx.x * 128 + lane * 4;
+  const int r_start = r_lo + (blockIdx.y * 4 + threadIdx.y) * kHsRows;
+  if (r_start >= r_hi) return;  // warp-uniform
+  const int r_end = min(r_start + kHsRows, r_hi);
+  const bool active = c0 < c_hi;
+  const bool east_scalar = (lane == 31) || (c0 + 4 >= c_hi);
+  const long long colsl = cols;
+
+  auto load_row = [&](int r) -> float4 {
+    if (!active) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return __ldg(reinterpret_cast<const float4*>(src + r * colsl + c0));
+  };
+
+  float4 north = load_row(r_start > 0 ? r_start - 1 : 0);
+  float4 center = load_row(r_start);
+  for (int r = r_start; r < r_end; r++) {
+    const float4 south = load_row(r + 1 < rows ? r + 1 : rows - 1);
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (active) p = __ldcs(reinterpret_cast<const float4*>(power + r * colsl + c0));
+    float west = __shfl_up_sync(0xffffffffu, center.w, 1);
+    float east = __shfl_down_sync(0xffffffffu, center.x, 1);
+    if (active) {
+      if (lane == 0) west = c0 > 0 ? __ldg(src + r * colsl + c0 - 1) : center.x;
+      if (east_scalar) east = c0 + 4 < cols ? __ldg(src + r * colsl + c0 + 4) : center.w;
+      float4 out;
+      out.x = hs_cell(center.x, north.x, south.x, west, center.y, p.x, k);
+      out.y = hs_cell(center.y, north.y, south.y, center.x, center.z, p.y, k);
+      out.z = hs_cell(center.z, north.z, south.z, center.y, center.w, p.z, k);
+      out.w = hs_cell(center.w, north.w, south.w, center.z, east, p.w, k);
+      *reinterpret_cast<float4*>(dst + r * colsl + c0) = out;
+    }
+    north = center;
+    center = south;
+  }
+}
+
+// Generic path: any geometry or alignment; one thread per cell of the cell
+// rectangle, indices evaluated with i32 wrap exactly as the DSL does, every
+// access bounds-checked (a trap records the logical block and skips).
+__global__ void __launch_bounds__(256) hotspot_cells(const float* src, const float* power,
+                                                     float* dst, long long len_src,
+                                                     long long len_pow, long long len_dst,
+                                                     int rows, int cols, int r_lo, int r_hi,
+                                                     int c_lo, int c_hi, HsConst k, KDesc d,
+                                                     long long zbase) {
+  const long long w = c_hi - c_lo;
+  const long long total = w * (long long)(r_hi - r_lo);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = r_lo + (int)(i / w);
+    const int c = c_lo + (int)(i % w);
+    const int rn = max(r - 1, 0), rs = min(r + 1, rows - 1);
+    const int cw = max(c - 1, 0), ce = min(c + 1, cols - 1);
+    const int idx = wrap_mad(r, cols, c);
+    const int in_ = wrap_mad(rn, cols, c), is_ = wrap_mad(rs, cols, c);
+    const int iw = wrap_mad(r, cols, cw), ie = wrap_mad(r, cols, ce);
+    if (idx < 0 || idx >= len_src || in_ < 0 || in_ >= len_src || is_ < 0 || is_ >= len_src ||
+        iw < 0 || iw >= len_src || ie < 0 || ie >= len_src || idx >= len_pow || idx >= len_dst) {
+      const long long blk = zbase + (long long)(r / d.by) * d.gx + c / d.bx;
+      record_fault(d, BF_TRAP_OUT_OF_BOUNDS, blk);
+      continue;
+    }
+    dst[idx] = hs_cell(src[idx], src[in_], src[is_], src[iw], src[ie], power[idx], k);
+  }
+}
+
+static int launch_hotspot(LaunchCtx& ctx) {
+  const ArgVal& S = ctx.args[0];
+  const ArgVal& P = ctx.args[1];
+  const ArgVal& D = ctx.args[2];
+  const int rows = ctx.args[3].i32;
+  const int cols = ctx.args[4].i32;
+  HsConst k{ctx.args[5].f64, ctx.args[6].f64, ctx.args[7].f64, ctx.args[8].f64,
+            ctx.args[9].f64};
+  if (rows <= 0 || cols <= 0) return BF_OK;
+  const long long bx = ctx.block[0], by = ctx.block[1];
+  const long long plane = (long long)ctx.grid[0] * ctx.grid[1];
+  long long zbase = (ctx.first / plane) * plane;
+  const long long need = (long long)rows * cols;
+  const bool in_bounds = need <= INT_MAX && S.len >= need && P.len >= need && D.len >= need;
+  for (auto& rc : ctx.xy_rects()) {
+    long long c_lo = rc.x0 * bx, c_hi = rc.x1 * bx;
+    long long r_lo = rc.y0 * by, r_hi = rc.y1 * by;
+    if (c_hi > cols) c_hi = cols;
+    if (r_hi > rows) r_hi = rows;
+    if (c_lo >= c_hi || r_lo >= r_hi) continue;
+    // c/r beyond INT_MAX would wrap in the DSL; such launches are rejected
+    if (c_hi > INT_MAX || r_hi > INT_MAX) {
+      *ctx.error = "hotspot: cell coordinates beyond i32 range";
+      return BF_E_UNSUPPORTED;
+    }
+    const bool aligned = (cols % 4 == 0) && (c_lo % 4 == 0) && (c_hi % 4 == 0);
+    if (in_bounds && aligned) {
+      dim3 grid((unsigned)((c_hi - c_lo + 127) / 128),
+                (unsigned)((r_hi - r_lo + 4 * kHsRows - 1) / (4 * kHsRows)));
+      hotspot_strip<<<grid, dim3(32, 4), 0, ctx.stream>>>(
+          (const float*)S.ptr, (const float*)P.ptr, (float*)D.ptr, rows, cols, (int)r_lo,
+          (int)r_hi, (int)c_lo, (int)c_hi, k);
+    } else {
+      long long zb = zbase;
+      if (zb + (rc.y0 * ctx.grid[0] + rc.x0) < ctx.first) zb += plane;
+      int grid = stream_grid((c_hi - c_lo) * (r_hi - r_lo), 256, ctx.num_sms, 8);
+      hotspot_cells<<<grid, 256, 0, ctx.stream>>>(
+          (const float*)S.ptr, (const float*)P.ptr, (float*)D.ptr, S.len, P.len, D.len, rows,
+          cols, (int)r_lo, (int)r_hi, (int)c_lo, (int)c_hi, k, ctx.desc(), zb);
+    }
+    BF_CUDA_LAUNCH_CHECK(ctx);
+  }
+  return BF_OK;
+}
+
+static Registrar reg_hotspot("hotspot",
+                             {{BF_SLOT_HANDLE, BF_F32, "src"},
+                              {BF_SLOT_HANDLE, BF_F32, "power"},
+                              {BF_SLOT_HANDLE, BF_F32, "dst"},
+                              {BF_SLOT_I32, BF_I32, "rows"},
+                              {BF_SLOT_I32, BF_I32, "cols"},
+                              {BF_SLOT_F32, BF_F32, "sdc"},
+                              {BF_SLOT_F32, BF_F32, "rx1"},
+                              {BF_SLOT_F32, BF_F32, "ry1"},
+                              {BF_SLOT_F32, BF_F32, "rz1"},
+                              {BF_SLOT_F32, BF_F32, "amb"}},
+                             launch_hotspot);
+
+}  // namespace bf

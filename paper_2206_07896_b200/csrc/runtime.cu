@@ -1,0 +1,1126 @@
+// libbfgpu.so — the launch runtime and memory shim behind include/bfgpu.h.
+//
+// Reference: /root/reference/pkg/src/blockfuse/runtime.py (Runtime, TaskQueue,
+// KernelTask, RuntimeCounters, resolve_grain) and arena.py (DeviceArena).
+//
+// B200 mapping
+//   * DeviceArena  -> handle table over cudaMalloc'd HBM buffers (zero-filled),
+//                     pinned staging for host copies; frees are deferred to the
+//                     next quiescence point so a free can never race a kernel.
+//   * TaskQueue    -> the same FIFO/cursor protocol, run by the host dispatcher.
+//   * pool workers -> `pool_size` in-order CUDA streams on the arena's device;
+//                     each fetched range of `grain` logical blocks becomes one
+//                     grid launch on the next worker stream (round robin).
+//   * hold_blocks  -> a gate kernel spinning on a host-mapped flag is queued in
+//                     front of each worker's work until the next synchronize.
+//   * traps        -> a device fault word (first wins) plus host-detected traps,
+//                     surfaced at synchronize as BF_E_FAULT.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "bf_internal.h"
+#include "common.cuh"
+
+namespace bf {
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  return fail(BF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                  \
+  do {                                            \
+    cudaError_t e__ = (call);                     \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+static const int kScalarSize[4] = {4, 8, 4, 8};
+
+// ---------------------------------------------------------------------------
+// registry
+// ---------------------------------------------------------------------------
+
+std::vector<KernelEntry>& registry() {
+  static std::vector<KernelEntry> r;
+  return r;
+}
+
+const KernelEntry* find_kernel(const char* name) {
+  for (auto& k : registry())
+    if (std::strcmp(k.name, name) == 0) return &k;
+  return nullptr;
+}
+
+KDesc LaunchCtx::desc() const {
+  KDesc d;
+  d.gx = grid[0]; d.gy = grid[1]; d.gz = grid[2];
+  d.bx = block[0]; d.by = block[1]; d.bz = block[2];
+  d.first = first; d.count = count;
+  d.executed = executed;
+  d.fault = fault;
+  d.task = task;
+  return d;
+}
+
+void LaunchCtx::host_trap(int kind, long long blk, const std::string& msg) const {
+  if (trap->kind == BF_TRAP_NONE) {
+    trap->kind = kind;
+    trap->block = blk;
+    trap->message = msg;
+  }
+}
+
+long long LaunchCtx::first_block_with_x(long long x) const {
+  long long gx = grid[0];
+  long long x0 = first % gx;
+  long long delta = (x - x0 + gx) % gx;
+  return first + delta;
+}
+
+std::vector<std::pair<long long, long long>> LaunchCtx::x_intervals() const {
+  std::vector<std::pair<long long, long long>> out;
+  long long gx = grid[0];
+  if (count >= gx) {
+    out.push_back({0, gx});
+    return out;
+  }
+  long long x0 = first % gx;
+  if (x0 + count <= gx) {
+    out.push_back({x0, x0 + count});
+  } else {
+    out.push_back({0, x0 + count - gx});
+    out.push_back({x0, gx});
+  }
+  return out;
+}
+
+std::vector<LaunchCtx::Rect> LaunchCtx::xy_rects() const {
+  std::vector<Rect> out;
+  long long gx = grid[0], gy = grid[1];
+  long long plane = gx * gy;
+  if (count >= plane) {
+    out.push_back({0, gx, 0, gy});
+    return out;
+  }
+  // at most two segments (the range crosses at most one z boundary)
+  long long s = first % plane;
+  std::vector<std::pair<long long, long long>> segs;
+  if (s + count <= plane) {
+    segs.push_back({s, s + count});
+  } else {
+    segs.push_back({s, plane});
+    segs.push_back({0, s + count - plane});
+  }
+  for (auto& sg : segs) {
+    long long p0 = sg.first, p1 = sg.second;  // [p0, p1) within the plane
+    long long y0 = p0 / gx, x0 = p0 % gx;
+    long long yl = (p1 - 1) / gx, xl = (p1 - 1) % gx;  // last block
+    if (y0 == yl) {
+      out.push_back({x0, xl + 1, y0, y0 + 1});
+      continue;
+    }
+    long long full_lo = y0, full_hi = yl + 1;
+    if (x0 > 0) {
+      out.push_back({x0, gx, y0, y0 + 1});
+      full_lo = y0 + 1;
+    }
+    if (xl < gx - 1) {
+      out.push_back({0, xl + 1, yl, yl + 1});
+      full_hi = yl;
+    }
+    if (full_hi > full_lo) out.push_back({0, gx, full_lo, full_hi});
+  }
+  return out;
+}
+
+__global__ void mark_kernel(int* executed, long long first, long long count) {
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b = first + (long long)blockIdx.x * blockDim.x + threadIdx.x; b < first + count;
+       b += stride)
+    atomicAdd(executed + b, 1);
+}
+
+// ---------------------------------------------------------------------------
+// arena
+// ---------------------------------------------------------------------------
+
+struct Buffer {
+  int32_t scalar;
+  int64_t length;
+  void* ptr;
+};
+
+}  // namespace bf
+
+struct bf_arena {
+  int device = 0;
+  uint32_t next_handle = 1;
+  std::map<uint32_t, bf::Buffer> buffers;
+  std::vector<void*> zombies;     // freed buffers awaiting a quiescence point
+  cudaStream_t copy_stream = nullptr;
+  void* staging[2] = {nullptr, nullptr};
+  size_t staging_bytes = 0;
+  cudaEvent_t staging_ev[2] = {nullptr, nullptr};
+  int live_runtimes = 0;
+};
+
+namespace bf {
+
+static int set_device(int dev) {
+  cudaError_t e = cudaSetDevice(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  return BF_OK;
+}
+
+static Buffer* lookup(bf_arena* a, uint32_t h) {
+  auto it = a->buffers.find(h);
+  return it == a->buffers.end() ? nullptr : &it->second;
+}
+
+static void release_zombies(bf_arena* a) {
+  for (void* p : a->zombies) cudaFree(p);
+  a->zombies.clear();
+}
+
+static const size_t kStagingChunk = 32u << 20;  // 32 MiB double-buffered staging
+
+static int ensure_staging(bf_arena* a) {
+  if (a->staging[0]) return BF_OK;
+  for (int i = 0; i < 2; i++) {
+    CK(cudaHostAlloc(&a->staging[i], kStagingChunk, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&a->staging_ev[i], cudaEventDisableTiming));
+  }
+  a->staging_bytes = kStagingChunk;
+  return BF_OK;
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
+}  // namespace bf
+
+// ---------------------------------------------------------------------------
+// task queue (TaskQueue, runtime.py:146-205)
+// ---------------------------------------------------------------------------
+
+struct bf_queue {
+  struct Entry {
+    uint64_t tag;
+    int64_t total;
+    int64_t grain;
+    int64_t cursor = 0;
+    int64_t fetches = 0;
+  };
+  std::mutex mu;
+  std::deque<Entry> tasks;
+  std::map<uint64_t, std::pair<int64_t, int64_t>> retired;  // tag -> (fetches, cursor)
+  bool closed = false;
+  int64_t fetch_count = 0;
+  int64_t queue_waits = 0;
+};
+
+// ---------------------------------------------------------------------------
+// runtime
+// ---------------------------------------------------------------------------
+
+namespace bf {
+
+struct FetchRecord {
+  uint64_t task;
+  int worker;
+  long long first, count;
+  cudaEvent_t done;
+};
+
+struct TaskRec {
+  std::string kernel;
+  int64_t total = 0;
+  int64_t grain = 0;
+  int64_t fetches = 0;
+  int64_t cursor = 0;
+  int64_t completed = 0;        // blocks of retired fetches
+  int* executed_dev = nullptr;  // BF_FLAG_INSTRUMENT
+  std::vector<std::pair<long long, long long>> done_ranges;
+};
+
+__global__ void gate_kernel(volatile int* gate, DevFault* fault) {
+  // Spin until the host opens the gate at synchronize; bail out after 120 s
+  // so a host that never synchronizes cannot wedge the device.
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*gate == 0) {
+    __nanosleep(2000);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 120ull * 1000000000ull) {
+      if (atomicCAS(&fault->kind, 0, BF_TRAP_NON_UNIFORM_TRIP) == 0) fault->block = -1;
+      return;
+    }
+  }
+}
+
+__global__ void delay_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+}  // namespace bf
+
+struct bf_runtime {
+  bf_arena* arena = nullptr;
+  int device = 0;
+  int pool = 1;
+  uint32_t flags = 0;
+  double block_delay = 0.0;
+  std::mt19937_64 rng;
+  int num_sms = 148;
+  bool shut_down = false;
+  std::vector<cudaStream_t> streams;
+  std::vector<bool> gated;       // worker already has a gate queued
+  volatile int* gate_host = nullptr;
+  int* gate_dev = nullptr;
+  bool holding = false;
+  bf::DevFault* fault_dev = nullptr;
+  bf::HostTrap trap;             // first trap (host- or device-detected)
+  uint64_t trap_task = 0;
+  std::string trap_kernel;
+  bf_queue queue;
+  std::map<uint64_t, bf::TaskRec> tasks;
+  std::deque<bf::FetchRecord> inflight;
+  std::vector<cudaEvent_t> event_pool;
+  uint64_t next_task = 1;
+  uint64_t rr = 0;               // round-robin worker cursor
+  // counters
+  int64_t blocks_executed = 0;
+  int64_t syncs = 0;
+  std::vector<int64_t> busy;
+};
+
+namespace bf {
+
+static cudaEvent_t get_event(bf_runtime* rt) {
+  if (!rt->event_pool.empty()) {
+    cudaEvent_t e = rt->event_pool.back();
+    rt->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
+// Retire completed fetches (all of them when `wait`).
+static int retire(bf_runtime* rt, bool wait) {
+  while (!rt->inflight.empty()) {
+    FetchRecord& f = rt->inflight.front();
+    if (wait) {
+      cudaError_t e = cudaEventSynchronize(f.done);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+    } else {
+      cudaError_t e = cudaEventQuery(f.done);
+      if (e == cudaErrorNotReady) {
+        // fetches on other workers may have finished; keep FIFO simple and
+        // scan the rest without blocking
+        bool any = false;
+        for (auto it = rt->inflight.begin() + 1; it != rt->inflight.end();) {
+          if (cudaEventQuery(it->done) == cudaSuccess) {
+            TaskRec& t = rt->tasks[it->task];
+            t.completed += it->count;
+            t.done_ranges.push_back({it->first, it->count});
+            rt->blocks_executed += it->count;
+            rt->busy[it->worker] += it->count;
+            rt->event_pool.push_back(it->done);
+            it = rt->inflight.erase(it);
+            any = true;
+          } else {
+            cudaGetLastError();
+            ++it;
+          }
+        }
+        (void)any;
+        return BF_OK;
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventQuery");
+    }
+    TaskRec& t = rt->tasks[f.task];
+    t.completed += f.count;
+    t.done_ranges.push_back({f.first, f.count});
+    rt->blocks_executed += f.count;
+    rt->busy[f.worker] += f.count;
+    rt->event_pool.push_back(f.done);
+    rt->inflight.pop_front();
+  }
+  return BF_OK;
+}
+
+static void open_gate(bf_runtime* rt) {
+  if (rt->gate_host) *rt->gate_host = 1;
+  rt->holding = false;
+  std::fill(rt->gated.begin(), rt->gated.end(), false);
+}
+
+static int sync_workers(bf_runtime* rt) {
+  open_gate(rt);
+  for (auto s : rt->streams) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  }
+  return retire(rt, true);
+}
+
+static void absorb_device_fault(bf_runtime* rt) {
+  DevFault f;
+  if (cudaMemcpy(&f, rt->fault_dev, sizeof(f), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (f.kind != BF_TRAP_NONE && rt->trap.kind == BF_TRAP_NONE) {
+    rt->trap.kind = f.kind;
+    rt->trap.block = f.block;
+    auto it = rt->tasks.find(f.task);
+    rt->trap_task = f.task;
+    rt->trap_kernel = it == rt->tasks.end() ? "?" : it->second.kernel;
+    static const char* names[] = {"", "index out of range", "division by zero",
+                                  "type fault", "non-uniform trip / gate timeout"};
+    rt->trap.message = std::string(names[f.kind < 5 ? f.kind : 0]) + " (device)";
+  }
+}
+
+static void fill_fault(bf_runtime* rt, bf_fault* out) {
+  if (!out) return;
+  std::memset(out, 0, sizeof(*out));
+  out->kind = rt->trap.kind;
+  out->block_id = rt->trap.block;
+  out->task_id = rt->trap_task;
+  std::snprintf(out->kernel, sizeof(out->kernel), "%s", rt->trap_kernel.c_str());
+  std::snprintf(out->message, sizeof(out->message), "%s", rt->trap.message.c_str());
+}
+
+}  // namespace bf
+
+using namespace bf;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int bf_abi_version(void) { return BFGPU_ABI_VERSION; }
+
+const char* bf_last_error(void) { return g_last_error.c_str(); }
+
+int bf_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return fail(BF_E_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *count = n;
+  return BF_OK;
+}
+
+// ---- arena ---------------------------------------------------------------
+
+int bf_arena_create(int32_t device, bf_arena** out) {
+  if (!out) return fail(BF_E_INVALID, "null out");
+  int rc = set_device(device);
+  if (rc) return rc;
+  auto* a = new bf_arena();
+  a->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&a->copy_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete a;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  *out = a;
+  return BF_OK;
+}
+
+int bf_arena_destroy(bf_arena* a) {
+  if (!a) return BF_OK;
+  set_device(a->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : a->buffers) cudaFree(kv.second.ptr);
+  release_zombies(a);
+  for (int i = 0; i < 2; i++) {
+    if (a->staging[i]) cudaFreeHost(a->staging[i]);
+    if (a->staging_ev[i]) cudaEventDestroy(a->staging_ev[i]);
+  }
+  if (a->copy_stream) cudaStreamDestroy(a->copy_stream);
+  delete a;
+  return BF_OK;
+}
+
+int bf_alloc(bf_arena* a, int32_t scalar, int64_t length, uint32_t* handle) {
+  if (!a || !handle) return fail(BF_E_INVALID, "null argument");
+  if (scalar < 0 || scalar > 3) return fail(BF_E_INVALID, "bad scalar type");
+  if (length < 0) return fail(BF_E_INVALID, "negative buffer length " + std::to_string(length));
+  int rc = set_device(a->device);
+  if (rc) return rc;
+  size_t bytes = (size_t)length * kScalarSize[scalar];
+  void* p = nullptr;
+  // always allocate at least one 512 B line so every handle has a distinct,
+  // 16 B-aligned pointer and vector loads past a ragged tail stay mapped
+  size_t alloc = ((bytes + 511) / 512) * 512;
+  if (alloc == 0) alloc = 512;
+  CK(cudaMalloc(&p, alloc));
+  CK(cudaMemsetAsync(p, 0, alloc, a->copy_stream));
+  CK(cudaStreamSynchronize(a->copy_stream));
+  uint32_t h = a->next_handle++;
+  a->buffers[h] = Buffer{scalar, length, p};
+  *handle = h;
+  return BF_OK;
+}
+
+int bf_free(bf_arena* a, uint32_t h) {
+  if (!a) return fail(BF_E_INVALID, "null arena");
+  auto it = a->buffers.find(h);
+  if (it == a->buffers.end())
+    return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+  a->zombies.push_back(it->second.ptr);
+  a->buffers.erase(it);
+  if (a->live_runtimes == 0) {
+    set_device(a->device);
+    cudaDeviceSynchronize();
+    release_zombies(a);
+  }
+  return BF_OK;
+}
+
+int bf_buffer_info(bf_arena* a, uint32_t h, int32_t* scalar, int64_t* length,
+                   uint64_t* device_ptr) {
+  if (!a) return fail(BF_E_INVALID, "null arena");
+  Buffer* b = lookup(a, h);
+  if (!b) return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+  if (scalar) *scalar = b->scalar;
+  if (length) *length = b->length;
+  if (device_ptr) *device_ptr = (uint64_t)(uintptr_t)b->ptr;
+  return BF_OK;
+}
+
+static int check_range(Buffer* b, int64_t nbytes, int64_t offset) {
+  int64_t cap = b->length * kScalarSize[b->scalar];
+  if (nbytes < 0 || offset < 0 || offset + nbytes > cap)
+    return fail(BF_E_INVALID, "byte range [" + std::to_string(offset) + ", " +
+                                  std::to_string(offset + nbytes) + ") outside buffer of " +
+                                  std::to_string(cap) + " bytes");
+  return BF_OK;
+}
+
+int bf_upload(bf_arena* a, uint32_t h, const void* src, int64_t nbytes, int64_t offset) {
+  if (!a) return fail(BF_E_INVALID, "null arena");
+  Buffer* b = lookup(a, h);
+  if (!b) return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+  int rc = check_range(b, nbytes, offset);
+  if (rc) return rc;
+  if (nbytes == 0) return BF_OK;
+  rc = set_device(a->device);
+  if (rc) return rc;
+  char* dst = (char*)b->ptr + offset;
+  if (is_pinned(src)) {
+    CK(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyHostToDevice, a->copy_stream));
+    CK(cudaStreamSynchronize(a->copy_stream));
+    return BF_OK;
+  }
+  rc = ensure_staging(a);
+  if (rc) return rc;
+  // double-buffered: memcpy into staging[i] while staging[i^1] is in flight
+  int64_t done = 0;
+  int i = 0;
+  while (done < nbytes) {
+    int64_t n = std::min<int64_t>(nbytes - done, (int64_t)a->staging_bytes);
+    CK(cudaEventSynchronize(a->staging_ev[i]));
+    std::memcpy(a->staging[i], (const char*)src + done, n);
+    CK(cudaMemcpyAsync(dst + done, a->staging[i], n, cudaMemcpyHostToDevice, a->copy_stream));
+    CK(cudaEventRecord(a->staging_ev[i], a->copy_stream));
+    done += n;
+    i ^= 1;
+  }
+  CK(cudaStreamSynchronize(a->copy_stream));
+  return BF_OK;
+}
+
+int bf_download(bf_arena* a, uint32_t h, void* dstp, int64_t nbytes, int64_t offset) {
+  if (!a) return fail(BF_E_INVALID, "null arena");
+  Buffer* b = lookup(a, h);
+  if (!b) return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+  int rc = check_range(b, nbytes, offset);
+  if (rc) return rc;
+  if (nbytes == 0) return BF_OK;
+  rc = set_device(a->device);
+  if (rc) return rc;
+  const char* src = (const char*)b->ptr + offset;
+  if (is_pinned(dstp)) {
+    CK(cudaMemcpyAsync(dstp, src, nbytes, cudaMemcpyDeviceToHost, a->copy_stream));
+    CK(cudaStreamSynchronize(a->copy_stream));
+    return BF_OK;
+  }
+  rc = ensure_staging(a);
+  if (rc) return rc;
+  // pipeline: D2H chunk k+1 in flight while chunk k is memcpy'd out
+  int64_t chunk = (int64_t)a->staging_bytes;
+  int64_t nchunks = (nbytes + chunk - 1) / chunk;
+  for (int64_t k = 0; k < nchunks; k++) {
+    int i = (int)(k & 1);
+    int64_t off = k * chunk;
+    int64_t n = std::min<int64_t>(nbytes - off, chunk);
+    CK(cudaMemcpyAsync(a->staging[i], src + off, n, cudaMemcpyDeviceToHost, a->copy_stream));
+    CK(cudaEventRecord(a->staging_ev[i], a->copy_stream));
+    if (k > 0) {
+      int j = i ^ 1;
+      int64_t poff = (k - 1) * chunk;
+      int64_t pn = std::min<int64_t>(nbytes - poff, chunk);
+      CK(cudaEventSynchronize(a->staging_ev[j]));
+      std::memcpy((char*)dstp + poff, a->staging[j], pn);
+    }
+  }
+  {
+    int64_t k = nchunks - 1;
+    int i = (int)(k & 1);
+    int64_t off = k * chunk;
+    int64_t n = std::min<int64_t>(nbytes - off, chunk);
+    CK(cudaEventSynchronize(a->staging_ev[i]));
+    std::memcpy((char*)dstp + off, a->staging[i], n);
+  }
+  return BF_OK;
+}
+
+int bf_fill32(bf_arena* a, uint32_t h, uint32_t pattern, int64_t offset, int64_t nbytes) {
+  if (!a) return fail(BF_E_INVALID, "null arena");
+  Buffer* b = lookup(a, h);
+  if (!b) return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+  int rc = check_range(b, nbytes, offset);
+  if (rc) return rc;
+  if ((offset | nbytes) & 3) return fail(BF_E_INVALID, "fill32 needs 4-byte alignment");
+  if (nbytes == 0) return BF_OK;
+  rc = set_device(a->device);
+  if (rc) return rc;
+  char* p = (char*)b->ptr + offset;
+  if (pattern == 0 || pattern == 0xffffffffu) {
+    CK(cudaMemsetAsync(p, pattern & 0xff, nbytes, a->copy_stream));
+  } else {
+    // cudaMemset2D trick is byte-wise; use the driver-free path: a pinned
+    // pattern chunk replicated by copies.
+    std::vector<uint32_t> pat((size_t)std::min<int64_t>(nbytes / 4, 1 << 20), pattern);
+    int64_t chunk = (int64_t)pat.size() * 4;
+    for (int64_t off = 0; off < nbytes; off += chunk) {
+      int64_t n = std::min(chunk, nbytes - off);
+      CK(cudaMemcpyAsync(p + off, pat.data(), n, cudaMemcpyHostToDevice, a->copy_stream));
+    }
+  }
+  CK(cudaStreamSynchronize(a->copy_stream));
+  return BF_OK;
+}
+
+int bf_copy(bf_arena* a, uint32_t dst, int64_t dst_offset, uint32_t src, int64_t src_offset,
+            int64_t nbytes) {
+  if (!a) return fail(BF_E_INVALID, "null arena");
+  Buffer* d = lookup(a, dst);
+  Buffer* s = lookup(a, src);
+  if (!d || !s) return fail(BF_E_DANGLING, "dangling buffer handle");
+  int rc = check_range(d, nbytes, dst_offset);
+  if (rc) return rc;
+  rc = check_range(s, nbytes, src_offset);
+  if (rc) return rc;
+  if (nbytes == 0) return BF_OK;
+  rc = set_device(a->device);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync((char*)d->ptr + dst_offset, (char*)s->ptr + src_offset, nbytes,
+                     cudaMemcpyDeviceToDevice, a->copy_stream));
+  CK(cudaStreamSynchronize(a->copy_stream));
+  return BF_OK;
+}
+
+// ---- task queue ------------------------------------------------------------
+
+int bf_queue_create(bf_queue** out) {
+  if (!out) return fail(BF_E_INVALID, "null out");
+  *out = new bf_queue();
+  return BF_OK;
+}
+
+int bf_queue_destroy(bf_queue* q) {
+  delete q;
+  return BF_OK;
+}
+
+int bf_queue_push(bf_queue* q, uint64_t tag, int64_t total, int64_t grain) {
+  if (!q) return fail(BF_E_INVALID, "null queue");
+  std::lock_guard<std::mutex> g(q->mu);
+  if (q->closed) return fail(BF_E_SHUTDOWN, "launch after shutdown");
+  if (total < 1 || grain < 1) return fail(BF_E_INVALID, "total and grain must be >= 1");
+  bf_queue::Entry e;
+  e.tag = tag;
+  e.total = total;
+  e.grain = grain;
+  q->tasks.push_back(e);
+  return BF_OK;
+}
+
+int bf_queue_fetch(bf_queue* q, int32_t* got, uint64_t* tag, int64_t* first, int64_t* count) {
+  if (!q || !got) return fail(BF_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(q->mu);
+  if (q->tasks.empty()) {
+    *got = 0;
+    return BF_OK;
+  }
+  bf_queue::Entry& t = q->tasks.front();
+  int64_t f = t.cursor;
+  int64_t c = std::min(t.grain, t.total - f);
+  t.cursor = f + c;
+  t.fetches += 1;
+  q->fetch_count += 1;
+  *got = 1;
+  if (tag) *tag = t.tag;
+  if (first) *first = f;
+  if (count) *count = c;
+  if (t.cursor == t.total) {
+    q->retired[t.tag] = {t.fetches, t.cursor};
+    q->tasks.pop_front();
+  }
+  return BF_OK;
+}
+
+int bf_queue_close(bf_queue* q) {
+  if (!q) return fail(BF_E_INVALID, "null queue");
+  std::lock_guard<std::mutex> g(q->mu);
+  q->closed = true;
+  return BF_OK;
+}
+
+int bf_queue_is_empty(bf_queue* q, int32_t* empty) {
+  if (!q || !empty) return fail(BF_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(q->mu);
+  *empty = q->tasks.empty() ? 1 : 0;
+  return BF_OK;
+}
+
+int bf_queue_task(bf_queue* q, uint64_t tag, int64_t* fetches, int64_t* cursor) {
+  if (!q) return fail(BF_E_INVALID, "null queue");
+  std::lock_guard<std::mutex> g(q->mu);
+  for (auto& t : q->tasks)
+    if (t.tag == tag) {
+      if (fetches) *fetches = t.fetches;
+      if (cursor) *cursor = t.cursor;
+      return BF_OK;
+    }
+  auto it = q->retired.find(tag);
+  if (it == q->retired.end()) return fail(BF_E_INVALID, "unknown task tag");
+  if (fetches) *fetches = it->second.first;
+  if (cursor) *cursor = it->second.second;
+  return BF_OK;
+}
+
+int bf_queue_counters(bf_queue* q, int64_t* fetch_count, int64_t* queue_waits) {
+  if (!q) return fail(BF_E_INVALID, "null queue");
+  std::lock_guard<std::mutex> g(q->mu);
+  if (fetch_count) *fetch_count = q->fetch_count;
+  if (queue_waits) *queue_waits = q->queue_waits;
+  return BF_OK;
+}
+
+// ---- grain -----------------------------------------------------------------
+
+int bf_resolve_grain(int32_t policy, int64_t fixed_grain, int64_t grid_size, int64_t pool_size,
+                     int32_t has_atomics, int64_t estimate, int64_t light_threshold,
+                     int64_t* grain) {
+  if (!grain) return fail(BF_E_INVALID, "null out");
+  if (grid_size < 1 || pool_size < 1)
+    return fail(BF_E_INVALID, "grid_size and pool_size must be >= 1");
+  int64_t average = (grid_size + pool_size - 1) / pool_size;
+  int64_t g;
+  if (policy == BF_POLICY_AVERAGE) {
+    g = average;
+  } else if (policy == BF_POLICY_FIXED) {
+    if (fixed_grain < 1) return fail(BF_E_INVALID, "grain must be >= 1");
+    g = std::min(fixed_grain, grid_size);
+  } else if (policy == BF_POLICY_AUTO) {
+    g = average;
+    if (has_atomics > 0) {
+      g = std::min(2 * average, grid_size);
+    } else if (has_atomics == 0 && estimate >= 0 && estimate < light_threshold) {
+      g = std::min(std::max(average, grid_size / 2), grid_size);
+    }
+  } else {
+    return fail(BF_E_INVALID, "unknown policy");
+  }
+  *grain = std::max<int64_t>(g, 1);
+  return BF_OK;
+}
+
+// ---- runtime ---------------------------------------------------------------
+
+int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double block_delay,
+                      uint64_t seed, bf_runtime** out) {
+  if (!a || !out) return fail(BF_E_INVALID, "null argument");
+  if (pool_size < 1)
+    return fail(BF_E_INVALID, "pool size must be >= 1, got " + std::to_string(pool_size));
+  int rc = set_device(a->device);
+  if (rc) return rc;
+  auto* rt = new bf_runtime();
+  rt->arena = a;
+  rt->device = a->device;
+  rt->pool = pool_size;
+  rt->flags = flags;
+  rt->block_delay = block_delay;
+  rt->rng.seed(seed);
+  rt->busy.assign(pool_size, 0);
+  rt->gated.assign(pool_size, false);
+  cudaDeviceGetAttribute(&rt->num_sms, cudaDevAttrMultiProcessorCount, a->device);
+  for (int i = 0; i < pool_size; i++) {
+    cudaStream_t s;
+    cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      for (auto x : rt->streams) cudaStreamDestroy(x);
+      delete rt;
+      return cuda_fail(e, "cudaStreamCreate");
+    }
+    rt->streams.push_back(s);
+  }
+  void* gh = nullptr;
+  if (cudaHostAlloc(&gh, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
+    cudaGetLastError();
+    for (auto x : rt->streams) cudaStreamDestroy(x);
+    delete rt;
+    return fail(BF_E_CUDA, "cudaHostAlloc(gate) failed");
+  }
+  rt->gate_host = (volatile int*)gh;
+  *rt->gate_host = (flags & BF_FLAG_HOLD_BLOCKS) ? 0 : 1;
+  rt->holding = (flags & BF_FLAG_HOLD_BLOCKS) != 0;
+  cudaHostGetDevicePointer((void**)&rt->gate_dev, gh, 0);
+  if (cudaMalloc(&rt->fault_dev, sizeof(DevFault)) != cudaSuccess ||
+      cudaMemset(rt->fault_dev, 0, sizeof(DevFault)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BF_E_CUDA, "fault word allocation failed");
+  }
+  a->live_runtimes++;
+  *out = rt;
+  return BF_OK;
+}
+
+int bf_shutdown(bf_runtime* rt) {
+  if (!rt) return fail(BF_E_INVALID, "null runtime");
+  if (rt->shut_down) return BF_OK;
+  rt->shut_down = true;
+  set_device(rt->device);
+  bf_queue_close(&rt->queue);
+  int rc = sync_workers(rt);
+  absorb_device_fault(rt);
+  return rc;
+}
+
+int bf_runtime_destroy(bf_runtime* rt) {
+  if (!rt) return BF_OK;
+  bf_shutdown(rt);
+  set_device(rt->device);
+  for (auto s : rt->streams) cudaStreamDestroy(s);
+  for (auto e : rt->event_pool) cudaEventDestroy(e);
+  for (auto& kv : rt->tasks)
+    if (kv.second.executed_dev) cudaFree(kv.second.executed_dev);
+  if (rt->fault_dev) cudaFree(rt->fault_dev);
+  if (rt->gate_host) cudaFreeHost((void*)rt->gate_host);
+  rt->arena->live_runtimes--;
+  if (rt->arena->live_runtimes == 0) release_zombies(rt->arena);
+  delete rt;
+  return BF_OK;
+}
+
+int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const int32_t block[3],
+              int64_t shmem_bytes, const bf_slot* slots, int32_t nslots, int32_t warp_size,
+              int64_t grain, uint64_t* task_id) {
+  if (!rt || !kernel || !grid || !block) return fail(BF_E_INVALID, "null argument");
+  if (rt->shut_down) return fail(BF_E_SHUTDOWN, "launch after shutdown");
+  for (int i = 0; i < 3; i++)
+    if (grid[i] < 1 || block[i] < 1) return fail(BF_E_INVALID, "dim3 components must be >= 1");
+  int64_t total = (int64_t)grid[0] * grid[1] * grid[2];
+  int64_t bsize = (int64_t)block[0] * block[1] * block[2];
+  if (total > 2147483647LL || bsize > 2147483647LL)
+    return fail(BF_E_INVALID, "dim3 product overflows i32");
+  if (grain < 1) return fail(BF_E_INVALID, "grain must be >= 1");
+  if (grain > total) grain = total;
+  const KernelEntry* ke = find_kernel(kernel);
+  if (!ke)
+    return fail(BF_E_UNKNOWN_KERNEL,
+                std::string("no sm_100a kernel registered for '") + kernel + "'");
+  int rc = set_device(rt->device);
+  if (rc) return rc;
+
+  uint64_t id = rt->next_task++;
+  TaskRec& tr = rt->tasks[id];
+  tr.kernel = kernel;
+  tr.total = total;
+  tr.grain = grain;
+  if (task_id) *task_id = id;
+
+  // unpack_args (executor.py:48-75): positional kind check; in the reference
+  // a mismatch traps inside the worker and surfaces at sync as RuntimeFault.
+  std::vector<ArgVal> args(ke->params.size());
+  HostTrap pre;
+  if ((size_t)nslots != ke->params.size()) {
+    pre.kind = BF_TRAP_TYPE_FAULT;
+    pre.message = "expected " + std::to_string(ke->params.size()) + " arguments, got " +
+                  std::to_string(nslots);
+  } else {
+    for (size_t i = 0; i < ke->params.size() && pre.kind == BF_TRAP_NONE; i++) {
+      const ParamSpec& p = ke->params[i];
+      const bf_slot& s = slots[i];
+      ArgVal& v = args[i];
+      v.kind = s.kind;
+      if (p.kind == BF_SLOT_HANDLE) {
+        if (s.kind != BF_SLOT_HANDLE) {
+          pre.kind = BF_TRAP_TYPE_FAULT;
+          pre.message = std::string("param '") + p.name + "' needs a buffer handle";
+          break;
+        }
+        Buffer* b = lookup(rt->arena, s.v.handle);
+        if (!b) {
+          pre.kind = BF_TRAP_OUT_OF_BOUNDS;
+          pre.message = "dangling buffer handle " + std::to_string(s.v.handle);
+          break;
+        }
+        if (b->scalar != p.scalar) {
+          pre.kind = BF_TRAP_TYPE_FAULT;
+          pre.message = std::string("param '") + p.name + "' wants a buffer of a different scalar type";
+          break;
+        }
+        v.scalar = b->scalar;
+        v.ptr = b->ptr;
+        v.len = b->length;
+        v.handle = s.v.handle;
+      } else {
+        if (s.kind != p.kind) {
+          pre.kind = BF_TRAP_TYPE_FAULT;
+          pre.message = std::string("param '") + p.name + "' has the wrong scalar kind";
+          break;
+        }
+        v.i32 = s.v.i32;
+        v.i64 = s.v.i64;
+        v.f64 = s.v.f64;
+      }
+    }
+  }
+
+  if ((rt->flags & BF_FLAG_INSTRUMENT) && total > 0) {
+    CK(cudaMallocAsync((void**)&tr.executed_dev, total * sizeof(int), rt->streams[0]));
+    CK(cudaMemsetAsync(tr.executed_dev, 0, total * sizeof(int), rt->streams[0]));
+    CK(cudaStreamSynchronize(rt->streams[0]));
+  }
+
+  // push + dispatch: the host dispatcher plays the pool's fetch loop
+  rc = bf_queue_push(&rt->queue, id, total, grain);
+  if (rc) return rc;
+  for (;;) {
+    int32_t got = 0;
+    uint64_t tag;
+    int64_t first, count;
+    bf_queue_fetch(&rt->queue, &got, &tag, &first, &count);
+    if (!got) break;
+    tr.fetches += 1;
+    tr.cursor = first + count;
+    int w = (int)(rt->rr++ % (uint64_t)rt->pool);
+    cudaStream_t s = rt->streams[w];
+    if (rt->holding && !rt->gated[w]) {
+      gate_kernel<<<1, 1, 0, s>>>((volatile int*)rt->gate_dev, rt->fault_dev);
+      rt->gated[w] = true;
+    }
+    if (rt->block_delay > 0.0) {
+      std::uniform_real_distribution<double> u(0.0, rt->block_delay);
+      delay_kernel<<<1, 1, 0, s>>>((unsigned long long)(u(rt->rng) * 1e9));
+    }
+    if (pre.kind != BF_TRAP_NONE) {
+      // reference: the trap aborts the worker's range (runtime.py:335-343)
+      if (rt->trap.kind == BF_TRAP_NONE) {
+        rt->trap = pre;
+        rt->trap.block = first;
+        rt->trap_task = id;
+        rt->trap_kernel = kernel;
+      }
+    } else {
+      LaunchCtx ctx;
+      ctx.name = kernel;
+      for (int i = 0; i < 3; i++) {
+        ctx.grid[i] = grid[i];
+        ctx.block[i] = block[i];
+      }
+      ctx.first = first;
+      ctx.count = count;
+      ctx.shmem = shmem_bytes;
+      ctx.warp_size = warp_size;
+      ctx.args = args.data();
+      ctx.nargs = (int)args.size();
+      ctx.stream = s;
+      ctx.num_sms = rt->num_sms;
+      ctx.executed = tr.executed_dev;
+      ctx.fault = rt->fault_dev;
+      ctx.task = id;
+      HostTrap ht;
+      std::string err;
+      ctx.trap = &ht;
+      ctx.error = &err;
+      int lrc = ke->launch(ctx);
+      if (lrc != BF_OK) return fail(lrc, std::string(kernel) + ": " + err);
+      if (tr.executed_dev) {
+        int g = (int)std::min<long long>((count + 255) / 256, 1184);
+        mark_kernel<<<g, 256, 0, s>>>(tr.executed_dev, first, count);
+      }
+      if (ht.kind != BF_TRAP_NONE && rt->trap.kind == BF_TRAP_NONE) {
+        rt->trap = ht;
+        rt->trap_task = id;
+        rt->trap_kernel = kernel;
+      }
+    }
+    FetchRecord fr;
+    fr.task = id;
+    fr.worker = w;
+    fr.first = first;
+    fr.count = count;
+    fr.done = get_event(rt);
+    CK(cudaEventRecord(fr.done, s));
+    rt->inflight.push_back(fr);
+  }
+  return BF_OK;
+}
+
+int bf_synchronize(bf_runtime* rt, bf_fault* fault) {
+  if (!rt) return fail(BF_E_INVALID, "null runtime");
+  int rc = set_device(rt->device);
+  if (rc) return rc;
+  rc = sync_workers(rt);
+  if (rc) return rc;
+  rt->syncs += 1;
+  absorb_device_fault(rt);
+  if (rt->arena->live_runtimes <= 1) release_zombies(rt->arena);
+  if (rt->flags & BF_FLAG_HOLD_BLOCKS) {
+    // the reference re-arms only on hold_new_blocks(); nothing to do here
+  }
+  if (rt->trap.kind != BF_TRAP_NONE) {
+    fill_fault(rt, fault);
+    return fail(BF_E_FAULT, "block " + std::to_string(rt->trap.block) + ": [" +
+                                std::to_string(rt->trap.kind) + "] " + rt->trap.message);
+  }
+  if (fault) std::memset(fault, 0, sizeof(*fault));
+  return BF_OK;
+}
+
+int bf_hold_new_blocks(bf_runtime* rt) {
+  if (!rt) return fail(BF_E_INVALID, "null runtime");
+  *rt->gate_host = 0;
+  rt->holding = true;
+  std::fill(rt->gated.begin(), rt->gated.end(), false);
+  return BF_OK;
+}
+
+int bf_task_get(bf_runtime* rt, uint64_t task_id, bf_task_info* out) {
+  if (!rt || !out) return fail(BF_E_INVALID, "null argument");
+  auto it = rt->tasks.find(task_id);
+  if (it == rt->tasks.end()) return fail(BF_E_INVALID, "unknown task");
+  retire(rt, false);
+  const TaskRec& t = it->second;
+  out->total_blocks = t.total;
+  out->block_per_fetch = t.grain;
+  out->curr_block_id = t.cursor;
+  out->fetches = t.fetches;
+  out->remaining = t.total - t.completed;
+  return BF_OK;
+}
+
+int bf_task_executed(bf_runtime* rt, uint64_t task_id, int32_t* executed, int64_t n) {
+  if (!rt || !executed) return fail(BF_E_INVALID, "null argument");
+  auto it = rt->tasks.find(task_id);
+  if (it == rt->tasks.end()) return fail(BF_E_INVALID, "unknown task");
+  TaskRec& t = it->second;
+  if (n != t.total) return fail(BF_E_INVALID, "executed[] length mismatch");
+  set_device(rt->device);
+  if (t.executed_dev) {
+    // device-observed counts are only meaningful once the fetches drained;
+    // the copy is ordered after every worker's work
+    for (auto s : rt->streams) {
+      if (*rt->gate_host == 0) break;  // held: nothing has run yet
+      CK(cudaStreamSynchronize(s));
+    }
+    if (*rt->gate_host == 0) {
+      std::memset(executed, 0, n * sizeof(int32_t));
+      return BF_OK;
+    }
+    CK(cudaMemcpy(executed, t.executed_dev, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    return BF_OK;
+  }
+  retire(rt, false);
+  std::memset(executed, 0, n * sizeof(int32_t));
+  for (auto& r : t.done_ranges)
+    for (long long b = r.first; b < r.first + r.second; b++) executed[b] += 1;
+  return BF_OK;
+}
+
+int bf_counters_get(bf_runtime* rt, bf_counters* out, int64_t* busy, int32_t n) {
+  if (!rt || !out) return fail(BF_E_INVALID, "null argument");
+  retire(rt, false);
+  int64_t fc = 0, qw = 0;
+  bf_queue_counters(&rt->queue, &fc, &qw);
+  out->fetch_count = fc;
+  out->queue_waits = qw;
+  out->blocks_executed = rt->blocks_executed;
+  out->syncs = rt->syncs;
+  out->pool_size = rt->pool;
+  if (busy)
+    for (int i = 0; i < n && i < rt->pool; i++) busy[i] = rt->busy[i];
+  return BF_OK;
+}
+
+int bf_worker_stream(bf_runtime* rt, int32_t worker, void** stream) {
+  if (!rt || !stream) return fail(BF_E_INVALID, "null argument");
+  if (worker < 0 || worker >= rt->pool) return fail(BF_E_INVALID, "worker out of range");
+  *stream = (void*)rt->streams[worker];
+  return BF_OK;
+}
+
+// ---- registry --------------------------------------------------------------
+
+int bf_kernel_count(int32_t* count) {
+  if (!count) return fail(BF_E_INVALID, "null out");
+  *count = (int32_t)registry().size();
+  return BF_OK;
+}
+
+int bf_kernel_info(int32_t index, char* name, int32_t name_cap, int32_t* nparams, int32_t* kinds,
+                   int32_t* scalars, int32_t cap) {
+  if (index < 0 || index >= (int32_t)registry().size()) return fail(BF_E_INVALID, "bad index");
+  const KernelEntry& k = registry()[index];
+  if (name && name_cap > 0) std::snprintf(name, name_cap, "%s", k.name);
+  if (nparams) *nparams = (int32_t)k.params.size();
+  for (int i = 0; i < (int)k.params.size() && i < cap; i++) {
+    if (kinds) kinds[i] = k.params[i].kind;
+    if (scalars) scalars[i] = k.params[i].scalar;
+  }
+  return BF_OK;
+}
+
+}  // extern "C"
