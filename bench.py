@@ -1,0 +1,355 @@
+"""bench.py — B200 throughput of the launch runtime's hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload hotspot] [--size 8192] [--iters 100]
+
+Default workload (BASELINE.json configs[1]): hotspot 2D thermal stencil,
+8192 x 8192 f32 cells, 100 iterations per step, each iteration one launch of
+the `hotspot` kernel through the reference-shaped API (Runtime.launch ->
+C ABI -> sm_100a kernel).  Metric: algorithmic HBM GB/s at 12 B per cell and
+iteration (read src + power, write dst), plus elements/s.
+
+value  = algorithmic bytes of the K timed steps / device time (CUDA events on
+         the worker stream, inputs resident in HBM, max over ranks)
+e2e    = the same metric through the public API with host buffers: pinned
+         host -> device upload of temp + power, 100 launches, download of the
+         final grid, every step
+roofline / cpu_baseline / clocks: see DESIGN.md.
+
+`--impl reference` times the CPU reference path (the oracle restatement in
+oracle/oracle.c, all host threads) on a bounded sample of the same workload.
+Multi-GPU: launched by torchrun, one process per GPU; rows are partitioned in
+contiguous bands (the average grain law over ranks) with ghost-zone halos
+exchanged over NCCL every `--halo` iterations (paper_2206_07896_b200.parallel).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_CELL_ITER = 12  # read src f32 + power f32, write dst f32
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+def dist_env() -> tuple[int, int, int]:
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# hotspot workload
+# ---------------------------------------------------------------------------
+
+def cpu_baseline_hotspot(size: int, iters_full: int, budget_s: float, threads: int) -> dict:
+    """The oracle port (oracle/oracle.c, OpenMP over blocks) on a bounded
+    sample: the full 8192^2 grid for as many iterations as fit the budget."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import instances as I
+    import oracle
+    temp, power = I.hotspot_inputs(size, size, 0)
+    params = I.hotspot_params(size, size)
+    t0 = time.perf_counter()
+    oracle.hotspot_iterate(temp, power, size, size, params, 1, nthreads=threads)
+    one = time.perf_counter() - t0
+    iters = max(1, min(iters_full, int(budget_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.hotspot_iterate(temp, power, size, size, params, iters, nthreads=threads)
+    dt = time.perf_counter() - t0
+    gbs = BYTES_PER_CELL_ITER * size * size * iters / dt / 1e9
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"hotspot {size}x{size}, {iters} iteration(s) of {iters_full}, "
+                      f"{dt:.2f} s, oracle/oracle.c OpenMP",
+            "elem_per_s": size * size * iters / dt}
+
+
+def run_reference_arm(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    steps_t = []
+    base = None
+    for _ in range(args.warmup):
+        cpu_baseline_hotspot(args.size, args.iters, args.cpu_budget / 4, threads)
+    for _ in range(args.steps):
+        base = cpu_baseline_hotspot(args.size, args.iters, args.cpu_budget, threads)
+        steps_t.append(base["value"])
+    value = statistics.median(steps_t)
+    cells_iter = args.size * args.size * args.iters
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": BYTES_PER_CELL_ITER * cells_iter / (value * 1e9) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"hotspot {args.size}x{args.size} f32, {args.iters} iterations",
+                   "bytes_per_cell_iter": BYTES_PER_CELL_ITER},
+        "cpu_baseline": base,
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "per-kernel GB/s & elem/s vs HBM roofline at 1/2/4/8 B200; speedup vs CPU runtime"
+
+
+def run_ours(args) -> None:
+    import torch
+
+    from paper_2206_07896_b200 import ArgSlot, DeviceArena, Dim3, PackedArgs, Runtime, routines
+    from paper_2206_07896_b200.parallel import HotspotBands
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import instances as I
+
+    size, iters = args.size, args.iters
+    params = I.hotspot_params(size, size)
+    temp, power = I.hotspot_inputs(size, size, 0)
+    bands = HotspotBands(size, size, world, rank, halo=args.halo if world > 1 else 0)
+    r0, r1 = bands.local_rows  # global rows held locally (incl. ghost rows)
+    lrows = r1 - r0
+    arena = DeviceArena(local)
+    cells = lrows * size
+    h_src, h_pow, h_dst = (arena.alloc("f32", cells) for _ in range(3))
+    arena.upload_numpy(h_src, temp[r0 * size:r1 * size])
+    arena.upload_numpy(h_pow, power[r0 * size:r1 * size])
+    routine = routines.get("hotspot")
+    bx, by = 16, 16
+    grid = Dim3(-(-size // bx), -(-lrows // by))
+    block = Dim3(bx, by)
+
+    def slots(src, dst):
+        return PackedArgs([ArgSlot("handle", src), ArgSlot("handle", h_pow), ArgSlot("handle", dst),
+                           ArgSlot("i32", lrows), ArgSlot("i32", size), ArgSlot("f32", params["sdc"]),
+                           ArgSlot("f32", params["rx1"]), ArgSlot("f32", params["ry1"]),
+                           ArgSlot("f32", params["rz1"]), ArgSlot("f32", params["amb"])])
+
+    packs = [slots(h_src, h_dst), slots(h_dst, h_src)]
+    rt = Runtime(arena, pool_size=1)
+    stream = torch.cuda.ExternalStream(rt.worker_stream(0), device=torch.device("cuda", local))
+    exch = bands.exchanger(arena, stream) if world > 1 else None
+
+    def step(events=None) -> int:
+        """One full run: `iters` ping-pong launches (+ halo exchanges)."""
+        cur = 0
+        for it in range(iters):
+            if events is not None:
+                events[it][0].record(stream)
+            rt.launch(routine, grid, block, 0, packs[cur])
+            if events is not None:
+                events[it][1].record(stream)
+            cur ^= 1
+            if exch is not None and (it + 1) % bands.halo == 0 and it + 1 < iters:
+                exch.exchange(h_dst if cur == 1 else h_src)
+        return cur
+
+    # warm-up
+    for _ in range(args.warmup):
+        step()
+    rt.device_synchronize()
+    barrier(world)
+
+    # timed region: K steps, inputs resident (3 x 256 MiB > 126 MB L2)
+    per_launch = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(iters)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for k in range(args.steps):
+            step(per_launch[k])
+        stop.record(stream)
+        rt.device_synchronize()
+        torch.cuda.synchronize()
+    barrier(world)
+    dev_ms = max_over_ranks(start.elapsed_time(stop), world)
+    launch_ms = [a.elapsed_time(b) for ev in per_launch for a, b in ev]
+    avg_launch_ms = statistics.mean(launch_ms)
+
+    total_cells = size * size * iters * args.steps  # whole job (strong scaling)
+    value = BYTES_PER_CELL_ITER * total_cells / (dev_ms * 1e-3) / 1e9
+    peaks = _peaks()
+    local_bytes = BYTES_PER_CELL_ITER * lrows * size  # per launch, this rank
+    achieved = local_bytes / (avg_launch_ms * 1e-3) / 1e9
+
+    # end-to-end through the public API with host buffers (pinned)
+    h_temp = torch.from_numpy(temp[r0 * size:r1 * size].copy()).pin_memory().numpy()
+    h_power = torch.from_numpy(power[r0 * size:r1 * size].copy()).pin_memory().numpy()
+    h_out = torch.empty(cells, dtype=torch.float32).pin_memory().numpy()
+    e2e_times = []
+    for k in range(args.warmup + args.steps):
+        barrier(world)
+        t0 = time.perf_counter()
+        arena.upload_numpy(h_src, h_temp)
+        arena.upload_numpy(h_pow, h_power)
+        cur = step()
+        rt.device_synchronize()
+        arena.download_into(h_src if cur == 0 else h_dst, h_out)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            e2e_times.append(max_over_ranks(dt, world))
+    e2e_s = statistics.median(e2e_times)
+    e2e_value = BYTES_PER_CELL_ITER * size * size * iters / e2e_s / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_hotspot(size, iters, args.cpu_budget, len(os.sched_getaffinity(0)))
+
+    traffic = None
+    prof = ROOT / "profiles" / "hotspot_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"hotspot {size}x{size} f32, {iters} iterations per step",
+                       "grid_launch": f"{grid.x}x{grid.y} blocks of {bx}x{by}",
+                       "bytes_per_cell_iter": BYTES_PER_CELL_ITER,
+                       "l2": "inputs larger than L2 (3 x 256 MiB vs 126 MB)",
+                       "parallelism": f"row bands x{world}" + (f", ghost halo {bands.halo}" if world > 1 else ""),
+                       "elem_per_s": total_cells / (dev_ms * 1e-3)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                         "traffic": traffic, "peak_source": peaks["source"],
+                         "kernel": "hotspot_strip", "avg_launch_us": round(avg_launch_ms * 1e3, 3)},
+            "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": 2 * cells * 4 * world, "d2h_bytes_per_step": cells * 4 * world,
+                    "ms_per_step": round(e2e_s * 1e3, 3)},
+            "gpu_launches": iters * args.steps,
+            "clocks": clocks.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    rt.shutdown()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["hotspot"], default="hotspot")
+    ap.add_argument("--size", type=int, default=8192)
+    ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--halo", type=int, default=8)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

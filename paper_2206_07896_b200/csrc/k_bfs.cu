@@ -1,0 +1,105 @@
+// bfs — paper_2206_07896_b200/kernels/bfs.kn: one level-synchronous step of a
+// top-down BFS over a CSR graph (Rodinia bfs, one launch per level).
+//
+// For u < nv with lvl[u] == cur: every out-neighbour v with lvl[v] == -1 gets
+// lvl[v] = cur + 1 and changed[0] = 1.  All writers of lvl[v] write the same
+// value and a vertex discovered in this launch has cur+1 != cur, so the
+// result is independent of the order the device visits vertices in — it is
+// exactly the reference's sequential result (executor.py:422-489).
+//
+// B200 mapping: one thread per vertex scan (coalesced lvl reads), the CSR row
+// pair read once, neighbour levels read through L2.  This is the per-launch
+// semantics the reference API exposes; the whole-traversal driver with a
+// frontier queue is bfs_levels (k_bfs_driver).
+#include <climits>
+
+#include "bf_internal.h"
+#include "common.cuh"
+
+namespace bf {
+
+__device__ __forceinline__ long long bfs_block_of_x(const KDesc& d, long long x) {
+  long long x0 = d.first % d.gx;
+  return d.first + ((x - x0) % d.gx + d.gx) % d.gx;
+}
+
+__global__ void __launch_bounds__(256) bfs_step(const int* __restrict__ row, long long lr,
+                                                const int* __restrict__ col, long long lcol,
+                                                int* lvl, long long ll, int* changed,
+                                                long long lch, long long lo, long long hi, int cur,
+                                                int bx, KDesc k) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool any = false;
+  for (long long u = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; u < hi; u += stride) {
+    if (u >= ll) {
+      record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
+      continue;
+    }
+    if (lvl[u] != cur) continue;
+    if (u + 1 >= lr) {
+      record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
+      continue;
+    }
+    const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
+    for (int e = e0; e < e1; e++) {
+      if (e < 0 || e >= lcol) {
+        record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
+        break;
+      }
+      const int v = __ldg(col + e);
+      if (v < 0 || v >= ll) {
+        record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
+        break;
+      }
+      if (lvl[v] == -1) {
+        lvl[v] = (int)((unsigned)cur + 1u);
+        any = true;
+      }
+    }
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) {
+    if (lch < 1) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, k.first);
+    else changed[0] = 1;
+  }
+}
+
+static int launch_bfs(LaunchCtx& ctx) {
+  const ArgVal& R = ctx.args[0];
+  const ArgVal& Co = ctx.args[1];
+  const ArgVal& L = ctx.args[2];
+  const ArgVal& Ch = ctx.args[3];
+  const long long nv = ctx.args[4].i32;
+  const int cur = ctx.args[5].i32;
+  const long long bx = ctx.block[0];
+  if ((long long)ctx.grid[1] * ctx.grid[2] * ctx.block[1] * ctx.block[2] != 1) {
+    // duplicated vertex threads are harmless here (idempotent), but keep the
+    // geometry contract uniform with the other graph kernels
+    *ctx.error = "bfs: only 1D grids/blocks are supported";
+    return BF_E_UNSUPPORTED;
+  }
+  if ((long long)ctx.grid[0] * bx - 1 > INT_MAX) {
+    *ctx.error = "bfs: vertex id beyond i32";
+    return BF_E_UNSUPPORTED;
+  }
+  for (auto& xi : ctx.x_intervals()) {
+    long long lo = xi.first * bx, hi = std::min(xi.second * bx, nv);
+    if (lo >= hi) continue;
+    int grid = stream_grid(hi - lo, 256 * 4, ctx.num_sms, 8);
+    bfs_step<<<grid, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len,
+                                           (int*)L.ptr, L.len, (int*)Ch.ptr, Ch.len, lo, hi, cur,
+                                           (int)bx, ctx.desc());
+    BF_CUDA_LAUNCH_CHECK(ctx);
+  }
+  return BF_OK;
+}
+
+static Registrar reg_bfs("bfs",
+                         {{BF_SLOT_HANDLE, BF_I32, "row"},
+                          {BF_SLOT_HANDLE, BF_I32, "col"},
+                          {BF_SLOT_HANDLE, BF_I32, "lvl"},
+                          {BF_SLOT_HANDLE, BF_I32, "changed"},
+                          {BF_SLOT_I32, BF_I32, "nv"},
+                          {BF_SLOT_I32, BF_I32, "cur"}},
+                         launch_bfs);
+
+}  // namespace bf

@@ -1,0 +1,528 @@
+// The reference corpus kernels other than vecadd (blockfuse/corpus/*.kn):
+// reverse, reduce, hist, hist_stride, fir, wreduce.
+//
+// Each kernel reproduces the reference interpreter's result for the launch
+// geometry exactly (executor.py:422-489 lockstep order where the result
+// depends on it; integer sums wrap mod 2^32, which makes every integer
+// reduction order-free).  Physical CTAs are sized for the B200, not copied
+// from the logical geometry: single-block grid-stride kernels (fir,
+// hist_stride) are spread over the whole GPU, histograms are privatised per
+// lane in shared memory, reductions use warp shuffles.
+#include <climits>
+
+#include "bf_internal.h"
+#include "common.cuh"
+
+namespace bf {
+
+// lowest linear block id of the fetch range whose blockIdx.x is x
+__device__ __forceinline__ long long block_of_x(const KDesc& d, long long x) {
+  long long x0 = d.first % d.gx;
+  return d.first + ((x - x0) % d.gx + d.gx) % d.gx;
+}
+
+// Split the fetch range into x-intervals with a uniform copy count: each
+// logical block (x, y, z) of the range runs the same body, so an x that
+// appears in c rows of the range is executed c times (what matters for
+// atomics).  At most three pieces: head row, full rows, tail row.
+struct XPiece {
+  long long x0, x1, copies;
+};
+
+static std::vector<XPiece> x_pieces(const LaunchCtx& ctx) {
+  std::vector<XPiece> out;
+  long long gx = ctx.grid[0];
+  long long b = ctx.first, e = ctx.first + ctx.count;
+  long long hx = b % gx;
+  if (hx != 0) {
+    long long stop = std::min(e, b - hx + gx);
+    out.push_back({hx, hx + (stop - b), 1});
+    b = stop;
+  }
+  long long full = (e - b) / gx;
+  if (full > 0) {
+    out.push_back({0, gx, full});
+    b += full * gx;
+  }
+  if (b < e) out.push_back({0, e - b, 1});
+  return out;
+}
+
+// ===========================================================================
+// reverse (corpus/reverse.kn): s[t] = d[t]; barrier; d[t] = s[n - t - 1]
+// One CTA walks the fetch's logical blocks in order, so consecutive blocks
+// see each other's writes exactly as in the sequential reference.
+// ===========================================================================
+__global__ void __launch_bounds__(1024) reverse_seq(int* d, long long ld, int n, long long ls,
+                                                    KDesc k) {
+  extern __shared__ int s[];
+  __shared__ int trap;
+  const long long B = (long long)k.bx * k.by * k.bz;
+  if (threadIdx.x == 0) trap = 0;
+  for (long long blk = k.first; blk < k.first + k.count; blk++) {
+    for (long long i = threadIdx.x; i < ls; i += blockDim.x) s[i] = 0;
+    __syncthreads();
+    for (long long t = threadIdx.x; t < B; t += blockDim.x) {
+      int tx = (int)(t % k.bx);
+      if (tx >= ld || tx >= ls) {
+        atomicExch(&trap, 1);
+      } else {
+        s[tx] = d[tx];
+      }
+    }
+    __syncthreads();
+    if (trap) {
+      if (threadIdx.x == 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, blk);
+      return;
+    }
+    for (long long t = threadIdx.x; t < B; t += blockDim.x) {
+      int tx = (int)(t % k.bx);
+      int tr = (int)((unsigned)n - (unsigned)tx - 1u);
+      if (tr < 0 || tr >= ls || tx >= ld) {
+        atomicExch(&trap, 1);
+      } else {
+        d[tx] = s[tr];
+      }
+    }
+    __syncthreads();
+    if (trap) {
+      if (threadIdx.x == 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, blk);
+      return;
+    }
+  }
+}
+
+static int launch_reverse(LaunchCtx& ctx) {
+  const ArgVal& D = ctx.args[0];
+  const int n = ctx.args[1].i32;
+  long long ls = ctx.shmem / 4;
+  if (ls * 4 > 200 * 1024) {
+    *ctx.error = "reverse: dynamic shared memory above 200 KiB";
+    return BF_E_UNSUPPORTED;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(reverse_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaGetLastError();
+    attr = true;
+  }
+  long long B = (long long)ctx.block[0] * ctx.block[1] * ctx.block[2];
+  int threads = (int)std::min<long long>(1024, ((B + 31) / 32) * 32);
+  size_t smem = (size_t)std::max<long long>(ls, 1) * 4;
+  reverse_seq<<<1, threads, smem, ctx.stream>>>((int*)D.ptr, D.len, n, ls, ctx.desc());
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  return BF_OK;
+}
+
+// ===========================================================================
+// reduce (corpus/reduce.kn): per-block tree sum in shared i32 buf[256].
+// With an m-fold block (blockDim.y*z = m) every tree phase runs m times in
+// thread order; a phase only reads slots it does not write, so each pass is
+// buf[t] += buf[t+s] and m passes give buf[t] += m*buf[t+s] (mod 2^32).
+// m == 1: the sum of the block's slice, computed with warp shuffles.
+// ===========================================================================
+__device__ __forceinline__ int warp_sum(int v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// one warp per logical block x; loads coalesced; m == 1
+__global__ void __launch_bounds__(256) reduce_warp(const int* __restrict__ x, long long lx,
+                                                   int* __restrict__ out, long long lout, int n,
+                                                   long long x0, long long x1, KDesc k) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  for (long long bx = x0 + (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; bx < x1;
+       bx += warps) {
+    long long lo = bx * k.bx;
+    long long hi = lo + k.bx;
+    if (hi > n) hi = n;
+    if (hi > lx || bx >= lout) {
+      if (lane == 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, block_of_x(k, bx));
+      continue;
+    }
+    unsigned s = 0;
+    for (long long i = lo + lane; i < hi; i += 32) s += (unsigned)__ldg(x + i);
+    int v = warp_sum((int)s);
+    if (lane == 0) out[bx] = v;
+  }
+}
+
+// exact tree emulation for m-fold blocks: one CTA of blockDim.x threads
+__global__ void __launch_bounds__(256) reduce_tree(const int* x, long long lx, int* out,
+                                                   long long lout, int n, long long x0,
+                                                   long long x1, int m, KDesc k) {
+  __shared__ int buf[256];
+  const int t = threadIdx.x;  // blockDim.x == k.bx <= 256
+  for (long long bx = x0 + blockIdx.x; bx < x1; bx += gridDim.x) {
+    long long id = bx * k.bx + t;
+    int v = 0;
+    bool oob = false;
+    if (id < n && (int)id == id) {
+      if (id >= lx) oob = true; else v = x[id];
+    }
+    buf[t] = v;
+    if (__syncthreads_or(oob) || bx >= lout) {
+      if (t == 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, block_of_x(k, bx));
+      __syncthreads();
+      continue;
+    }
+    for (int s = 1; s < k.bx; s += s) {
+      int add = 0;
+      if (t % (2 * s) == 0 && t + s < k.bx) add = buf[t + s];
+      __syncthreads();
+      if (add) buf[t] = (int)((unsigned)buf[t] + (unsigned)m * (unsigned)add);
+      __syncthreads();
+    }
+    if (t == 0) out[bx] = buf[0];
+    __syncthreads();
+  }
+}
+
+static int launch_reduce(LaunchCtx& ctx) {
+  const ArgVal& X = ctx.args[0];
+  const ArgVal& O = ctx.args[1];
+  const int n = ctx.args[2].i32;
+  const int bx = ctx.block[0];
+  const long long m = (long long)ctx.block[1] * ctx.block[2];
+  if (bx > 256) {  // buf[t] = 0 for t = 256 traps in the first block
+    ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first, "shared store index 256 out of range [0, 256)");
+    return BF_OK;
+  }
+  if ((long long)ctx.grid[0] * bx - 1 > INT_MAX) {
+    *ctx.error = "reduce: blockIdx.x*blockDim.x beyond i32";
+    return BF_E_UNSUPPORTED;
+  }
+  for (auto& xi : ctx.x_intervals()) {
+    long long nx = xi.second - xi.first;
+    if (m == 1) {
+      int grid = stream_grid(nx, 8, ctx.num_sms, 8);
+      reduce_warp<<<grid, 256, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr, O.len, n,
+                                                xi.first, xi.second, ctx.desc());
+    } else {
+      int grid = (int)std::min<long long>(nx, (long long)ctx.num_sms * 8);
+      reduce_tree<<<grid, bx, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr, O.len, n,
+                                               xi.first, xi.second, (int)m, ctx.desc());
+    }
+    BF_CUDA_LAUNCH_CHECK(ctx);
+  }
+  return BF_OK;
+}
+
+// ===========================================================================
+// hist / hist_stride: counts[pix[i] % nbins] += copies for i in [lo, hi).
+// Per-lane privatised counters for nbins <= 32 (bin-major, lane-minor: no
+// bank conflicts, no shared atomics), CTA-shared atomics for nbins <= 8192,
+// global atomics beyond.  One global atomic per bin per CTA at the end.
+// ===========================================================================
+constexpr int kHistLaneBins = 32;
+constexpr int kHistSmemBins = 8192;
+
+__device__ __forceinline__ int c_mod(int a, int b) {
+  return b == -1 ? 0 : a % b;  // C remainder, truncating toward zero
+}
+
+template <int MODE>  // 0: per-lane counters, 1: CTA shared atomics, 2: global atomics
+__global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, int* counts,
+                                                  long long lc, long long lo, long long hi,
+                                                  int nbins, unsigned copies, KDesc k,
+                                                  long long xbase, int bx_div) {
+  extern __shared__ unsigned sh[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = nbins < 0 ? -nbins : nbins;  // |nbins| bounds the remainder
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < 8 * kHistLaneBins * 32; i += blockDim.x) sh[i] = 0;
+  } else if (MODE == 1) {
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+  }
+  __syncthreads();
+  unsigned* mine = sh + warp * (kHistLaneBins * 32) + lane;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
+    int b = c_mod(__ldcs(pix + i), nbins);
+    if (b < 0 || b >= lc) {
+      long long blk = bx_div > 0 ? block_of_x(k, xbase + (i - lo) / bx_div) : k.first;
+      record_fault(k, BF_TRAP_OUT_OF_BOUNDS, blk);
+      continue;
+    }
+    if (MODE == 0) {
+      mine[b * 32] += copies;
+    } else if (MODE == 1) {
+      atomicAdd(sh + b, copies);
+    } else {
+      atomicAdd((unsigned*)counts + b, copies);
+    }
+  }
+  if (MODE == 2) return;
+  __syncthreads();
+  if (MODE == 0) {
+    // bins x 256 lanes -> one total per bin
+    for (int b = warp; b < nb && b < kHistLaneBins; b += blockDim.x / 32) {
+      unsigned s = 0;
+      for (int w = 0; w < (int)(blockDim.x / 32); w++) s += sh[w * (kHistLaneBins * 32) + b * 32 + lane];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0 && s && b < lc) atomicAdd((unsigned*)counts + b, s);
+    }
+  } else {
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      if (sh[b] && b < lc) atomicAdd((unsigned*)counts + b, sh[b]);
+  }
+}
+
+static int hist_issue(LaunchCtx& ctx, const ArgVal& P, const ArgVal& Cn, long long lo, long long hi,
+                      int nbins, unsigned copies, long long xbase, int bx_div) {
+  if (lo >= hi) return BF_OK;
+  int nb = nbins < 0 ? -nbins : nbins;
+  int grid = stream_grid(hi - lo, 256 * 16, ctx.num_sms, 4);
+  KDesc d = ctx.desc();
+  if (nb <= kHistLaneBins) {
+    size_t smem = 8 * kHistLaneBins * 32 * sizeof(unsigned);  // 8 warps x 32 bins x 32 lanes
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(hist_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    hist_range<0><<<grid, 256, smem, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi,
+                                                  nbins, copies, d, xbase, bx_div);
+  } else if (nb <= kHistSmemBins) {
+    hist_range<1><<<grid, 256, nb * sizeof(unsigned), ctx.stream>>>(
+        (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, nbins, copies, d, xbase, bx_div);
+  } else {
+    hist_range<2><<<grid, 256, 0, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi,
+                                                nbins, copies, d, xbase, bx_div);
+  }
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  return BF_OK;
+}
+
+static int launch_hist(LaunchCtx& ctx) {
+  const ArgVal& P = ctx.args[0];
+  const ArgVal& Cn = ctx.args[1];
+  const long long n = ctx.args[2].i32;
+  const int nbins = ctx.args[3].i32;
+  const long long bx = ctx.block[0];
+  const long long m = (long long)ctx.block[1] * ctx.block[2];
+  if (ctx.grid[0] * bx - 1 > INT_MAX) {
+    *ctx.error = "hist: blockIdx.x*blockDim.x beyond i32";
+    return BF_E_UNSUPPORTED;
+  }
+  for (auto& pc : x_pieces(ctx)) {
+    long long lo = pc.x0 * bx, hi = std::min(pc.x1 * bx, n);
+    if (lo >= hi) continue;
+    if (nbins == 0) {
+      ctx.host_trap(BF_TRAP_DIV_BY_ZERO, ctx.first_block_with_x(pc.x0), "integer modulo by zero");
+      continue;
+    }
+    if (hi > P.len) {
+      long long bad = std::max<long long>(lo, P.len);
+      ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first_block_with_x(bad / bx),
+                    "load index " + std::to_string(bad) + " out of range");
+      hi = P.len;
+    }
+    int rc = hist_issue(ctx, P, Cn, lo, hi, nbins, (unsigned)(pc.copies * m), pc.x0, (int)bx);
+    if (rc) return rc;
+  }
+  return BF_OK;
+}
+
+static int launch_hist_stride(LaunchCtx& ctx) {
+  const ArgVal& P = ctx.args[0];
+  const ArgVal& Cn = ctx.args[1];
+  const long long k = ctx.args[2].i32;
+  const int nbins = ctx.args[3].i32;
+  const long long bx = ctx.block[0];
+  const long long m = (long long)ctx.block[1] * ctx.block[2];
+  // every logical block and thread copy sweeps pix[t + j*bx], t < bx, j < k
+  long long hi = k > 0 ? k * bx : 0;
+  if (hi <= 0) return BF_OK;
+  if (hi - 1 > INT_MAX) {
+    *ctx.error = "hist_stride: index beyond i32";
+    return BF_E_UNSUPPORTED;
+  }
+  if (nbins == 0) {
+    ctx.host_trap(BF_TRAP_DIV_BY_ZERO, ctx.first, "integer modulo by zero");
+    return BF_OK;
+  }
+  if (hi > P.len) {
+    ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first, "load index out of range");
+    hi = P.len;
+  }
+  return hist_issue(ctx, P, Cn, 0, hi, nbins, (unsigned)(ctx.count * m), 0, 0);
+}
+
+// ===========================================================================
+// fir (corpus/fir.kn): y[o] = sum_i w[i] * x[o + i], o < m*blockDim.x.
+// Products of two f32 are exact in f64, so fma(w, x, acc) == acc + w*x and
+// the f64 accumulation in tap order matches the reference bit for bit.
+// CTA tile: 1024 outputs; x tile + (taps-1) halo staged in shared memory.
+// ===========================================================================
+constexpr int kFirTile = 1024;
+
+__global__ void __launch_bounds__(256) fir_tile(const float* __restrict__ x,
+                                                float* __restrict__ y,
+                                                const float* __restrict__ w, int taps,
+                                                long long nout) {
+  extern __shared__ float xs[];  // kFirTile + taps - 1
+  __shared__ double ws[64];
+  for (long long base = (long long)blockIdx.x * kFirTile; base < nout;
+       base += (long long)gridDim.x * kFirTile) {
+    const int span = kFirTile + taps - 1;
+    const long long avail = nout + taps - 1 - base;  // x elements in range
+    __syncthreads();
+    for (int i = threadIdx.x; i < span; i += blockDim.x) xs[i] = i < avail ? __ldg(x + base + i) : 0.f;
+    for (int i = threadIdx.x; i < taps && i < 64; i += blockDim.x) ws[i] = (double)__ldg(w + i);
+    __syncthreads();
+    const int o0 = threadIdx.x * 4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < taps; i++) {
+      const double wi = i < 64 ? ws[i] : (double)__ldg(w + i);
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[q] = fma(wi, (double)xs[o0 + q + i], acc[q]);
+    }
+    const long long o = base + o0;
+    if (o + 3 < nout) {
+      *reinterpret_cast<float4*>(y + o) =
+          make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
+    } else {
+      for (int q = 0; q < 4; q++)
+        if (o + q < nout) y[o + q] = (float)acc[q];
+    }
+  }
+}
+
+static int launch_fir(LaunchCtx& ctx) {
+  const ArgVal& X = ctx.args[0];
+  const ArgVal& Y = ctx.args[1];
+  const ArgVal& W = ctx.args[2];
+  const int taps = ctx.args[3].i32;
+  const long long m = ctx.args[4].i32;
+  const long long bx = ctx.block[0];
+  long long nout = m > 0 ? m * bx : 0;
+  if (nout <= 0) return BF_OK;
+  if (nout + (taps > 0 ? taps : 0) > (long long)INT_MAX) {
+    *ctx.error = "fir: index beyond i32";
+    return BF_E_UNSUPPORTED;
+  }
+  int t = taps > 0 ? taps : 0;
+  if (nout > Y.len || (t > 0 && (t > W.len || nout + t - 1 > X.len))) {
+    ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first, "fir index out of range");
+    return BF_OK;
+  }
+  if (t + kFirTile > 48 * 1024 / 4) {
+    *ctx.error = "fir: more than 11264 taps";
+    return BF_E_UNSUPPORTED;
+  }
+  int grid = stream_grid(nout, kFirTile, ctx.num_sms, 4);
+  fir_tile<<<grid, 256, (kFirTile + (t > 0 ? t - 1 : 0)) * sizeof(float), ctx.stream>>>(
+      (const float*)X.ptr, (float*)Y.ptr, (const float*)W.ptr, t, nout);
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  return BF_OK;
+}
+
+// ===========================================================================
+// wreduce (corpus/wreduce.kn), warp mode: v = (id < n) ? x[id] : 0;
+// v += shfl_down(v, d) for d = 16, 8, 4, 2, 1 with the reference's clamp (a
+// source lane at or beyond min(warp_size, active lanes) reads its own value,
+// interp.py:276-283); lanes with threadIdx.x % 32 == 0 add v to out[0].
+// One CTA per logical block (logical tid == physical thread); the logical
+// warp size must divide 32 so logical warps sit inside physical warps.
+// ===========================================================================
+__global__ void __launch_bounds__(1024) wreduce_blocks(const int* __restrict__ x, long long lx,
+                                                       int* out, long long lout, int n, int ws,
+                                                       KDesc k) {
+  __shared__ unsigned part[32];
+  __shared__ int trap;
+  const long long B = (long long)k.bx * k.by * k.bz;
+  for (long long blk = k.first + blockIdx.x; blk < k.first + k.count; blk += gridDim.x) {
+    const long long bxi = blk % k.gx;
+    unsigned total = 0;
+    if (threadIdx.x == 0) trap = 0;
+    __syncthreads();
+    for (long long c0 = 0; c0 < B; c0 += blockDim.x) {  // chunks of logical tids
+      const long long tid = c0 + threadIdx.x;
+      const bool live = tid < B;
+      const int tx = (int)(tid % k.bx);
+      const int id = (int)((unsigned)bxi * (unsigned)k.bx + (unsigned)tx);
+      int v = 0;
+      if (live && id < n) {
+        if (id < 0 || id >= lx) trap = 1; else v = __ldg(x + id);
+      }
+      // lanes of this logical warp that exist
+      const long long w0 = (tid / ws) * ws;
+      const int L = (int)min((long long)ws, B - w0);
+      const int i = (int)(tid - w0);
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) {
+        int other = __shfl_down_sync(0xffffffffu, v, d);
+        v = (int)((unsigned)v + (unsigned)(i + d < L ? other : v));
+      }
+      unsigned contrib = (live && tx % 32 == 0) ? (unsigned)v : 0u;
+      for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = contrib;
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int wi = 0; wi < (int)(blockDim.x + 31) / 32; wi++) total += part[wi];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (trap || lout < 1) {
+        record_fault(k, BF_TRAP_OUT_OF_BOUNDS, blk);
+      } else if (total) {
+        atomicAdd((unsigned*)out, total);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static int launch_wreduce(LaunchCtx& ctx) {
+  const ArgVal& X = ctx.args[0];
+  const ArgVal& O = ctx.args[1];
+  const int n = ctx.args[2].i32;
+  int ws = ctx.warp_size > 0 ? ctx.warp_size : 32;
+  if (ws > 32 || (32 % ws) != 0) {
+    *ctx.error = "wreduce: warp_size must divide 32 (got " + std::to_string(ws) + ")";
+    return BF_E_UNSUPPORTED;
+  }
+  long long B = (long long)ctx.block[0] * ctx.block[1] * ctx.block[2];
+  int threads = (int)std::min<long long>(1024, ((B + 31) / 32) * 32);
+  int grid = (int)std::min<long long>(ctx.count, (long long)ctx.num_sms * 16);
+  wreduce_blocks<<<grid, threads, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr, O.len, n,
+                                                   ws, ctx.desc());
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  return BF_OK;
+}
+
+static Registrar reg_reverse("reverse", {{BF_SLOT_HANDLE, BF_I32, "d"}, {BF_SLOT_I32, BF_I32, "n"}},
+                             launch_reverse);
+static Registrar reg_reduce("reduce",
+                            {{BF_SLOT_HANDLE, BF_I32, "x"},
+                             {BF_SLOT_HANDLE, BF_I32, "out"},
+                             {BF_SLOT_I32, BF_I32, "n"}},
+                            launch_reduce);
+static Registrar reg_hist("hist",
+                          {{BF_SLOT_HANDLE, BF_I32, "pix"},
+                           {BF_SLOT_HANDLE, BF_I32, "counts"},
+                           {BF_SLOT_I32, BF_I32, "n"},
+                           {BF_SLOT_I32, BF_I32, "nbins"}},
+                          launch_hist);
+static Registrar reg_hist_stride("hist_stride",
+                                 {{BF_SLOT_HANDLE, BF_I32, "pix"},
+                                  {BF_SLOT_HANDLE, BF_I32, "counts"},
+                                  {BF_SLOT_I32, BF_I32, "k"},
+                                  {BF_SLOT_I32, BF_I32, "nbins"}},
+                                 launch_hist_stride);
+static Registrar reg_fir("fir",
+                         {{BF_SLOT_HANDLE, BF_F32, "x"},
+                          {BF_SLOT_HANDLE, BF_F32, "y"},
+                          {BF_SLOT_HANDLE, BF_F32, "w"},
+                          {BF_SLOT_I32, BF_I32, "taps"},
+                          {BF_SLOT_I32, BF_I32, "m"}},
+                         launch_fir);
+static Registrar reg_wreduce("wreduce",
+                             {{BF_SLOT_HANDLE, BF_I32, "x"},
+                              {BF_SLOT_HANDLE, BF_I32, "out"},
+                              {BF_SLOT_I32, BF_I32, "n"}},
+                             launch_wreduce);
+
+}  // namespace bf

@@ -178,6 +178,7 @@ struct bf_arena {
   size_t staging_bytes = 0;
   cudaEvent_t staging_ev[2] = {nullptr, nullptr};
   int live_runtimes = 0;
+  bool destroy_pending = false;  // destroyed while runtimes still reference it
 };
 
 namespace bf {
@@ -464,8 +465,20 @@ int bf_arena_create(int32_t device, bf_arena** out) {
   return BF_OK;
 }
 
+static void arena_free(bf_arena* a);
+
 int bf_arena_destroy(bf_arena* a) {
   if (!a) return BF_OK;
+  if (a->live_runtimes > 0) {
+    // a runtime still points at this arena: free it with the last runtime
+    a->destroy_pending = true;
+    return BF_OK;
+  }
+  arena_free(a);
+  return BF_OK;
+}
+
+static void arena_free(bf_arena* a) {
   set_device(a->device);
   cudaDeviceSynchronize();
   for (auto& kv : a->buffers) cudaFree(kv.second.ptr);
@@ -476,7 +489,6 @@ int bf_arena_destroy(bf_arena* a) {
   }
   if (a->copy_stream) cudaStreamDestroy(a->copy_stream);
   delete a;
-  return BF_OK;
 }
 
 int bf_alloc(bf_arena* a, int32_t scalar, int64_t length, uint32_t* handle) {
@@ -847,8 +859,12 @@ int bf_runtime_destroy(bf_runtime* rt) {
     if (kv.second.executed_dev) cudaFree(kv.second.executed_dev);
   if (rt->fault_dev) cudaFree(rt->fault_dev);
   if (rt->gate_host) cudaFreeHost((void*)rt->gate_host);
-  rt->arena->live_runtimes--;
-  if (rt->arena->live_runtimes == 0) release_zombies(rt->arena);
+  bf_arena* a = rt->arena;
+  a->live_runtimes--;
+  if (a->live_runtimes == 0) {
+    release_zombies(a);
+    if (a->destroy_pending) arena_free(a);
+  }
   delete rt;
   return BF_OK;
 }
@@ -929,7 +945,7 @@ int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const i
   }
 
   if ((rt->flags & BF_FLAG_INSTRUMENT) && total > 0) {
-    CK(cudaMallocAsync((void**)&tr.executed_dev, total * sizeof(int), rt->streams[0]));
+    CK(cudaMalloc((void**)&tr.executed_dev, total * sizeof(int)));
     CK(cudaMemsetAsync(tr.executed_dev, 0, total * sizeof(int), rt->streams[0]));
     CK(cudaStreamSynchronize(rt->streams[0]));
   }

@@ -1,0 +1,121 @@
+"""Multi-GPU block partitioning (one process per GPU).
+
+The reference's only parallelism is block-level data parallelism: a grid's
+independent blocks are handed out to pool workers in coarse ranges, the
+average grain being ceil(totalBlocks / pool) (runtime.py:78-101,
+PAPER.md:101-110).  Across GPUs the workers are the ranks: rank r owns the
+r-th contiguous range of `ceil(total / world)` units (rows of the hotspot
+grid, logical blocks of a 1D launch), and only kernels whose blocks exchange
+data need a collective:
+
+  * hotspot — row bands with ghost zones: each rank also holds `halo` rows
+    of each neighbour band and recomputes them; after `halo` iterations the
+    invalid region (which grows one row per iteration from a ghost edge) has
+    just reached the owned rows, so `halo` rows per side are exchanged with
+    NCCL point-to-point every `halo` iterations.
+  * hist / hist_stride / wreduce / kmeans — per-rank partial counts or sums
+    combined with one all-reduce.
+  * vecadd / nn / fir / reduce — disjoint outputs, no collective.
+
+Everything here is backend-agnostic torch.distributed (NCCL on GPUs, gloo in
+the CPU tests).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+
+def average_grain(total: int, world: int) -> int:
+    """ceil(total / world): the Average fetch policy with ranks as workers."""
+    if total < 1 or world < 1:
+        raise ValueError("total and world must be >= 1")
+    return -(-total // world)
+
+
+def rank_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """[first, last) units owned by `rank` under the average grain."""
+    g = average_grain(total, world)
+    lo = min(total, rank * g)
+    return lo, min(total, lo + g)
+
+
+@dataclass
+class HotspotBands:
+    rows: int
+    cols: int
+    world: int
+    rank: int
+    halo: int = 0
+
+    def __post_init__(self):
+        self.own = rank_range(self.rows, self.world, self.rank)
+        if self.world > 1:
+            if self.halo < 1:
+                raise ValueError("multi-rank hotspot needs halo >= 1")
+            g = average_grain(self.rows, self.world)
+            if g < self.halo:
+                raise ValueError(f"band of {g} rows is thinner than the halo ({self.halo})")
+        lo = max(0, self.own[0] - self.halo)
+        hi = min(self.rows, self.own[1] + self.halo)
+        self.local_rows = (lo, hi)
+
+    @property
+    def up(self) -> int | None:
+        return self.rank - 1 if self.rank > 0 and self.own[0] > 0 else None
+
+    @property
+    def down(self) -> int | None:
+        return self.rank + 1 if self.rank + 1 < self.world and self.own[1] < self.rows else None
+
+    def own_slice(self) -> tuple[int, int]:
+        """Owned rows in local row coordinates."""
+        lo = self.local_rows[0]
+        return self.own[0] - lo, self.own[1] - lo
+
+    def exchanger(self, arena, stream=None) -> "HaloExchange":
+        import torch
+
+        def view(handle):
+            return torch.as_tensor(arena.cuda_array(handle), device=torch.device("cuda", arena.device))
+        return HaloExchange(self, view, stream)
+
+
+class HaloExchange:
+    """Refresh the ghost rows of a local grid from the neighbour ranks."""
+
+    def __init__(self, bands: HotspotBands, view: Callable, stream=None):
+        self.b = bands
+        self.view = view
+        self.stream = stream
+
+    def exchange(self, handle) -> None:
+        import torch
+        import torch.distributed as dist
+
+        b, cols, h = self.b, self.b.cols, self.b.halo
+        t = self.view(handle)
+        o0, o1 = b.own_slice()
+        l0, l1 = 0, b.local_rows[1] - b.local_rows[0]
+        ops = []
+        if b.up is not None:
+            ops.append(dist.P2POp(dist.isend, t[o0 * cols:(o0 + h) * cols], b.up))
+            ops.append(dist.P2POp(dist.irecv, t[l0 * cols:o0 * cols], b.up))
+        if b.down is not None:
+            ops.append(dist.P2POp(dist.isend, t[(o1 - h) * cols:o1 * cols], b.down))
+            ops.append(dist.P2POp(dist.irecv, t[o1 * cols:l1 * cols], b.down))
+        if not ops:
+            return
+        ctx = torch.cuda.stream(self.stream) if self.stream is not None else _null()
+        with ctx:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

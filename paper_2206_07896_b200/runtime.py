@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import logging
 import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional, Union
 
@@ -370,7 +371,10 @@ class Runtime:
                 (_lib.FLAG_INSTRUMENT if instrument else 0)
         check(_lib.lib().bf_runtime_create(arena.native, self.pool_size, flags, float(block_delay),
                                            seed & (2**64 - 1), C.byref(self._native)))
-        self._tasks: list[KernelTask] = []
+        # weak: a task keeps its runtime alive (it reads the native record),
+        # the runtime must not keep its tasks alive (no reference cycle, so
+        # runtime -> arena teardown order stays refcount-driven)
+        self._tasks: "weakref.WeakSet[KernelTask]" = weakref.WeakSet()
         self._shut_down = False
 
     # -- host API ---------------------------------------------------------------
@@ -396,7 +400,7 @@ class Runtime:
         check(rc)
         task._rt = self
         task._id = tid.value
-        self._tasks.append(task)
+        self._tasks.add(task)
         return task
 
     def device_synchronize(self) -> None:
@@ -411,7 +415,7 @@ class Runtime:
         check(rc)
 
     def unfinished_tasks(self) -> list:
-        return [t for t in self._tasks if t.remaining > 0]
+        return sorted((t for t in self._tasks if t.remaining > 0), key=lambda t: t._id)
 
     def hold_new_blocks(self) -> None:
         check(_lib.lib().bf_hold_new_blocks(self._native))
