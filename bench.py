@@ -316,7 +316,7 @@ def run_ours(args) -> None:
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                          "traffic": traffic, "peak_source": peaks["source"],
-                         "kernel": "hotspot_strip", "avg_launch_us": round(avg_launch_ms * 1e3, 3)},
+                         "kernel": "hotspot_band", "avg_launch_us": round(avg_launch_ms * 1e3, 3)},
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": 2 * cells * 4 * world, "d2h_bytes_per_step": cells * 4 * world,
                     "ms_per_step": round(e2e_s * 1e3, 3)},

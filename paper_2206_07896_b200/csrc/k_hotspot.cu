@@ -7,13 +7,14 @@
 // (arena.py:111-116).  The f32 scalar params carry doubles (hostprog.py:
 // 390-414).  No FMA contraction: dadd/dsub/dmul are the _rn intrinsics.
 //
-// B200 mapping (fast path): a warp owns a 128-column x RS-row strip; each lane
-// holds a float4 of the north/centre/south rows in registers and slides down
-// the strip, so every row of `src` is loaded once per strip (+2 halo rows
-// per RS rows, served by L2).  West/east neighbours come from warp shuffles;
+// B200 mapping (fast path): a warp owns a 128-column x band-row strip; each
+// lane holds a float4 of the north/centre/south rows in registers and slides
+// down the strip, so every row of `src` is loaded once per strip (+2 halo
+// rows per band, served by L2).  West/east neighbours come from warp shuffles;
 // lanes at the strip edge load one scalar.  Algorithmic traffic per cell and
 // iteration: 12 B (read src + power, write dst).
 #include <climits>
+#include <cstdlib>
 
 #include "bf_internal.h"
 #include "common.cuh"
@@ -38,40 +39,83 @@ __device__ __forceinline__ float hs_cell(float tcf, float tnf, float tsf, float 
   return __double2float_rn(dadd(tc, delta));
 }
 
-constexpr int kHsRows = 16;  // rows per warp strip
-
-// blockDim = (32, 4): warp w of CTA (X, Y) owns columns
-// [c_lo + X*128, +128) and rows [r_lo + (Y*4 + w)*RS, +RS).
-__global__ void __launch_bounds__(128) hotspot_strip(const float* __restrict__ src,
-                                                     const float* __restrict__ power,
-                                                     float* __restrict__ dst, int rows, int cols,
-                                                     int r_lo, int r_hi, int c_lo, int c_hi,
-                                                     HsConst k) {
-  const int lane = threadIdx.x;
-  const int c0 = c_lo + blockIdx.x * 128 + lane * 4;
-  const int r_start = r_lo + (blockIdx.y * 4 + threadIdx.y) * kHsRows;
-  if (r_start >= r_hi) return;  // warp-uniform
-  const int r_end = min(r_start + kHsRows, r_hi);
+// Work split: the cell rectangle is cut into G column groups of 128 columns
+// (one warp wide) and `bands` row bands; warp w owns (band w / G, group
+// w % G), so neighbouring column groups run on neighbouring warps at the same
+// time (their shared edge columns hit L1/L2) and every warp gets the same
+// number of rows to within one: no tail wave (grid = resident warps).
+// The row loop is software-pipelined one row ahead: the south row, power
+// row and edge scalars of row r+1 are in flight while row r is computed.
+template <int PF>
+__global__ void __launch_bounds__(128) hotspot_band(const float* __restrict__ src,
+                                                    const float* __restrict__ power,
+                                                    float* __restrict__ dst, int rows, int cols,
+                                                    int r_lo, int r_hi, int c_lo, int c_hi,
+                                                    int groups, int bands, HsConst k) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (w >= groups * bands) return;  // warp-uniform
+  const int band = w / groups, g = w % groups;
+  const long long nr = r_hi - r_lo;
+  const int r_start = r_lo + (int)(nr * band / bands);
+  const int r_end = r_lo + (int)(nr * (band + 1) / bands);
+  if (r_start >= r_end) return;
+  const int c0 = c_lo + g * 128 + lane * 4;
   const bool active = c0 < c_hi;
+  const bool west_scalar = lane == 0;
   const bool east_scalar = (lane == 31) || (c0 + 4 >= c_hi);
   const long long colsl = cols;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
 
-  auto load_row = [&](int r) -> float4 {
-    if (!active) return make_float4(0.f, 0.f, 0.f, 0.f);
-    return __ldg(reinterpret_cast<const float4*>(src + r * colsl + c0));
+  auto row4 = [&](int r) -> float4 {
+    return active ? __ldg(reinterpret_cast<const float4*>(src + r * colsl + c0)) : zero;
   };
+  auto pow4 = [&](int r) -> float4 {
+    return active ? __ldcs(reinterpret_cast<const float4*>(power + r * colsl + c0)) : zero;
+  };
+  auto west_of = [&](int r) -> float {
+    return (active && west_scalar && c0 > 0) ? __ldg(src + r * colsl + c0 - 1) : 0.f;
+  };
+  auto east_of = [&](int r) -> float {
+    return (active && east_scalar && c0 + 4 < cols) ? __ldg(src + r * colsl + c0 + 4) : 0.f;
+  };
+  auto clamp_row = [&](int r) { return r < r_end ? r : r_end - 1; };
 
-  float4 north = load_row(r_start > 0 ? r_start - 1 : 0);
-  float4 center = load_row(r_start);
+  // ring of PF rows in flight: slot i holds (south row of r+i, power/edges of r+i)
+  float4 north = row4(r_start > 0 ? r_start - 1 : 0);
+  float4 center = row4(r_start);
+  float4 sq[PF], pq[PF];
+  float wq[PF], eq[PF];
+#pragma unroll
+  for (int i = 0; i < PF; i++) {
+    const int rr = clamp_row(r_start + i);
+    sq[i] = row4(rr + 1 < rows ? rr + 1 : rows - 1);
+    pq[i] = pow4(rr);
+    wq[i] = west_of(rr);
+    eq[i] = east_of(rr);
+  }
   for (int r = r_start; r < r_end; r++) {
-    const float4 south = load_row(r + 1 < rows ? r + 1 : rows - 1);
-    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (active) p = __ldcs(reinterpret_cast<const float4*>(power + r * colsl + c0));
+    const float4 south = sq[0], p = pq[0];
+    const float we = wq[0], ee = eq[0];
+#pragma unroll
+    for (int i = 0; i < PF - 1; i++) {
+      sq[i] = sq[i + 1];
+      pq[i] = pq[i + 1];
+      wq[i] = wq[i + 1];
+      eq[i] = eq[i + 1];
+    }
+    {
+      const int rr = clamp_row(r + PF);
+      sq[PF - 1] = row4(rr + 1 < rows ? rr + 1 : rows - 1);
+      pq[PF - 1] = pow4(rr);
+      wq[PF - 1] = west_of(rr);
+      eq[PF - 1] = east_of(rr);
+    }
     float west = __shfl_up_sync(0xffffffffu, center.w, 1);
     float east = __shfl_down_sync(0xffffffffu, center.x, 1);
+    if (west_scalar) west = c0 > 0 ? we : center.x;
+    if (east_scalar) east = c0 + 4 < cols ? ee : center.w;
     if (active) {
-      if (lane == 0) west = c0 > 0 ? __ldg(src + r * colsl + c0 - 1) : center.x;
-      if (east_scalar) east = c0 + 4 < cols ? __ldg(src + r * colsl + c0 + 4) : center.w;
       float4 out;
       out.x = hs_cell(center.x, north.x, south.x, west, center.y, p.x, k);
       out.y = hs_cell(center.y, north.y, south.y, center.x, center.z, p.y, k);
@@ -82,6 +126,38 @@ __global__ void __launch_bounds__(128) hotspot_strip(const float* __restrict__ s
     north = center;
     center = south;
   }
+}
+
+static int hotspot_pf() {
+  static int pf = -1;
+  if (pf < 0) {
+    const char* e = getenv("BF_HOTSPOT_PF");
+    pf = e ? atoi(e) : 1;
+    if (pf < 1 || pf > 4) pf = 1;
+  }
+  return pf;
+}
+
+typedef void (*HsBandFn)(const float*, const float*, float*, int, int, int, int, int, int, int, int,
+                         HsConst);
+static HsBandFn hotspot_band_fn(int pf) {
+  switch (pf) {
+    case 1: return hotspot_band<1>;
+    case 3: return hotspot_band<3>;
+    case 4: return hotspot_band<4>;
+    default: return hotspot_band<2>;
+  }
+}
+
+static int hotspot_resident_warps(int num_sms, int pf) {
+  static int per_sm[5] = {0, 0, 0, 0, 0};
+  if (per_sm[pf] == 0) {
+    int ctas = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, hotspot_band_fn(pf), 128, 0);
+    cudaGetLastError();
+    per_sm[pf] = ctas > 0 ? ctas * 4 : 16;
+  }
+  return per_sm[pf] * num_sms;
 }
 
 // Generic path: any geometry or alignment; one thread per cell of the cell
@@ -141,11 +217,15 @@ static int launch_hotspot(LaunchCtx& ctx) {
     }
     const bool aligned = (cols % 4 == 0) && (c_lo % 4 == 0) && (c_hi % 4 == 0);
     if (in_bounds && aligned) {
-      dim3 grid((unsigned)((c_hi - c_lo + 127) / 128),
-                (unsigned)((r_hi - r_lo + 4 * kHsRows - 1) / (4 * kHsRows)));
-      hotspot_strip<<<grid, dim3(32, 4), 0, ctx.stream>>>(
-          (const float*)S.ptr, (const float*)P.ptr, (float*)D.ptr, rows, cols, (int)r_lo,
-          (int)r_hi, (int)c_lo, (int)c_hi, k);
+      const int groups = (int)((c_hi - c_lo + 127) / 128);
+      const int pf = hotspot_pf();
+      const int warps = hotspot_resident_warps(ctx.num_sms, pf);
+      int bands = std::max(1, warps / groups);
+      if (bands > r_hi - r_lo) bands = (int)(r_hi - r_lo);
+      const int grid = (groups * bands + 3) / 4;
+      hotspot_band_fn(pf)<<<grid, 128, 0, ctx.stream>>>((const float*)S.ptr, (const float*)P.ptr,
+                                                 (float*)D.ptr, rows, cols, (int)r_lo, (int)r_hi,
+                                                 (int)c_lo, (int)c_hi, groups, bands, k);
     } else {
       long long zb = zbase;
       if (zb + (rc.y0 * ctx.grid[0] + rc.x0) < ctx.first) zb += plane;
