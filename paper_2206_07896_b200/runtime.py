@@ -151,12 +151,16 @@ def resolve_grain(policy: FetchPolicy, grid_size: int, pool_size: int,
     """Blocks claimed per fetch for one launch (native bf_resolve_grain)."""
     if grid_size < 1 or pool_size < 1:
         raise ValueError("grid_size and pool_size must be >= 1")
-    if isinstance(policy, Average):
+    # duck-typed so the reference's own policy objects work too
+    kind = type(policy).__name__
+    if kind == "Average":
         code, fixed, thr = _lib.POLICY_AVERAGE, 0, 0
-    elif isinstance(policy, Fixed):
-        code, fixed, thr = _lib.POLICY_FIXED, policy.grain, 0
+    elif kind == "Fixed":
+        code, fixed, thr = _lib.POLICY_FIXED, int(policy.grain), 0
+    elif kind == "AutoAggressive":
+        code, fixed, thr = _lib.POLICY_AUTO, 0, int(policy.light_kernel_threshold)
     else:
-        code, fixed, thr = _lib.POLICY_AUTO, 0, policy.light_kernel_threshold
+        raise ValueError(f"unknown fetch policy {policy!r}")
     atomics, est = -1, -1
     if kernel_stats is not None:
         atomics = 1 if kernel_stats.has_atomics() else 0

@@ -23,15 +23,28 @@ def has_gpu() -> bool:
         return False
 
 
-REFERENCE_SRC = Path("/root/reference/pkg/src")
+# The unmodified reference package: the read-only source tree in this
+# container, or its pip install under baseline/_ref (git-ignored; it travels
+# to the GPU box with the snapshot, /root/reference does not).
+REFERENCE_PATHS = [Path("/root/reference/pkg/src"), ROOT / "baseline" / "_ref"]
+
+
+def reference_path():
+    for p in REFERENCE_PATHS:
+        if (p / "blockfuse" / "__init__.py").exists():
+            return p
+    return None
 
 
 @pytest.fixture(scope="session")
 def reference():
-    """The reference package, when this container has it (never on the GPU box)."""
-    if not REFERENCE_SRC.exists():
-        pytest.skip("reference not available")
-    if str(REFERENCE_SRC) not in sys.path:
-        sys.path.append(str(REFERENCE_SRC))
+    """The reference package `blockfuse`, or skip when it is unavailable."""
+    p = reference_path()
+    if p is None:
+        pytest.skip("reference package not available")
+    if str(p) not in sys.path:
+        sys.path.append(str(p))
     import blockfuse
+    import blockfuse.bench  # noqa: F401
+    import blockfuse.runtime  # noqa: F401
     return blockfuse

@@ -1,0 +1,184 @@
+"""Drop-in tests: the UNMODIFIED reference package drives this runtime.
+
+The reference's own harness functions (blockfuse.bench.runtime_outputs,
+run_sweep, blockfuse.runtime.run_host_program) look up `Runtime` and
+`DeviceArena` as module globals (bench.py:20-24, runtime.py:414-416); the
+tests swap in this package's classes and compare against the reference's own
+lockstep oracle (`reference_outputs`, executor.run_reference) with the
+reference's own comparator (`outputs_equal`, bench.py:245-259).
+
+The reference is imported from /root/reference (this container) or from its
+pip install under baseline/_ref (the GPU box).
+"""
+
+import random
+from contextlib import contextmanager
+
+import pytest
+
+from conftest import has_gpu
+
+import paper_2206_07896_b200 as ours
+from paper_2206_07896_b200 import routines
+
+
+@contextmanager
+def our_runtime(bf):
+    """Point the reference harness at the B200 runtime."""
+    import blockfuse.bench as B
+    import blockfuse.runtime as R
+    saved = (B.Runtime, B.DeviceArena, R.Runtime, R.DeviceArena)
+    B.Runtime = R.Runtime = ours.Runtime
+    B.DeviceArena = R.DeviceArena = ours.DeviceArena
+    try:
+        yield
+    finally:
+        B.Runtime, B.DeviceArena, R.Runtime, R.DeviceArena = saved
+
+
+# ---------------------------------------------------------------------------
+# CPU: routine resolution of the reference's own MpmdKernel objects
+# ---------------------------------------------------------------------------
+
+def test_reference_kernels_resolve(reference):
+    from blockfuse.bench import CORPUS
+    for name, case in CORPUS.items():
+        mk = case.compiled()
+        got = routines.resolve(mk)
+        assert got[0] == name
+        assert got[1] == case.warp_mode
+        r = routines.get(name)
+        assert r.has_atomics() == mk.has_atomics()
+        assert r.static_instruction_estimate() == mk.static_instruction_estimate()
+        assert [n for n, _ in r.params] == [p.name for p in mk.param_signature]
+
+
+def test_our_kn_kernels_resolve(reference):
+    from blockfuse.parser import parse_unit
+    from blockfuse.transform import transform
+    for name in ("hotspot", "nn", "kmeans", "bfs"):
+        kp = parse_unit(routines.kernel_source(name))[name]
+        mk = transform(kp)
+        assert routines.resolve(mk)[0] == name
+        r = routines.get(name)
+        assert r.has_atomics() == mk.has_atomics()
+        assert r.static_instruction_estimate() == mk.static_instruction_estimate()
+
+
+def test_foreign_body_under_a_known_name_is_rejected(reference):
+    from blockfuse.parser import parse
+    from blockfuse.transform import transform
+    mk = transform(parse("kernel vecadd(a: global f32[], b: global f32[], c: global f32[], n: i32) {"
+                         " let id: i32 = blockIdx.x * blockDim.x + threadIdx.x;"
+                         " if (id < n) { c[id] = a[id] - b[id]; } }"))
+    with pytest.raises(routines.KernelNotImplemented):
+        routines.resolve(mk)
+
+
+def test_fingerprints_match_reference_transform(reference):
+    """paper_2206_07896_b200/fingerprints.json is what gen_golden.py wrote."""
+    from blockfuse.bench import CORPUS
+    for name, case in CORPUS.items():
+        assert routines.expected_fingerprint(name) == routines.fingerprint_of(case.compiled().to_dict())
+
+
+# ---------------------------------------------------------------------------
+# GPU: the reference harness on the B200 runtime
+# ---------------------------------------------------------------------------
+
+gpu = pytest.mark.gpu
+
+
+@pytest.fixture
+def need_gpu():
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+
+
+@gpu
+def test_reference_equivalence_sweep_on_b200(need_gpu, reference):
+    """test_acceptance.py:96-115 with our Runtime/DeviceArena swapped in."""
+    from blockfuse.bench import CORPUS, EQUIVALENCE_CASES, outputs_equal, reference_outputs, runtime_outputs
+    rng = random.Random(20260823)
+    failures = []
+    for name in EQUIVALENCE_CASES:
+        case = CORPUS[name]
+        compiled = case.compiled()
+        for i in range(50):
+            inst = case.random_instance(rng)
+            want = reference_outputs(case, inst)
+            with our_runtime(reference):
+                got, task, counters = runtime_outputs(case, inst, pool_size=2, compiled=compiled)
+            if not outputs_equal(got, want, rel_tol=0.0):
+                failures.append((name, i))
+            assert task.remaining == 0
+            assert counters.blocks_executed == inst.grid.total
+    assert not failures, failures
+
+
+@gpu
+def test_reference_sweep_fetch_counts(need_gpu, reference):
+    """test_bench.py:36-58: fetch counts follow the grain on the device runtime."""
+    from blockfuse.bench import run_sweep
+    with our_runtime(reference):
+        report = run_sweep("vecadd", [1, 2, "average"], pool=2, repeats=1)
+        total = report.rows[0].blocks_executed
+        for row in report.rows:
+            assert row.blocks_executed == total
+            assert row.fetch_count == -(-total // row.grain)
+        (row,) = run_sweep("vecadd", [10 ** 6], pool=4, repeats=1).rows
+        assert row.grain == row.blocks_executed and row.fetch_count == 1
+
+
+HOST_SCRIPTS = ["vecadd", "reverse", "reduce", "hist", "hist_stride", "fir", "wreduce"]
+
+
+@gpu
+@pytest.mark.parametrize("name", HOST_SCRIPTS)
+def test_reference_host_programs_on_b200(need_gpu, reference, name):
+    """The corpus demo scripts through the reference's host driver
+    (run_host_program: implicit syncs, conflict detector) on our runtime."""
+    from blockfuse.bench import load_host_script, load_kernel
+    from blockfuse.hostprog import parse_host
+    from blockfuse.runtime import run_host_program
+    kernels = {name: load_kernel(name)}
+    program = parse_host(load_host_script(name), kernels)
+    warp = name == "wreduce"
+    want = run_host_program(program, kernels, pool_size=2, warp_mode=warp)
+    with our_runtime(reference):
+        got = run_host_program(program, kernels, pool_size=2, warp_mode=warp, hold_blocks=True)
+    assert got.conflicts == []
+    assert got.downloads == want.downloads
+    assert all(t.remaining == 0 for t in got.tasks)
+
+
+@gpu
+def test_reference_implicit_syncs_under_adversarial_schedule(need_gpu, reference):
+    """test_acceptance.py:181-268 (the soundness half) with corpus kernels: the
+    inserted syncs keep every host op clear of unfinished launches even when
+    the device holds all blocks until the next sync."""
+    from blockfuse.bench import load_kernel
+    from blockfuse.hostprog import Alloc, BufferArg, Download, HostProgram, Launch, ScalarArg, Upload
+    from blockfuse.runtime import run_host_program
+    from blockfuse.syntax import Dim3
+    kernels = {"vecadd": load_kernel("vecadd")}
+    rng = random.Random(99)
+    bufs = ["b0", "b1", "b2", "b3"]
+    for trial in range(40):
+        ops = [Alloc(b, "f32", 64) for b in bufs]
+        for _ in range(rng.randint(2, 6)):
+            kind = rng.randrange(3)
+            if kind == 0:
+                a, b, c = rng.sample(bufs, 3)
+                ops.append(Launch("vecadd", Dim3(2), Dim3(32), 0,
+                                  [BufferArg(a), BufferArg(b), BufferArg(c), ScalarArg(64, "i32")]))
+            elif kind == 1:
+                ops.append(Upload(rng.choice(bufs), f"fill:rand:{trial}"))
+            else:
+                ops.append(Download(rng.choice(bufs), f"out{len(ops)}.bin"))
+        program = HostProgram(ops)
+        want = run_host_program(program, kernels, pool_size=2)
+        with our_runtime(reference):
+            got = run_host_program(program, kernels, pool_size=2, hold_blocks=True)
+        assert got.conflicts == []
+        assert got.downloads == want.downloads

@@ -1,0 +1,112 @@
+"""Multi-rank partitioning on CPU (gloo, world sizes 2 and 3).
+
+The GPU path runs the same `HotspotBands` / `HaloExchange` code with NCCL
+and the sm_100a kernel as the step; here the step is the pinned CPU oracle,
+so the test checks the partition + ghost-zone exchange protocol: the
+row-banded run must equal the single-grid run bit for bit."""
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _hotspot_worker(rank, world, port, rows, cols, iters, halo, out_q):
+    sys.path[:0] = [str(ROOT), str(ROOT / "oracle")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import instances as I
+        import oracle
+        from paper_2206_07896_b200.parallel import HaloExchange, HotspotBands
+
+        temp, power = I.hotspot_inputs(rows, cols, 3)
+        params = I.hotspot_params(rows, cols)
+        b = HotspotBands(rows, cols, world, rank, halo=halo)
+        r0, r1 = b.local_rows
+        lrows = r1 - r0
+        bufs = [temp[r0 * cols:r1 * cols].copy(), np.zeros(lrows * cols, np.float32)]
+        pw = power[r0 * cols:r1 * cols].copy()
+        ex = HaloExchange(b, lambda h: torch.from_numpy(bufs[h]))
+        cur = 0
+        for it in range(iters):
+            step = I.hotspot(lrows, cols, 16, 16)
+            step.buffer("src").values = bufs[cur]
+            step.buffer("power").values = pw
+            out, trap = oracle.run(step)
+            assert trap is None
+            bufs[cur ^ 1][:] = out["dst"]
+            cur ^= 1
+            if (it + 1) % b.halo == 0 and it + 1 < iters:
+                ex.exchange(cur)
+        o0, o1 = b.own_slice()
+        from paper_2206_07896_b200.parallel import average_grain
+        g = average_grain(rows, world)
+        mine = torch.zeros(g * cols, dtype=torch.float32)  # gloo gathers equal sizes
+        mine[:(o1 - o0) * cols] = torch.from_numpy(bufs[cur][o0 * cols:o1 * cols])
+        full = [torch.zeros(g * cols, dtype=torch.float32) for _ in range(world)]
+        dist.all_gather(full, mine)
+        if rank == 0:
+            out_q.put(torch.cat(full).numpy()[:rows * cols])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,rows,cols,iters,halo", [(2, 40, 36, 7, 3), (3, 50, 20, 9, 4),
+                                                        (2, 33, 16, 5, 5)])
+def test_hotspot_bands_match_single_grid(world, rows, cols, iters, halo):
+    import instances as I
+    import oracle
+    temp, power = I.hotspot_inputs(rows, cols, 3)
+    want = oracle.hotspot_iterate(temp, power, rows, cols, I.hotspot_params(rows, cols), iters)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hotspot_worker, args=(r, world, port, rows, cols, iters, halo, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=90)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_rank_ranges_follow_average_grain():
+    from paper_2206_07896_b200.parallel import average_grain, rank_range
+    for total in (1, 7, 64, 1000):
+        for world in (1, 2, 3, 8):
+            g = average_grain(total, world)
+            covered = []
+            for r in range(world):
+                lo, hi = rank_range(total, world, r)
+                assert hi - lo <= g
+                covered += list(range(lo, hi))
+            assert covered == list(range(total))
+
+
+def test_band_validation():
+    from paper_2206_07896_b200.parallel import HotspotBands
+    with pytest.raises(ValueError):
+        HotspotBands(16, 16, 2, 0, halo=0)
+    with pytest.raises(ValueError):
+        HotspotBands(16, 16, 4, 0, halo=8)  # bands of 4 rows < halo
+    b = HotspotBands(100, 8, 4, 1, halo=5)
+    assert b.own == (25, 50) and b.local_rows == (20, 55) and b.up == 0 and b.down == 2
