@@ -295,6 +295,19 @@ def run_ours(args) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_hotspot(size, iters, args.cpu_budget, len(os.sched_getaffinity(0)))
+        pyref = None
+        try:
+            import benchkit
+            pyref = benchkit.python_reference_sample()
+        except Exception as e:  # reported, not hidden
+            pyref = {"error": repr(e)}
+        if pyref is not None:
+            cpu["python_reference_vecadd"] = pyref
+
+    kernels = None
+    kernel_launches = 0
+    if rank == 0 and world == 1 and not args.no_kernels:
+        kernels, kernel_launches = per_kernel_table(arena, rt, torch, stream, args)
 
     traffic = None
     prof = ROOT / "profiles" / "hotspot_traffic.json"
@@ -325,11 +338,58 @@ def run_ours(args) -> None:
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if kernels is not None:
+            line["kernels"] = kernels
+            line["kernel_table_launches"] = kernel_launches
         print(json.dumps(line), flush=True)
+        if kernels is not None:
+            out = ROOT / "profiles" / "last_bench_kernels.json"
+            try:
+                out.parent.mkdir(exist_ok=True)
+                out.write_text(json.dumps(kernels, indent=1) + "\n")
+            except OSError:
+                pass
     rt.shutdown()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def per_kernel_table(arena, rt, torch, stream, args) -> tuple[dict, int]:
+    """Every other kernel of the path at full size (benchkit.py), N=1."""
+    import benchkit
+    device = torch.device("cuda", arena.device)
+    peaks = _peaks()
+    cases = benchkit.build_cases(arena, torch, device, scale=args.kernel_scale)
+    if not args.no_bfs:
+        cases.append(benchkit.bfs_case(arena, torch, device, log_v=args.bfs_log_v))
+    torch.cuda.synchronize()
+    threads = len(os.sched_getaffinity(0))
+    table, launches = {}, 0
+    for c in cases:
+        r = benchkit.time_case(c, rt, torch, stream, reps=args.steps, warmup=args.warmup)
+        launches += r["launches"] * args.steps
+        gbs = c.bytes_per_step / r["dev_s"] / 1e9
+        ent = {"kernel": c.kernel, "gbs": round(gbs, 2), "frac_hbm": round(gbs / peaks["hbm_gbs"], 4),
+               f"{c.unit_elem}_per_s": c.elems_per_step / r["dev_s"],
+               "ms_per_step": round(r["dev_s"] * 1e3, 4), "wall_ms_per_step": round(r["wall_s"] * 1e3, 4),
+               "launches_per_step": r["launches"], "bytes_per_step": c.bytes_per_step,
+               "checked": r["checked"]}
+        if c.note:
+            ent["note"] = c.note
+        if hasattr(c, "levels"):
+            ent["levels"] = c.levels["n"]
+        if not args.no_cpu:
+            try:
+                cpu = benchkit.cpu_sample(c.name, threads)
+            except Exception as e:
+                cpu = {"error": repr(e)}
+            if cpu is not None:
+                ent["cpu_baseline"] = cpu
+                if "elem_per_s" in cpu:
+                    ent["speedup_vs_cpu_port"] = round(c.elems_per_step / r["dev_s"] / cpu["elem_per_s"], 1)
+        table[c.name] = ent
+    return table, launches
 
 
 def main() -> None:
@@ -344,6 +404,10 @@ def main() -> None:
     ap.add_argument("--halo", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel table")
+    ap.add_argument("--no-bfs", action="store_true")
+    ap.add_argument("--kernel-scale", type=int, default=28, help="log2 elements per kernel case")
+    ap.add_argument("--bfs-log-v", type=int, default=26)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -1,0 +1,409 @@
+"""Per-kernel measurement cases for bench.py (one B200, inputs resident).
+
+Each case issues its launches through the reference-shaped API
+(Runtime.launch -> C ABI -> sm_100a kernel) on worker stream 0 and is timed
+with CUDA events on that stream.  Algorithmic bytes per launch follow
+SURVEY.md §8(d) / DESIGN.md; sizes put every working set well above the
+126 MB L2 (except the latency cases, which are labelled).  Synthetic inputs
+are generated on the device with torch (plumbing) directly into the arena's
+buffers.  A light full-size check against a plain PyTorch computation runs
+once per case where one is cheap (exact for these kernels); full parity is
+the job of tests/.
+"""
+
+from __future__ import annotations
+
+import os
+import statistics
+import sys
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Callable, Optional
+
+ROOT = Path(__file__).resolve().parent
+
+
+@dataclass
+class Case:
+    name: str
+    kernel: str                 # device kernel measured (ncu name)
+    bytes_per_step: float       # algorithmic bytes of one step
+    elems_per_step: float
+    unit_elem: str
+    launches: list              # [(routine, grid, block, shmem, packed)]
+    note: str = ""
+    check: Optional[Callable[[], bool]] = None
+    host_loop: Optional[Callable] = None  # custom step (bfs), returns launches issued
+    reset: Optional[Callable[[], None]] = None
+
+
+def _t(arena, h, torch, device):
+    return torch.as_tensor(arena.cuda_array(h), device=device)
+
+
+def build_cases(arena, torch, device, scale: int = 28) -> list:
+    """Cases at 2^scale elements (default 2^28: 1-3 GiB per array)."""
+    from paper_2206_07896_b200 import ArgSlot, Dim3, PackedArgs, routines
+
+    g = torch.Generator(device=device)
+    g.manual_seed(1234)
+    n = 1 << scale
+    cases = []
+
+    def alloc(scalar, length):
+        return arena.alloc(scalar, length)
+
+    # --- vecadd, PR1 config (2^20, grid 4096 x 256): latency-bound ---------
+    h = [alloc("f32", 1 << 20) for _ in range(3)]
+    for x in h[:2]:
+        _t(arena, x, torch, device).uniform_(-1, 1, generator=g)
+    pk = PackedArgs([ArgSlot("handle", h[0]), ArgSlot("handle", h[1]), ArgSlot("handle", h[2]),
+                     ArgSlot("i32", 1 << 20)])
+    cases.append(Case("vecadd_pr1", "vecadd_stream", 12 * (1 << 20), 1 << 20, "elem",
+                      [(routines.get("vecadd"), Dim3(4096), Dim3(256), 0, pk)],
+                      note="PR1: 2^20 f32, grid 4096x256; 12.6 MB fits L2 (latency case)"))
+
+    # --- vecadd, 2^28 -----------------------------------------------------
+    va = [alloc("f32", n) for _ in range(3)]
+    ta = [_t(arena, x, torch, device) for x in va]
+    ta[0].uniform_(-1, 1, generator=g)
+    ta[1].uniform_(-1, 1, generator=g)
+    pk = PackedArgs([ArgSlot("handle", va[0]), ArgSlot("handle", va[1]), ArgSlot("handle", va[2]),
+                     ArgSlot("i32", n)])
+    cases.append(Case("vecadd", "vecadd_stream", 12 * n, n, "elem",
+                      [(routines.get("vecadd"), Dim3(n // 256), Dim3(256), 0, pk)],
+                      check=lambda: bool(torch.equal(ta[2], ta[0] + ta[1]))))
+
+    # --- nn, 2^28 records -------------------------------------------------
+    ll = alloc("f32", 2 * n)
+    d = alloc("f32", n)
+    tl = _t(arena, ll, torch, device)
+    tl[0::2].uniform_(-90, 90, generator=g)
+    tl[1::2].uniform_(-180, 180, generator=g)
+    td = _t(arena, d, torch, device)
+    pk = PackedArgs([ArgSlot("handle", ll), ArgSlot("handle", d), ArgSlot("i32", n),
+                     ArgSlot("f32", 30.0), ArgSlot("f32", 90.0)])
+
+    def nn_check():
+        k = 1 << 22
+        a = tl[0:2 * k:2].double() - 30.0
+        b = tl[1:2 * k:2].double() - 90.0
+        return bool(torch.equal(td[:k], torch.sqrt(a * a + b * b).float()))
+    cases.append(Case("nn", "nn_stream", 12 * n, n, "record",
+                      [(routines.get("nn"), Dim3(n // 256), Dim3(256), 0, pk)], check=nn_check))
+
+    # --- hist, 2^28 pixels, 16 bins -----------------------------------------
+    pix = alloc("i32", n)
+    cnt = alloc("i32", 16)
+    tp = _t(arena, pix, torch, device)
+    tp.random_(0, 1 << 16, generator=g)
+    tc = _t(arena, cnt, torch, device)
+    pk = PackedArgs([ArgSlot("handle", pix), ArgSlot("handle", cnt), ArgSlot("i32", n), ArgSlot("i32", 16)])
+
+    def hist_check():
+        want = torch.bincount((tp % 16).long(), minlength=16)
+        return bool(torch.equal(tc.long(), want))
+    cases.append(Case("hist", "hist_range", 4 * n, n, "pixel",
+                      [(routines.get("hist"), Dim3(n // 256), Dim3(256), 0, pk)], check=hist_check,
+                      reset=lambda: tc.zero_()))
+
+    # --- hist_stride: one block of 256 threads, k = n / 256 strides ------------
+    pk = PackedArgs([ArgSlot("handle", pix), ArgSlot("handle", cnt), ArgSlot("i32", n // 256),
+                     ArgSlot("i32", 16)])
+    cases.append(Case("hist_stride", "hist_range", 4 * n, n, "pixel",
+                      [(routines.get("hist_stride"), Dim3(1), Dim3(256), 0, pk)], check=hist_check,
+                      reset=lambda: tc.zero_(),
+                      note="grid 1 x 256 threads: the single logical block is spread over all SMs"))
+
+    # --- reduce: per-block sums, block 256 ------------------------------------
+    rout = alloc("i32", n // 256)
+    to = _t(arena, rout, torch, device)
+    pk = PackedArgs([ArgSlot("handle", pix), ArgSlot("handle", rout), ArgSlot("i32", n)])
+
+    def reduce_check():
+        want = tp.view(-1, 256).long().sum(1)
+        want = ((want + 2**31) % 2**32 - 2**31).int()
+        return bool(torch.equal(to, want))
+    cases.append(Case("reduce", "reduce_warp", 4 * n + 4 * (n // 256), n, "elem",
+                      [(routines.get("reduce"), Dim3(n // 256), Dim3(256), 0, pk)], check=reduce_check))
+
+    # --- wreduce (warp mode, warp 32), block 256 ------------------------------
+    wout = alloc("i32", 1)
+    tw = _t(arena, wout, torch, device)
+    pk = PackedArgs([ArgSlot("handle", pix), ArgSlot("handle", wout), ArgSlot("i32", n)])
+
+    def wreduce_check():
+        s = int(tp.long().sum().item())
+        return int(tw.item()) == ((s + 2**31) % 2**32 - 2**31)
+    cases.append(Case("wreduce", "wreduce_blocks", 4 * n, n, "elem",
+                      [(routines.get("wreduce", warp_size=32), Dim3(n // 256), Dim3(256), 0, pk)],
+                      check=wreduce_check, reset=lambda: tw.zero_()))
+
+    # --- fir: 1 block x 256 threads, m = n/256 strides, 8 taps ----------------
+    taps = 8
+    fx = alloc("f32", n + taps)
+    fy = alloc("f32", n)
+    fw = alloc("f32", taps)
+    tfx = _t(arena, fx, torch, device)
+    tfx.uniform_(-1, 1, generator=g)
+    tfw = _t(arena, fw, torch, device)
+    tfw.uniform_(-1, 1, generator=g)
+    tfy = _t(arena, fy, torch, device)
+    pk = PackedArgs([ArgSlot("handle", fx), ArgSlot("handle", fy), ArgSlot("handle", fw),
+                     ArgSlot("i32", taps), ArgSlot("i32", n // 256)])
+
+    def fir_check():
+        k = 1 << 20
+        acc = torch.zeros(k, dtype=torch.float64, device=device)
+        for i in range(taps):
+            acc = acc + tfw[i].double() * tfx[i:i + k].double()
+        return bool(torch.equal(tfy[:k], acc.float()))
+    cases.append(Case("fir", "fir_tile", 8 * n + 4 * (taps - 1), n, "output",
+                      [(routines.get("fir"), Dim3(1), Dim3(256), 0, pk)], check=fir_check,
+                      note="grid 1 x 256 threads, 8 taps"))
+
+    # --- kmeans: 16M points x 32 features, k = 16 -----------------------------
+    npts, nf, k = 1 << 24, 32, 16
+    kf = alloc("f32", npts * nf)
+    kc = alloc("f32", k * nf)
+    km = alloc("i32", npts)
+    ks = alloc("f32", k * nf)
+    kn = alloc("i32", k)
+    tkf = _t(arena, kf, torch, device)
+    tkf.uniform_(0, 1, generator=g)
+    tkc = _t(arena, kc, torch, device)
+    tkc.copy_(tkf.view(nf, npts)[:, :k].t().contiguous().view(-1))
+    tks, tkn = _t(arena, ks, torch, device), _t(arena, kn, torch, device)
+    pk = PackedArgs([ArgSlot("handle", kf), ArgSlot("handle", kc), ArgSlot("handle", km),
+                     ArgSlot("handle", ks), ArgSlot("handle", kn), ArgSlot("i32", npts),
+                     ArgSlot("i32", nf), ArgSlot("i32", k)])
+
+    def km_reset():
+        tks.zero_()
+        tkn.zero_()
+    cases.append(Case("kmeans", "kmeans_assign", npts * (4 * nf + 4), npts, "point",
+                      [(routines.get("kmeans"), Dim3(npts // 256), Dim3(256), 0, pk)],
+                      check=lambda: int(tkn.long().sum().item()) == npts, reset=km_reset,
+                      note="16M x 32 f32, k=16: one assignment + accumulation pass; f64 distances"))
+    return cases
+
+
+def bfs_case(arena, torch, device, log_v: int = 26, deg: int = 8) -> Case:
+    """BFS over a random graph (2^log_v vertices x deg out-edges), full
+    traversal from vertex 0: one `bfs` launch per level plus a 4-byte read of
+    the changed flag (Rodinia's host loop)."""
+    from paper_2206_07896_b200 import ArgSlot, Dim3, PackedArgs, routines
+
+    nv = 1 << log_v
+    ne = nv * deg
+    row = arena.alloc("i32", nv + 1)
+    col = arena.alloc("i32", ne)
+    lvl = arena.alloc("i32", nv)
+    chg = arena.alloc("i32", 1)
+    g = torch.Generator(device=device)
+    g.manual_seed(99)
+    trow = _t(arena, row, torch, device)
+    trow.copy_(torch.arange(0, nv + 1, dtype=torch.int64, device=device).mul_(deg).int())
+    tcol = _t(arena, col, torch, device)
+    tcol.random_(0, nv, generator=g)
+    tl = _t(arena, lvl, torch, device)
+    tch = _t(arena, chg, torch, device)
+    routine = routines.get("bfs")
+    levels = {"n": 0}
+
+    def reset():
+        tl.fill_(-1)
+        tl[0] = 0
+
+    def step(rt, stream):
+        cur = 0
+        while True:
+            arena.fill_value(chg, 0)  # synchronous, ordered before the launch
+            pk = PackedArgs([ArgSlot("handle", row), ArgSlot("handle", col), ArgSlot("handle", lvl),
+                             ArgSlot("handle", chg), ArgSlot("i32", nv), ArgSlot("i32", cur)])
+            rt.launch(routine, Dim3(nv // 256), Dim3(256), 0, pk)
+            rt.device_synchronize()
+            if int(tch.item()) == 0:
+                break
+            cur += 1
+        levels["n"] = cur + 1
+        return cur + 1
+
+    def check():
+        lv = tl.long()
+        src = torch.repeat_interleave(torch.arange(nv, device=device), deg)
+        dst = tcol.long()
+        lu, lw = lv[src], lv[dst]
+        ok = bool((lv[0] == 0).item())
+        # every edge out of a reached vertex reaches its target within +1
+        ok &= bool(((lu < 0) | ((lw >= 0) & (lw <= lu + 1))).all().item())
+        # every reached vertex at level L > 0 has an in-edge from level L-1
+        has_pred = torch.zeros(nv, dtype=torch.bool, device=device)
+        m = (lu >= 0) & (lw == lu + 1)
+        has_pred[dst[m]] = True
+        ok &= bool(((lv <= 0) | has_pred).all().item())
+        return ok
+
+    c = Case("bfs", "bfs_step", 4 * ne + 12 * nv, ne, "edge", [], host_loop=step, reset=reset,
+             check=check, note=f"2^{log_v} vertices x {deg} random out-edges, full traversal; "
+                               "bytes = compulsory 4|E| + 12|V|, elem = edges (TEPS)")
+    c.levels = levels
+    return c
+
+
+def time_case(case: Case, rt, torch, stream, reps: int, warmup: int) -> dict:
+    """Device time per step (events on the worker stream) and per launch."""
+    def issue():
+        if case.host_loop is not None:
+            return case.host_loop(rt, stream)
+        for launch in case.launches:
+            rt.launch(*launch)
+        return len(case.launches)
+
+    for _ in range(warmup):
+        if case.reset:
+            case.reset()
+            torch.cuda.synchronize()
+        issue()
+    rt.device_synchronize()
+    torch.cuda.synchronize()
+    times = []
+    nlaunch = 0
+    for _ in range(reps):
+        if case.reset:
+            case.reset()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(stream)
+        nlaunch = issue()
+        b.record(stream)
+        rt.device_synchronize()
+        b.synchronize()
+        wall = time.perf_counter() - t0
+        times.append((a.elapsed_time(b) * 1e-3, wall))
+    ok = None
+    if case.check is not None:
+        try:
+            ok = bool(case.check())
+        except Exception as e:  # a failed check is reported, never hidden
+            ok = f"check error: {e!r}"
+    dev = statistics.median(t for t, _ in times)
+    wall = statistics.median(w for _, w in times)
+    return {"dev_s": dev, "wall_s": wall, "launches": nlaunch, "checked": ok}
+
+
+def cpu_sample(name: str, threads: int, budget: float = 0.5) -> Optional[dict]:
+    """Oracle port (oracle/oracle.c) throughput on a bounded sample of the
+    same kernel, in elements/s; one thread unless the kernel's blocks are
+    independent (nn, hotspot use OpenMP)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import random
+
+    import instances as I
+    import numpy as np
+    import oracle
+
+    rng = random.Random(5)
+    if name in ("vecadd", "vecadd_pr1"):
+        n = 1 << 22
+        inst = I.vecadd(rng)
+        inst.grid, inst.block = I.Geom(n // 256), I.Geom(256)
+        a = np.random.default_rng(1).uniform(-1, 1, n).astype(np.float32)
+        inst.buffers = [I.Buf("a", "f32", n, a), I.Buf("b", "f32", n, a), I.Buf("c", "f32", n, np.zeros(n, np.float32))]
+        inst.args[3] = ("i32", n)
+        elems, nt = n, 1
+    elif name == "nn":
+        n = 1 << 22
+        inst = I.nn(n, 256)
+        elems, nt = n, threads
+    elif name in ("hist", "hist_stride", "reduce", "wreduce"):
+        n = 1 << 22
+        pix = np.random.default_rng(2).integers(0, 1 << 16, n).astype(np.int32)
+        if name == "hist":
+            inst = I.Instance("hist", I.Geom(n // 256), I.Geom(256), 0,
+                              [I.Buf("pix", "i32", n, pix), I.Buf("counts", "i32", 16, np.zeros(16, np.int32))],
+                              [("buf", "pix"), ("buf", "counts"), ("i32", n), ("i32", 16)], ["counts"])
+        elif name == "hist_stride":
+            inst = I.Instance("hist_stride", I.Geom(1), I.Geom(256), 0,
+                              [I.Buf("pix", "i32", n, pix), I.Buf("counts", "i32", 16, np.zeros(16, np.int32))],
+                              [("buf", "pix"), ("buf", "counts"), ("i32", n // 256), ("i32", 16)], ["counts"])
+        elif name == "reduce":
+            inst = I.Instance("reduce", I.Geom(n // 256), I.Geom(256), 0,
+                              [I.Buf("x", "i32", n, pix), I.Buf("out", "i32", n // 256, np.zeros(n // 256, np.int32))],
+                              [("buf", "x"), ("buf", "out"), ("i32", n)], ["out"])
+        else:
+            inst = I.Instance("wreduce", I.Geom(n // 256), I.Geom(256), 0,
+                              [I.Buf("x", "i32", n, pix), I.Buf("out", "i32", 1, np.zeros(1, np.int32))],
+                              [("buf", "x"), ("buf", "out"), ("i32", n)], ["out"])
+        elems, nt = n, 1
+    elif name == "fir":
+        m = 1 << 14
+        x = np.random.default_rng(3).uniform(-1, 1, m * 256 + 8).astype(np.float32)
+        w = np.random.default_rng(4).uniform(-1, 1, 8).astype(np.float32)
+        inst = I.Instance("fir", I.Geom(1), I.Geom(256), 0,
+                          [I.Buf("x", "f32", x.size, x), I.Buf("y", "f32", m * 256, np.zeros(m * 256, np.float32)),
+                           I.Buf("w", "f32", 8, w)],
+                          [("buf", "x"), ("buf", "y"), ("buf", "w"), ("i32", 8), ("i32", m)], ["y"])
+        elems, nt = m * 256, 1
+    elif name == "kmeans":
+        inst = I.kmeans(1 << 15, 32, 16, 256)
+        elems, nt = 1 << 15, 1
+    elif name == "bfs":
+        nv = 1 << 20
+        row, col = I.random_graph(nv, 8, 1)
+        t0 = time.perf_counter()
+        oracle.bfs_full(row, col, nv, 0)
+        dt = time.perf_counter() - t0
+        return {"elem_per_s": col.size / dt, "cores": 1, "kind": "port",
+                "sample": f"bfs 2^20 vertices x 8, frontier-queue restatement, {dt:.2f} s"}
+    else:
+        return None
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.run(inst, nthreads=nt)
+        reps += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"elem_per_s": elems / dt, "cores": nt, "kind": "port",
+            "sample": f"{name} {elems} elements, oracle/oracle.c, {reps} run(s) of {dt:.3f} s"}
+
+
+def python_reference_sample(budget_elems: int = 1 << 14) -> Optional[dict]:
+    """The unmodified reference runtime (blockfuse, pure Python thread pool)
+    on vecadd 2^14 elements, pool = host cores: the CPU runtime itself."""
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "blockfuse" / "__init__.py").exists() and str(p) not in sys.path:
+            sys.path.append(str(p))
+            break
+    try:
+        import random
+
+        from blockfuse.bench import CORPUS, materialize
+        from blockfuse.runtime import Runtime
+        from blockfuse.arena import DeviceArena
+        from blockfuse.syntax import Dim3
+    except Exception:
+        return None
+    case = CORPUS["vecadd"]
+    inst = case.random_instance(random.Random(1))
+    n = budget_elems
+    inst.grid, inst.block = Dim3(n // 256), Dim3(256)
+    for b in inst.buffers:
+        b.length = n
+        b.values = [0.5] * n
+    inst.args[3] = ("i32", n)
+    arena = DeviceArena()
+    packed, _ = materialize(inst, arena)
+    pool = len(os.sched_getaffinity(0))
+    mk = case.compiled()
+    t0 = time.perf_counter()
+    with Runtime(arena, pool_size=pool) as rt:
+        rt.launch(mk, inst.grid, inst.block, 0, packed)
+        rt.device_synchronize()
+    dt = time.perf_counter() - t0
+    return {"elem_per_s": n / dt, "gbs": 12 * n / dt / 1e9, "cores": pool, "kind": "reference",
+            "sample": f"blockfuse Runtime, vecadd {n} elements, pool {pool}, {dt:.2f} s"}
