@@ -23,40 +23,82 @@ __device__ __forceinline__ long long bfs_block_of_x(const KDesc& d, long long x)
   return d.first + ((x - x0) % d.gx + d.gx) % d.gx;
 }
 
+// Expand frontier vertex u: edges in chunks of 8 with all col loads, then all
+// lvl loads, in flight together (random reads dominate this kernel).
+__device__ __forceinline__ bool bfs_expand(const int* __restrict__ row, long long lr,
+                                           const int* __restrict__ col, long long lcol, int* lvl,
+                                           long long ll, long long u, int cur, bool& bad) {
+  if (u + 1 >= lr) {
+    bad = true;
+    return false;
+  }
+  const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
+  bool any = false;
+  for (int e = e0; e < e1; e += 8) {
+    int v[8], lv[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      v[i] = -1;
+      if (e + i < e1) {
+        if (e + i < 0 || e + i >= lcol) bad = true; else v[i] = __ldg(col + e + i);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      lv[i] = 0;
+      if (e + i < e1 && e + i >= 0 && e + i < lcol) {
+        if (v[i] < 0 || v[i] >= ll) bad = true; else lv[i] = lvl[v[i]];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      if (lv[i] == -1 && e + i < e1 && v[i] >= 0 && v[i] < ll) {
+        lvl[v[i]] = (int)((unsigned)cur + 1u);
+        any = true;
+      }
+    }
+    if (bad) break;
+  }
+  return any;
+}
+
+// One thread per 4 consecutive vertices: the frontier test reads lvl as int4.
 __global__ void __launch_bounds__(256) bfs_step(const int* __restrict__ row, long long lr,
                                                 const int* __restrict__ col, long long lcol,
                                                 int* lvl, long long ll, int* changed,
                                                 long long lch, long long lo, long long hi, int cur,
                                                 int bx, KDesc k) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  bool any = false;
-  for (long long u = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; u < hi; u += stride) {
-    if (u >= ll) {
-      record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
-      continue;
-    }
-    if (lvl[u] != cur) continue;
-    if (u + 1 >= lr) {
-      record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
-      continue;
-    }
-    const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
-    for (int e = e0; e < e1; e++) {
-      if (e < 0 || e >= lcol) {
-        record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
-        break;
+  bool any = false, bad = false;
+  long long bad_u = -1;
+  const bool vec = (lo % 4 == 0) && hi <= ll;
+  const long long groups = (hi - lo + 3) / 4;
+  for (long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += stride) {
+    const long long u0 = lo + 4 * gi;
+    int l4[4];
+    if (vec && u0 + 3 < hi) {
+      const int4 t = *reinterpret_cast<const int4*>(lvl + u0);
+      l4[0] = t.x; l4[1] = t.y; l4[2] = t.z; l4[3] = t.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const long long u = u0 + q;
+        l4[q] = (u < hi && u < ll) ? lvl[u] : INT_MIN;
+        if (u < hi && u >= ll && bad_u < 0) bad_u = u;
       }
-      const int v = __ldg(col + e);
-      if (v < 0 || v >= ll) {
-        record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, u / bx));
-        break;
-      }
-      if (lvl[v] == -1) {
-        lvl[v] = (int)((unsigned)cur + 1u);
-        any = true;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const long long u = u0 + q;
+      if (u < hi && l4[q] == cur) {
+        bool b = false;
+        any |= bfs_expand(row, lr, col, lcol, lvl, ll, u, cur, b);
+        if (b && bad_u < 0) bad_u = u;
       }
     }
   }
+  if (bad_u >= 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, bad_u / bx));
+  (void)bad;
   if (__syncthreads_or(any) && threadIdx.x == 0) {
     if (lch < 1) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, k.first);
     else changed[0] = 1;
@@ -84,7 +126,7 @@ static int launch_bfs(LaunchCtx& ctx) {
   for (auto& xi : ctx.x_intervals()) {
     long long lo = xi.first * bx, hi = std::min(xi.second * bx, nv);
     if (lo >= hi) continue;
-    int grid = stream_grid(hi - lo, 256 * 4, ctx.num_sms, 8);
+    int grid = stream_grid((hi - lo + 3) / 4, 256, ctx.num_sms, 8);
     bfs_step<<<grid, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len,
                                            (int*)L.ptr, L.len, (int*)Ch.ptr, Ch.len, lo, hi, cur,
                                            (int)bx, ctx.desc());

@@ -126,7 +126,9 @@ __device__ __forceinline__ int warp_sum(int v) {
   return v;
 }
 
-// one warp per logical block x; loads coalesced; m == 1
+// one warp per logical block x; loads coalesced (int4 when the block's
+// slice is 16 B aligned); m == 1
+template <bool VEC>
 __global__ void __launch_bounds__(256) reduce_warp(const int* __restrict__ x, long long lx,
                                                    int* __restrict__ out, long long lout, int n,
                                                    long long x0, long long x1, KDesc k) {
@@ -142,7 +144,17 @@ __global__ void __launch_bounds__(256) reduce_warp(const int* __restrict__ x, lo
       continue;
     }
     unsigned s = 0;
-    for (long long i = lo + lane; i < hi; i += 32) s += (unsigned)__ldg(x + i);
+    if (VEC) {  // lo % 4 == 0
+      const int4* x4 = reinterpret_cast<const int4*>(x + lo);
+      const long long nv = (hi - lo) / 4;
+      for (long long i = lane; i < nv; i += 32) {
+        const int4 v = __ldcs(x4 + i);
+        s += (unsigned)v.x + (unsigned)v.y + (unsigned)v.z + (unsigned)v.w;
+      }
+      for (long long i = lo + nv * 4 + lane; i < hi; i += 32) s += (unsigned)x[i];
+    } else {
+      for (long long i = lo + lane; i < hi; i += 32) s += (unsigned)__ldg(x + i);
+    }
     int v = warp_sum((int)s);
     if (lane == 0) out[bx] = v;
   }
@@ -197,8 +209,12 @@ static int launch_reduce(LaunchCtx& ctx) {
     long long nx = xi.second - xi.first;
     if (m == 1) {
       int grid = stream_grid(nx, 8, ctx.num_sms, 8);
-      reduce_warp<<<grid, 256, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr, O.len, n,
-                                                xi.first, xi.second, ctx.desc());
+      if (bx % 4 == 0)
+        reduce_warp<true><<<grid, 256, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr,
+                                                        O.len, n, xi.first, xi.second, ctx.desc());
+      else
+        reduce_warp<false><<<grid, 256, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr,
+                                                         O.len, n, xi.first, xi.second, ctx.desc());
     } else {
       int grid = (int)std::min<long long>(nx, (long long)ctx.num_sms * 8);
       reduce_tree<<<grid, bx, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr, O.len, n,
@@ -222,14 +238,60 @@ __device__ __forceinline__ int c_mod(int a, int b) {
   return b == -1 ? 0 : a % b;  // C remainder, truncating toward zero
 }
 
+// a % nbins for a >= 0 by multiply-high (Granlund-Montgomery, divisor
+// |nbins| fixed per launch); negative a (C remainder is negative: the bin
+// traps) takes the hardware path.
+struct FastMod {
+  unsigned d, m;
+  int s1, s2;
+  int nbins;
+};
+
+static FastMod make_fastmod(int nbins) {
+  FastMod f;
+  f.nbins = nbins;
+  unsigned long long d = nbins < 0 ? (unsigned long long)(-(long long)nbins) : (unsigned long long)nbins;
+  f.d = (unsigned)d;
+  int l = 0;
+  while ((1ull << l) < d) l++;
+  f.m = (unsigned)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+  f.s1 = l < 1 ? l : 1;
+  f.s2 = l > 1 ? l - 1 : 0;
+  return f;
+}
+
+__device__ __forceinline__ int fast_mod(int a, const FastMod& f) {
+  if (a < 0) return c_mod(a, f.nbins);
+  const unsigned n = (unsigned)a;
+  const unsigned t = __umulhi(n, f.m);
+  const unsigned q = (t + ((n - t) >> f.s1)) >> f.s2;
+  return (int)(n - q * f.d);
+}
+
 template <int MODE>  // 0: per-lane counters, 1: CTA shared atomics, 2: global atomics
+__device__ __forceinline__ void hist_add(unsigned* sh, unsigned* mine, int* counts, long long lc,
+                                         int b, unsigned copies, bool& bad) {
+  if (b < 0 || b >= lc) {
+    bad = true;
+    return;
+  }
+  if (MODE == 0) {
+    mine[b * 32] += copies;
+  } else if (MODE == 1) {
+    atomicAdd(sh + b, copies);
+  } else {
+    atomicAdd((unsigned*)counts + b, copies);
+  }
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, int* counts,
                                                   long long lc, long long lo, long long hi,
-                                                  int nbins, unsigned copies, KDesc k,
+                                                  FastMod fm, unsigned copies, KDesc k,
                                                   long long xbase, int bx_div) {
   extern __shared__ unsigned sh[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nb = nbins < 0 ? -nbins : nbins;  // |nbins| bounds the remainder
+  const int nb = (int)fm.d;  // |nbins| bounds the remainder
   if (MODE == 0) {
     for (int i = threadIdx.x; i < 8 * kHistLaneBins * 32; i += blockDim.x) sh[i] = 0;
   } else if (MODE == 1) {
@@ -237,21 +299,44 @@ __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, i
   }
   __syncthreads();
   unsigned* mine = sh + warp * (kHistLaneBins * 32) + lane;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
-    int b = c_mod(__ldcs(pix + i), nbins);
-    if (b < 0 || b >= lc) {
-      long long blk = bx_div > 0 ? block_of_x(k, xbase + (i - lo) / bx_div) : k.first;
-      record_fault(k, BF_TRAP_OUT_OF_BOUNDS, blk);
-      continue;
+  bool bad = false;
+  // scalar head to a 16 B boundary, int4 body (4 loads in flight), scalar tail
+  long long vlo = (lo + 3) & ~3LL;
+  if (vlo > hi) vlo = hi;
+  long long vhi = hi & ~3LL;
+  if (vhi < vlo) vhi = vlo;
+  if (tid < vlo - lo) hist_add<MODE>(sh, mine, counts, lc, fast_mod(pix[lo + tid], fm), copies, bad);
+  if (tid < hi - vhi) hist_add<MODE>(sh, mine, counts, lc, fast_mod(pix[vhi + tid], fm), copies, bad);
+  const int4* p4 = reinterpret_cast<const int4*>(pix);
+  const long long end = vhi / 4;
+  long long g = vlo / 4 + tid;
+  for (; g + 3 * stride < end; g += 4 * stride) {
+    int4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = __ldcs(p4 + g + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].x, fm), copies, bad);
+      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].y, fm), copies, bad);
+      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].z, fm), copies, bad);
+      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].w, fm), copies, bad);
     }
-    if (MODE == 0) {
-      mine[b * 32] += copies;
-    } else if (MODE == 1) {
-      atomicAdd(sh + b, copies);
-    } else {
-      atomicAdd((unsigned*)counts + b, copies);
-    }
+  }
+  for (; g < end; g += stride) {
+    const int4 v = __ldcs(p4 + g);
+    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.x, fm), copies, bad);
+    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.y, fm), copies, bad);
+    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.z, fm), copies, bad);
+    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.w, fm), copies, bad);
+  }
+  if (bad) {
+    // exact block of the first bad pixel is not tracked on this path: the
+    // fetch's first block whose range holds one is reported (kind is exact)
+    long long blk = k.first;
+    if (bx_div > 0) blk = block_of_x(k, xbase + ((vlo > lo ? lo : vlo) - lo) / bx_div);
+    record_fault(k, BF_TRAP_OUT_OF_BOUNDS, blk);
   }
   if (MODE == 2) return;
   __syncthreads();
@@ -272,8 +357,9 @@ __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, i
 static int hist_issue(LaunchCtx& ctx, const ArgVal& P, const ArgVal& Cn, long long lo, long long hi,
                       int nbins, unsigned copies, long long xbase, int bx_div) {
   if (lo >= hi) return BF_OK;
-  int nb = nbins < 0 ? -nbins : nbins;
-  int grid = stream_grid(hi - lo, 256 * 16, ctx.num_sms, 4);
+  const FastMod fm = make_fastmod(nbins);
+  const long long nb = fm.d;
+  int grid = stream_grid(hi - lo, 256 * 16, ctx.num_sms, 6);
   KDesc d = ctx.desc();
   if (nb <= kHistLaneBins) {
     size_t smem = 8 * kHistLaneBins * 32 * sizeof(unsigned);  // 8 warps x 32 bins x 32 lanes
@@ -283,13 +369,13 @@ static int hist_issue(LaunchCtx& ctx, const ArgVal& P, const ArgVal& Cn, long lo
       attr = true;
     }
     hist_range<0><<<grid, 256, smem, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi,
-                                                  nbins, copies, d, xbase, bx_div);
+                                                  fm, copies, d, xbase, bx_div);
   } else if (nb <= kHistSmemBins) {
     hist_range<1><<<grid, 256, nb * sizeof(unsigned), ctx.stream>>>(
-        (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, nbins, copies, d, xbase, bx_div);
+        (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, fm, copies, d, xbase, bx_div);
   } else {
     hist_range<2><<<grid, 256, 0, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi,
-                                                nbins, copies, d, xbase, bx_div);
+                                                fm, copies, d, xbase, bx_div);
   }
   BF_CUDA_LAUNCH_CHECK(ctx);
   return BF_OK;
@@ -390,6 +476,55 @@ __global__ void __launch_bounds__(256) fir_tile(const float* __restrict__ x,
   }
 }
 
+// taps <= 13: each thread computes 4 consecutive outputs from a window of
+// <= 16 x values read as aligned float4 (neighbouring threads' windows
+// overlap in L1); w lives in registers as doubles.
+constexpr int kFirRegTaps = 13;
+
+__global__ void __launch_bounds__(256) fir_reg(const float* __restrict__ x, long long lx,
+                                               float* __restrict__ y,
+                                               const float* __restrict__ w, int taps,
+                                               long long nout) {
+  double wd[kFirRegTaps];
+#pragma unroll
+  for (int i = 0; i < kFirRegTaps; i++) wd[i] = i < taps ? (double)__ldg(w + i) : 0.0;
+  const int nvec = (3 + taps + 3) / 4;  // float4 chunks covering 3 + taps floats
+  const long long groups = (nout + 3) / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+    const long long o = 4 * g;
+    float xv[16];
+    if (o + 4 * nvec <= lx) {
+      const float4* x4 = reinterpret_cast<const float4*>(x + o);
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (j < nvec) {
+          const float4 v = __ldg(x4 + j);
+          xv[4 * j] = v.x; xv[4 * j + 1] = v.y; xv[4 * j + 2] = v.z; xv[4 * j + 3] = v.w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j++) xv[j] = (o + j < lx) ? __ldg(x + o + j) : 0.f;
+    }
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < kFirRegTaps; i++) {
+      if (i < taps) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[q] = fma(wd[i], (double)xv[q + i], acc[q]);
+      }
+    }
+    if (o + 3 < nout) {
+      __stcs(reinterpret_cast<float4*>(y + o),
+             make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]));
+    } else {
+      for (int q = 0; q < 4; q++)
+        if (o + q < nout) y[o + q] = (float)acc[q];
+    }
+  }
+}
+
 static int launch_fir(LaunchCtx& ctx) {
   const ArgVal& X = ctx.args[0];
   const ArgVal& Y = ctx.args[1];
@@ -406,6 +541,13 @@ static int launch_fir(LaunchCtx& ctx) {
   int t = taps > 0 ? taps : 0;
   if (nout > Y.len || (t > 0 && (t > W.len || nout + t - 1 > X.len))) {
     ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first, "fir index out of range");
+    return BF_OK;
+  }
+  if (t <= kFirRegTaps) {
+    int grid = stream_grid((nout + 3) / 4, 256 * 4, ctx.num_sms, 8);
+    fir_reg<<<grid, 256, 0, ctx.stream>>>((const float*)X.ptr, X.len, (float*)Y.ptr,
+                                          (const float*)W.ptr, t, nout);
+    BF_CUDA_LAUNCH_CHECK(ctx);
     return BF_OK;
   }
   if (t + kFirTile > 48 * 1024 / 4) {
@@ -475,6 +617,47 @@ __global__ void __launch_bounds__(1024) wreduce_blocks(const int* __restrict__ x
   }
 }
 
+// Fast path (1D blocks, blockDim.x % 32 == 0, warp_size 32): every logical
+// warp is full, so lane 0's clamped shuffle chain yields exactly its warp's
+// sum and lane 0 is the only lane with threadIdx.x % 32 == 0: the launch adds
+// sum(x[id], id in the covered range, id < n) to out[0].  Streamed with int4
+// loads; one atomic per CTA.
+__global__ void __launch_bounds__(256) sum_range(const int* __restrict__ x, int* out,
+                                                 long long lo, long long hi, unsigned copies) {
+  __shared__ unsigned part[8];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned s = 0;
+  long long vlo = (lo + 3) & ~3LL;
+  if (vlo > hi) vlo = hi;
+  long long vhi = hi & ~3LL;
+  if (vhi < vlo) vhi = vlo;
+  if (tid < vlo - lo) s += (unsigned)x[lo + tid];
+  if (tid < hi - vhi) s += (unsigned)x[vhi + tid];
+  const int4* x4 = reinterpret_cast<const int4*>(x);
+  const long long end = vhi / 4;
+  long long g = vlo / 4 + tid;
+  for (; g + 3 * stride < end; g += 4 * stride) {
+    int4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = __ldcs(x4 + g + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; u++) s += (unsigned)v[u].x + (unsigned)v[u].y + (unsigned)v[u].z + (unsigned)v[u].w;
+  }
+  for (; g < end; g += stride) {
+    const int4 v = __ldcs(x4 + g);
+    s += (unsigned)v.x + (unsigned)v.y + (unsigned)v.z + (unsigned)v.w;
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) t += part[i];
+    if (t) atomicAdd((unsigned*)out, t * copies);
+  }
+}
+
 static int launch_wreduce(LaunchCtx& ctx) {
   const ArgVal& X = ctx.args[0];
   const ArgVal& O = ctx.args[1];
@@ -485,6 +668,26 @@ static int launch_wreduce(LaunchCtx& ctx) {
     return BF_E_UNSUPPORTED;
   }
   long long B = (long long)ctx.block[0] * ctx.block[1] * ctx.block[2];
+  const long long bx = ctx.block[0];
+  if (ws == 32 && B == bx && bx % 32 == 0 && O.len >= 1 &&
+      (long long)ctx.grid[0] * bx - 1 <= INT_MAX) {
+    for (auto& pc : x_pieces(ctx)) {
+      long long lo = pc.x0 * bx, hi = std::min<long long>(pc.x1 * bx, n);
+      if (lo >= hi) continue;
+      if (hi > X.len) {
+        long long bad = std::max<long long>(lo, X.len);
+        ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first_block_with_x(bad / bx),
+                      "load index " + std::to_string(bad) + " out of range");
+        hi = X.len;
+        if (lo >= hi) continue;
+      }
+      int grid = stream_grid((hi - lo + 3) / 4, 256 * 4, ctx.num_sms, 8);
+      sum_range<<<grid, 256, 0, ctx.stream>>>((const int*)X.ptr, (int*)O.ptr, lo, hi,
+                                              (unsigned)pc.copies);
+      BF_CUDA_LAUNCH_CHECK(ctx);
+    }
+    return BF_OK;
+  }
   int threads = (int)std::min<long long>(1024, ((B + 31) / 32) * 32);
   int grid = (int)std::min<long long>(ctx.count, (long long)ctx.num_sms * 16);
   wreduce_blocks<<<grid, threads, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr, O.len, n,

@@ -86,6 +86,141 @@ __global__ void __launch_bounds__(256) kmeans_assign(const float* __restrict__ f
     if (ssum[i] != 0.f) atomicAdd(sums + i, ssum[i]);
 }
 
+// Fast path (nf <= 32, k*nf <= 1024): membership by an f32 screen with an
+// exact f64 re-check of near-ties, sums by a warp transpose.
+//
+// Screen: for the argmin only s_c = |c|^2 - 2 f.c matters (|f|^2 is common).
+// In f32 with FMA, |s_c(f32) - s_c| <= E_c = (nf+4) 2^-22 (2 |f| |c| + |c|^2)
+// (dot-product error bound with Cauchy-Schwarz, plus the rounding of |c|^2),
+// orders of magnitude above the reference's own f64 rounding.  If the
+// screen's argmin i1 satisfies  s_c - E_c > s_i1 + E_i1  for every other c,
+// the reference's f64 scan (`c == 0 || dist < bestd`) returns i1 too;
+// otherwise (near-ties, exact ties, non-finite values) the point is re-scanned
+// with the reference's exact f64 recurrence.  Membership stays bit-exact.
+// Sums: each warp transposes its 32 points x nf features through shared
+// memory so lane j owns feature j, then adds point q's feature j into its
+// private per-warp row for cluster best_q (no atomics, no bank conflicts).
+constexpr int kKmWarps = 8;
+
+__global__ void __launch_bounds__(256) kmeans_fast(const float* __restrict__ f,
+                                                   const float* __restrict__ cent,
+                                                   int* __restrict__ member, float* sums,
+                                                   int* counts, int npts, int nf, int k,
+                                                   long long lo, long long hi) {
+  extern __shared__ float smf[];
+  const int kc = k > 0 ? k : 1;
+  float* cf = smf;                         // [kc*nf] centroids (f32 as stored)
+  float* cA = cf + kc * nf;                // [kc] error slope  (x |f|)
+  float* cB = cA + kc;                     // [kc] error offset
+  float* cn2 = cB + kc;                    // [kc] |c|^2 in f32
+  float* tile = cn2 + kc;                  // [8][32][33] transpose tiles
+  float* wsum = tile + kKmWarps * 32 * 33; // [8][kc*nf] per-warp sums
+  int* cnt = reinterpret_cast<int*>(wsum + kKmWarps * kc * nf);  // [kc]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < k * nf; i += blockDim.x) cf[i] = cent[i];
+  for (int i = threadIdx.x; i < kKmWarps * kc * nf; i += blockDim.x) wsum[i] = 0.f;
+  for (int i = threadIdx.x; i < kc; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const float errk = (float)(nf + 4) * 2.384185791015625e-7f * 1.01f;  // (nf+4) 2^-22, +1 %
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    float n2 = 0.f;
+    for (int l = 0; l < nf; l++) n2 = fmaf(cf[c * nf + l], cf[c * nf + l], n2);
+    cn2[c] = n2;
+    cA[c] = errk * 2.f * sqrtf(n2) * 1.01f;
+    cB[c] = errk * n2 + 1e-30f;
+  }
+  __syncthreads();
+  float* mytile = tile + warp * 32 * 33;
+  float* mysum = wsum + warp * kc * nf;
+  const long long wstride = (long long)gridDim.x * kKmWarps * 32;
+  for (long long base = lo + ((long long)blockIdx.x * kKmWarps + warp) * 32; base < hi; base += wstride) {
+    const long long p = base + lane;
+    const bool valid = p < hi;
+    float fv[32];
+#pragma unroll
+    for (int l = 0; l < 32; l++) fv[l] = (valid && l < nf) ? __ldcs(f + (long long)l * npts + p) : 0.f;
+    int best = 0;
+    if (valid && k > 1) {
+      float fn2 = 0.f;
+#pragma unroll
+      for (int l = 0; l < 32; l++) fn2 = fmaf(fv[l], fv[l], fn2);
+      const float fnorm = sqrtf(fn2) * 1.01f;
+      float tmin = INFINITY, hi1 = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
+      int i1 = 0, lo1i = -1;
+      bool finite = fn2 <= 3.0e38f;
+      for (int c = 0; c < k; c++) {
+        const float* cc = cf + c * nf;
+        float dot = 0.f;
+#pragma unroll
+        for (int l = 0; l < 32; l++)
+          if (l < nf) dot = fmaf(fv[l], cc[l], dot);
+        const float t = fmaf(-2.f, dot, cn2[c]);
+        const float e = fmaf(cA[c], fnorm, cB[c]);
+        finite &= fabsf(t) <= 3.0e38f;
+        if (t < tmin) {
+          tmin = t;
+          i1 = c;
+          hi1 = t + e;
+        }
+        const float l_ = t - e;
+        if (l_ < lo1) {
+          lo2 = lo1;
+          lo1 = l_;
+          lo1i = c;
+        } else if (l_ < lo2) {
+          lo2 = l_;
+        }
+      }
+      const float other = lo1i == i1 ? lo2 : lo1;
+      best = i1;
+      if (!finite || !(other > hi1)) {
+        // exact reference recurrence (kernels/kmeans.kn)
+        double bestd = 0.0;
+        best = 0;
+        for (int c = 0; c < k; c++) {
+          const float* cc = cf + c * nf;
+          double dist = 0.0;
+#pragma unroll
+          for (int l = 0; l < 32; l++) {
+            if (l < nf) {
+              const double diff = dsub((double)fv[l], (double)cc[l]);
+              dist = dadd(dist, dmul(diff, diff));
+            }
+          }
+          if (c == 0 || dist < bestd) {
+            bestd = dist;
+            best = c;
+          }
+        }
+      }
+    }
+    if (valid) {
+      member[p] = best;
+      atomicAdd(cnt + best, 1);
+    }
+    // transpose: lane q's features -> row q of the tile
+#pragma unroll
+    for (int l = 0; l < 32; l++)
+      if (l < nf) mytile[lane * 33 + l] = fv[l];
+    __syncwarp();
+    for (int q = 0; q < 32; q++) {
+      const int bq = __shfl_sync(0xffffffffu, best, q);
+      const bool vq = base + q < hi;
+      if (vq && lane < nf) mysum[bq * nf + lane] += mytile[q * 33 + lane];
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kc * nf; i += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < kKmWarps; w++) t += wsum[w * kc * nf + i];
+    if (t != 0.f) atomicAdd(sums + i, t);
+  }
+  for (int i = threadIdx.x; i < kc; i += blockDim.x)
+    if (cnt[i]) atomicAdd(counts + i, cnt[i]);
+}
+
 static int launch_kmeans(LaunchCtx& ctx) {
   const ArgVal& F = ctx.args[0];
   const ArgVal& Ce = ctx.args[1];
@@ -115,6 +250,22 @@ static int launch_kmeans(LaunchCtx& ctx) {
               hi <= M.len && (long long)kc * nf <= S.len && kc <= Cn.len;
     if (!ok) {
       ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first_block_with_x(xi.first), "kmeans index out of range");
+      continue;
+    }
+    if (nf <= kKmMaxF && kc * nf <= 1024) {
+      size_t smem = sizeof(float) * ((size_t)kc * nf + 3 * kc + kKmWarps * 32 * 33 +
+                                     (size_t)kKmWarps * kc * nf) + sizeof(int) * kc;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(kmeans_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaGetLastError();
+        attr = true;
+      }
+      int grid = stream_grid(hi - lo, 256 * 4, ctx.num_sms, 4);
+      kmeans_fast<<<grid, 256, smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr,
+                                                   (int*)M.ptr, (float*)S.ptr, (int*)Cn.ptr,
+                                                   (int)npts, nf, k, lo, hi);
+      BF_CUDA_LAUNCH_CHECK(ctx);
       continue;
     }
     size_t smem = (size_t)kc * nf * (sizeof(double) + sizeof(float)) + kc * sizeof(int);

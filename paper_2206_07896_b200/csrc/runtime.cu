@@ -348,7 +348,6 @@ static int retire(bf_runtime* rt, bool wait) {
       if (e == cudaErrorNotReady) {
         // fetches on other workers may have finished; keep FIFO simple and
         // scan the rest without blocking
-        bool any = false;
         for (auto it = rt->inflight.begin() + 1; it != rt->inflight.end();) {
           if (cudaEventQuery(it->done) == cudaSuccess) {
             TaskRec& t = rt->tasks[it->task];
@@ -358,13 +357,11 @@ static int retire(bf_runtime* rt, bool wait) {
             rt->busy[it->worker] += it->count;
             rt->event_pool.push_back(it->done);
             it = rt->inflight.erase(it);
-            any = true;
           } else {
             cudaGetLastError();
             ++it;
           }
         }
-        (void)any;
         return BF_OK;
       }
       if (e != cudaSuccess) return cuda_fail(e, "cudaEventQuery");

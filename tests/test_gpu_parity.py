@@ -95,3 +95,91 @@ def test_hotspot_sizes_vs_oracle():
         got, got_trap, _, _ = gpu_run(inst)
         assert trap is None and got_trap is None
         assert bit_equal(got["dst"], want["dst"]), (rows, cols, bx, by)
+
+
+def test_kmeans_vs_oracle_screen_and_ties():
+    """f32 screen + exact f64 re-check: membership and counts bit-exact over
+    shapes that hit the fast path (nf <= 32), the generic path (nf > 32),
+    duplicated centroids (exact ties), tiny k and huge coordinates."""
+    import instances as I
+    cases = [I.kmeans(3000, 32, 16, 256, seed=11), I.kmeans(2000, 7, 5, 128, seed=12),
+             I.kmeans(1500, 33, 4, 256, seed=13), I.kmeans(999, 16, 16, 96, seed=14, dup=True),
+             I.kmeans(500, 3, 1, 64, seed=15), I.kmeans(4096, 32, 16, 256, seed=16, dup=True)]
+    big = I.kmeans(1024, 8, 6, 128, seed=17)
+    f = big.buffer("f")
+    f.values = (np.asarray(f.values) * 1e6 - 3e5).astype(np.float32)  # large, signed
+    c = big.buffer("cent")
+    c.values = np.ascontiguousarray(np.asarray(f.values).reshape(8, 1024)[:, :6].T).reshape(-1)
+    cases.append(big)
+    for k, inst in enumerate(cases):
+        want, trap = oracle.run(inst)
+        got, got_trap, _, _ = gpu_run(inst)
+        assert trap is None and got_trap is None
+        assert bit_equal(got["member"], want["member"]), k
+        assert bit_equal(got["counts"], want["counts"]), k
+        w, g = want["sums"].astype(np.float64), got["sums"].astype(np.float64)
+        assert np.all(np.abs(w - g) <= SUMS_RTOL * np.maximum(np.maximum(abs(w), abs(g)), 1.0)), k
+
+
+def test_bfs_levels_vs_oracle():
+    """Every level launch of several traversals, bit-exact (levels and flag)."""
+    import instances as I
+    for nv, deg, seed in [(5000, 4, 1), (20000, 8, 2), (777, 1, 3), (3000, 13, 4)]:
+        lvl = None
+        for cur in range(200):
+            inst = I.bfs(nv, deg, cur=cur, seed=seed, block=256, lvl=lvl)
+            want, _ = oracle.run(inst)
+            got, got_trap, _, _ = gpu_run(inst)
+            assert got_trap is None
+            assert bit_equal(got["lvl"], want["lvl"]) and bit_equal(got["changed"], want["changed"])
+            lvl = want["lvl"]
+            if want["changed"][0] == 0:
+                break
+
+
+def test_nn_vs_oracle():
+    import instances as I
+    for n, blk, seed in [(100000, 256, 1), (12345, 100, 2), (7, 3, 3)]:
+        inst = I.nn(n, blk, seed=seed, target=(12.5, -77.25))
+        want, _ = oracle.run(inst)
+        got, got_trap, _, _ = gpu_run(inst)
+        assert got_trap is None and bit_equal(got["d"], want["d"])
+
+
+def test_large_random_corpus_vs_oracle():
+    """Bigger-than-golden shapes through the vectorised fast paths."""
+    import instances as I
+    rng = np.random.default_rng(5)
+    n = 1 << 18
+    pix = rng.integers(0, 1 << 16, n).astype(np.int32)
+    for nbins in (16, 7, 32, 33, 1000, 9000):
+        inst = I.Instance("hist", I.Geom(n // 256), I.Geom(256), 0,
+                          [I.Buf("pix", "i32", n, pix), I.Buf("counts", "i32", nbins, np.zeros(nbins, np.int32))],
+                          [("buf", "pix"), ("buf", "counts"), ("i32", n - 5), ("i32", nbins)], ["counts"])
+        want, _ = oracle.run(inst)
+        got, trap, _, _ = gpu_run(inst)
+        assert trap is None and bit_equal(got["counts"], want["counts"]), nbins
+    inst = I.Instance("reduce", I.Geom(n // 256), I.Geom(256), 0,
+                      [I.Buf("x", "i32", n, pix), I.Buf("out", "i32", n // 256, np.zeros(n // 256, np.int32))],
+                      [("buf", "x"), ("buf", "out"), ("i32", n - 3)], ["out"])
+    want, _ = oracle.run(inst)
+    got, trap, _, _ = gpu_run(inst)
+    assert trap is None and bit_equal(got["out"], want["out"])
+    for bx in (256, 96, 100):
+        inst = I.Instance("wreduce", I.Geom(n // bx), I.Geom(bx), 0,
+                          [I.Buf("x", "i32", n, pix), I.Buf("out", "i32", 1, np.zeros(1, np.int32))],
+                          [("buf", "x"), ("buf", "out"), ("i32", n - 77)], ["out"])
+        want, _ = oracle.run(inst)
+        got, trap, _, _ = gpu_run(inst)
+        assert trap is None and bit_equal(got["out"], want["out"]), bx
+    x = rng.uniform(-1, 1, n + 16).astype(np.float32)
+    for taps, bx, m in ((8, 256, 1024), (13, 64, 999), (1, 256, 7), (20, 128, 33)):
+        w = rng.uniform(-1, 1, taps).astype(np.float32)
+        nout = bx * m
+        inst = I.Instance("fir", I.Geom(1), I.Geom(bx), 0,
+                          [I.Buf("x", "f32", nout + taps, x[:nout + taps]),
+                           I.Buf("y", "f32", nout, np.zeros(nout, np.float32)), I.Buf("w", "f32", taps, w)],
+                          [("buf", "x"), ("buf", "y"), ("buf", "w"), ("i32", taps), ("i32", m)], ["y"])
+        want, _ = oracle.run(inst)
+        got, trap, _, _ = gpu_run(inst)
+        assert trap is None and bit_equal(got["y"], want["y"]), taps
