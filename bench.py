@@ -362,10 +362,13 @@ def per_kernel_table(arena, rt, torch, stream, args) -> tuple[dict, int]:
     peaks = _peaks()
     cases = benchkit.build_cases(arena, torch, device, scale=args.kernel_scale)
     if not args.no_bfs:
-        cases.append(benchkit.bfs_case(arena, torch, device, log_v=args.bfs_log_v))
+        cases.extend(benchkit.bfs_case(arena, torch, device, log_v=args.bfs_log_v))
     torch.cuda.synchronize()
     threads = len(os.sched_getaffinity(0))
     table, launches = {}, 0
+    if args.cases:
+        keep = set(args.cases.split(","))
+        cases = [c for c in cases if c.name in keep]
     for c in cases:
         r = benchkit.time_case(c, rt, torch, stream, reps=args.steps, warmup=args.warmup)
         launches += r["launches"] * args.steps
@@ -408,6 +411,7 @@ def main() -> None:
     ap.add_argument("--no-bfs", action="store_true")
     ap.add_argument("--kernel-scale", type=int, default=28, help="log2 elements per kernel case")
     ap.add_argument("--bfs-log-v", type=int, default=26)
+    ap.add_argument("--cases", default="", help="comma list: only these per-kernel cases")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

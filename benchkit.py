@@ -230,6 +230,7 @@ def bfs_case(arena, torch, device, log_v: int = 26, deg: int = 8) -> Case:
         levels["n"] = cur + 1
         return cur + 1
 
+
     def check():
         lv = tl.long()
         src = torch.repeat_interleave(torch.arange(nv, device=device), deg)
@@ -245,11 +246,33 @@ def bfs_case(arena, torch, device, log_v: int = 26, deg: int = 8) -> Case:
         ok &= bool(((lv <= 0) | has_pred).all().item())
         return ok
 
+    saved = {}
+
+    def check_and_save():
+        ok = check()
+        saved["lvl"] = tl.clone()
+        return ok
+
     c = Case("bfs", "bfs_step", 4 * ne + 12 * nv, ne, "edge", [], host_loop=step, reset=reset,
-             check=check, note=f"2^{log_v} vertices x {deg} random out-edges, full traversal; "
-                               "bytes = compulsory 4|E| + 12|V|, elem = edges (TEPS)")
+             check=check_and_save,
+             note=f"2^{log_v} vertices x {deg} random out-edges, full traversal by per-level "
+                  "launches (Rodinia host loop); bytes = compulsory 4|E| + 12|V|, elem = edges (TEPS)")
     c.levels = levels
-    return c
+
+    from paper_2206_07896_b200 import graph
+
+    def fused(rt, stream):
+        levels["fused_depth"] = graph.bfs_levels(rt, row, col, lvl, nv, 0)
+        return 1
+
+    def fused_check():
+        return bool(torch.equal(tl, saved["lvl"])) if "lvl" in saved else check()
+
+    f = Case("bfs_fused", "bfs_expand_queue", 4 * ne + 12 * nv, ne, "edge", [], host_loop=fused,
+             check=fused_check,
+             note="same graph, whole traversal fused on the device (bf_bfs_levels: frontier queues "
+                  "+ L2-resident visited bitmap); levels equal to the per-level launches")
+    return c, f
 
 
 def time_case(case: Case, rt, torch, stream, reps: int, warmup: int) -> dict:

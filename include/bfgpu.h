@@ -209,6 +209,17 @@ int bf_counters_get(bf_runtime *rt, bf_counters *out, int64_t *busy_blocks,
  * ordering collectives with launches. */
 int bf_worker_stream(bf_runtime *rt, int32_t worker, void **stream);
 
+/* ---- host-program drivers --------------------------------------------------- */
+/* Whole BFS traversal from `source` over the CSR graph in buffers (row, col)
+ * (Rodinia's bfs host loop fused on the device; kernels/bfs.kn is the
+ * per-level step).  Writes lvl[v] = hop distance from source, -1 when
+ * unreachable — exactly the levels of launching `bfs` with cur = 0, 1, ...
+ * until `changed` stays 0 after lvl = -1 except lvl[source] = 0.  *depth =
+ * max level + 1.  Runs on worker 0's stream after draining every worker;
+ * returns when done.  BF_E_FAULT when the CSR indexes out of range. */
+int bf_bfs_levels(bf_runtime *rt, uint32_t row, uint32_t col, uint32_t lvl,
+                  int32_t nv, int32_t source, int32_t *depth);
+
 /* ---- kernel registry ---------------------------------------------------- */
 int bf_kernel_count(int32_t *count);
 /* Name and parameter signature of registered kernel `index`: kinds[i] is a

@@ -12,6 +12,7 @@
 // semantics the reference API exposes; the whole-traversal driver with a
 // frontier queue is bfs_levels (k_bfs_driver).
 #include <climits>
+#include <cstdlib>
 
 #include "bf_internal.h"
 #include "common.cuh"
@@ -134,6 +135,249 @@ static int launch_bfs(LaunchCtx& ctx) {
   }
   return BF_OK;
 }
+
+// ===========================================================================
+// Fused traversal (the Rodinia host loop, on the device): bf_bfs_levels.
+// Level-synchronous top-down with two nv-bit bitmaps (8 MB each at 2^26
+// vertices, L2-resident):
+//   expand:  for u in frontier, v in out(u): if v's bit in `now` is clear,
+//            set it (fire-and-forget red.or).
+//   compact: next frontier = bits in `now` not in `prev` (a sweep over the
+//            bitmap, not over lvl[]), prev |= now; ids appended with a
+//            warp-aggregated atomic and lvl[id] = d + 1 written in id order
+//            (no random partial-sector writes).
+// The bitmap `now` is pinned in L2 with a persisting access-policy window.
+// Same levels as repeated `bfs` launches.  The per-edge "unvisited?" test is
+// an L2 hit instead of a random DRAM read of lvl[], and no load waits on an
+// atomic.
+// ===========================================================================
+__global__ void __launch_bounds__(256) bfs_init(int* lvl, unsigned* now, unsigned* prev,
+                                                long long nv, long long words, int src, int* q0,
+                                                int* sizes) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int4* l4 = reinterpret_cast<int4*>(lvl);
+  for (long long i = t; i < nv / 4; i += stride) l4[i] = make_int4(-1, -1, -1, -1);
+  for (long long i = (nv / 4) * 4 + t; i < nv; i += stride) lvl[i] = -1;
+  for (long long i = t; i < words; i += stride) {
+    now[i] = 0u;
+    prev[i] = 0u;
+  }
+  if (t == 0) {
+    sizes[0] = 1;
+    sizes[1] = 0;
+    sizes[2] = 0;
+    q0[0] = src;
+  }
+}
+
+__global__ void bfs_seed(int* lvl, unsigned* now, unsigned* prev, int src) {
+  lvl[src] = 0;
+  now[src >> 5] = 1u << (src & 31);
+  prev[src >> 5] = 1u << (src & 31);
+}
+
+constexpr int kBfsVPT = 4;  // frontier vertices per thread (independent chains)
+
+__global__ void __launch_bounds__(256) bfs_expand(const int* __restrict__ row,
+                                                  const int* __restrict__ col, long long ne,
+                                                  int* lvl, unsigned* now, long long nv,
+                                                  const int* __restrict__ q, int* sizes, int depth) {
+  const int qn = sizes[0];
+  const long long stride = (long long)gridDim.x * blockDim.x * kBfsVPT;
+  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kBfsVPT; i0 < qn;
+       i0 += stride) {
+    int e0[kBfsVPT], e1[kBfsVPT];
+#pragma unroll
+    for (int a = 0; a < kBfsVPT; a++) {
+      e0[a] = e1[a] = 0;
+      if (i0 + a < qn) {
+        const int u = __ldg(q + i0 + a);
+        e0[a] = __ldg(row + u);
+        e1[a] = __ldg(row + u + 1);
+        if (e0[a] < 0 || e1[a] > ne || e1[a] < e0[a]) {
+          sizes[2] = 1;
+          e1[a] = e0[a];
+        }
+      }
+    }
+    int maxd = 0;
+#pragma unroll
+    for (int a = 0; a < kBfsVPT; a++) maxd = max(maxd, e1[a] - e0[a]);
+    for (int j = 0; j < maxd; j += 4) {
+      int v[kBfsVPT][4];
+      unsigned w[kBfsVPT][4];
+#pragma unroll
+      for (int a = 0; a < kBfsVPT; a++)
+#pragma unroll
+        for (int t = 0; t < 4; t++) v[a][t] = (e0[a] + j + t < e1[a]) ? __ldcs(col + e0[a] + j + t) : -1;
+#pragma unroll
+      for (int a = 0; a < kBfsVPT; a++)
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          w[a][t] = 0xffffffffu;
+          if (v[a][t] >= 0) {
+            if (v[a][t] >= nv) sizes[2] = 1;
+            else w[a][t] = __ldcg(now + (v[a][t] >> 5));
+          }
+        }
+#pragma unroll
+      for (int a = 0; a < kBfsVPT; a++)
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          const unsigned bit = 1u << (v[a][t] & 31);
+          if (v[a][t] >= 0 && v[a][t] < nv && !(w[a][t] & bit))
+            atomicOr(now + (v[a][t] >> 5), bit);  // result unused: compiled to RED
+        }
+    }
+  }
+}
+
+// next frontier = now & ~prev, prev = now
+__global__ void __launch_bounds__(256) bfs_compact(unsigned* now, unsigned* prev, long long words,
+                                                   int* nq, int* sizes, int* lvl, int depth) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < words; i += stride) {
+    unsigned fresh = 0;
+    if (i < words) {
+      const unsigned nw = __ldcg(now + i);
+      fresh = nw & ~prev[i];
+      if (fresh) prev[i] = nw;
+    }
+    const int c = __popc(fresh);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(sizes + 1, total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = base + incl - c;
+    while (fresh) {
+      const int b = __ffs(fresh) - 1;
+      const int v = (int)(i * 32 + b);
+      nq[pos++] = v;
+      lvl[v] = depth + 1;
+      fresh &= fresh - 1;
+    }
+  }
+}
+
+}  // namespace bf
+
+extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, long long lr,
+                                  const int* col, long long lcol, int* lvl, long long ll,
+                                  int nv, int src, int* depth_out, char* err, int errcap) {
+  using namespace bf;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  if (nv <= 0 || src < 0 || src >= nv || lr < (long long)nv + 1 || ll < nv) {
+    snprintf(err, errcap, "bfs_levels: bad sizes (nv=%d src=%d len(row)=%lld len(lvl)=%lld)", nv,
+             src, lr, ll);
+    return BF_E_INVALID;
+  }
+  const long long words = ((long long)nv + 31) / 32;
+  // scratch (bitmaps, two frontier queues, counters) is kept per device and
+  // only grows: a traversal does no allocation after the first
+  struct Scratch {
+    long long cap_words = 0, cap_v = 0;
+    unsigned *now = nullptr, *prev = nullptr;
+    int *qa = nullptr, *qb = nullptr, *sizes = nullptr, *hs = nullptr;
+  };
+  static Scratch sc[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Scratch& S = sc[dev & 63];
+  cudaError_t e = cudaSuccess;
+  if (S.cap_v < nv) {
+    cudaStreamSynchronize(stream);
+    cudaFree(S.now);
+    cudaFree(S.prev);
+    cudaFree(S.qa);
+    cudaFree(S.qb);
+    S = Scratch();
+    e = cudaMalloc((void**)&S.now, words * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.prev, words * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.qa, (size_t)nv * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.qb, (size_t)nv * 4);
+    if (e == cudaSuccess) {
+      S.cap_v = nv;
+      S.cap_words = words;
+    }
+  }
+  if (e == cudaSuccess && !S.sizes) e = cudaMalloc((void**)&S.sizes, 16);
+  if (e == cudaSuccess && !S.hs) e = cudaMallocHost((void**)&S.hs, 16);
+  unsigned *now = S.now, *prev = S.prev;
+  int *qa = S.qa, *qb = S.qb, *sizes = S.sizes, *hs = S.hs;
+  int depth = 0;
+  // keep the visited bitmap resident in L2 while the graph streams through
+  cudaStreamAttrValue win = {};
+  bool windowed = false;
+  const char* wenv = getenv("BF_BFS_L2WIN");
+  if (e == cudaSuccess && wenv && atoi(wenv) > 0) {
+    int dev = 0, maxwin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    size_t want = (size_t)words * 4;
+    if (maxwin > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+      win.accessPolicyWindow.base_ptr = now;
+      win.accessPolicyWindow.num_bytes = want < (size_t)maxwin ? want : (size_t)maxwin;
+      win.accessPolicyWindow.hitRatio = 1.0f;
+      win.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      win.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      windowed = cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &win) == cudaSuccess;
+    }
+    cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    int g = stream_grid(nv, 256 * 4, num_sms, 8);
+    bfs_init<<<g, 256, 0, stream>>>(lvl, now, prev, nv, words, src, qa, sizes);
+    bfs_seed<<<1, 1, 0, stream>>>(lvl, now, prev, src);
+    int qn = 1;
+    int* q = qa;
+    int* nq = qb;
+    const int cgrid = stream_grid(words, 256, num_sms, 8);
+    while (qn > 0) {
+      int grid = stream_grid((qn + kBfsVPT - 1) / kBfsVPT, 256, num_sms, 8);
+      bfs_expand<<<grid, 256, 0, stream>>>(row, col, lcol, lvl, now, nv, q, sizes, depth);
+      bfs_compact<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lvl, depth);
+      cudaMemcpyAsync(hs, sizes, 12, cudaMemcpyDeviceToHost, stream);
+      e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) break;
+      if (hs[2]) {
+        snprintf(err, errcap, "bfs_levels: CSR index out of range");
+        e = cudaErrorInvalidValue;
+        break;
+      }
+      depth++;
+      qn = hs[1];
+      hs[0] = qn;
+      hs[1] = 0;
+      cudaMemcpyAsync(sizes, hs, 8, cudaMemcpyHostToDevice, stream);
+      int* t = q;
+      q = nq;
+      nq = t;
+    }
+  }
+  if (windowed) {
+    win.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &win);
+    cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+  }
+  cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    if (!err[0]) snprintf(err, errcap, "bfs_levels: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return e == cudaErrorInvalidValue ? BF_E_FAULT : BF_E_CUDA;
+  }
+  *depth_out = depth;
+  return BF_OK;
+}
+
+namespace bf {
 
 static Registrar reg_bfs("bfs",
                          {{BF_SLOT_HANDLE, BF_I32, "row"},

@@ -128,35 +128,55 @@ __device__ __forceinline__ int warp_sum(int v) {
 
 // one warp per logical block x; loads coalesced (int4 when the block's
 // slice is 16 B aligned); m == 1
-template <bool VEC>
+// one warp per logical block x (m == 1).  VEC (bx % 4 == 0, bx <= 128*MAXV):
+// the slice is read as <= MAXV int4 per lane, U blocks per iteration, every
+// load of the iteration issued before any shuffle tree (loads in flight per
+// lane: U*MAXV*16 B).  Otherwise a plain strided loop.
+template <int MAXV, int U>
 __global__ void __launch_bounds__(256) reduce_warp(const int* __restrict__ x, long long lx,
                                                    int* __restrict__ out, long long lout, int n,
                                                    long long x0, long long x1, KDesc k) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x / 32);
-  for (long long bx = x0 + (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; bx < x1;
-       bx += warps) {
-    long long lo = bx * k.bx;
-    long long hi = lo + k.bx;
-    if (hi > n) hi = n;
-    if (hi > lx || bx >= lout) {
-      if (lane == 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, block_of_x(k, bx));
-      continue;
-    }
-    unsigned s = 0;
-    if (VEC) {  // lo % 4 == 0
-      const int4* x4 = reinterpret_cast<const int4*>(x + lo);
-      const long long nv = (hi - lo) / 4;
-      for (long long i = lane; i < nv; i += 32) {
-        const int4 v = __ldcs(x4 + i);
-        s += (unsigned)v.x + (unsigned)v.y + (unsigned)v.z + (unsigned)v.w;
+  const long long w0 = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  for (long long b0 = x0 + w0 * U; b0 < x1; b0 += warps * U) {
+    unsigned s[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      s[u] = 0;
+      const long long bx = b0 + u;
+      long long lo = bx * k.bx, hi = lo + k.bx;
+      if (hi > n) hi = n;
+      const bool ok = bx < x1 && !(hi > lx || bx >= lout) && hi > lo;
+      if (MAXV > 0) {
+        const int4* x4 = reinterpret_cast<const int4*>(x + lo);
+        const long long nv = ok ? (hi - lo) / 4 : 0;
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+          if (lane + 32 * j < nv) {
+            const int4 v = __ldcs(x4 + lane + 32 * j);
+            s[u] += (unsigned)v.x + (unsigned)v.y + (unsigned)v.z + (unsigned)v.w;
+          }
+        }
+        if (ok)
+          for (long long i = lo + nv * 4 + lane; i < hi; i += 32) s[u] += (unsigned)x[i];
+      } else if (ok) {
+        for (long long i = lo + lane; i < hi; i += 32) s[u] += (unsigned)__ldg(x + i);
       }
-      for (long long i = lo + nv * 4 + lane; i < hi; i += 32) s += (unsigned)x[i];
-    } else {
-      for (long long i = lo + lane; i < hi; i += 32) s += (unsigned)__ldg(x + i);
     }
-    int v = warp_sum((int)s);
-    if (lane == 0) out[bx] = v;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const long long bx = b0 + u;
+      if (bx >= x1) break;
+      long long lo = bx * k.bx, hi = lo + k.bx;
+      if (hi > n) hi = n;
+      if (hi > lx || bx >= lout) {
+        if (lane == 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, block_of_x(k, bx));
+        continue;
+      }
+      const int v = warp_sum((int)s[u]);
+      if (lane == 0) out[bx] = v;
+    }
   }
 }
 
@@ -208,13 +228,19 @@ static int launch_reduce(LaunchCtx& ctx) {
   for (auto& xi : ctx.x_intervals()) {
     long long nx = xi.second - xi.first;
     if (m == 1) {
-      int grid = stream_grid(nx, 8, ctx.num_sms, 8);
-      if (bx % 4 == 0)
-        reduce_warp<true><<<grid, 256, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr,
-                                                        O.len, n, xi.first, xi.second, ctx.desc());
-      else
-        reduce_warp<false><<<grid, 256, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr,
-                                                         O.len, n, xi.first, xi.second, ctx.desc());
+      const int* xp = (const int*)X.ptr;
+      int* op = (int*)O.ptr;
+      KDesc d = ctx.desc();
+      if (bx % 4 == 0 && bx <= 128) {
+        int grid = stream_grid(nx, 8 * 8, ctx.num_sms, 8);
+        reduce_warp<1, 8><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
+      } else if (bx % 4 == 0 && bx <= 256) {
+        int grid = stream_grid(nx, 8 * 4, ctx.num_sms, 8);
+        reduce_warp<2, 4><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
+      } else {
+        int grid = stream_grid(nx, 8, ctx.num_sms, 8);
+        reduce_warp<0, 1><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
+      }
     } else {
       int grid = (int)std::min<long long>(nx, (long long)ctx.num_sms * 8);
       reduce_tree<<<grid, bx, 0, ctx.stream>>>((const int*)X.ptr, X.len, (int*)O.ptr, O.len, n,
@@ -268,10 +294,18 @@ __device__ __forceinline__ int fast_mod(int a, const FastMod& f) {
   return (int)(n - q * f.d);
 }
 
-template <int MODE>  // 0: per-lane counters, 1: CTA shared atomics, 2: global atomics
+// Bin of pixel a.  POW2: |nbins| is a power of two (a & mask for a >= 0).
+// SAFE: len(counts) >= |nbins|, so only a negative remainder can trap.
+template <bool POW2>
+__device__ __forceinline__ int hist_bin(int a, const FastMod& f) {
+  if (POW2) return a >= 0 ? (a & (int)(f.d - 1)) : c_mod(a, f.nbins);
+  return fast_mod(a, f);
+}
+
+template <int MODE, bool SAFE>  // MODE 0: per-lane counters, 1: CTA shared atomics, 2: global
 __device__ __forceinline__ void hist_add(unsigned* sh, unsigned* mine, int* counts, long long lc,
                                          int b, unsigned copies, bool& bad) {
-  if (b < 0 || b >= lc) {
+  if (SAFE ? b < 0 : (b < 0 || b >= lc)) {
     bad = true;
     return;
   }
@@ -284,7 +318,7 @@ __device__ __forceinline__ void hist_add(unsigned* sh, unsigned* mine, int* coun
   }
 }
 
-template <int MODE>
+template <int MODE, bool POW2, bool SAFE>
 __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, int* counts,
                                                   long long lc, long long lo, long long hi,
                                                   FastMod fm, unsigned copies, KDesc k,
@@ -307,8 +341,8 @@ __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, i
   if (vlo > hi) vlo = hi;
   long long vhi = hi & ~3LL;
   if (vhi < vlo) vhi = vlo;
-  if (tid < vlo - lo) hist_add<MODE>(sh, mine, counts, lc, fast_mod(pix[lo + tid], fm), copies, bad);
-  if (tid < hi - vhi) hist_add<MODE>(sh, mine, counts, lc, fast_mod(pix[vhi + tid], fm), copies, bad);
+  if (tid < vlo - lo) hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(pix[lo + tid], fm), copies, bad);
+  if (tid < hi - vhi) hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(pix[vhi + tid], fm), copies, bad);
   const int4* p4 = reinterpret_cast<const int4*>(pix);
   const long long end = vhi / 4;
   long long g = vlo / 4 + tid;
@@ -318,18 +352,18 @@ __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, i
     for (int u = 0; u < 4; u++) v[u] = __ldcs(p4 + g + u * stride);
 #pragma unroll
     for (int u = 0; u < 4; u++) {
-      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].x, fm), copies, bad);
-      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].y, fm), copies, bad);
-      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].z, fm), copies, bad);
-      hist_add<MODE>(sh, mine, counts, lc, fast_mod(v[u].w, fm), copies, bad);
+      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].x, fm), copies, bad);
+      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].y, fm), copies, bad);
+      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].z, fm), copies, bad);
+      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].w, fm), copies, bad);
     }
   }
   for (; g < end; g += stride) {
     const int4 v = __ldcs(p4 + g);
-    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.x, fm), copies, bad);
-    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.y, fm), copies, bad);
-    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.z, fm), copies, bad);
-    hist_add<MODE>(sh, mine, counts, lc, fast_mod(v.w, fm), copies, bad);
+    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.x, fm), copies, bad);
+    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.y, fm), copies, bad);
+    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.z, fm), copies, bad);
+    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.w, fm), copies, bad);
   }
   if (bad) {
     // exact block of the first bad pixel is not tracked on this path: the
@@ -354,28 +388,46 @@ __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, i
   }
 }
 
+template <int MODE, bool POW2, bool SAFE>
+static void hist_go(LaunchCtx& ctx, int grid, size_t smem, const ArgVal& P, const ArgVal& Cn,
+                    long long lo, long long hi, const FastMod& fm, unsigned copies, long long xbase,
+                    int bx_div) {
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(hist_range<MODE, POW2, SAFE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaGetLastError();
+    attr = true;
+  }
+  hist_range<MODE, POW2, SAFE><<<grid, 256, smem, ctx.stream>>>(
+      (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, fm, copies, ctx.desc(), xbase, bx_div);
+}
+
+template <int MODE>
+static void hist_go2(LaunchCtx& ctx, int grid, size_t smem, const ArgVal& P, const ArgVal& Cn,
+                     long long lo, long long hi, const FastMod& fm, unsigned copies,
+                     long long xbase, int bx_div) {
+  const bool pow2 = (fm.d & (fm.d - 1)) == 0;
+  const bool safe = Cn.len >= (long long)fm.d;
+  if (pow2 && safe) hist_go<MODE, true, true>(ctx, grid, smem, P, Cn, lo, hi, fm, copies, xbase, bx_div);
+  else if (pow2) hist_go<MODE, true, false>(ctx, grid, smem, P, Cn, lo, hi, fm, copies, xbase, bx_div);
+  else if (safe) hist_go<MODE, false, true>(ctx, grid, smem, P, Cn, lo, hi, fm, copies, xbase, bx_div);
+  else hist_go<MODE, false, false>(ctx, grid, smem, P, Cn, lo, hi, fm, copies, xbase, bx_div);
+}
+
 static int hist_issue(LaunchCtx& ctx, const ArgVal& P, const ArgVal& Cn, long long lo, long long hi,
                       int nbins, unsigned copies, long long xbase, int bx_div) {
   if (lo >= hi) return BF_OK;
   const FastMod fm = make_fastmod(nbins);
   const long long nb = fm.d;
   int grid = stream_grid(hi - lo, 256 * 16, ctx.num_sms, 6);
-  KDesc d = ctx.desc();
   if (nb <= kHistLaneBins) {
     size_t smem = 8 * kHistLaneBins * 32 * sizeof(unsigned);  // 8 warps x 32 bins x 32 lanes
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(hist_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-    hist_range<0><<<grid, 256, smem, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi,
-                                                  fm, copies, d, xbase, bx_div);
+    hist_go2<0>(ctx, grid, smem, P, Cn, lo, hi, fm, copies, xbase, bx_div);
   } else if (nb <= kHistSmemBins) {
-    hist_range<1><<<grid, 256, nb * sizeof(unsigned), ctx.stream>>>(
-        (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, fm, copies, d, xbase, bx_div);
+    hist_go2<1>(ctx, grid, nb * sizeof(unsigned), P, Cn, lo, hi, fm, copies, xbase, bx_div);
   } else {
-    hist_range<2><<<grid, 256, 0, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi,
-                                                fm, copies, d, xbase, bx_div);
+    hist_go2<2>(ctx, grid, 0, P, Cn, lo, hi, fm, copies, xbase, bx_div);
   }
   BF_CUDA_LAUNCH_CHECK(ctx);
   return BF_OK;

@@ -102,11 +102,16 @@ __global__ void __launch_bounds__(256) kmeans_assign(const float* __restrict__ f
 // private per-warp row for cluster best_q (no atomics, no bank conflicts).
 constexpr int kKmWarps = 8;
 
-__global__ void __launch_bounds__(256) kmeans_fast(const float* __restrict__ f,
+// NF: compile-time feature count (4, 8, 16 or 32; 0 = dynamic nf <= 32).
+// Centroid rows are read as 16 B broadcasts (one LDS.128 per 4 FMAs).
+template <int NF>
+__global__ void __launch_bounds__(256, 2) kmeans_fast(const float* __restrict__ f,
                                                    const float* __restrict__ cent,
                                                    int* __restrict__ member, float* sums,
-                                                   int* counts, int npts, int nf, int k,
+                                                   int* counts, int npts, int nf_dyn, int k,
                                                    long long lo, long long hi) {
+  const int nf = NF ? NF : nf_dyn;
+  constexpr int FM = NF ? NF : 32;  // register array extent
   extern __shared__ float smf[];
   const int kc = k > 0 ? k : 1;
   float* cf = smf;                         // [kc*nf] centroids (f32 as stored)
@@ -136,14 +141,14 @@ __global__ void __launch_bounds__(256) kmeans_fast(const float* __restrict__ f,
   for (long long base = lo + ((long long)blockIdx.x * kKmWarps + warp) * 32; base < hi; base += wstride) {
     const long long p = base + lane;
     const bool valid = p < hi;
-    float fv[32];
+    float fv[FM];
 #pragma unroll
-    for (int l = 0; l < 32; l++) fv[l] = (valid && l < nf) ? __ldcs(f + (long long)l * npts + p) : 0.f;
+    for (int l = 0; l < FM; l++) fv[l] = (valid && l < nf) ? __ldcs(f + (long long)l * npts + p) : 0.f;
     int best = 0;
     if (valid && k > 1) {
       float fn2 = 0.f;
 #pragma unroll
-      for (int l = 0; l < 32; l++) fn2 = fmaf(fv[l], fv[l], fn2);
+      for (int l = 0; l < FM; l++) fn2 = fmaf(fv[l], fv[l], fn2);
       const float fnorm = sqrtf(fn2) * 1.01f;
       float tmin = INFINITY, hi1 = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
       int i1 = 0, lo1i = -1;
@@ -151,9 +156,21 @@ __global__ void __launch_bounds__(256) kmeans_fast(const float* __restrict__ f,
       for (int c = 0; c < k; c++) {
         const float* cc = cf + c * nf;
         float dot = 0.f;
+        if (NF) {
+          const float4* c4 = reinterpret_cast<const float4*>(cc);
 #pragma unroll
-        for (int l = 0; l < 32; l++)
-          if (l < nf) dot = fmaf(fv[l], cc[l], dot);
+          for (int l = 0; l < FM / 4; l++) {
+            const float4 cv = c4[l];
+            dot = fmaf(fv[4 * l], cv.x, dot);
+            dot = fmaf(fv[4 * l + 1], cv.y, dot);
+            dot = fmaf(fv[4 * l + 2], cv.z, dot);
+            dot = fmaf(fv[4 * l + 3], cv.w, dot);
+          }
+        } else {
+#pragma unroll
+          for (int l = 0; l < FM; l++)
+            if (l < nf) dot = fmaf(fv[l], cc[l], dot);
+        }
         const float t = fmaf(-2.f, dot, cn2[c]);
         const float e = fmaf(cA[c], fnorm, cB[c]);
         finite &= fabsf(t) <= 3.0e38f;
@@ -181,7 +198,7 @@ __global__ void __launch_bounds__(256) kmeans_fast(const float* __restrict__ f,
           const float* cc = cf + c * nf;
           double dist = 0.0;
 #pragma unroll
-          for (int l = 0; l < 32; l++) {
+          for (int l = 0; l < FM; l++) {
             if (l < nf) {
               const double diff = dsub((double)fv[l], (double)cc[l]);
               dist = dadd(dist, dmul(diff, diff));
@@ -200,7 +217,7 @@ __global__ void __launch_bounds__(256) kmeans_fast(const float* __restrict__ f,
     }
     // transpose: lane q's features -> row q of the tile
 #pragma unroll
-    for (int l = 0; l < 32; l++)
+    for (int l = 0; l < FM; l++)
       if (l < nf) mytile[lane * 33 + l] = fv[l];
     __syncwarp();
     for (int q = 0; q < 32; q++) {
@@ -255,16 +272,18 @@ static int launch_kmeans(LaunchCtx& ctx) {
     if (nf <= kKmMaxF && kc * nf <= 1024) {
       size_t smem = sizeof(float) * ((size_t)kc * nf + 3 * kc + kKmWarps * 32 * 33 +
                                      (size_t)kKmWarps * kc * nf) + sizeof(int) * kc;
+      auto fn = nf == 32 ? kmeans_fast<32> : nf == 16 ? kmeans_fast<16> : nf == 8 ? kmeans_fast<8>
+              : nf == 4 ? kmeans_fast<4> : kmeans_fast<0>;
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(kmeans_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        for (auto g : {kmeans_fast<32>, kmeans_fast<16>, kmeans_fast<8>, kmeans_fast<4>, kmeans_fast<0>})
+          cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaGetLastError();
         attr = true;
       }
       int grid = stream_grid(hi - lo, 256 * 4, ctx.num_sms, 4);
-      kmeans_fast<<<grid, 256, smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr,
-                                                   (int*)M.ptr, (float*)S.ptr, (int*)Cn.ptr,
-                                                   (int)npts, nf, k, lo, hi);
+      fn<<<grid, 256, smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr,
+                                          (float*)S.ptr, (int*)Cn.ptr, (int)npts, nf, k, lo, hi);
       BF_CUDA_LAUNCH_CHECK(ctx);
       continue;
     }

@@ -34,7 +34,17 @@ __global__ void __launch_bounds__(256) nn_stream(const float* __restrict__ ll,
   if (tid < hi - vhi) d[vhi + tid] = nn_dist(ll[2 * (vhi + tid)], ll[2 * (vhi + tid) + 1], x, y);
   const float4* l4 = reinterpret_cast<const float4*>(ll);
   float4* d4 = reinterpret_cast<float4*>(d);
-  for (long long g = vlo / 4 + tid; g < vhi / 4; g += stride) {
+  long long g = vlo / 4 + tid;
+  const long long end = vhi / 4;
+  for (; g + stride < end; g += 2 * stride) {  // 4 x 16 B loads in flight
+    const float4 p0 = __ldcs(l4 + 2 * g), q0 = __ldcs(l4 + 2 * g + 1);
+    const float4 p1 = __ldcs(l4 + 2 * (g + stride)), q1 = __ldcs(l4 + 2 * (g + stride) + 1);
+    __stcs(d4 + g, make_float4(nn_dist(p0.x, p0.y, x, y), nn_dist(p0.z, p0.w, x, y),
+                               nn_dist(q0.x, q0.y, x, y), nn_dist(q0.z, q0.w, x, y)));
+    __stcs(d4 + g + stride, make_float4(nn_dist(p1.x, p1.y, x, y), nn_dist(p1.z, p1.w, x, y),
+                                        nn_dist(q1.x, q1.y, x, y), nn_dist(q1.z, q1.w, x, y)));
+  }
+  if (g < end) {
     const float4 p = __ldcs(l4 + 2 * g), q = __ldcs(l4 + 2 * g + 1);
     __stcs(d4 + g, make_float4(nn_dist(p.x, p.y, x, y), nn_dist(p.z, p.w, x, y),
                                nn_dist(q.x, q.y, x, y), nn_dist(q.z, q.w, x, y)));

@@ -1115,6 +1115,34 @@ int bf_worker_stream(bf_runtime* rt, int32_t worker, void** stream) {
   return BF_OK;
 }
 
+// ---- host-program drivers ---------------------------------------------------
+
+int bf_bfs_levels_impl(void* stream, int num_sms, const int* row, long long lr, const int* col,
+                       long long lcol, int* lvl, long long ll, int nv, int src, int* depth_out,
+                       char* err, int errcap);
+
+int bf_bfs_levels(bf_runtime* rt, uint32_t row, uint32_t col, uint32_t lvl, int32_t nv,
+                  int32_t source, int32_t* depth) {
+  if (!rt || !depth) return fail(BF_E_INVALID, "null argument");
+  if (rt->shut_down) return fail(BF_E_SHUTDOWN, "launch after shutdown");
+  Buffer* R = lookup(rt->arena, row);
+  Buffer* C = lookup(rt->arena, col);
+  Buffer* L = lookup(rt->arena, lvl);
+  if (!R || !C || !L) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (R->scalar != BF_I32 || C->scalar != BF_I32 || L->scalar != BF_I32)
+    return fail(BF_E_TYPEFAULT, "bfs_levels: row, col and lvl must be i32 buffers");
+  int rc = set_device(rt->device);
+  if (rc) return rc;
+  rc = sync_workers(rt);
+  if (rc) return rc;
+  char err[256] = {0};
+  rc = bf_bfs_levels_impl((void*)rt->streams[0], rt->num_sms, (const int*)R->ptr, R->length,
+                          (const int*)C->ptr, C->length, (int*)L->ptr, L->length, nv, source,
+                          depth, err, sizeof(err));
+  if (rc) return fail(rc, err);
+  return BF_OK;
+}
+
 // ---- registry --------------------------------------------------------------
 
 int bf_kernel_count(int32_t* count) {

@@ -183,3 +183,22 @@ def test_large_random_corpus_vs_oracle():
         want, _ = oracle.run(inst)
         got, trap, _, _ = gpu_run(inst)
         assert trap is None and bit_equal(got["y"], want["y"]), taps
+
+
+def test_bfs_levels_fused_vs_oracle():
+    """The fused traversal (bf_bfs_levels) gives exactly the levels of the
+    per-level launches (oracle full traversal)."""
+    import instances as I
+    from gpu_helpers import materialize
+    from paper_2206_07896_b200 import DeviceArena, Runtime, graph
+    for nv, deg, seed, src in [(5000, 4, 1, 0), (200000, 8, 2, 17), (777, 1, 3, 5), (3000, 13, 4, 2999)]:
+        row, col = I.random_graph(nv, deg, seed)
+        want, depth = oracle.bfs_full(row, col, nv, src)
+        arena = DeviceArena()
+        hr, hc, hl = arena.alloc("i32", nv + 1), arena.alloc("i32", col.size), arena.alloc("i32", nv)
+        arena.upload_numpy(hr, row)
+        arena.upload_numpy(hc, col)
+        with Runtime(arena) as rt:
+            got_depth = graph.bfs_levels(rt, hr, hc, hl, nv, src)
+        assert bit_equal(arena.to_numpy(hl), want)
+        assert got_depth == depth
