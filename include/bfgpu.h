@@ -220,6 +220,20 @@ int bf_worker_stream(bf_runtime *rt, int32_t worker, void **stream);
 int bf_bfs_levels(bf_runtime *rt, uint32_t row, uint32_t col, uint32_t lvl,
                   int32_t nv, int32_t source, int32_t *depth);
 
+/* Rodinia's hotspot host loop fused: the result of `iterations` ping-pong
+ * launches of `hotspot` (kernels/hotspot.kn) starting from buffer `a`, with
+ * `b` as the other buffer — bit-identical.  tsteps = 1: one streaming pass
+ * per iteration issued from C++; tsteps > 1: temporal blocking, `tsteps`
+ * iterations per pass through HBM (shared-memory tiles); 0 = default (1,
+ * the faster on B200 in round 1).  The result
+ * lands where the launch loop leaves it: `a` for even, `b` for odd
+ * `iterations`; the other buffer is scratch.  params = {step/Cap, 1/Rx,
+ * 1/Ry, 1/Rz, ambient} as doubles.  Asynchronous on worker 0's stream,
+ * ordered after everything already launched on the runtime. */
+int bf_hotspot_run(bf_runtime *rt, uint32_t a, uint32_t power, uint32_t b,
+                   int32_t rows, int32_t cols, const double params[5],
+                   int32_t iterations, int32_t tsteps);
+
 /* ---- kernel registry ---------------------------------------------------- */
 int bf_kernel_count(int32_t *count);
 /* Name and parameter signature of registered kernel `index`: kinds[i] is a

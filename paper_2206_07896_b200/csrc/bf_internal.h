@@ -100,6 +100,10 @@ inline int stream_grid(long long work_items, int items_per_cta, int num_sms,
   return (int)(need < cap ? need : cap);
 }
 
+// full-grid hotspot step with the streaming band kernel (k_hotspot.cu)
+int hotspot_step_full(cudaStream_t stream, int num_sms, const float* src, const float* power,
+                      float* dst, int rows, int cols, const double* kc);
+
 #define BF_CUDA_LAUNCH_CHECK(ctx)                                   \
   do {                                                              \
     cudaError_t e_ = cudaGetLastError();                            \

@@ -190,6 +190,29 @@ __global__ void __launch_bounds__(256) hotspot_cells(const float* src, const flo
   }
 }
 
+// One full-grid step (used by the fused host-loop driver, k_hotspot_fused.cu).
+int hotspot_step_full(cudaStream_t stream, int num_sms, const float* src, const float* power,
+                      float* dst, int rows, int cols, const double* kc) {
+  HsConst k{kc[0], kc[1], kc[2], kc[3], kc[4]};
+  if (cols % 4 == 0) {
+    const int groups = (cols + 127) / 128;
+    const int pf = hotspot_pf();
+    const int warps = hotspot_resident_warps(num_sms, pf);
+    int bands = std::max(1, warps / groups);
+    if (bands > rows) bands = rows;
+    const int grid = (groups * bands + 3) / 4;
+    hotspot_band_fn(pf)<<<grid, 128, 0, stream>>>(src, power, dst, rows, cols, 0, rows, 0, cols,
+                                                  groups, bands, k);
+  } else {
+    KDesc d{};
+    int grid = stream_grid((long long)rows * cols, 256, num_sms, 8);
+    hotspot_cells<<<grid, 256, 0, stream>>>(src, power, dst, (long long)rows * cols,
+                                           (long long)rows * cols, (long long)rows * cols, rows,
+                                           cols, 0, rows, 0, cols, k, d, 0);
+  }
+  return cudaGetLastError() == cudaSuccess ? BF_OK : BF_E_CUDA;
+}
+
 static int launch_hotspot(LaunchCtx& ctx) {
   const ArgVal& S = ctx.args[0];
   const ArgVal& P = ctx.args[1];

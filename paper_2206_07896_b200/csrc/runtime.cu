@@ -1143,6 +1143,42 @@ int bf_bfs_levels(bf_runtime* rt, uint32_t row, uint32_t col, uint32_t lvl, int3
   return BF_OK;
 }
 
+int bf_hotspot_run_impl(void* stream, int num_sms, float* a, float* b, const float* p, int rows,
+                        int cols, const double* kc, int iterations, int tsteps, char* err,
+                        int errcap);
+
+int bf_hotspot_run(bf_runtime* rt, uint32_t a, uint32_t power, uint32_t b, int32_t rows,
+                   int32_t cols, const double params[5], int32_t iterations, int32_t tsteps) {
+  if (!rt || !params) return fail(BF_E_INVALID, "null argument");
+  if (rt->shut_down) return fail(BF_E_SHUTDOWN, "launch after shutdown");
+  Buffer* A = lookup(rt->arena, a);
+  Buffer* P = lookup(rt->arena, power);
+  Buffer* B = lookup(rt->arena, b);
+  if (!A || !P || !B) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (A->scalar != BF_F32 || P->scalar != BF_F32 || B->scalar != BF_F32)
+    return fail(BF_E_TYPEFAULT, "hotspot_run: buffers must be f32");
+  long long need = (long long)rows * cols;
+  if (rows <= 0 || cols <= 0 || A->length < need || P->length < need || B->length < need)
+    return fail(BF_E_INVALID, "hotspot_run: buffers shorter than rows*cols");
+  if (a == b || a == power || b == power)
+    return fail(BF_E_INVALID, "hotspot_run: src, power and dst must be distinct buffers");
+  int rc = set_device(rt->device);
+  if (rc) return rc;
+  // order after every worker's queued work
+  for (int w = 1; w < rt->pool; w++) {
+    cudaEvent_t ev = get_event(rt);
+    cudaEventRecord(ev, rt->streams[w]);
+    cudaStreamWaitEvent(rt->streams[0], ev, 0);
+    rt->event_pool.push_back(ev);
+  }
+  char err[256] = {0};
+  rc = bf_hotspot_run_impl((void*)rt->streams[0], rt->num_sms, (float*)A->ptr, (float*)B->ptr,
+                           (const float*)P->ptr, rows, cols, params, iterations, tsteps, err,
+                           sizeof(err));
+  if (rc) return fail(rc, err);
+  return BF_OK;
+}
+
 // ---- registry --------------------------------------------------------------
 
 int bf_kernel_count(int32_t* count) {

@@ -202,3 +202,22 @@ def test_bfs_levels_fused_vs_oracle():
             got_depth = graph.bfs_levels(rt, hr, hc, hl, nv, src)
         assert bit_equal(arena.to_numpy(hl), want)
         assert got_depth == depth
+
+
+@pytest.mark.parametrize("tsteps", [0, 1, 2, 4, 8, 12, 16])
+def test_hotspot_run_fused_vs_oracle(tsteps):
+    """Temporal blocking == the per-launch ping-pong loop, bit for bit."""
+    import instances as I
+    from paper_2206_07896_b200 import DeviceArena, Runtime, stencil
+    for rows, cols, iters in [(200, 300, 7), (64, 128, 16), (131, 257, 5), (1, 9, 3), (700, 130, 20)]:
+        temp, power = I.hotspot_inputs(rows, cols, rows + cols)
+        params = I.hotspot_params(rows, cols)
+        want = oracle.hotspot_iterate(temp, power, rows, cols, params, iters)
+        arena = DeviceArena()
+        a, p, b = (arena.alloc("f32", rows * cols) for _ in range(3))
+        arena.upload_numpy(a, temp)
+        arena.upload_numpy(p, power)
+        with Runtime(arena) as rt:
+            res = stencil.hotspot_run(rt, a, p, b, rows, cols, params, iters, tsteps)
+            rt.device_synchronize()
+        assert bit_equal(arena.to_numpy(res), want), (rows, cols, iters, tsteps)
