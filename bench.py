@@ -382,6 +382,89 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def run_sweep(args) -> None:
+    """BASELINE configs[4]: vecadd / nn bandwidth sweep, footprint 1 MB ...
+    16 GB doubling, split over the ranks (contiguous logical-block ranges =
+    the average grain with ranks as workers); one JSON line with the table."""
+    import torch
+
+    from paper_2206_07896_b200 import ArgSlot, DeviceArena, Dim3, PackedArgs, Runtime, routines
+    from paper_2206_07896_b200.parallel import rank_range
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    peaks = _peaks()
+    rows = []
+    for kernel in ("vecadd", "nn"):
+        for e in range(15):
+            footprint = (1 << 20) << e  # 1 MB .. 16 GB
+            n = (footprint // 12) // 256 * 256
+            blocks = n // 256
+            lo_b, hi_b = rank_range(blocks, world, rank)
+            ent = {"kernel": kernel, "footprint_bytes": footprint, "n": n}
+            if kernel == "nn" and 2 * (n - 1) + 1 > 2**31 - 1:
+                ent["skipped"] = "ll[2*id] index beyond i32 in kernels/nn.kn (the reference traps)"
+                rows.append(ent)
+                continue
+            arena = DeviceArena(local)
+            rt = Runtime(arena)
+            stream = torch.cuda.ExternalStream(rt.worker_stream(0), device=device)
+            ln = (hi_b - lo_b) * 256  # local elements (local arrays, global ids offset)
+            if kernel == "vecadd":
+                hs = [arena.alloc("f32", max(ln, 1)) for _ in range(3)]
+                for h in hs[:2]:
+                    torch.as_tensor(arena.cuda_array(h), device=device).uniform_(-1, 1)
+                pk = PackedArgs([ArgSlot("handle", hs[0]), ArgSlot("handle", hs[1]),
+                                 ArgSlot("handle", hs[2]), ArgSlot("i32", ln)])
+                routine = routines.get("vecadd")
+            else:
+                hl, hd = arena.alloc("f32", max(2 * ln, 2)), arena.alloc("f32", max(ln, 1))
+                t = torch.as_tensor(arena.cuda_array(hl), device=device)
+                t.uniform_(-90, 90)
+                pk = PackedArgs([ArgSlot("handle", hl), ArgSlot("handle", hd), ArgSlot("i32", ln),
+                                 ArgSlot("f32", 30.0), ArgSlot("f32", 90.0)])
+                routine = routines.get("nn")
+            torch.cuda.synchronize()
+            grid = Dim3(max(1, hi_b - lo_b))
+            for _ in range(args.warmup):
+                rt.launch(routine, grid, Dim3(256), 0, pk)
+            rt.device_synchronize()
+            barrier(world)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                rt.launch(routine, grid, Dim3(256), 0, pk)
+            b.record(stream)
+            rt.device_synchronize()
+            b.synchronize()
+            ms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
+            gbs = 12 * n / (ms * 1e-3) / 1e9
+            ent.update({"gbs": round(gbs, 2), "elem_per_s": n / (ms * 1e-3), "us_per_launch": round(ms * 1e3, 3),
+                        "frac_roofline": round(gbs / (world * peaks["hbm_gbs"]), 4),
+                        "l2_resident": footprint / world < 126e6})
+            rows.append(ent)
+            rt.shutdown()
+            del rt, arena
+            torch.cuda.synchronize()
+    if rank == 0:
+        big = [r for r in rows if r.get("gbs") and r["footprint_bytes"] >= (1 << 30)]
+        best = max((r["gbs"] for r in big), default=None)
+        print(json.dumps({
+            "metric": METRIC, "value": best, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32/f64", "data": "synthetic",
+            "config": {"workload": "vecadd/nn sweep 1 MB..16 GB footprint (12 B/elem), split over ranks",
+                       "value": "best GB/s over points >= 1 GiB"},
+            "sweep": rows}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 def per_kernel_table(arena, rt, torch, stream, args) -> tuple[dict, int]:
     """Every other kernel of the path at full size (benchkit.py), N=1."""
     import benchkit
@@ -428,7 +511,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["hotspot"], default="hotspot")
+    ap.add_argument("--workload", choices=["hotspot", "sweep"], default="hotspot")
     ap.add_argument("--size", type=int, default=8192)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--halo", type=int, default=8)
@@ -444,6 +527,8 @@ def main() -> None:
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.workload == "sweep":
+        run_sweep(args)
     else:
         run_ours(args)
 

@@ -559,12 +559,16 @@ __global__ void __launch_bounds__(256) fir_reg(const float* __restrict__ x, long
 #pragma unroll
       for (int j = 0; j < 16; j++) xv[j] = (o + j < lx) ? __ldg(x + o + j) : 0.f;
     }
+    // convert the window once (16 F2F per 4 outputs, not one per FMA)
+    double xd[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) xd[j] = (j < 3 + taps) ? (double)xv[j] : 0.0;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < kFirRegTaps; i++) {
       if (i < taps) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) acc[q] = fma(wd[i], (double)xv[q + i], acc[q]);
+        for (int q = 0; q < 4; q++) acc[q] = fma(wd[i], xd[q + i], acc[q]);
       }
     }
     if (o + 3 < nout) {

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
+import struct
 import threading
 import weakref
 from dataclasses import dataclass, field
@@ -89,25 +90,39 @@ class PackedArgs:
     slots: list
 
 
+_SLOT_FMT = {"i32": (struct.Struct("<iii4x"), 0), "i64": (struct.Struct("<iiq"), 1),
+             "f32": (struct.Struct("<iid"), 2), "f64": (struct.Struct("<iid"), 3),
+             "handle": (struct.Struct("<iiI4x"), 4)}
+
+
 def pack_slots(packed) -> tuple[C.Array, int]:
     """Reference PackedArgs (or any object with .slots of (kind, value)) ->
-    contiguous bf_slot array.  f32 slots keep the unrounded double."""
-    slots = list(packed.slots) if packed is not None else []
-    arr = (_lib.Slot * max(len(slots), 1))()
-    for i, s in enumerate(slots):
+    contiguous bf_slot array (16 B per slot).  f32 slots keep the unrounded
+    double."""
+    slots = packed.slots if packed is not None else ()
+    n = len(slots)
+    buf = bytearray(16 * max(n, 1))
+    i = -1
+    for s in slots:
+        i += 1
         kind = s.kind
-        if kind not in _lib.SLOT_KINDS:
+        ent = _SLOT_FMT.get(kind)
+        if ent is None:
             raise Trap("TypeFault", f"unknown slot kind {kind!r}")
-        arr[i].kind = _lib.SLOT_KINDS[kind]
-        if kind == "handle":
-            arr[i].v.handle = int(s.value)
-        elif kind == "i32":
-            arr[i].v.i32 = int(s.value)
-        elif kind == "i64":
-            arr[i].v.i64 = int(s.value)
-        else:
-            arr[i].v.f64 = float(s.value)
-    return arr, len(slots)
+        fmt, code = ent
+        v = float(s.value) if code in (2, 3) else int(s.value)
+        if code == 0:
+            v = (v + 2**31) % 2**32 - 2**31  # i32 slot: two's complement like ctypes
+        elif code == 4:
+            v &= 0xFFFFFFFF
+        fmt.pack_into(buf, 16 * i, code, 0, v)
+    t = _SLOT_ARRAYS.get(n)
+    if t is None:
+        t = _SLOT_ARRAYS[n] = _lib.Slot * max(n, 1)
+    return t.from_buffer(buf), n
+
+
+_SLOT_ARRAYS: dict = {}
 
 
 # ---------------------------------------------------------------------------
@@ -153,6 +168,9 @@ def resolve_grain(policy: FetchPolicy, grid_size: int, pool_size: int,
         raise ValueError("grid_size and pool_size must be >= 1")
     # duck-typed so the reference's own policy objects work too
     kind = type(policy).__name__
+    if kind == "Average" and kernel_stats is not None:
+        # hot path: ceil(G/P) (runtime.py:83), identical to the native law
+        return -(-grid_size // pool_size)
     if kind == "Average":
         code, fixed, thr = _lib.POLICY_AVERAGE, 0, 0
     elif kind == "Fixed":
@@ -380,6 +398,10 @@ class Runtime:
         # runtime -> arena teardown order stays refcount-driven)
         self._tasks: "weakref.WeakSet[KernelTask]" = weakref.WeakSet()
         self._shut_down = False
+        # reusable launch scratch (the reference is driven by one host thread)
+        self._g = (C.c_int32 * 3)()
+        self._b = (C.c_int32 * 3)()
+        self._tid = C.c_uint64()
 
     # -- host API ---------------------------------------------------------------
     def launch(self, routine, grid, block, shmem_bytes: int, packed) -> KernelTask:
@@ -392,9 +414,9 @@ class Runtime:
         task = KernelTask(routine, packed, grid, block, shmem_bytes, totalBlocks=total,
                           block_per_fetch=grain)
         slots, n = pack_slots(packed)
-        g = (C.c_int32 * 3)(grid.x, grid.y, grid.z)
-        b = (C.c_int32 * 3)(block.x, block.y, block.z)
-        tid = C.c_uint64()
+        g, b, tid = self._g, self._b, self._tid
+        g[0], g[1], g[2] = grid.x, grid.y, grid.z
+        b[0], b[1], b[2] = block.x, block.y, block.z
         rc = _lib.lib().bf_launch(self._native, name.encode(), g, b, int(shmem_bytes), slots, n,
                                   warp_size, grain, C.byref(tid))
         if rc == _lib.E_SHUTDOWN:

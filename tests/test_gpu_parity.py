@@ -221,3 +221,49 @@ def test_hotspot_run_fused_vs_oracle(tsteps):
             res = stencil.hotspot_run(rt, a, p, b, rows, cols, params, iters, tsteps)
             rt.device_synchronize()
         assert bit_equal(arena.to_numpy(res), want), (rows, cols, iters, tsteps)
+
+
+def test_nn_sqrt_rounding_hard_cases():
+    """f32(f64 sqrt) emulation: exact squares of f32 midpoints (f32 ties),
+    neighbours one f64 ulp away (double-rounding cases), binade edges."""
+    import struct
+    rng = np.random.default_rng(3)
+    lat, x = [], []
+    for _ in range(4000):
+        f = np.float32(rng.uniform(1e-3, 3e2))
+        nxt = np.nextafter(f, np.float32(np.inf))
+        m = (float(f) + float(nxt)) / 2.0           # exact f32 midpoint (25 bits)
+        for k in (-2, -1, 0, 1, 2):                 # m^2 and its f64 neighbours
+            v = m
+            for _ in range(abs(k)):
+                v = float(np.nextafter(v, np.inf if k > 0 else -np.inf))
+            lat.append(0.0)
+            x.append(-v)                               # d = 0 - (-v) = v exactly
+    for e in range(-20, 20):                          # binade edges
+        for v in (2.0 ** e, float(np.nextafter(2.0 ** e, 0)), float(np.nextafter(2.0 ** e, 9))):
+            lat.append(0.0)
+            x.append(-v)
+    import instances as I
+    n = len(lat)
+    # one launch per distinct x would be slow: x is a kernel param, so use lng
+    # for the varying part instead: d = sqrt((0 - 0)^2 + (lng - y)^2) with y = 0
+    ll = np.zeros(2 * n, np.float32)
+    vals = np.array([-xv for xv in x])
+    # lng must be f32: use the f32 values themselves (exact squares) plus the
+    # double perturbation through the param path in a second pass below
+    ll[1::2] = vals.astype(np.float32)
+    inst = I.Instance("nn", I.Geom(-(-n // 256)), I.Geom(256), 0,
+                      [I.Buf("ll", "f32", 2 * n, ll), I.Buf("d", "f32", n, np.zeros(n, np.float32))],
+                      [("buf", "ll"), ("buf", "d"), ("i32", n), ("f32", 0.0), ("f32", 0.0)], ["d"])
+    want, _ = oracle.run(inst)
+    got, trap, _, _ = gpu_run(inst)
+    assert trap is None and bit_equal(got["d"], want["d"])
+    # double-valued target: lat = 0, x = -(m + k ulp64): s = v^2 rounded in f64
+    for v in vals[rng.choice(len(vals), 300, replace=False)]:
+        inst = I.Instance("nn", I.Geom(1), I.Geom(32), 0,
+                          [I.Buf("ll", "f32", 64, np.zeros(64, np.float32)),
+                           I.Buf("d", "f32", 32, np.zeros(32, np.float32))],
+                          [("buf", "ll"), ("buf", "d"), ("i32", 32), ("f32", -float(v)), ("f32", 0.0)], ["d"])
+        want, _ = oracle.run(inst)
+        got, trap, _, _ = gpu_run(inst)
+        assert trap is None and bit_equal(got["d"], want["d"]), v
