@@ -223,9 +223,9 @@ int bf_bfs_levels(bf_runtime *rt, uint32_t row, uint32_t col, uint32_t lvl,
 /* Rodinia's hotspot host loop fused: the result of `iterations` ping-pong
  * launches of `hotspot` (kernels/hotspot.kn) starting from buffer `a`, with
  * `b` as the other buffer — bit-identical.  tsteps = 1: one streaming pass
- * per iteration issued from C++; tsteps > 1: temporal blocking, `tsteps`
- * iterations per pass through HBM (shared-memory tiles); 0 = default (1,
- * the faster on B200 in round 1).  The result
+ * per iteration; 2..4: register-wavefront temporal blocking (`tsteps`
+ * iterations per pass through HBM); 8/12/16: shared-memory tiles; 0 =
+ * default (4, the fastest on B200 in round 1).  The result
  * lands where the launch loop leaves it: `a` for even, `b` for odd
  * `iterations`; the other buffer is scratch.  params = {step/Cap, 1/Rx,
  * 1/Ry, 1/Rz, ambient} as doubles.  Asynchronous on worker 0's stream,

@@ -121,6 +121,169 @@ __global__ void __launch_bounds__(512) hotspot_tb(const float* __restrict__ src,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register wavefront (temporal blocking without shared memory).
+// A warp owns a strip of 32 lanes x 4 columns (float4 per lane) and a band of
+// rows; lanes 0 and 31 are halo, lanes 1..30 the strip's 120 output columns
+// (strips overlap by 8 columns).  T time levels advance together down the
+// rows: in wave i level 0 takes row i (loaded once from HBM) and level L
+// computes row i-L from the last three rows of level L-1, which stay in
+// registers as f64 copies of their f32-rounded values (exact), so a cell
+// costs 13 f64 ops + 3 converts per level.  West/east neighbours come from
+// warp shuffles.  Border rows clamp: level L's "row -1" is its row 0 and its
+// "row rows" is row rows-1 (the DSL's max/min clamps).  Invalid columns
+// spread one column per level from a strip edge, so T <= 4 keeps lanes 1..30
+// exact.  Bit-identical to T launches of hotspot.kn.
+// ---------------------------------------------------------------------------
+struct D4 {
+  double x, y, z, w;
+};
+
+__device__ __forceinline__ D4 d4_of(float4 v) {
+  return D4{(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+}
+
+__device__ __forceinline__ double hs_cell_d(double tc, double tn, double ts, double tw, double te,
+                                            double p, const HsConstF& k, float& out) {
+  const double two_tc = dmul(2.0, tc);
+  const double a = dsub(dadd(ts, tn), two_tc);
+  const double b = dsub(dadd(te, tw), two_tc);
+  const double c = dsub(k.amb, tc);
+  double acc = dadd(p, dmul(a, k.ry1));
+  acc = dadd(acc, dmul(b, k.rx1));
+  acc = dadd(acc, dmul(c, k.rz1));
+  out = __double2float_rn(dadd(tc, dmul(k.sdc, acc)));
+  return (double)out;
+}
+
+constexpr int kWaveOut = 120;  // output columns per strip
+
+template <int T>
+__global__ void __launch_bounds__(128) hotspot_wave(const float* __restrict__ src,
+                                                    const float* __restrict__ power,
+                                                    float* __restrict__ dst, int rows, int cols,
+                                                    HsConstF k, int strips, int bands) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (w >= strips * bands) return;  // warp-uniform
+  const int strip = w % strips, band = w / strips;
+  const int rs = (int)((long long)rows * band / bands);
+  const int re = (int)((long long)rows * (band + 1) / bands);
+  if (rs >= re) return;
+  const int c0 = strip * kWaveOut;
+  const int cl = c0 - 4 + 4 * lane;
+  const bool in_grid = cl >= 0 && cl + 3 < cols;
+  const bool out_lane = lane >= 1 && lane <= 30 && in_grid;
+  const bool left_edge = cl == 0, right_edge = cl + 3 == cols - 1;
+  const long long colsl = cols;
+
+  auto load_src = [&](int r) -> float4 {
+    r = r < 0 ? 0 : (r > rows - 1 ? rows - 1 : r);
+    return in_grid ? __ldg(reinterpret_cast<const float4*>(src + r * colsl + cl))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto load_pow = [&](int r) -> float4 {
+    r = r < 0 ? 0 : (r > rows - 1 ? rows - 1 : r);
+    return in_grid ? __ldg(reinterpret_cast<const float4*>(power + r * colsl + cl))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+
+  D4 R[T][3];  // R[L] = rows (j-2, j-1, j) of level L, j its newest row
+  float4 P[T];  // P[m] = power row i-1-m
+#pragma unroll
+  for (int L = 0; L < T; L++) {
+    R[L][0] = R[L][1] = R[L][2] = D4{0, 0, 0, 0};
+    P[L] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int i0 = rs - T, i1 = re - 1 + T;
+  // one wave of prefetch: the input and power rows of wave i+1 are in flight
+  // while wave i computes
+  float4 nxt_src = load_src(i0), nxt_pow = load_pow(i0 - 1);
+#pragma unroll 1
+  for (int i = i0; i <= i1; i++) {
+    const float4 cur_src = nxt_src, cur_pow = nxt_pow;
+    nxt_src = load_src(i + 1);
+    nxt_pow = load_pow(i);
+    // level 0: extended row i of the input (rows clamp at the borders)
+    {
+      const D4 v = d4_of(cur_src);
+      R[0][0] = R[0][1];
+      R[0][1] = R[0][2];
+      R[0][2] = v;
+    }
+#pragma unroll
+    for (int m = T - 1; m > 0; m--) P[m] = P[m - 1];
+    P[0] = cur_pow;
+#pragma unroll
+    for (int L = 1; L <= T; L++) {
+      const int j = i - L;  // row computed at level L in this wave
+      D4 nv;
+      float4 fo = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j == rows) {
+        nv = R[L < T ? L : 0][2];  // ext row rows == row rows-1 (only needed below level T)
+      } else {
+        const D4 n = R[L - 1][0], c = R[L - 1][1], s = R[L - 1][2];
+        double west = __shfl_up_sync(0xffffffffu, c.w, 1);
+        double east = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (left_edge) west = c.x;
+        if (right_edge) east = c.w;
+        const float4 pw = P[L - 1];
+        nv.x = hs_cell_d(c.x, n.x, s.x, west, c.y, (double)pw.x, k, fo.x);
+        nv.y = hs_cell_d(c.y, n.y, s.y, c.x, c.z, (double)pw.y, k, fo.y);
+        nv.z = hs_cell_d(c.z, n.z, s.z, c.y, c.w, (double)pw.z, k, fo.z);
+        nv.w = hs_cell_d(c.w, n.w, s.w, c.z, east, (double)pw.w, k, fo.w);
+      }
+      if (L < T) {
+        R[L][0] = R[L][1];
+        R[L][1] = R[L][2];
+        R[L][2] = nv;
+        if (j == 0) R[L][1] = nv;  // ext row -1 of level L is its row 0
+      } else if (j >= rs && j < re && out_lane) {
+        *reinterpret_cast<float4*>(dst + j * colsl + cl) = fo;
+      }
+    }
+  }
+}
+
+template <int T>
+static int wave_pass(cudaStream_t stream, int num_sms, const float* a, const float* p, float* b,
+                     int rows, int cols, const HsConstF& k) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    int ctas = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, hotspot_wave<T>, 128, 0);
+    cudaGetLastError();
+    per_sm = ctas > 0 ? ctas * 4 : 8;
+  }
+  const int strips = (cols + kWaveOut - 1) / kWaveOut;
+  int bands = std::max(1, per_sm * num_sms / strips);
+  if (bands > rows) bands = rows;
+  const int grid = (strips * bands + 3) / 4;
+  hotspot_wave<T><<<grid, 128, 0, stream>>>(a, p, b, rows, cols, k, strips, bands);
+  return cudaGetLastError() == cudaSuccess ? BF_OK : BF_E_CUDA;
+}
+
+static int wave_run(cudaStream_t stream, int num_sms, float* a, float* b, const float* p, int rows,
+                    int cols, const HsConstF& k, int iterations, int T, float** result) {
+  float* cur = a;
+  float* nxt = b;
+  for (int done = 0; done < iterations;) {
+    const int t = std::min(T, iterations - done);
+    int rc;
+    switch (t) {
+      case 1: rc = wave_pass<1>(stream, num_sms, cur, p, nxt, rows, cols, k); break;
+      case 2: rc = wave_pass<2>(stream, num_sms, cur, p, nxt, rows, cols, k); break;
+      case 3: rc = wave_pass<3>(stream, num_sms, cur, p, nxt, rows, cols, k); break;
+      default: rc = wave_pass<4>(stream, num_sms, cur, p, nxt, rows, cols, k); break;
+    }
+    if (rc) return rc;
+    done += t;
+    std::swap(cur, nxt);
+  }
+  *result = cur;
+  return BF_OK;
+}
+
 template <int T>
 static int run_passes(cudaStream_t stream, float* a, float* b, const float* p, int rows, int cols,
                       const HsConstF& k, int iterations, float** result) {
@@ -164,11 +327,15 @@ extern "C" int bf_hotspot_run_impl(void* stream_v, int num_sms, float* a, float*
   HsConstF k{kc[0], kc[1], kc[2], kc[3], kc[4]};
   if (tsteps <= 0) {
     const char* e = getenv("BF_HOTSPOT_T");
-    tsteps = e ? atoi(e) : 1;
+    tsteps = e ? atoi(e) : 4;  // register wavefront, 4 levels: fastest in round 1
   }
   float* res = nullptr;
   int rc = BF_OK;
-  if (tsteps == 1) {
+  const char* we = getenv("BF_HOTSPOT_WAVE");
+  const bool wave = (we ? atoi(we) : 1) && cols % 4 == 0;
+  if (wave && tsteps >= 2 && tsteps <= 4) {
+    rc = wave_run(stream, num_sms, a, b, p, rows, cols, k, iterations, tsteps, &res);
+  } else if (tsteps == 1) {
     // measured fastest on B200 (round 1): the streaming band kernel per
     // iteration, issued back to back from C++ (no per-launch host work)
     float* cur = a;
@@ -179,6 +346,9 @@ extern "C" int bf_hotspot_run_impl(void* stream_v, int num_sms, float* a, float*
     }
     res = cur;
   } else switch (tsteps) {
+    case 3:  // wave unavailable (cols % 4 != 0): shared-memory tiles
+      rc = run_passes<4>(stream, a, b, p, rows, cols, k, iterations, &res);
+      break;
     case 2: rc = run_passes<2>(stream, a, b, p, rows, cols, k, iterations, &res); break;
     case 4: rc = run_passes<4>(stream, a, b, p, rows, cols, k, iterations, &res); break;
     case 12: rc = run_passes<12>(stream, a, b, p, rows, cols, k, iterations, &res); break;

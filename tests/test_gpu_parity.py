@@ -204,7 +204,7 @@ def test_bfs_levels_fused_vs_oracle():
         assert got_depth == depth
 
 
-@pytest.mark.parametrize("tsteps", [0, 1, 2, 4, 8, 12, 16])
+@pytest.mark.parametrize("tsteps", [0, 1, 2, 3, 4, 8, 12, 16])
 def test_hotspot_run_fused_vs_oracle(tsteps):
     """Temporal blocking == the per-launch ping-pong loop, bit for bit."""
     import instances as I
