@@ -467,6 +467,57 @@ def run_sweep(args) -> None:
         dist.destroy_process_group()
 
 
+def run_grain(args) -> None:
+    """the paper's grain-size study on the GPU runtime.
+    A fetch of `grain` logical blocks is one grid launch on a worker stream,
+    so the grain trades launch count against per-launch parallelism exactly
+    as block_per_fetch trades fetch count against load balance on the CPU
+    pool.  Reports fetches, wall time per launch+sync and
+    device throughput for vecadd and hist at pool sizes 1/4/8."""
+    import torch
+
+    from paper_2206_07896_b200 import (ArgSlot, Average, DeviceArena, Dim3, Fixed, PackedArgs,
+                                       Runtime, routines)
+    torch.cuda.set_device(0)
+    device = torch.device("cuda", 0)
+    n = 1 << 24
+    blocks = n // 256
+    arena = DeviceArena(0)
+    a, b, c = (arena.alloc("f32", n) for _ in range(3))
+    pix, cnt = arena.alloc("i32", n), arena.alloc("i32", 16)
+    for h in (a, b):
+        torch.as_tensor(arena.cuda_array(h), device=device).uniform_(-1, 1)
+    torch.as_tensor(arena.cuda_array(pix), device=device).random_(0, 1 << 16)
+    torch.cuda.synchronize()
+    cases = {
+        "vecadd": (routines.get("vecadd"), PackedArgs([ArgSlot("handle", a), ArgSlot("handle", b),
+                                                        ArgSlot("handle", c), ArgSlot("i32", n)]), 12 * n),
+        "hist": (routines.get("hist"), PackedArgs([ArgSlot("handle", pix), ArgSlot("handle", cnt),
+                                                    ArgSlot("i32", n), ArgSlot("i32", 16)]), 4 * n),
+    }
+    rows = []
+    for name, (routine, pk, nbytes) in cases.items():
+        for pool in (1, 4, 8):
+            for grain in (1, 16, 256, 4096, "average"):
+                policy = Average() if grain == "average" else Fixed(grain)
+                rt = Runtime(arena, pool_size=pool, policy=policy)
+                rt.launch(routine, Dim3(blocks), Dim3(256), 0, pk)
+                rt.device_synchronize()
+                reps = 3
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    task = rt.launch(routine, Dim3(blocks), Dim3(256), 0, pk)
+                    rt.device_synchronize()
+                wall = (time.perf_counter() - t0) / reps
+                rows.append({"kernel": name, "pool": pool, "grain": grain,
+                             "block_per_fetch": task.block_per_fetch, "fetches": task.fetches,
+                             "wall_ms": round(wall * 1e3, 4), "gbs": round(nbytes / wall / 1e9, 2)})
+                rt.shutdown()
+    print(json.dumps({"metric": "grain-size study (fetches vs launch+sync wall time)", "value": None,
+                      "unit": "GB/s", "n_gpus": 1, "config": {"workload": "vecadd/hist 2^24, 65536 blocks x 256"},
+                      "grain": rows}), flush=True)
+
+
 def per_kernel_table(arena, rt, torch, stream, args) -> tuple[dict, int]:
     """Every other kernel of the path at full size (benchkit.py), N=1."""
     import benchkit
@@ -513,7 +564,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["hotspot", "sweep"], default="hotspot")
+    ap.add_argument("--workload", choices=["hotspot", "sweep", "grain"], default="hotspot")
     ap.add_argument("--size", type=int, default=8192)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--halo", type=int, default=8)
@@ -531,6 +582,8 @@ def main() -> None:
         run_reference_arm(args)
     elif args.workload == "sweep":
         run_sweep(args)
+    elif args.workload == "grain":
+        run_grain(args)
     else:
         run_ours(args)
 
