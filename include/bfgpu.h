@@ -234,6 +234,17 @@ int bf_hotspot_run(bf_runtime *rt, uint32_t a, uint32_t power, uint32_t b,
                    int32_t rows, int32_t cols, const double params[5],
                    int32_t iterations, int32_t tsteps);
 
+/* ---- JIT kernels ---------------------------------------- */
+/* Compile CUDA `source` (generated from a reference MpmdKernel by
+ * paper_2206_07896_b200/codegen.py) with NVRTC for sm_100a and register its
+ * extern "C" `entry` under `key`; bf_launch(key, ...) then runs it through
+ * the same fetch protocol as a hand-written kernel.  kinds/scalars as in
+ * bf_kernel_info; dyn_scalar is the bf_scalar of the extern shared array, or
+ * -1.  Idempotent per key; BF_E_INVALID carries the NVRTC log. */
+int bf_jit_register(const char *key, const char *source, const char *entry,
+                    int32_t nparams, const int32_t *kinds, const int32_t *scalars,
+                    int32_t dyn_scalar);
+
 /* ---- kernel registry ---------------------------------------------------- */
 int bf_kernel_count(int32_t *count);
 /* Name and parameter signature of registered kernel `index`: kinds[i] is a

@@ -37,7 +37,7 @@ EXPORTS = [
     "bf_synchronize", "bf_hold_new_blocks", "bf_task_get", "bf_task_executed",
     "bf_counters_get", "bf_worker_stream",
     "bf_kernel_count", "bf_kernel_info",
-    "bf_bfs_levels", "bf_hotspot_run",
+    "bf_bfs_levels", "bf_hotspot_run", "bf_jit_register",
 ]
 
 
@@ -114,6 +114,7 @@ def _declare(lib) -> None:
         "bf_kernel_count": (C.c_int, [I32P]),
         "bf_bfs_levels": (C.c_int, [P, u32, u32, u32, i32, i32, I32P]),
         "bf_hotspot_run": (C.c_int, [P, u32, u32, u32, i32, i32, C.POINTER(dbl), i32, i32]),
+        "bf_jit_register": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, i32, I32P, I32P, i32]),
         "bf_kernel_info": (C.c_int, [i32, C.c_char_p, i32, I32P, I32P, I32P, i32]),
     }
     for name, (res, args) in sig.items():

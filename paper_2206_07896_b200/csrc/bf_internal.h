@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -50,6 +51,7 @@ struct LaunchCtx {
   unsigned long long task;
   HostTrap* trap;            // host-side trap sink (first wins)
   std::string* error;        // BF_E_UNSUPPORTED / BF_E_CUDA message sink
+  const void* user = nullptr;  // KernelEntry::user (JIT kernels)
 
   KDesc desc() const;
   // Record a trap detected on the host before launching (e.g. an affine
@@ -78,15 +80,17 @@ struct KernelEntry {
   const char* name;
   std::vector<ParamSpec> params;
   LauncherFn launch;
+  const void* user = nullptr;
 };
 
-// Registry (populated by static registrars in each k_*.cu file).
-std::vector<KernelEntry>& registry();
+// Registry (static registrars in each k_*.cu file, plus JIT kernels added at
+// run time; a deque keeps entry addresses stable).
+std::deque<KernelEntry>& registry();
 const KernelEntry* find_kernel(const char* name);
 
 struct Registrar {
   Registrar(const char* name, std::vector<ParamSpec> params, LauncherFn fn) {
-    registry().push_back(KernelEntry{name, std::move(params), fn});
+    registry().push_back(KernelEntry{name, std::move(params), fn, nullptr});
   }
 };
 

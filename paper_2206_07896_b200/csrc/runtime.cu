@@ -11,8 +11,10 @@
 //   * pool workers -> `pool_size` in-order CUDA streams on the arena's device;
 //                     each fetched range of `grain` logical blocks becomes one
 //                     grid launch on the next worker stream (round robin).
-//   * hold_blocks  -> a gate kernel spinning on a host-mapped flag is queued in
-//                     front of each worker's work until the next synchronize.
+//   * hold_blocks  -> fetched ranges are kept on the host and issued, in
+//                     launch order, at the next synchronize: no block runs
+//                     before it, and nothing occupies the device meanwhile
+//                     (copies and JIT module loads proceed).
 //   * traps        -> a device fault word (first wins) plus host-detected traps,
 //                     surfaced at synchronize as BF_E_FAULT.
 #include <cuda_runtime.h>
@@ -56,8 +58,8 @@ static const int kScalarSize[4] = {4, 8, 4, 8};
 // registry
 // ---------------------------------------------------------------------------
 
-std::vector<KernelEntry>& registry() {
-  static std::vector<KernelEntry> r;
+std::deque<KernelEntry>& registry() {
+  static std::deque<KernelEntry> r;
   return r;
 }
 
@@ -248,6 +250,18 @@ struct bf_queue {
 
 namespace bf {
 
+struct Fetch {
+  const KernelEntry* ke = nullptr;
+  std::shared_ptr<std::vector<ArgVal>> args;
+  HostTrap pre;
+  uint64_t task = 0;
+  int worker = 0;
+  long long first = 0, count = 0;
+  int grid[3], block[3];
+  int64_t shmem = 0;
+  int warp_size = 0;
+};
+
 struct FetchRecord {
   uint64_t task;
   int worker;
@@ -265,22 +279,6 @@ struct TaskRec {
   int* executed_dev = nullptr;  // BF_FLAG_INSTRUMENT
   std::vector<std::pair<long long, long long>> done_ranges;
 };
-
-__global__ void gate_kernel(volatile int* gate, DevFault* fault) {
-  // Spin until the host opens the gate at synchronize; bail out after 120 s
-  // so a host that never synchronizes cannot wedge the device.
-  unsigned long long t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (*gate == 0) {
-    __nanosleep(2000);
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 120ull * 1000000000ull) {
-      if (atomicCAS(&fault->kind, 0, BF_TRAP_NON_UNIFORM_TRIP) == 0) fault->block = -1;
-      return;
-    }
-  }
-}
 
 __global__ void delay_kernel(unsigned long long ns) {
   unsigned long long t0, t;
@@ -303,10 +301,7 @@ struct bf_runtime {
   int num_sms = 148;
   bool shut_down = false;
   std::vector<cudaStream_t> streams;
-  std::vector<bool> gated;       // worker already has a gate queued
-  volatile int* gate_host = nullptr;
-  int* gate_dev = nullptr;
-  bool holding = false;
+  bool holding = false;          // hold_blocks: launches wait on the host
   bf::DevFault* fault_dev = nullptr;
   bf::HostTrap trap;             // first trap (host- or device-detected)
   uint64_t trap_task = 0;
@@ -314,6 +309,7 @@ struct bf_runtime {
   bf_queue queue;
   std::map<uint64_t, bf::TaskRec> tasks;
   std::deque<bf::FetchRecord> inflight;
+  std::deque<bf::Fetch> deferred;  // held launches (hold_blocks)
   std::vector<cudaEvent_t> event_pool;
   uint64_t next_task = 1;
   uint64_t rr = 0;               // round-robin worker cursor
@@ -377,14 +373,23 @@ static int retire(bf_runtime* rt, bool wait) {
   return BF_OK;
 }
 
-static void open_gate(bf_runtime* rt) {
-  if (rt->gate_host) *rt->gate_host = 1;
+static int issue_fetch(bf_runtime* rt, Fetch& f);
+
+// Release a hold: issue every deferred fetch in launch order.
+static int open_gate(bf_runtime* rt) {
   rt->holding = false;
-  std::fill(rt->gated.begin(), rt->gated.end(), false);
+  while (!rt->deferred.empty()) {
+    Fetch f = std::move(rt->deferred.front());
+    rt->deferred.pop_front();
+    int rc = issue_fetch(rt, f);
+    if (rc) return rc;
+  }
+  return BF_OK;
 }
 
 static int sync_workers(bf_runtime* rt) {
-  open_gate(rt);
+  int rc = open_gate(rt);
+  if (rc) return rc;
   for (auto s : rt->streams) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
@@ -405,7 +410,7 @@ static void absorb_device_fault(bf_runtime* rt) {
     rt->trap_task = f.task;
     rt->trap_kernel = it == rt->tasks.end() ? "?" : it->second.kernel;
     static const char* names[] = {"", "index out of range", "division by zero",
-                                  "type fault", "non-uniform trip / gate timeout"};
+                                  "type fault", "non-uniform trip"};
     rt->trap.message = std::string(names[f.kind < 5 ? f.kind : 0]) + " (device)";
   }
 }
@@ -802,7 +807,6 @@ int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double blo
   rt->block_delay = block_delay;
   rt->rng.seed(seed);
   rt->busy.assign(pool_size, 0);
-  rt->gated.assign(pool_size, false);
   cudaDeviceGetAttribute(&rt->num_sms, cudaDevAttrMultiProcessorCount, a->device);
   for (int i = 0; i < pool_size; i++) {
     cudaStream_t s;
@@ -814,17 +818,7 @@ int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double blo
     }
     rt->streams.push_back(s);
   }
-  void* gh = nullptr;
-  if (cudaHostAlloc(&gh, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
-    cudaGetLastError();
-    for (auto x : rt->streams) cudaStreamDestroy(x);
-    delete rt;
-    return fail(BF_E_CUDA, "cudaHostAlloc(gate) failed");
-  }
-  rt->gate_host = (volatile int*)gh;
-  *rt->gate_host = (flags & BF_FLAG_HOLD_BLOCKS) ? 0 : 1;
   rt->holding = (flags & BF_FLAG_HOLD_BLOCKS) != 0;
-  cudaHostGetDevicePointer((void**)&rt->gate_dev, gh, 0);
   if (cudaMalloc(&rt->fault_dev, sizeof(DevFault)) != cudaSuccess ||
       cudaMemset(rt->fault_dev, 0, sizeof(DevFault)) != cudaSuccess) {
     cudaGetLastError();
@@ -855,7 +849,6 @@ int bf_runtime_destroy(bf_runtime* rt) {
   for (auto& kv : rt->tasks)
     if (kv.second.executed_dev) cudaFree(kv.second.executed_dev);
   if (rt->fault_dev) cudaFree(rt->fault_dev);
-  if (rt->gate_host) cudaFreeHost((void*)rt->gate_host);
   bf_arena* a = rt->arena;
   a->live_runtimes--;
   if (a->live_runtimes == 0) {
@@ -865,6 +858,74 @@ int bf_runtime_destroy(bf_runtime* rt) {
   delete rt;
   return BF_OK;
 }
+
+}  // extern "C"
+
+namespace bf {
+// One fetched block range, issued as one grid launch on a worker stream.
+static int issue_fetch(bf_runtime* rt, Fetch& f) {
+  cudaStream_t s = rt->streams[f.worker];
+  TaskRec& tr = rt->tasks[f.task];
+  if (rt->block_delay > 0.0) {
+    std::uniform_real_distribution<double> u(0.0, rt->block_delay);
+    delay_kernel<<<1, 1, 0, s>>>((unsigned long long)(u(rt->rng) * 1e9));
+  }
+  if (f.pre.kind != BF_TRAP_NONE) {
+    // reference: the trap aborts the worker's range (runtime.py:335-343)
+    if (rt->trap.kind == BF_TRAP_NONE) {
+      rt->trap = f.pre;
+      rt->trap.block = f.first;
+      rt->trap_task = f.task;
+      rt->trap_kernel = tr.kernel;
+    }
+  } else {
+    LaunchCtx ctx;
+    ctx.name = f.ke->name;
+    for (int i = 0; i < 3; i++) {
+      ctx.grid[i] = f.grid[i];
+      ctx.block[i] = f.block[i];
+    }
+    ctx.first = f.first;
+    ctx.count = f.count;
+    ctx.shmem = f.shmem;
+    ctx.warp_size = f.warp_size;
+    ctx.args = f.args->data();
+    ctx.nargs = (int)f.args->size();
+    ctx.stream = s;
+    ctx.num_sms = rt->num_sms;
+    ctx.executed = tr.executed_dev;
+    ctx.fault = rt->fault_dev;
+    ctx.task = f.task;
+    HostTrap ht;
+    std::string err;
+    ctx.trap = &ht;
+    ctx.error = &err;
+    ctx.user = f.ke->user;
+    int lrc = f.ke->launch(ctx);
+    if (lrc != BF_OK) return fail(lrc, std::string(f.ke->name) + ": " + err);
+    if (tr.executed_dev) {
+      int g = (int)std::min<long long>((f.count + 255) / 256, 1184);
+      mark_kernel<<<g, 256, 0, s>>>(tr.executed_dev, f.first, f.count);
+    }
+    if (ht.kind != BF_TRAP_NONE && rt->trap.kind == BF_TRAP_NONE) {
+      rt->trap = ht;
+      rt->trap_task = f.task;
+      rt->trap_kernel = tr.kernel;
+    }
+  }
+  FetchRecord fr;
+  fr.task = f.task;
+  fr.worker = f.worker;
+  fr.first = f.first;
+  fr.count = f.count;
+  fr.done = get_event(rt);
+  CK(cudaEventRecord(fr.done, s));
+  rt->inflight.push_back(fr);
+  return BF_OK;
+}
+}  // namespace bf
+
+extern "C" {
 
 int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const int32_t block[3],
               int64_t shmem_bytes, const bf_slot* slots, int32_t nslots, int32_t warp_size,
@@ -950,6 +1011,7 @@ int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const i
   // push + dispatch: the host dispatcher plays the pool's fetch loop
   rc = bf_queue_push(&rt->queue, id, total, grain);
   if (rc) return rc;
+  auto shared_args = std::make_shared<std::vector<ArgVal>>(std::move(args));
   for (;;) {
     int32_t got = 0;
     uint64_t tag;
@@ -958,66 +1020,28 @@ int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const i
     if (!got) break;
     tr.fetches += 1;
     tr.cursor = first + count;
-    int w = (int)(rt->rr++ % (uint64_t)rt->pool);
-    cudaStream_t s = rt->streams[w];
-    if (rt->holding && !rt->gated[w]) {
-      gate_kernel<<<1, 1, 0, s>>>((volatile int*)rt->gate_dev, rt->fault_dev);
-      rt->gated[w] = true;
+    Fetch f;
+    f.ke = ke;
+    f.args = shared_args;
+    f.pre = pre;
+    f.task = id;
+    f.worker = (int)(rt->rr++ % (uint64_t)rt->pool);
+    f.first = first;
+    f.count = count;
+    for (int k = 0; k < 3; k++) {
+      f.grid[k] = grid[k];
+      f.block[k] = block[k];
     }
-    if (rt->block_delay > 0.0) {
-      std::uniform_real_distribution<double> u(0.0, rt->block_delay);
-      delay_kernel<<<1, 1, 0, s>>>((unsigned long long)(u(rt->rng) * 1e9));
-    }
-    if (pre.kind != BF_TRAP_NONE) {
-      // reference: the trap aborts the worker's range (runtime.py:335-343)
-      if (rt->trap.kind == BF_TRAP_NONE) {
-        rt->trap = pre;
-        rt->trap.block = first;
-        rt->trap_task = id;
-        rt->trap_kernel = kernel;
-      }
+    f.shmem = shmem_bytes;
+    f.warp_size = warp_size;
+    if (rt->holding) {
+      // hold_blocks: nothing reaches the device before the next synchronize
+      // (runtime.py:219-222, 311); launches stay queued on the host
+      rt->deferred.push_back(std::move(f));
     } else {
-      LaunchCtx ctx;
-      ctx.name = kernel;
-      for (int i = 0; i < 3; i++) {
-        ctx.grid[i] = grid[i];
-        ctx.block[i] = block[i];
-      }
-      ctx.first = first;
-      ctx.count = count;
-      ctx.shmem = shmem_bytes;
-      ctx.warp_size = warp_size;
-      ctx.args = args.data();
-      ctx.nargs = (int)args.size();
-      ctx.stream = s;
-      ctx.num_sms = rt->num_sms;
-      ctx.executed = tr.executed_dev;
-      ctx.fault = rt->fault_dev;
-      ctx.task = id;
-      HostTrap ht;
-      std::string err;
-      ctx.trap = &ht;
-      ctx.error = &err;
-      int lrc = ke->launch(ctx);
-      if (lrc != BF_OK) return fail(lrc, std::string(kernel) + ": " + err);
-      if (tr.executed_dev) {
-        int g = (int)std::min<long long>((count + 255) / 256, 1184);
-        mark_kernel<<<g, 256, 0, s>>>(tr.executed_dev, first, count);
-      }
-      if (ht.kind != BF_TRAP_NONE && rt->trap.kind == BF_TRAP_NONE) {
-        rt->trap = ht;
-        rt->trap_task = id;
-        rt->trap_kernel = kernel;
-      }
+      rc = issue_fetch(rt, f);
+      if (rc) return rc;
     }
-    FetchRecord fr;
-    fr.task = id;
-    fr.worker = w;
-    fr.first = first;
-    fr.count = count;
-    fr.done = get_event(rt);
-    CK(cudaEventRecord(fr.done, s));
-    rt->inflight.push_back(fr);
   }
   return BF_OK;
 }
@@ -1045,9 +1069,7 @@ int bf_synchronize(bf_runtime* rt, bf_fault* fault) {
 
 int bf_hold_new_blocks(bf_runtime* rt) {
   if (!rt) return fail(BF_E_INVALID, "null runtime");
-  *rt->gate_host = 0;
   rt->holding = true;
-  std::fill(rt->gated.begin(), rt->gated.end(), false);
   return BF_OK;
 }
 
@@ -1076,10 +1098,10 @@ int bf_task_executed(bf_runtime* rt, uint64_t task_id, int32_t* executed, int64_
     // device-observed counts are only meaningful once the fetches drained;
     // the copy is ordered after every worker's work
     for (auto s : rt->streams) {
-      if (*rt->gate_host == 0) break;  // held: nothing has run yet
+      if (rt->holding) break;  // held: nothing has run yet
       CK(cudaStreamSynchronize(s));
     }
-    if (*rt->gate_host == 0) {
+    if (rt->holding) {
       std::memset(executed, 0, n * sizeof(int32_t));
       return BF_OK;
     }
@@ -1176,6 +1198,23 @@ int bf_hotspot_run(bf_runtime* rt, uint32_t a, uint32_t power, uint32_t b, int32
                            (const float*)P->ptr, rows, cols, params, iterations, tsteps, err,
                            sizeof(err));
   if (rc) return fail(rc, err);
+  return BF_OK;
+}
+
+// ---- JIT kernels ---------------------------------------------------------------
+
+int bf_jit_register_impl(const char* key, const char* source, const char* entry, int32_t nparams,
+                         const int32_t* kinds, const int32_t* scalars, int32_t dyn_scalar,
+                         char* log, int32_t logcap);
+
+int bf_jit_register(const char* key, const char* source, const char* entry, int32_t nparams,
+                    const int32_t* kinds, const int32_t* scalars, int32_t dyn_scalar) {
+  if (!key || !source || !entry || nparams < 0 || (nparams > 0 && (!kinds || !scalars)))
+    return fail(BF_E_INVALID, "null argument");
+  std::vector<char> log(16384, 0);
+  int rc = bf_jit_register_impl(key, source, entry, nparams, kinds, scalars, dyn_scalar,
+                                log.data(), (int32_t)log.size());
+  if (rc) return fail(rc, log.data());
   return BF_OK;
 }
 

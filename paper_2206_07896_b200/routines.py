@@ -6,12 +6,13 @@ intrinsics, `has_atomics()` and `static_instruction_estimate()` feed the
 AutoAggressive grain (runtime.py:78-101) and `to_dict()` is a stable
 fingerprint of the kernel body.
 
-`Runtime.launch` accepts either a reference `MpmdKernel` (duck-typed; its
-fingerprint must match the kernel this package implements — a different body
-under a known name is rejected, never silently run) or a `Routine` from this
-module, which carries the same fields for the kernels implemented as sm_100a
-code.  The fingerprints were produced from the reference's own `transform()`
-by oracle/gen_golden.py (see tests/golden/fingerprints.json).
+`Runtime.launch` accepts either a reference `MpmdKernel` (duck-typed) or a
+`Routine` from this module, which carries the same fields for the kernels
+implemented as hand-written sm_100a code.  A reference kernel whose name and
+body fingerprint match a registered kernel runs the hand-written kernel (the
+fingerprints were produced from the reference's own `transform()` by
+oracle/gen_golden.py); any other reference kernel is compiled from its AST
+by codegen.py + NVRTC (bf_jit_register) — never run on the CPU.
 """
 
 from __future__ import annotations
@@ -26,8 +27,8 @@ KERNEL_DIR = Path(__file__).resolve().parent / "kernels"
 
 
 class KernelNotImplemented(Exception):
-    """No sm_100a implementation exists for this routine (there is no CPU
-    fallback)."""
+    """No sm_100a implementation exists and none can be generated for this
+    routine (there is no CPU fallback)."""
 
 
 @dataclass(frozen=True)
@@ -124,24 +125,64 @@ def expected_fingerprint(name: str) -> Optional[str]:
     return _fps.get(name)
 
 
-def resolve(routine) -> tuple[str, bool, int]:
-    """(name, warp_mode, warp_size) for a Routine or a reference MpmdKernel.
+# Tests set this to route even the registered kernels through the JIT path.
+FORCE_JIT = False
+_jit_keys: dict = {}
 
-    Raises KernelNotImplemented for names without an sm_100a kernel and for a
-    reference kernel whose body differs from the implemented one."""
+
+def _jit_key(routine) -> str:
+    """Compile (once per process) a reference MpmdKernel through codegen.py +
+    NVRTC and return its registry key."""
+    import ctypes as C
+
+    from . import _lib, codegen
+    fp = codegen.fingerprint(routine)
+    key = "jit:" + fp[:32]
+    if key in _jit_keys:
+        return key
+    try:
+        src, entry, spec = codegen.generate(routine)
+    except codegen.CodegenError as e:
+        raise KernelNotImplemented(f"kernel {routine.name!r}: cannot generate CUDA: {e}") from None
+    n = len(spec)
+    kinds = (C.c_int32 * max(n, 1))(*[_lib.SLOT_KINDS[k] for k, _ in spec])
+    scal = (C.c_int32 * max(n, 1))(*[_lib.SCALARS[s] if s else 0 for _, s in spec])
+    dyn = getattr(routine.shared_layout, "dynamic_scalar", None)
+    rc = _lib.lib().bf_jit_register(key.encode(), src.encode(), entry.encode(), n, kinds, scal,
+                                    _lib.SCALARS[dyn] if dyn else -1)
+    if rc != _lib.OK:
+        raise KernelNotImplemented(f"kernel {routine.name!r}: JIT compile failed: {_lib.last_error()}")
+    _jit_keys[key] = src
+    return key
+
+
+def resolve(routine) -> tuple[str, bool, int]:
+    """(registry key, warp_mode, warp_size) for a Routine or a reference
+    MpmdKernel.
+
+    A registered name with a matching body runs its hand-written sm_100a
+    kernel.  Any other reference kernel (a different body under a known
+    name, or an unregistered name) is compiled from its AST (codegen.py,
+    NVRTC) and runs through the same runtime.  A `Routine` for an unknown
+    name, or an object without an AST, raises KernelNotImplemented."""
     name = getattr(routine, "name", None)
     if not isinstance(name, str):
         raise TypeError(f"launch routine must have a .name, got {routine!r}")
-    if name not in _TABLE:
-        raise KernelNotImplemented(
-            f"kernel {name!r} has no sm_100a implementation (registered: {', '.join(_TABLE)})")
-    if not isinstance(routine, Routine) and hasattr(routine, "to_dict"):
-        want = expected_fingerprint(name)
-        got = fingerprint_of(routine.to_dict())
-        if want is not None and got != want:
-            raise KernelNotImplemented(
-                f"kernel {name!r}: body differs from the implemented one (fingerprint {got[:12]} "
-                f"!= {want[:12]}); only the registered kernels run on the GPU")
     warp_mode = bool(getattr(routine, "warp_mode", False))
     warp_size = int(getattr(routine, "warp_size", 32)) if warp_mode else 0
-    return name, warp_mode, warp_size
+    has_ast = hasattr(routine, "sections") and hasattr(routine, "to_dict")
+    registered = name in _TABLE
+    if registered and not FORCE_JIT:
+        if isinstance(routine, Routine) or not hasattr(routine, "to_dict"):
+            return name, warp_mode, warp_size
+        want = expected_fingerprint(name)
+        got = fingerprint_of(routine.to_dict())
+        if want is None or got == want:
+            return name, warp_mode, warp_size
+    if has_ast:
+        return _jit_key(routine), warp_mode, warp_size
+    if registered:
+        return name, warp_mode, warp_size
+    raise KernelNotImplemented(
+        f"kernel {name!r} has no sm_100a implementation and no AST to compile "
+        f"(registered: {', '.join(_TABLE)})")

@@ -65,14 +65,22 @@ def test_our_kn_kernels_resolve(reference):
         assert r.static_instruction_estimate() == mk.static_instruction_estimate()
 
 
-def test_foreign_body_under_a_known_name_is_rejected(reference):
+def test_foreign_body_under_a_known_name_is_not_the_registered_kernel(reference):
+    """A different body under a registered name goes to the JIT path (its
+    own generated kernel), never to the hand-written `vecadd`."""
     from blockfuse.parser import parse
     from blockfuse.transform import transform
+    from paper_2206_07896_b200 import codegen
     mk = transform(parse("kernel vecadd(a: global f32[], b: global f32[], c: global f32[], n: i32) {"
                          " let id: i32 = blockIdx.x * blockDim.x + threadIdx.x;"
                          " if (id < n) { c[id] = a[id] - b[id]; } }"))
-    with pytest.raises(routines.KernelNotImplemented):
-        routines.resolve(mk)
+    src, entry, spec = codegen.generate(mk)
+    assert "(double)(" in src and entry.startswith("bfjit_")
+    try:
+        key = routines.resolve(mk)[0]
+    except routines.KernelNotImplemented:
+        return  # no device to load the module on: still not the registered kernel
+    assert key.startswith("jit:")
 
 
 def test_fingerprints_match_reference_transform(reference):
