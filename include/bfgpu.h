@@ -190,6 +190,14 @@ int bf_runtime_destroy(bf_runtime *rt);
 int bf_launch(bf_runtime *rt, const char *kernel, const int32_t grid[3],
               const int32_t block[3], int64_t shmem_bytes, const bf_slot *slots,
               int32_t nslots, int32_t warp_size, int64_t grain, uint64_t *task_id);
+/* One worker's share of a launch: only logical blocks [first, first+count)
+ * of the grid run (the fetched range of runtime.py:175-201 handed to this
+ * process — ranks of a multi-GPU job are the workers, parallel.py).  The
+ * task has `count` blocks; executed[] is indexed relative to `first`. */
+int bf_launch_range(bf_runtime *rt, const char *kernel, const int32_t grid[3],
+                    const int32_t block[3], int64_t shmem_bytes, const bf_slot *slots,
+                    int32_t nslots, int32_t warp_size, int64_t first, int64_t count,
+                    int64_t grain, uint64_t *task_id);
 /* Runtime.device_synchronize (runtime.py:269-278): releases a hold, waits for
  * every worker, increments syncs, and returns BF_E_FAULT with *fault filled
  * if any launch trapped (now or earlier). */

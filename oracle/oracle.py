@@ -60,8 +60,13 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def run(inst, nthreads: int = 1):
+def run(inst, nthreads: int = 1, block_range=None):
+    """block_range=(first, count): run only those logical blocks."""
     L = lib()
+    if block_range is None:
+        L.or_set_range(C.c_longlong(0), C.c_longlong(-1))
+    else:
+        L.or_set_range(C.c_longlong(block_range[0]), C.c_longlong(block_range[1]))
     bufs = {b.name: _arr(b) for b in inst.buffers}
     g = Geom(inst.grid.x, inst.grid.y, inst.grid.z, inst.block.x, inst.block.y, inst.block.z)
     t = OTrap()
@@ -105,6 +110,7 @@ def hotspot_iterate(temp: np.ndarray, power: np.ndarray, rows: int, cols: int, p
                     iterations: int, bx: int = 16, by: int = 16, nthreads: int = 1) -> np.ndarray:
     """`iterations` ping-pong launches of hotspot.kn; returns the final grid."""
     L = lib()
+    L.or_set_range(C.c_longlong(0), C.c_longlong(-1))
     a = np.ascontiguousarray(temp, np.float32).copy()
     b = np.zeros_like(a)
     p = np.ascontiguousarray(power, np.float32)

@@ -33,7 +33,7 @@ EXPORTS = [
     "bf_queue_create", "bf_queue_destroy", "bf_queue_push", "bf_queue_fetch",
     "bf_queue_close", "bf_queue_is_empty", "bf_queue_task", "bf_queue_counters",
     "bf_resolve_grain",
-    "bf_runtime_create", "bf_shutdown", "bf_runtime_destroy", "bf_launch",
+    "bf_runtime_create", "bf_shutdown", "bf_runtime_destroy", "bf_launch", "bf_launch_range",
     "bf_synchronize", "bf_hold_new_blocks", "bf_task_get", "bf_task_executed",
     "bf_counters_get", "bf_worker_stream",
     "bf_kernel_count", "bf_kernel_info",
@@ -105,6 +105,8 @@ def _declare(lib) -> None:
         "bf_shutdown": (C.c_int, [P]),
         "bf_runtime_destroy": (C.c_int, [P]),
         "bf_launch": (C.c_int, [P, C.c_char_p, I32P, I32P, i64, C.POINTER(Slot), i32, i32, i64, U64P]),
+        "bf_launch_range": (C.c_int, [P, C.c_char_p, I32P, I32P, i64, C.POINTER(Slot), i32, i32, i64, i64,
+                                      i64, U64P]),
         "bf_synchronize": (C.c_int, [P, C.POINTER(Fault)]),
         "bf_hold_new_blocks": (C.c_int, [P]),
         "bf_task_get": (C.c_int, [P, u64, C.POINTER(TaskInfo)]),

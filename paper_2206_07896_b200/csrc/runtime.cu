@@ -276,6 +276,7 @@ struct TaskRec {
   int64_t fetches = 0;
   int64_t cursor = 0;
   int64_t completed = 0;        // blocks of retired fetches
+  int64_t base = 0;             // first logical block (bf_launch_range)
   int* executed_dev = nullptr;  // BF_FLAG_INSTRUMENT
   std::vector<std::pair<long long, long long>> done_ranges;
 };
@@ -874,7 +875,7 @@ static int issue_fetch(bf_runtime* rt, Fetch& f) {
     // reference: the trap aborts the worker's range (runtime.py:335-343)
     if (rt->trap.kind == BF_TRAP_NONE) {
       rt->trap = f.pre;
-      rt->trap.block = f.first;
+      rt->trap.block = f.first;  // absolute block id
       rt->trap_task = f.task;
       rt->trap_kernel = tr.kernel;
     }
@@ -905,7 +906,7 @@ static int issue_fetch(bf_runtime* rt, Fetch& f) {
     if (lrc != BF_OK) return fail(lrc, std::string(f.ke->name) + ": " + err);
     if (tr.executed_dev) {
       int g = (int)std::min<long long>((f.count + 255) / 256, 1184);
-      mark_kernel<<<g, 256, 0, s>>>(tr.executed_dev, f.first, f.count);
+      mark_kernel<<<g, 256, 0, s>>>(tr.executed_dev - tr.base, f.first, f.count);
     }
     if (ht.kind != BF_TRAP_NONE && rt->trap.kind == BF_TRAP_NONE) {
       rt->trap = ht;
@@ -927,17 +928,25 @@ static int issue_fetch(bf_runtime* rt, Fetch& f) {
 
 extern "C" {
 
-int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const int32_t block[3],
-              int64_t shmem_bytes, const bf_slot* slots, int32_t nslots, int32_t warp_size,
-              int64_t grain, uint64_t* task_id) {
+static int launch_impl(bf_runtime* rt, const char* kernel, const int32_t grid[3],
+                       const int32_t block[3], int64_t shmem_bytes, const bf_slot* slots,
+                       int32_t nslots, int32_t warp_size, int64_t range_first,
+                       int64_t range_count, int64_t grain, uint64_t* task_id) {
   if (!rt || !kernel || !grid || !block) return fail(BF_E_INVALID, "null argument");
   if (rt->shut_down) return fail(BF_E_SHUTDOWN, "launch after shutdown");
   for (int i = 0; i < 3; i++)
     if (grid[i] < 1 || block[i] < 1) return fail(BF_E_INVALID, "dim3 components must be >= 1");
-  int64_t total = (int64_t)grid[0] * grid[1] * grid[2];
+  int64_t gtotal = (int64_t)grid[0] * grid[1] * grid[2];
   int64_t bsize = (int64_t)block[0] * block[1] * block[2];
-  if (total > 2147483647LL || bsize > 2147483647LL)
+  if (gtotal > 2147483647LL || bsize > 2147483647LL)
     return fail(BF_E_INVALID, "dim3 product overflows i32");
+  if (range_count < 0) {
+    range_first = 0;
+    range_count = gtotal;
+  }
+  if (range_first < 0 || range_count < 1 || range_first + range_count > gtotal)
+    return fail(BF_E_INVALID, "block range outside the grid");
+  const int64_t total = range_count;  // blocks of this task
   if (grain < 1) return fail(BF_E_INVALID, "grain must be >= 1");
   if (grain > total) grain = total;
   const KernelEntry* ke = find_kernel(kernel);
@@ -951,6 +960,7 @@ int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const i
   TaskRec& tr = rt->tasks[id];
   tr.kernel = kernel;
   tr.total = total;
+  tr.base = range_first;
   tr.grain = grain;
   if (task_id) *task_id = id;
 
@@ -1026,7 +1036,7 @@ int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const i
     f.pre = pre;
     f.task = id;
     f.worker = (int)(rt->rr++ % (uint64_t)rt->pool);
-    f.first = first;
+    f.first = range_first + first;  // absolute logical block ids
     f.count = count;
     for (int k = 0; k < 3; k++) {
       f.grid[k] = grid[k];
@@ -1044,6 +1054,21 @@ int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const i
     }
   }
   return BF_OK;
+}
+
+int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const int32_t block[3],
+              int64_t shmem_bytes, const bf_slot* slots, int32_t nslots, int32_t warp_size,
+              int64_t grain, uint64_t* task_id) {
+  return launch_impl(rt, kernel, grid, block, shmem_bytes, slots, nslots, warp_size, 0, -1, grain,
+                     task_id);
+}
+
+int bf_launch_range(bf_runtime* rt, const char* kernel, const int32_t grid[3],
+                    const int32_t block[3], int64_t shmem_bytes, const bf_slot* slots,
+                    int32_t nslots, int32_t warp_size, int64_t first, int64_t count,
+                    int64_t grain, uint64_t* task_id) {
+  return launch_impl(rt, kernel, grid, block, shmem_bytes, slots, nslots, warp_size, first, count,
+                     grain, task_id);
 }
 
 int bf_synchronize(bf_runtime* rt, bf_fault* fault) {
@@ -1111,7 +1136,7 @@ int bf_task_executed(bf_runtime* rt, uint64_t task_id, int32_t* executed, int64_
   retire(rt, false);
   std::memset(executed, 0, n * sizeof(int32_t));
   for (auto& r : t.done_ranges)
-    for (long long b = r.first; b < r.first + r.second; b++) executed[b] += 1;
+    for (long long b = r.first; b < r.first + r.second; b++) executed[b - t.base] += 1;
   return BF_OK;
 }
 

@@ -14,8 +14,11 @@ data need a collective:
     just reached the owned rows, so `halo` rows per side are exchanged with
     NCCL point-to-point every `halo` iterations.
   * hist / hist_stride / wreduce / kmeans — per-rank partial counts or sums
-    combined with one all-reduce.
-  * vecadd / nn / fir / reduce — disjoint outputs, no collective.
+    combined with one all-reduce (launch_sharded, COMBINE).
+  * vecadd / nn / fir / reduce — disjoint outputs: no exchange is needed for
+    the computation; launch_sharded assembles the full output on every rank
+    with one all-gather when the caller wants it replicated.
+  * bfs level step — monotone levels and flag: all-reduce MAX.
 
 Everything here is backend-agnostic torch.distributed (NCCL on GPUs, gloo in
 the CPU tests).
@@ -119,3 +122,101 @@ class _null:
 
     def __exit__(self, *a):
         return False
+
+
+# ---------------------------------------------------------------------------
+# sharded launches of the other kernels: each rank runs its block range
+# (bf_launch_range), then the outputs are combined with one collective per
+# buffer.  Specs name how each output buffer combines:
+#   "sum"   — integer/float accumulators (atomics): ranks > 0 zero their copy
+#             before the launch so the initial value is counted once, then an
+#             all-reduce SUM (ints exact; f32 sums order-dependent, as the
+#             reference's own atomics);
+#   "max"   — monotone flags/levels (bfs: lvl only moves -1 -> cur+1, changed
+#             0 -> 1): all-reduce MAX;
+#   "owned" — disjoint writes: every rank keeps the values it changed, merged
+#             by an all-gather of (changed mask, values) — generic over any
+#             kernel whose blocks write disjoint elements.
+# ---------------------------------------------------------------------------
+
+COMBINE = {
+    "vecadd": {"c": "owned"},
+    "nn": {"d": "owned"},
+    "reduce": {"out": "owned"},
+    "fir": {"y": "owned"},
+    "hist": {"counts": "sum"},
+    "hist_stride": {"counts": "sum"},
+    "wreduce": {"out": "sum"},
+    "kmeans": {"member": "owned", "sums": "sum", "counts": "sum"},
+    "bfs": {"lvl": "max", "changed": "max"},
+}
+
+
+class Combiner:
+    """Prepare (before the rank's launch) and combine (after it) the output
+    buffers of one sharded launch; tensors are 1-D torch views."""
+
+    def __init__(self, spec: dict, world: int, rank: int):
+        self.spec = spec
+        self.world = world
+        self.rank = rank
+        self.before: dict = {}
+
+    def prepare(self, tensors: dict) -> None:
+        for name, op in self.spec.items():
+            t = tensors[name]
+            if op == "sum" and self.rank != 0:
+                t.zero_()
+            elif op == "owned":
+                self.before[name] = t.clone()
+
+    def finish(self, tensors: dict) -> None:
+        import torch
+        import torch.distributed as dist
+
+        for name, op in self.spec.items():
+            t = tensors[name]
+            if op == "sum":
+                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            elif op == "max":
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            else:
+                b = self.before.pop(name)
+                changed = (t.view(torch.uint8).view(-1, t.element_size()) !=
+                           b.view(torch.uint8).view(-1, t.element_size())).any(dim=1)
+                masks = [torch.zeros_like(changed) for _ in range(self.world)]
+                vals = [torch.empty_like(t) for _ in range(self.world)]
+                dist.all_gather(masks, changed)
+                dist.all_gather(vals, t)
+                out = b.clone()
+                for m, v in zip(masks, vals):
+                    out[m] = v[m]
+                t.copy_(out)
+
+
+def launch_sharded(rt, arena, routine, grid, block, shmem: int, packed, outputs: dict,
+                   world: int, rank: int):
+    """Run this rank's share of a launch and combine the outputs.
+
+    outputs: {param name: buffer handle} of the buffers the kernel writes.
+    Returns the rank's KernelTask."""
+    import torch
+    name = getattr(routine, "name", "")
+    spec = {p: op for p, op in COMBINE.get(name, {}).items() if p in outputs}
+    if set(spec) != set(outputs):
+        missing = set(outputs) - set(spec)
+        raise ValueError(f"no combine rule for {name}: {sorted(missing)}")
+    device = torch.device("cuda", arena.device)
+    tensors = {p: torch.as_tensor(arena.cuda_array(h), device=device) for p, h in outputs.items()}
+    comb = Combiner(spec, world, rank)
+    torch.cuda.synchronize(device)
+    comb.prepare(tensors)
+    torch.cuda.synchronize(device)
+    first, hi = rank_range(grid.x * grid.y * grid.z, world, rank)
+    task = None
+    if hi > first:
+        task = rt.launch_range(routine, grid, block, shmem, packed, first, hi - first)
+    rt.device_synchronize()
+    comb.finish(tensors)
+    torch.cuda.synchronize(device)
+    return task

@@ -406,10 +406,20 @@ class Runtime:
     # -- host API ---------------------------------------------------------------
     def launch(self, routine, grid, block, shmem_bytes: int, packed) -> KernelTask:
         """Enqueue a kernel; returns immediately, never waits for the device."""
+        return self._launch(routine, grid, block, shmem_bytes, packed, None)
+
+    def launch_range(self, routine, grid, block, shmem_bytes: int, packed, first: int,
+                     count: int) -> KernelTask:
+        """Enqueue only logical blocks [first, first+count) of the grid: one
+        worker's share (multi-GPU ranks, parallel.py).  The task has `count`
+        blocks; its executed[] is indexed from `first`."""
+        return self._launch(routine, grid, block, shmem_bytes, packed, (first, count))
+
+    def _launch(self, routine, grid, block, shmem_bytes, packed, rng) -> KernelTask:
         if self._shut_down:
             raise PoolShutdown("launch after shutdown")
         name, warp_mode, warp_size = routines.resolve(routine)
-        total = grid.x * grid.y * grid.z
+        total = grid.x * grid.y * grid.z if rng is None else rng[1]
         grain = resolve_grain(self.policy, total, self.pool_size, routine)
         task = KernelTask(routine, packed, grid, block, shmem_bytes, totalBlocks=total,
                           block_per_fetch=grain)
@@ -417,8 +427,12 @@ class Runtime:
         g, b, tid = self._g, self._b, self._tid
         g[0], g[1], g[2] = grid.x, grid.y, grid.z
         b[0], b[1], b[2] = block.x, block.y, block.z
-        rc = _lib.lib().bf_launch(self._native, name.encode(), g, b, int(shmem_bytes), slots, n,
-                                  warp_size, grain, C.byref(tid))
+        if rng is None:
+            rc = _lib.lib().bf_launch(self._native, name.encode(), g, b, int(shmem_bytes), slots, n,
+                                      warp_size, grain, C.byref(tid))
+        else:
+            rc = _lib.lib().bf_launch_range(self._native, name.encode(), g, b, int(shmem_bytes), slots,
+                                            n, warp_size, int(rng[0]), int(rng[1]), grain, C.byref(tid))
         if rc == _lib.E_SHUTDOWN:
             raise PoolShutdown("launch after shutdown")
         if rc == _lib.E_UNKNOWN_KERNEL:

@@ -267,3 +267,65 @@ def test_nn_sqrt_rounding_hard_cases():
         want, _ = oracle.run(inst)
         got, trap, _, _ = gpu_run(inst)
         assert trap is None and bit_equal(got["d"], want["d"]), v
+
+
+def test_launch_range_covers_grid():
+    """Three block-range launches tiling the grid == one full launch."""
+    import random
+    import instances as I
+    from gpu_helpers import materialize
+    from paper_2206_07896_b200 import DeviceArena, Dim3, Runtime, routines
+    rng = random.Random(31)
+    for make in (I.vecadd, I.hist, I.reduce, I.wreduce):
+        inst = make(rng)
+        want, trap = oracle.run(inst)
+        arena = DeviceArena()
+        packed, handles = materialize(inst, arena)
+        G = inst.grid.total
+        cuts = sorted({0, G // 3, (2 * G) // 3, G})
+        with Runtime(arena, pool_size=2, instrument=True) as rt:
+            r = routines.get(inst.kernel)
+            tasks = [rt.launch_range(r, Dim3(inst.grid.x), Dim3(inst.block.x), inst.shmem, packed, a, b - a)
+                     for a, b in zip(cuts, cuts[1:]) if b > a]
+            rt.device_synchronize()
+        for t in tasks:
+            assert t.executed == [1] * t.totalBlocks
+        for buf in inst.outputs:
+            assert bit_equal(arena.to_numpy(handles[buf]), want[buf]), inst.kernel
+
+
+def test_launch_sharded_single_rank_nccl():
+    """parallel.launch_sharded end to end on the device (world of one, NCCL)."""
+    import os
+    import random
+    import socket
+    import torch
+    import torch.distributed as dist
+    import instances as I
+    from gpu_helpers import materialize
+    from paper_2206_07896_b200 import DeviceArena, Dim3, Runtime, routines
+    from paper_2206_07896_b200.parallel import COMBINE, launch_sharded
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = random.Random(41)
+        for inst in [I.vecadd(rng), I.hist(rng), I.kmeans(1000, 8, 4, 128, seed=2)]:
+            want, _ = oracle.run(inst)
+            arena = DeviceArena()
+            packed, handles = materialize(inst, arena)
+            outs = {n: handles[n] for n in COMBINE[inst.kernel]}
+            with Runtime(arena) as rt:
+                launch_sharded(rt, arena, routines.get(inst.kernel), Dim3(inst.grid.x), Dim3(inst.block.x),
+                               0, packed, outs, 1, 0)
+            for n in outs:
+                g = arena.to_numpy(handles[n])
+                if n == "sums":
+                    assert np.allclose(g, want[n], rtol=1e-4, atol=1e-4)
+                else:
+                    assert bit_equal(g, want[n]), (inst.kernel, n)
+    finally:
+        dist.destroy_process_group()

@@ -110,3 +110,78 @@ def test_band_validation():
         HotspotBands(16, 16, 4, 0, halo=8)  # bands of 4 rows < halo
     b = HotspotBands(100, 8, 4, 1, halo=5)
     assert b.own == (25, 50) and b.local_rows == (20, 55) and b.up == 0 and b.down == 2
+
+
+def _shard_worker(rank, world, port, out_q):
+    sys.path[:0] = [str(ROOT), str(ROOT / "oracle")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import random as _r
+
+        import instances as I
+        import oracle
+        from paper_2206_07896_b200.parallel import COMBINE, Combiner, rank_range
+        rng = _r.Random(77)
+        cases = [I.vecadd(rng), I.reduce(rng), I.hist(rng), I.wreduce(rng), I.nn(3000, 128, seed=4),
+                 I.kmeans(1500, 8, 5, 128, seed=5), I.bfs(4000, 4, cur=0, seed=6, block=128)]
+        results = []
+        for inst in cases:
+            first, hi = rank_range(inst.grid.total, world, rank)
+            spec = COMBINE[inst.kernel]
+            # this rank's buffers start from the instance's initial values
+            init = {b.name: torch.from_numpy(np.array(b.values, dtype=oracle._NP[b.scalar]).reshape(-1)[: b.length].copy())
+                    for b in inst.buffers}
+            comb = Combiner(spec, world, rank)
+            tens = {n: init[n] for n in spec}
+            comb.prepare(tens)
+            for b in inst.buffers:  # feed prepared values to the oracle run
+                if b.name in tens:
+                    b.values = tens[b.name].numpy()
+            if hi > first:
+                outs, trap = oracle.run(inst, block_range=(first, hi - first))
+                assert trap is None
+            else:
+                outs = {b.name: init[b.name].numpy() for b in inst.buffers}
+            res = {n: torch.from_numpy(np.ascontiguousarray(outs[n])) for n in spec}
+            comb.before = {n: t for n, t in comb.before.items()}
+            comb.finish(res)
+            results.append({n: t.numpy().copy() for n, t in res.items()})
+        if rank == 0:
+            out_q.put(results)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_launches_match_single_launch(world):
+    """Block-range shards + combine collectives == one full launch (oracle):
+    owned writes (vecadd, reduce, nn, kmeans member), integer sums (hist,
+    wreduce, kmeans counts), float sums within 1e-4, monotone max (bfs)."""
+    import random as _r
+
+    import instances as I
+    import oracle
+    rng = _r.Random(77)
+    cases = [I.vecadd(rng), I.reduce(rng), I.hist(rng), I.wreduce(rng), I.nn(3000, 128, seed=4),
+             I.kmeans(1500, 8, 5, 128, seed=5), I.bfs(4000, 4, cur=0, seed=6, block=128)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2206_07896_b200.parallel import COMBINE
+    for inst, res in zip(cases, got):
+        want, trap = oracle.run(inst)
+        assert trap is None
+        for name in COMBINE[inst.kernel]:
+            w, g = want[name], res[name]
+            if inst.kernel == "kmeans" and name == "sums":
+                assert np.allclose(g, w, rtol=1e-4, atol=1e-4), inst.kernel
+            else:
+                assert np.array_equal(g.view(np.uint8), w.view(np.uint8)), (inst.kernel, name)
