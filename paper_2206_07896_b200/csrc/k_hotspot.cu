@@ -128,6 +128,106 @@ __global__ void __launch_bounds__(128) hotspot_band(const float* __restrict__ sr
   }
 }
 
+// Same work split, but the rows in flight live in shared memory instead of
+// registers: each lane streams its own float4 of the src/power rows (and the
+// strip-edge scalars) D-2 rows ahead of the south row with cp.async into a
+// lane-private ring of D slots, so the loads in flight per SM are no longer
+// paid for with registers (occupancy) — Little's law at ~6.4 TB/s needs
+// ~60 KB in flight per SM.  Every lane reads back only what it copied itself,
+// so the ring needs no warp barrier: cp.async.wait_group orders the RAW, and
+// a slot is rewritten two iterations after its last read (WAR by program
+// order of consumed registers).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) hotspot_async(const float* __restrict__ src,
+                                                     const float* __restrict__ power,
+                                                     float* __restrict__ dst, int rows, int cols,
+                                                     int r_lo, int r_hi, int c_lo, int c_hi,
+                                                     int groups, int bands, HsConst k) {
+  static_assert(D >= 3, "ring needs north/centre/south + one row in flight");
+  __shared__ __align__(16) float4 ring[4][D][64];  // [warp][slot][src lanes | power lanes]
+  __shared__ float edge[4][D][2];                  // [warp][slot][west, east]
+  const int lane = threadIdx.x & 31;
+  const int wi = threadIdx.x >> 5;
+  const int w = blockIdx.x * 4 + wi;
+  if (w >= groups * bands) return;  // warp-uniform
+  const int band = w / groups, g = w % groups;
+  const long long nr = r_hi - r_lo;
+  const int r_start = r_lo + (int)(nr * band / bands);
+  const int r_end = r_lo + (int)(nr * (band + 1) / bands);
+  if (r_start >= r_end) return;
+  const int n = r_end - r_start;
+  const int c0 = c_lo + g * 128 + lane * 4;
+  const bool active = c0 < c_hi;
+  const bool west_scalar = lane == 0;
+  const bool east_scalar = (lane == 31) || (c0 + 4 >= c_hi);
+  const bool west_load = active && west_scalar && c0 > 0;
+  const bool east_load = active && east_scalar && c0 + 4 < cols;
+  const long long colsl = cols;
+
+  // row sequence q = 0 .. n+1: clamp(r_start - 1 + q); centre rows are 1..n
+  auto issue = [&](int q, int s) {
+    if (active && q <= n + 1) {
+      int r = r_start - 1 + q;
+      r = r < 0 ? 0 : (r >= rows ? rows - 1 : r);
+      const float* row = src + r * colsl;
+      cp_async16(&ring[wi][s][lane], row + c0);
+      if (q >= 1 && q <= n) {
+        cp_async16(&ring[wi][s][32 + lane], power + r * colsl + c0);
+        if (west_load) cp_async4(&edge[wi][s][0], row + c0 - 1);
+        if (east_load) cp_async4(&edge[wi][s][1], row + c0 + 4);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int q = 0; q < D - 1; q++) issue(q, q);
+  cp_async_wait<D - 3>();
+  float4 north = ring[wi][0][lane];
+  float4 center = ring[wi][1][lane];
+  int s_c = 1;          // slot of the centre row
+  int s_i = D - 1;      // slot the next issue writes
+  for (int q = 1; q <= n; q++) {
+    issue(q + D - 2, s_i);
+    s_i = s_i + 1 == D ? 0 : s_i + 1;
+    cp_async_wait<D - 3>();
+    const int s_s = s_c + 1 == D ? 0 : s_c + 1;
+    const float4 south = ring[wi][s_s][lane];
+    const float4 p = ring[wi][s_c][32 + lane];
+    float west = __shfl_up_sync(0xffffffffu, center.w, 1);
+    float east = __shfl_down_sync(0xffffffffu, center.x, 1);
+    if (west_scalar) west = c0 > 0 ? edge[wi][s_c][0] : center.x;
+    if (east_scalar) east = c0 + 4 < cols ? edge[wi][s_c][1] : center.w;
+    if (active) {
+      float4 out;
+      out.x = hs_cell(center.x, north.x, south.x, west, center.y, p.x, k);
+      out.y = hs_cell(center.y, north.y, south.y, center.x, center.z, p.y, k);
+      out.z = hs_cell(center.z, north.z, south.z, center.y, center.w, p.z, k);
+      out.w = hs_cell(center.w, north.w, south.w, center.z, east, p.w, k);
+      *reinterpret_cast<float4*>(dst + (r_start + q - 1) * colsl + c0) = out;
+    }
+    north = center;
+    center = south;
+    s_c = s_s;
+  }
+  cp_async_wait<0>();
+}
+
 static int hotspot_pf() {
   static int pf = -1;
   if (pf < 0) {
@@ -138,9 +238,28 @@ static int hotspot_pf() {
   return pf;
 }
 
+// kernel variant: 0 = register prefetch (hotspot_band<PF>), D >= 3 =
+// shared-memory ring of D slots (hotspot_async<D>).  BF_HOTSPOT_RING.
+static int hotspot_ring() {
+  static int d = -1;
+  if (d < 0) {
+    const char* e = getenv("BF_HOTSPOT_RING");
+    d = e ? atoi(e) : 0;
+    if (d != 0 && d != 3 && d != 4 && d != 6 && d != 8) d = 0;
+  }
+  return d;
+}
+
 typedef void (*HsBandFn)(const float*, const float*, float*, int, int, int, int, int, int, int, int,
                          HsConst);
 static HsBandFn hotspot_band_fn(int pf) {
+  switch (hotspot_ring()) {
+    case 3: return hotspot_async<3>;
+    case 4: return hotspot_async<4>;
+    case 6: return hotspot_async<6>;
+    case 8: return hotspot_async<8>;
+    default: break;
+  }
   switch (pf) {
     case 1: return hotspot_band<1>;
     case 3: return hotspot_band<3>;

@@ -175,10 +175,17 @@ struct bf_arena {
   uint32_t next_handle = 1;
   std::map<uint32_t, bf::Buffer> buffers;
   std::vector<void*> zombies;     // freed buffers awaiting a quiescence point
+  // host<->device copies: uploads/fills/copies on copy_stream, downloads on
+  // d2h_stream with their own staging, so a download issued from one host
+  // thread overlaps an upload from another (both PCIe directions busy).
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr;
   void* staging[2] = {nullptr, nullptr};
+  void* dl_staging[2] = {nullptr, nullptr};
   size_t staging_bytes = 0;
   cudaEvent_t staging_ev[2] = {nullptr, nullptr};
+  cudaEvent_t dl_ev[2] = {nullptr, nullptr};
+  std::mutex mu;  // buffers map + staging allocation
   int live_runtimes = 0;
   bool destroy_pending = false;  // destroyed while runtimes still reference it
 };
@@ -192,6 +199,7 @@ static int set_device(int dev) {
 }
 
 static Buffer* lookup(bf_arena* a, uint32_t h) {
+  std::lock_guard<std::mutex> g(a->mu);
   auto it = a->buffers.find(h);
   return it == a->buffers.end() ? nullptr : &it->second;
 }
@@ -203,11 +211,14 @@ static void release_zombies(bf_arena* a) {
 
 static const size_t kStagingChunk = 32u << 20;  // 32 MiB double-buffered staging
 
-static int ensure_staging(bf_arena* a) {
-  if (a->staging[0]) return BF_OK;
+static int ensure_staging(bf_arena* a, bool download) {
+  std::lock_guard<std::mutex> g(a->mu);
+  void** st = download ? a->dl_staging : a->staging;
+  cudaEvent_t* ev = download ? a->dl_ev : a->staging_ev;
+  if (st[0]) return BF_OK;
   for (int i = 0; i < 2; i++) {
-    CK(cudaHostAlloc(&a->staging[i], kStagingChunk, cudaHostAllocDefault));
-    CK(cudaEventCreateWithFlags(&a->staging_ev[i], cudaEventDisableTiming));
+    CK(cudaHostAlloc(&st[i], kStagingChunk, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
   }
   a->staging_bytes = kStagingChunk;
   return BF_OK;
@@ -460,7 +471,9 @@ int bf_arena_create(int32_t device, bf_arena** out) {
   auto* a = new bf_arena();
   a->device = device;
   cudaError_t e = cudaStreamCreateWithFlags(&a->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->d2h_stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
+    if (a->copy_stream) cudaStreamDestroy(a->copy_stream);
     delete a;
     return cuda_fail(e, "cudaStreamCreate");
   }
@@ -489,8 +502,11 @@ static void arena_free(bf_arena* a) {
   for (int i = 0; i < 2; i++) {
     if (a->staging[i]) cudaFreeHost(a->staging[i]);
     if (a->staging_ev[i]) cudaEventDestroy(a->staging_ev[i]);
+    if (a->dl_staging[i]) cudaFreeHost(a->dl_staging[i]);
+    if (a->dl_ev[i]) cudaEventDestroy(a->dl_ev[i]);
   }
   if (a->copy_stream) cudaStreamDestroy(a->copy_stream);
+  if (a->d2h_stream) cudaStreamDestroy(a->d2h_stream);
   delete a;
 }
 
@@ -509,6 +525,7 @@ int bf_alloc(bf_arena* a, int32_t scalar, int64_t length, uint32_t* handle) {
   CK(cudaMalloc(&p, alloc));
   CK(cudaMemsetAsync(p, 0, alloc, a->copy_stream));
   CK(cudaStreamSynchronize(a->copy_stream));
+  std::lock_guard<std::mutex> g(a->mu);
   uint32_t h = a->next_handle++;
   a->buffers[h] = Buffer{scalar, length, p};
   *handle = h;
@@ -517,11 +534,14 @@ int bf_alloc(bf_arena* a, int32_t scalar, int64_t length, uint32_t* handle) {
 
 int bf_free(bf_arena* a, uint32_t h) {
   if (!a) return fail(BF_E_INVALID, "null arena");
-  auto it = a->buffers.find(h);
-  if (it == a->buffers.end())
-    return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
-  a->zombies.push_back(it->second.ptr);
-  a->buffers.erase(it);
+  {
+    std::lock_guard<std::mutex> g(a->mu);
+    auto it = a->buffers.find(h);
+    if (it == a->buffers.end())
+      return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+    a->zombies.push_back(it->second.ptr);
+    a->buffers.erase(it);
+  }
   if (a->live_runtimes == 0) {
     set_device(a->device);
     cudaDeviceSynchronize();
@@ -565,7 +585,7 @@ int bf_upload(bf_arena* a, uint32_t h, const void* src, int64_t nbytes, int64_t 
     CK(cudaStreamSynchronize(a->copy_stream));
     return BF_OK;
   }
-  rc = ensure_staging(a);
+  rc = ensure_staging(a, false);
   if (rc) return rc;
   // double-buffered: memcpy into staging[i] while staging[i^1] is in flight
   int64_t done = 0;
@@ -594,11 +614,11 @@ int bf_download(bf_arena* a, uint32_t h, void* dstp, int64_t nbytes, int64_t off
   if (rc) return rc;
   const char* src = (const char*)b->ptr + offset;
   if (is_pinned(dstp)) {
-    CK(cudaMemcpyAsync(dstp, src, nbytes, cudaMemcpyDeviceToHost, a->copy_stream));
-    CK(cudaStreamSynchronize(a->copy_stream));
+    CK(cudaMemcpyAsync(dstp, src, nbytes, cudaMemcpyDeviceToHost, a->d2h_stream));
+    CK(cudaStreamSynchronize(a->d2h_stream));
     return BF_OK;
   }
-  rc = ensure_staging(a);
+  rc = ensure_staging(a, true);
   if (rc) return rc;
   // pipeline: D2H chunk k+1 in flight while chunk k is memcpy'd out
   int64_t chunk = (int64_t)a->staging_bytes;
@@ -607,14 +627,14 @@ int bf_download(bf_arena* a, uint32_t h, void* dstp, int64_t nbytes, int64_t off
     int i = (int)(k & 1);
     int64_t off = k * chunk;
     int64_t n = std::min<int64_t>(nbytes - off, chunk);
-    CK(cudaMemcpyAsync(a->staging[i], src + off, n, cudaMemcpyDeviceToHost, a->copy_stream));
-    CK(cudaEventRecord(a->staging_ev[i], a->copy_stream));
+    CK(cudaMemcpyAsync(a->dl_staging[i], src + off, n, cudaMemcpyDeviceToHost, a->d2h_stream));
+    CK(cudaEventRecord(a->dl_ev[i], a->d2h_stream));
     if (k > 0) {
       int j = i ^ 1;
       int64_t poff = (k - 1) * chunk;
       int64_t pn = std::min<int64_t>(nbytes - poff, chunk);
-      CK(cudaEventSynchronize(a->staging_ev[j]));
-      std::memcpy((char*)dstp + poff, a->staging[j], pn);
+      CK(cudaEventSynchronize(a->dl_ev[j]));
+      std::memcpy((char*)dstp + poff, a->dl_staging[j], pn);
     }
   }
   {
@@ -622,8 +642,8 @@ int bf_download(bf_arena* a, uint32_t h, void* dstp, int64_t nbytes, int64_t off
     int i = (int)(k & 1);
     int64_t off = k * chunk;
     int64_t n = std::min<int64_t>(nbytes - off, chunk);
-    CK(cudaEventSynchronize(a->staging_ev[i]));
-    std::memcpy((char*)dstp + off, a->staging[i], n);
+    CK(cudaEventSynchronize(a->dl_ev[i]));
+    std::memcpy((char*)dstp + off, a->dl_staging[i], n);
   }
   return BF_OK;
 }
