@@ -104,13 +104,32 @@ def test_kmeans_vs_oracle_screen_and_ties():
     import instances as I
     cases = [I.kmeans(3000, 32, 16, 256, seed=11), I.kmeans(2000, 7, 5, 128, seed=12),
              I.kmeans(1500, 33, 4, 256, seed=13), I.kmeans(999, 16, 16, 96, seed=14, dup=True),
-             I.kmeans(500, 3, 1, 64, seed=15), I.kmeans(4096, 32, 16, 256, seed=16, dup=True)]
+             I.kmeans(500, 3, 1, 64, seed=15), I.kmeans(4096, 32, 16, 256, seed=16, dup=True),
+             I.kmeans(2000, 4, 13, 128, seed=18), I.kmeans(3001, 32, 7, 256, seed=19, dup=True)]
     big = I.kmeans(1024, 8, 6, 128, seed=17)
     f = big.buffer("f")
     f.values = (np.asarray(f.values) * 1e6 - 3e5).astype(np.float32)  # large, signed
     c = big.buffer("cent")
     c.values = np.ascontiguousarray(np.asarray(f.values).reshape(8, 1024)[:, :6].T).reshape(-1)
     cases.append(big)
+    # tensor-core screen edge cases (nf = 32, k = 16, npts % 4 == 0): a centroid
+    # one ulp away from another (near-ties), subnormal-scale points, and
+    # non-finite features (the reference scan's NaN semantics)
+    edge = I.kmeans(2048, 32, 16, 256, seed=20)
+    c = np.asarray(edge.buffer("cent").values).copy()
+    c[2 * 32:3 * 32] = c[:32]
+    c[2 * 32 + 5] = np.nextafter(c[5], np.float32(2))
+    c[3 * 32:4 * 32] = c[32:64]
+    c[3 * 32 + 31] = np.nextafter(c[32 + 31], np.float32(-2))
+    edge.buffer("cent").values = c
+    fe = np.asarray(edge.buffer("f").values).copy().reshape(32, 2048)
+    fe[:, 100:140] *= np.float32(1e-30)
+    fe[3, 7] = np.nan
+    fe[0, 9] = np.inf
+    fe[:, 11] = np.float32(3e38)
+    fe[:, 13] = c[:32]  # a point exactly on centroid 0 (= centroid 2 but one ulp)
+    edge.buffer("f").values = fe.reshape(-1)
+    cases.append(edge)
     for k, inst in enumerate(cases):
         want, trap = oracle.run(inst)
         got, got_trap, _, _ = gpu_run(inst)
@@ -118,6 +137,9 @@ def test_kmeans_vs_oracle_screen_and_ties():
         assert bit_equal(got["member"], want["member"]), k
         assert bit_equal(got["counts"], want["counts"]), k
         w, g = want["sums"].astype(np.float64), got["sums"].astype(np.float64)
+        fin = np.isfinite(w)
+        assert np.array_equal(np.isnan(w), np.isnan(g)) and np.array_equal(w[np.isinf(w)], g[np.isinf(w)]), k
+        w, g = w[fin], g[fin]
         assert np.all(np.abs(w - g) <= SUMS_RTOL * np.maximum(np.maximum(abs(w), abs(g)), 1.0)), k
 
 
