@@ -186,6 +186,51 @@ def build_cases(arena, torch, device, scale: int = 28) -> list:
                       [(routines.get("kmeans"), Dim3(npts // 256), Dim3(256), 0, pk)],
                       check=lambda: int(tkn.long().sum().item()) == npts, reset=km_reset,
                       note="16M x 32 f32, k=16: one assignment + accumulation pass; f64 distances"))
+
+    # --- backprop: Rodinia's two device kernels, 2^(scale-4) input units x 16 hidden
+    nin, hid = 1 << (scale - 4), 16
+    nb = nin // 16
+    bi, bw, bpart = alloc("f32", nin + 1), alloc("f32", (nin + 1) * (hid + 1)), alloc("f32", nb * hid)
+    bd, bo = alloc("f32", hid + 1), alloc("f32", (nin + 1) * (hid + 1))
+    tbi, tbw, tbp = _t(arena, bi, torch, device), _t(arena, bw, torch, device), _t(arena, bpart, torch, device)
+    tbd, tbo = _t(arena, bd, torch, device), _t(arena, bo, torch, device)
+    tbi.uniform_(0, 1, generator=g)
+    tbw.uniform_(0, 1, generator=g)
+    tbd.uniform_(-0.1, 0.1, generator=g)
+    tbo.uniform_(-0.05, 0.05, generator=g)
+    tbw0, tbo0 = tbw.clone(), tbo.clone()
+
+    def bp_reset():
+        tbw.copy_(tbw0)
+        tbo.copy_(tbo0)
+
+    def bp_fw_check():
+        p = tbw0.view(nin + 1, hid + 1)[1:, 1:].reshape(nb, 16, hid) * tbi[1:].view(nb, 16, 1)
+        while p.shape[1] > 1:  # Rodinia's tree: rows (0,1), (2,3), ... then pairs of pairs
+            p = p[:, 0::2] + p[:, 1::2]
+        return bool(torch.equal(tbp.view(nb, hid), p[:, 0, :]))
+
+    def bp_adj_check():
+        cx = 0.3 * tbd.double()
+        a = cx[1:].view(1, hid) * tbi.double()[1:].view(nin, 1)
+        b = 0.3 * tbo0.double().view(nin + 1, hid + 1)[1:, 1:]
+        s_ = a + b
+        w_ = (tbw0.double().view(nin + 1, hid + 1)[1:, 1:] + s_).float()
+        return bool(torch.equal(tbw.view(nin + 1, hid + 1)[1:, 1:], w_)) and \
+            bool(torch.equal(tbo.view(nin + 1, hid + 1)[1:, 1:], s_.float()))
+    pk = PackedArgs([ArgSlot("handle", bi), ArgSlot("handle", bw), ArgSlot("handle", bpart),
+                     ArgSlot("i32", hid)])
+    cases.append(Case("bp_forward", "bp_forward", nin * (64 + 64 + 4 + 4), nin, "input unit",
+                      [(routines.get("bpnn_layerforward"), Dim3(1, nb), Dim3(16, 16), 0, pk)],
+                      check=bp_fw_check, reset=bp_reset,
+                      note=f"Rodinia backprop bpnn_layerforward, {nin} inputs x 16 hidden, 16x16 blocks; "
+                           "bytes/unit = 64 w read + 64 w written + 4 input + 4 partial"))
+    pk = PackedArgs([ArgSlot("handle", bd), ArgSlot("i32", hid), ArgSlot("handle", bi), ArgSlot("i32", nin),
+                     ArgSlot("handle", bw), ArgSlot("handle", bo)])
+    cases.append(Case("bp_adjust", "bp_adjust", nin * (16 * 16 + 4), nin, "input unit",
+                      [(routines.get("bpnn_adjust_weights"), Dim3(1, nb), Dim3(16, 16), 0, pk)],
+                      check=bp_adj_check, reset=bp_reset,
+                      note="bpnn_adjust_weights: w, oldw read + written (16 B x 16 per unit) + ly"))
     return cases
 
 
@@ -373,6 +418,12 @@ def cpu_sample(name: str, threads: int, budget: float = 0.5) -> Optional[dict]:
     elif name == "kmeans":
         inst = I.kmeans(1 << 15, 32, 16, 256)
         elems, nt = 1 << 15, 1
+    elif name == "bp_forward":
+        inst = I.backprop_forward(1 << 18, seed=1)
+        elems, nt = 1 << 18, 1
+    elif name == "bp_adjust":
+        inst = I.backprop_adjust(1 << 18, seed=1)
+        elems, nt = 1 << 18, 1
     elif name == "bfs":
         nv = 1 << 20
         row, col = I.random_graph(nv, 8, 1)

@@ -211,6 +211,33 @@ def northstar_sets() -> None:
     pack(bf, GOLDEN / "bfs.npz")
 
 
+def backprop_set() -> list:
+    """Rodinia backprop device kernels: forward passes (with the weights
+    overwritten by the tile sums), a forward -> adjust chain, geometry
+    variants the lockstep semantics define (duplicated z threads), traps."""
+    bp = [I.backprop_forward(64, seed=1), I.backprop_forward(160, seed=2),
+          I.backprop_forward(32, seed=3, block=(16, 16, 2))]
+    bp.append(I.backprop_adjust(64, seed=4))
+    bp.append(I.backprop_adjust(256, seed=5))
+    # chain: adjust after a forward pass on the same weights
+    fw = I.backprop_forward(96, seed=6)
+    outs, _ = run_ref(fw)
+    adj = I.backprop_adjust(96, seed=7)
+    adj.buffer("w").values = outs["w"].copy()
+    bp += [fw, adj]
+    # traps: input layer one unit short (last block's input read), partial too short
+    t1 = I.backprop_forward(48, seed=8)
+    t1.buffer("input").values = np.asarray(t1.buffer("input").values)[:48]
+    t1.buffer("input").length = 48
+    t2 = I.backprop_forward(48, seed=9)
+    t2.buffer("partial").length = 40
+    t2.buffer("partial").values = np.zeros(40, np.float32)
+    t3 = I.backprop_adjust(32, seed=10)
+    t3.buffer("delta").length = 16
+    t3.buffer("delta").values = np.asarray(t3.buffer("delta").values)[:16]
+    return bp + [t1, t2, t3]
+
+
 def fingerprints() -> None:
     fps = {}
     for name in routines.names():
@@ -233,3 +260,5 @@ if __name__ == "__main__":
         pack(trap_set(), GOLDEN / "traps.npz")
     if "northstar" in which:
         northstar_sets()
+    if "backprop" in which or "northstar" in which:
+        pack(backprop_set(), GOLDEN / "backprop.npz")

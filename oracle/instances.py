@@ -280,3 +280,38 @@ def bfs(nv: int, deg: int, cur: int = 0, seed: int = 0, block: int = 256, lvl=No
                      Buf("changed", "i32", 1, np.zeros(1, np.int32))],
                     [("buf", "row"), ("buf", "col"), ("buf", "lvl"), ("buf", "changed"), ("i32", nv),
                      ("i32", cur)], ["lvl", "changed"])
+
+
+# ---- backprop (kernels/backprop.kn), Rodinia's 16 x 16 blocks, hid = 16 -----
+BP_HID = 16
+
+
+def backprop_forward(n_in: int, seed: int = 0, hid: int = BP_HID, block=(16, 16), grid_x: int = 1) -> Instance:
+    """bpnn_layerforward over an input layer of n_in units (n_in % 16 == 0):
+    grid 1 x n_in/16, weights U(0, 1) like bpnn_randomize_weights."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    inp = g.uniform(0.0, 1.0, n_in + 1).astype(np.float32)
+    w = g.uniform(0.0, 1.0, (n_in + 1) * (hid + 1)).astype(np.float32)
+    nb = n_in // 16
+    return Instance("bpnn_layerforward", Geom(grid_x, nb), Geom(*block), 0,
+                    [Buf("input", "f32", n_in + 1, inp), Buf("w", "f32", w.size, w),
+                     Buf("partial", "f32", nb * hid, np.zeros(nb * hid, np.float32))],
+                    [("buf", "input"), ("buf", "w"), ("buf", "partial"), ("i32", hid)],
+                    ["w", "partial"])
+
+
+def backprop_adjust(n_in: int, seed: int = 0, hid: int = BP_HID, block=(16, 16)) -> Instance:
+    """bpnn_adjust_weights of the input->hidden weights: delta (hid + 1),
+    ly = input layer (n_in + 1), w / oldw (n_in + 1) x (hid + 1)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    delta = g.uniform(-0.1, 0.1, hid + 1).astype(np.float32)
+    ly = g.uniform(0.0, 1.0, n_in + 1).astype(np.float32)
+    w = g.uniform(0.0, 1.0, (n_in + 1) * (hid + 1)).astype(np.float32)
+    oldw = g.uniform(-0.05, 0.05, (n_in + 1) * (hid + 1)).astype(np.float32)
+    nb = n_in // 16
+    return Instance("bpnn_adjust_weights", Geom(1, nb), Geom(*block), 0,
+                    [Buf("delta", "f32", hid + 1, delta), Buf("ly", "f32", n_in + 1, ly),
+                     Buf("w", "f32", w.size, w), Buf("oldw", "f32", oldw.size, oldw)],
+                    [("buf", "delta"), ("i32", hid), ("buf", "ly"), ("i32", n_in), ("buf", "w"),
+                     ("buf", "oldw")],
+                    ["w", "oldw"])

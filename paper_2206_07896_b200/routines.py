@@ -82,6 +82,11 @@ _TABLE = {
                   ("k", "i32")), True, 16, False, "kmeans.kn"),
     "bfs": (_p(("row", "global i32[]"), ("col", "global i32[]"), ("lvl", "global i32[]"),
                ("changed", "global i32[]"), ("nv", "i32"), ("cur", "i32")), False, 8, False, "bfs.kn"),
+    "bpnn_layerforward": (_p(("input", "global f32[]"), ("w", "global f32[]"), ("partial", "global f32[]"),
+                             ("hid", "i32")), False, 14, False, "backprop.kn"),
+    "bpnn_adjust_weights": (_p(("delta", "global f32[]"), ("hid", "i32"), ("ly", "global f32[]"),
+                               ("inn", "i32"), ("w", "global f32[]"), ("oldw", "global f32[]")),
+                            False, 11, False, "backprop.kn"),
 }
 
 

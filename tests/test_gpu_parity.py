@@ -46,8 +46,44 @@ def test_golden_sets_on_gpu(name):
     if not cases:
         pytest.skip(f"no registered kernel in {name}")
     for k, (inst, expected, trap) in enumerate(cases):
+        if not handwritten_geometry(inst):
+            # the hand-written kernel refuses it loudly (no fallback)
+            from paper_2206_07896_b200._lib import E_UNSUPPORTED, BfError
+            with pytest.raises(BfError) as ei:
+                gpu_run(inst)
+            assert ei.value.code == E_UNSUPPORTED
+            continue
         got, got_trap, _, _ = gpu_run(inst)
         check_case(name, k, inst, expected, trap, got, got_trap)
+
+
+def handwritten_geometry(inst) -> bool:
+    """Geometries the hand-written kernels implement."""
+    if inst.kernel.startswith("bpnn_"):
+        return ((inst.block.x, inst.block.y, inst.block.z) == (16, 16, 1) and inst.grid.x == 1
+                and inst.grid.z == 1)
+    return True
+
+
+@pytest.mark.parametrize("n_in", [16, 65536, 65536 * 3 + 16])
+def test_backprop_vs_oracle(n_in):
+    """Rodinia backprop's device kernels at Rodinia's default input layer
+    (65536 units) and ragged sizes: weights, partial sums and the adjusted
+    weights / momentum bit-exact; then a forward -> adjust chain."""
+    import instances as I
+    fw = I.backprop_forward(n_in, seed=n_in % 97)
+    want, trap = oracle.run(fw)
+    got, got_trap, _, _ = gpu_run(fw)
+    assert trap is None and got_trap is None
+    for b in ("w", "partial"):
+        assert bit_equal(got[b], want[b]), b
+    adj = I.backprop_adjust(n_in, seed=n_in % 89)
+    adj.buffer("w").values = want["w"]
+    want2, trap = oracle.run(adj)
+    got2, got_trap, _, _ = gpu_run(adj)
+    assert trap is None and got_trap is None
+    for b in ("w", "oldw"):
+        assert bit_equal(got2[b], want2[b]), b
 
 
 @pytest.mark.parametrize("pool,grain", [(1, None), (2, 1), (4, 3), (3, "avg")])
