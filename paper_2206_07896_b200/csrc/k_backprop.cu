@@ -32,62 +32,214 @@ namespace bf {
 
 constexpr int kBpHid = 16;
 
-// blocks [b0, b1): warp w handles blocks 2w, 2w+1 of its grid-stride step
+// Both kernels stream the contiguous region of their logical blocks: blocks
+// [b0, b1) own the floats [272 b0 + 17, 272 b1 + 17) of w (rows 16 b0 + 1 ..
+// 16 b1, all 17 columns).  A region offset of 17 (mod 4) means the interior
+// is moved with 16 B vector accesses and at most 3 + 1 edge floats singly.
+constexpr int kBpChunk = 16;                 // logical blocks per CTA step (forward)
+constexpr int kBpChunkF = 272 * kBpChunk;    // floats per chunk
+
+// forward: the region of kBpChunk blocks moves through a two-buffer
+// shared-memory ring: the aligned interior comes in by one bulk copy (TMA,
+// completing on the buffer's mbarrier) issued a step ahead, the <= 3 + 1 edge
+// floats by plain loads; one thread per (block, column) replays the tree in
+// shared memory (conflict-free: 17-float pitch) and the interior goes back by
+// one bulk store (column 0, the bias weights, is rewritten unchanged: it lies
+// inside the CTA's own rows).
+struct BpChunk {
+  long long c0, g0, g1, a0, a1;
+  int nblk;
+  __device__ BpChunk(long long c, long long b1) {
+    c0 = c;
+    nblk = (int)min((long long)kBpChunk, b1 - c);
+    g0 = 272 * c0 + 17;
+    g1 = 272 * (c0 + nblk) + 17;
+    a0 = (g0 + 3) & ~3LL;
+    a1 = g1 & ~3LL;
+  }
+};
+
 __global__ void __launch_bounds__(256) bp_forward(const float* __restrict__ input, float* __restrict__ w,
                                                   float* __restrict__ partial, long long b0, long long b1) {
-  const int lane = threadIdx.x & 31;
-  const int col = lane & 15, half = lane >> 4;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long pair = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);; pair += warps) {
-    const long long by = b0 + 2 * pair + half;
-    if (b0 + 2 * pair >= b1) break;
-    const bool on = by < b1;
-    // input node of row `col` of this lane's block, shuffled to the column lanes
+  __shared__ __align__(16) float sm[2][kBpChunkF + 8];
+  __shared__ __align__(8) uint64_t full[2];
+  const long long cstride = (long long)gridDim.x * kBpChunk;
+  const long long first = b0 + (long long)blockIdx.x * kBpChunk;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long c, int buf) {  // thread 0
+    const BpChunk k(c, b1);
+    const uint32_t bytes = (uint32_t)((k.a1 - k.a0) * 4);
+    mbar_arrive_expect_tx(&full[buf], bytes);
+    bulk_g2s(sm[buf] + 4, w + k.a0, bytes, &full[buf], policy_evict_first());
+  };
+  if (threadIdx.x == 0 && first < b1) issue(first, 0);
+  int n = 0;
+  for (long long c0 = first; c0 < b1; c0 += cstride, n++) {
+    const int buf = n & 1;
+    const BpChunk k(c0, b1);
+    if (threadIdx.x == 0 && c0 + cstride < b1) {
+      bulk_wait_read<0>();  // the other buffer's bulk store has left shared memory
+      issue(c0 + cstride, buf ^ 1);
+    }
+    float* Sa = sm[buf] + 4;             // a0 -> 16 B aligned
+    const int sh = (int)(k.a0 - k.g0);   // 0..3 leading edge floats
+    float* Sg = Sa - sh;                 // g0
+    if (threadIdx.x < sh) Sg[threadIdx.x] = w[k.g0 + threadIdx.x];
+    if (threadIdx.x < (int)(k.g1 - k.a1)) Sa[(k.a1 - k.a0) + threadIdx.x] = w[k.a1 + threadIdx.x];
+    const int blk = threadIdx.x >> 4, col = threadIdx.x & 15;
+    const bool on = blk < k.nblk;  // whole warps stay converged for the shuffles
+    const long long by = c0 + blk;
     const float node_mine = on ? __ldg(input + 16 * by + col + 1) : 0.f;
+    mbar_wait(&full[buf], (n >> 1) & 1);
+    __syncthreads();  // edge floats visible
+    float* T = Sg + 272 * blk + col + 1;  // row 0 of the block, this column
     float p[16];
-    const long long base = 272 * by + 17 + col + 1;  // row 0 of the block, this column
 #pragma unroll
-    for (int r = 0; r < 16; r++) p[r] = on ? __ldcs(w + base + 17 * r) : 0.f;
-#pragma unroll
-    for (int r = 0; r < 16; r++) p[r] = __fmul_rn(p[r], __shfl_sync(0xffffffffu, node_mine, (lane & 16) | r));
+    for (int r = 0; r < 16; r++) {
+      const float nd = __shfl_sync(0xffffffffu, node_mine, (threadIdx.x & 16) | r);
+      p[r] = on ? __fmul_rn(T[17 * r], nd) : 0.f;
+    }
     // Rodinia's tree: wm[ty] += wm[ty + s] for ty % 2s == 0, s = 1, 2, 4, 8
 #pragma unroll
-    for (int s = 1; s < 16; s *= 2)
+    for (int s2 = 1; s2 < 16; s2 *= 2)
 #pragma unroll
-      for (int r = 0; r < 16; r += 2 * s) p[r] = __fadd_rn(p[r], p[r + s]);
+      for (int r = 0; r < 16; r += 2 * s2) p[r] = __fadd_rn(p[r], p[r + s2]);
     if (on) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) __stcs(w + base + 17 * r, p[r]);
+      for (int r = 0; r < 16; r++) T[17 * r] = p[r];
       partial[16 * by + col] = p[0];
     }
+    fence_proxy_async();  // tile writes before the bulk store (async proxy)
+    __syncthreads();
+    if (threadIdx.x < sh) w[k.g0 + threadIdx.x] = Sg[threadIdx.x];
+    if (threadIdx.x < (int)(k.g1 - k.a1)) w[k.a1 + threadIdx.x] = Sa[(k.a1 - k.a0) + threadIdx.x];
+    if (threadIdx.x == 0) {
+      bulk_s2g(w + k.a0, Sa, (uint32_t)((k.a1 - k.a0) * 4));
+      bulk_commit();
+    }
+    __syncthreads();  // edge reads done before the buffer is refilled
   }
+  if (threadIdx.x == 0) bulk_wait_read<0>();
 }
+
+// adjust: elementwise over the region; element g = 17 row + col (col != 0):
+// ix = g, iy = row, delta index = col (DSL: index, iy = 16by+ty+1, ix = tx+1).
+__device__ __forceinline__ float bp_upd(float wv, float& ov, double cx, double l) {
+  const double s = dadd(dmul(cx, l), dmul(0.3, (double)ov));
+  ov = __double2float_rn(s);
+  return __double2float_rn(dadd((double)wv, s));
+}
+
+// adjust: the same two-buffer bulk-copy ring over the w and oldw regions of
+// kBpChunkA blocks; every element of the region is updated in shared memory
+// (column 0 is left as loaded) and both regions go back by bulk stores.
+constexpr int kBpChunkA = 8;
+constexpr int kBpChunkAF = 272 * kBpChunkA;
 
 __global__ void __launch_bounds__(256) bp_adjust(const float* __restrict__ delta, const float* __restrict__ ly,
                                                  float* __restrict__ w, float* __restrict__ oldw, long long b0,
                                                  long long b1, bool bias) {
-  // element e of the range = (block, row, col): 256 per block
-  const long long n = (b1 - b0) * 256;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const int col = threadIdx.x & 15;  // blockDim.x % 16 == 0 and stride % 16 == 0
-  const double cx = dmul(0.3, (double)__ldg(delta + col + 1));
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
-    const long long by = b0 + (e >> 8);
-    const int ty = (int)((e >> 4) & 15);
-    const long long ix = 272 * by + 17 * ty + col + 18;
-    const double l = (double)__ldg(ly + 16 * by + ty + 1);
-    const double o = (double)__ldcs(oldw + ix);
-    const double wv = (double)__ldcs(w + ix);
-    const double s = dadd(dmul(cx, l), dmul(0.3, o));
-    __stcs(w + ix, __double2float_rn(dadd(wv, s)));
-    __stcs(oldw + ix, __double2float_rn(s));
+  __shared__ __align__(16) float sw[2][kBpChunkAF + 8];
+  __shared__ __align__(16) float so[2][kBpChunkAF + 8];
+  __shared__ __align__(8) uint64_t full[2];
+  static_assert(kBpChunkA * 16 * 2 == 256, "two threads per weight row");
+  double cx[8];  // 0.3 * delta[col] of this thread's eight columns
+#pragma unroll
+  for (int j = 0; j < 8; j++) cx[j] = dmul(0.3, (double)__ldg(delta + 1 + 8 * (threadIdx.x & 1) + j));
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_barrier_init();
   }
+  __syncthreads();
+  const long long cstride = (long long)gridDim.x * kBpChunkA;
+  const long long first = b0 + (long long)blockIdx.x * kBpChunkA;
+  auto region = [&](long long c, long long& g0, long long& g1, long long& a0, long long& a1) {
+    const long long nb = min((long long)kBpChunkA, b1 - c);
+    g0 = 272 * c + 17;
+    g1 = 272 * (c + nb) + 17;
+    a0 = (g0 + 3) & ~3LL;
+    a1 = g1 & ~3LL;
+  };
+  auto issue = [&](long long c, int buf) {  // thread 0
+    long long g0, g1, a0, a1;
+    region(c, g0, g1, a0, a1);
+    const uint32_t bytes = (uint32_t)((a1 - a0) * 4);
+    const uint64_t pol = policy_evict_first();
+    mbar_arrive_expect_tx(&full[buf], 2 * bytes);
+    bulk_g2s(sw[buf] + 4, w + a0, bytes, &full[buf], pol);
+    bulk_g2s(so[buf] + 4, oldw + a0, bytes, &full[buf], pol);
+  };
+  if (threadIdx.x == 0 && first < b1) issue(first, 0);
+  int n = 0;
+  for (long long c0 = first; c0 < b1; c0 += cstride, n++) {
+    const int buf = n & 1;
+    if (threadIdx.x == 0 && c0 + cstride < b1) {
+      bulk_wait_read<0>();
+      issue(c0 + cstride, buf ^ 1);
+    }
+    long long g0, g1, a0, a1;
+    region(c0, g0, g1, a0, a1);
+    const int sh = (int)(a0 - g0), tl = (int)(g1 - a1);
+    float* W = sw[buf] + 4 - sh;  // g0
+    float* O = so[buf] + 4 - sh;
+    const int len = (int)(g1 - g0);
+    if (threadIdx.x < sh) {
+      W[threadIdx.x] = w[g0 + threadIdx.x];
+      O[threadIdx.x] = oldw[g0 + threadIdx.x];
+    }
+    if (threadIdx.x < tl) {
+      W[len - tl + threadIdx.x] = w[a1 + threadIdx.x];
+      O[len - tl + threadIdx.x] = oldw[a1 + threadIdx.x];
+    }
+    mbar_wait(&full[buf], (n >> 1) & 1);
+    __syncthreads();
+    // two threads per row (columns 1-8 and 9-16): ly[row] is read and
+    // converted once per 8 elements, 0.3*delta[col] stays in registers.
+    // Row r of the region = weight row 16 c0 + 1 + r; element (r, col) is
+    // region index 17 r + col.
+    {
+      const int r = threadIdx.x >> 1, cb = 1 + 8 * (threadIdx.x & 1);
+      if (r < len / 17) {
+        const double l = (double)__ldg(ly + 16 * c0 + 1 + r);
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int i = 17 * r + cb + j;
+          const double sv = dadd(dmul(cx[j], l), dmul(0.3, (double)O[i]));
+          O[i] = __double2float_rn(sv);
+          W[i] = __double2float_rn(dadd((double)W[i], sv));
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x < sh) {
+      w[g0 + threadIdx.x] = W[threadIdx.x];
+      oldw[g0 + threadIdx.x] = O[threadIdx.x];
+    }
+    if (threadIdx.x < tl) {
+      w[a1 + threadIdx.x] = W[len - tl + threadIdx.x];
+      oldw[a1 + threadIdx.x] = O[len - tl + threadIdx.x];
+    }
+    if (threadIdx.x == 0) {
+      bulk_s2g(w + a0, sw[buf] + 4, (uint32_t)((a1 - a0) * 4));
+      bulk_s2g(oldw + a0, so[buf] + 4, (uint32_t)((a1 - a0) * 4));
+      bulk_commit();
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bulk_wait_read<0>();
   if (bias && blockIdx.x == 0 && threadIdx.x < 16) {  // row 0 (bias), block 0's ty == 0 threads
     const int x = threadIdx.x + 1;
     const double o = (double)oldw[x];
-    const double s = dadd(dmul(0.3, (double)delta[x]), dmul(0.3, o));
-    w[x] = __double2float_rn(dadd((double)w[x], s));
-    oldw[x] = __double2float_rn(s);
+    const double sv = dadd(dmul(0.3, (double)delta[x]), dmul(0.3, o));
+    w[x] = __double2float_rn(dadd((double)w[x], sv));
+    oldw[x] = __double2float_rn(sv);
   }
 }
 
@@ -126,7 +278,12 @@ static int launch_bp_forward(LaunchCtx& ctx) {
     b1 = bad;
   }
   if (b0 >= b1) return BF_OK;
-  const int grid = stream_grid((b1 - b0 + 1) / 2, 8, ctx.num_sms, 8);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bp_forward, 256, 0);
+    per_sm = std::max(per_sm, 1);
+  }
+  const int grid = stream_grid(b1 - b0, kBpChunk, ctx.num_sms, per_sm);
   bp_forward<<<grid, 256, 0, ctx.stream>>>((const float*)In.ptr, (float*)W.ptr, (float*)P.ptr, b0, b1);
   BF_CUDA_LAUNCH_CHECK(ctx);
   return BF_OK;
@@ -150,7 +307,12 @@ static int launch_bp_adjust(LaunchCtx& ctx) {
   }
   if (b0 >= b1) return BF_OK;
   const bool bias = b0 == 0;
-  const int grid = stream_grid((b1 - b0) * 256, 256 * 4, ctx.num_sms, 8);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bp_adjust, 256, 0);
+    per_sm = std::max(per_sm, 1);
+  }
+  const int grid = stream_grid(b1 - b0, kBpChunkA, ctx.num_sms, per_sm);
   bp_adjust<<<grid, 256, 0, ctx.stream>>>((const float*)D.ptr, (const float*)L.ptr, (float*)W.ptr, (float*)O.ptr,
                                           b0, b1, bias);
   BF_CUDA_LAUNCH_CHECK(ctx);
