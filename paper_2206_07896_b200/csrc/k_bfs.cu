@@ -233,6 +233,163 @@ __global__ void __launch_bounds__(256) bfs_expand(const int* __restrict__ row,
   }
 }
 
+// Expansion with whole-adjacency vector loads: two frontier vertices per
+// thread, eight edges per vertex per step; an 8-edge chunk starting at a
+// multiple of 4 is fetched as two 16 B loads (the full 32 B sector at once,
+// default caching), anything else edge by edge.  All 16 targets' bitmap
+// words are loaded before any RED is issued.
+constexpr int kBfsV2 = 2;
+template <bool TEST>
+__global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
+                                                    const int* __restrict__ col, long long ne,
+                                                    unsigned* now, long long nv,
+                                                    const int* __restrict__ q, int* sizes) {
+  const int qn = sizes[0];
+  const long long stride = (long long)gridDim.x * blockDim.x * kBfsV2;
+  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kBfsV2; i0 < qn; i0 += stride) {
+    int e0[kBfsV2], e1[kBfsV2];
+#pragma unroll
+    for (int a = 0; a < kBfsV2; a++) {
+      e0[a] = e1[a] = 0;
+      if (i0 + a < qn) {
+        const int u = __ldg(q + i0 + a);
+        const int2 rr = (u & 1) ? make_int2(__ldg(row + u), __ldg(row + u + 1))
+                                : __ldg(reinterpret_cast<const int2*>(row + u));
+        e0[a] = rr.x;
+        e1[a] = rr.y;
+        if (e0[a] < 0 || e1[a] > ne || e1[a] < e0[a]) {
+          sizes[2] = 1;
+          e1[a] = e0[a];
+        }
+      }
+    }
+    const int maxd = max(e1[0] - e0[0], e1[1] - e0[1]);
+    for (int j = 0; j < maxd; j += 8) {
+      int v[kBfsV2][8];
+#pragma unroll
+      for (int a = 0; a < kBfsV2; a++) {
+        const int b = e0[a] + j;
+        if (b + 8 <= e1[a] && (b & 3) == 0) {
+          const int4 x = __ldg(reinterpret_cast<const int4*>(col + b));
+          const int4 y = __ldg(reinterpret_cast<const int4*>(col + b + 4));
+          v[a][0] = x.x; v[a][1] = x.y; v[a][2] = x.z; v[a][3] = x.w;
+          v[a][4] = y.x; v[a][5] = y.y; v[a][6] = y.z; v[a][7] = y.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; t++) v[a][t] = b + t < e1[a] ? __ldg(col + b + t) : -1;
+        }
+      }
+      unsigned w[kBfsV2][8];
+#pragma unroll
+      for (int a = 0; a < kBfsV2; a++)
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+          w[a][t] = 0xffffffffu;
+          if (v[a][t] >= 0) {
+            if (v[a][t] >= nv) sizes[2] = 1;
+            else w[a][t] = TEST ? __ldcg(now + (v[a][t] >> 5)) : 0u;
+          }
+        }
+#pragma unroll
+      for (int a = 0; a < kBfsV2; a++)
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+          const unsigned bit = 1u << (v[a][t] & 31);
+          if (v[a][t] >= 0 && v[a][t] < nv && !(w[a][t] & bit)) atomicOr(now + (v[a][t] >> 5), bit);
+        }
+    }
+  }
+}
+
+// Level bytes: while depth + 1 < 255 the compaction records a vertex's level
+// in a byte array (64 MB at 2^26 vertices, L2-resident) instead of scattering
+// 4 B writes over the 256 MB lvl array; bfs_finish converts once, densely.
+__global__ void __launch_bounds__(256) bfs_compact8(unsigned* now, unsigned* prev, long long words,
+                                                    int* nq, int* sizes, unsigned char* lv8, int* lvl,
+                                                    int depth) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const bool bytes = depth + 1 < 255;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < words; i += stride) {
+    unsigned fresh = 0;
+    if (i < words) {
+      const unsigned nw = __ldcg(now + i);
+      fresh = nw & ~prev[i];
+      if (fresh) prev[i] = nw;
+    }
+    const int c = __popc(fresh);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(sizes + 1, total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = base + incl - c;
+    while (fresh) {
+      const int b = __ffs(fresh) - 1;
+      const int v = (int)(i * 32 + b);
+      nq[pos++] = v;
+      if (bytes) lv8[v] = (unsigned char)(depth + 1);
+      else lvl[v] = depth + 1;
+      fresh &= fresh - 1;
+    }
+  }
+}
+
+// lvl[v] from the level bytes (0xFF: unvisited, or a level >= 255 already in lvl)
+__global__ void __launch_bounds__(256) bfs_finish(const unsigned char* __restrict__ lv8, int* lvl, long long nv,
+                                                  bool deep) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const uchar4* b4 = reinterpret_cast<const uchar4*>(lv8);
+  int4* l4 = reinterpret_cast<int4*>(lvl);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv / 4; i += stride) {
+    const uchar4 b = b4[i];
+    int4 o = deep ? l4[i] : make_int4(-1, -1, -1, -1);
+    if (b.x != 0xFF) o.x = b.x;
+    if (b.y != 0xFF) o.y = b.y;
+    if (b.z != 0xFF) o.z = b.z;
+    if (b.w != 0xFF) o.w = b.w;
+    __stcs(l4 + i, o);
+  }
+  for (long long i = nv / 4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const unsigned char b = lv8[i];
+    lvl[i] = b != 0xFF ? (int)b : (deep ? lvl[i] : -1);
+  }
+}
+
+__global__ void __launch_bounds__(256) bfs_init8(unsigned char* lv8, unsigned* now, unsigned* prev,
+                                                 long long nv, long long words, int src, int* q0, int* sizes) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  uint4* b16 = reinterpret_cast<uint4*>(lv8);
+  for (long long i = t; i < nv / 16; i += stride) b16[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+  for (long long i = nv / 16 * 16 + t; i < nv; i += stride) lv8[i] = 0xFF;
+  for (long long i = t; i < words; i += stride) {
+    now[i] = 0u;
+    prev[i] = 0u;
+  }
+  if (t == 0) {
+    sizes[0] = 1;
+    sizes[1] = 0;
+    sizes[2] = 0;
+    q0[0] = src;
+  }
+}
+
+__global__ void bfs_seed8(unsigned char* lv8, unsigned* now, unsigned* prev, int src) {
+  lv8[src] = 0;
+  now[src >> 5] = 1u << (src & 31);
+  prev[src >> 5] = 1u << (src & 31);
+}
+
+__global__ void __launch_bounds__(256) bfs_fill_m1(int* lvl, long long nv) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) lvl[i] = -1;
+}
+
 // next frontier = now & ~prev, prev = now
 __global__ void __launch_bounds__(256) bfs_compact(unsigned* now, unsigned* prev, long long words,
                                                    int* nq, int* sizes, int* lvl, int depth) {
@@ -285,6 +442,7 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
     long long cap_words = 0, cap_v = 0;
     unsigned *now = nullptr, *prev = nullptr;
     int *qa = nullptr, *qb = nullptr, *sizes = nullptr, *hs = nullptr;
+    unsigned char* lv8 = nullptr;
   };
   static Scratch sc[64];
   int dev = 0;
@@ -297,11 +455,16 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
     cudaFree(S.prev);
     cudaFree(S.qa);
     cudaFree(S.qb);
-    S = Scratch();
+    cudaFree(S.lv8);
+    S.now = S.prev = nullptr;
+    S.qa = S.qb = nullptr;
+    S.lv8 = nullptr;
+    S.cap_v = S.cap_words = 0;
     e = cudaMalloc((void**)&S.now, words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.prev, words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.qa, (size_t)nv * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.qb, (size_t)nv * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.lv8, (size_t)nv + 16);
     if (e == cudaSuccess) {
       S.cap_v = nv;
       S.cap_words = words;
@@ -311,6 +474,13 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   if (e == cudaSuccess && !S.hs) e = cudaMallocHost((void**)&S.hs, 16);
   unsigned *now = S.now, *prev = S.prev;
   int *qa = S.qa, *qb = S.qb, *sizes = S.sizes, *hs = S.hs;
+  unsigned char* lv8 = S.lv8;
+  static int variant = -1;  // 1: scalar-edge expansion + direct lvl writes (round-1 path)
+  if (variant < 0) {
+    const char* ve = getenv("BF_BFS_V");
+    variant = ve ? atoi(ve) : 2;
+  }
+  bool deep = false;
   int depth = 0;
   // keep the visited bitmap resident in L2 while the graph streams through
   cudaStreamAttrValue win = {};
@@ -333,16 +503,34 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   }
   if (e == cudaSuccess) {
     int g = stream_grid(nv, 256 * 4, num_sms, 8);
-    bfs_init<<<g, 256, 0, stream>>>(lvl, now, prev, nv, words, src, qa, sizes);
-    bfs_seed<<<1, 1, 0, stream>>>(lvl, now, prev, src);
+    if (variant == 1) {
+      bfs_init<<<g, 256, 0, stream>>>(lvl, now, prev, nv, words, src, qa, sizes);
+      bfs_seed<<<1, 1, 0, stream>>>(lvl, now, prev, src);
+    } else {
+      bfs_init8<<<g, 256, 0, stream>>>(lv8, now, prev, nv, words, src, qa, sizes);
+      bfs_seed8<<<1, 1, 0, stream>>>(lv8, now, prev, src);
+    }
     int qn = 1;
     int* q = qa;
     int* nq = qb;
     const int cgrid = stream_grid(words, 256, num_sms, 8);
     while (qn > 0) {
-      int grid = stream_grid((qn + kBfsVPT - 1) / kBfsVPT, 256, num_sms, 8);
-      bfs_expand<<<grid, 256, 0, stream>>>(row, col, lcol, lvl, now, nv, q, sizes, depth);
-      bfs_compact<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lvl, depth);
+      if (variant == 1) {
+        int grid = stream_grid((qn + kBfsVPT - 1) / kBfsVPT, 256, num_sms, 8);
+        bfs_expand<<<grid, 256, 0, stream>>>(row, col, lcol, lvl, now, nv, q, sizes, depth);
+        bfs_compact<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lvl, depth);
+      } else {
+        if (depth + 1 >= 255 && !deep) {  // levels beyond a byte: lvl written directly from here on
+          bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, nv);
+          deep = true;
+        }
+        int grid = stream_grid((qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
+        if (variant == 3)
+          bfs_expand_v<false><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
+        else
+          bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
+        bfs_compact8<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lv8, lvl, depth);
+      }
       cudaMemcpyAsync(hs, sizes, 12, cudaMemcpyDeviceToHost, stream);
       e = cudaStreamSynchronize(stream);
       if (e != cudaSuccess) break;
@@ -360,6 +548,7 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
       q = nq;
       nq = t;
     }
+    if (e == cudaSuccess && variant != 1) bfs_finish<<<g, 256, 0, stream>>>(lv8, lvl, nv, deep);
   }
   if (windowed) {
     win.accessPolicyWindow.num_bytes = 0;

@@ -249,8 +249,25 @@ def test_bfs_levels_fused_vs_oracle():
     import instances as I
     from gpu_helpers import materialize
     from paper_2206_07896_b200 import DeviceArena, Runtime, graph
-    for nv, deg, seed, src in [(5000, 4, 1, 0), (200000, 8, 2, 17), (777, 1, 3, 5), (3000, 13, 4, 2999)]:
-        row, col = I.random_graph(nv, deg, seed)
+    graphs = [(I.random_graph(nv, deg, seed), nv, src)
+              for nv, deg, seed, src in [(5000, 4, 1, 0), (200000, 8, 2, 17), (777, 1, 3, 5), (3000, 13, 4, 2999)]]
+    # variable degrees (unaligned adjacency starts) and a 700-vertex chain with
+    # side branches: depth > 255 exercises the levels beyond the byte array
+    g = np.random.default_rng(9)
+    nv = 50000
+    degs = g.integers(0, 13, nv)
+    row = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
+    col = g.integers(0, nv, int(row[-1])).astype(np.int32)
+    graphs.append(((row, col), nv, 3))
+    nv = 1400
+    adj = [[i + 1] if i < 699 else [] for i in range(nv)]
+    for i in range(0, 700, 7):
+        adj[i].append(700 + i % 700)
+        adj[700 + i % 700].append(700 + (i + 350) % 700)
+    row = np.concatenate([[0], np.cumsum([len(a) for a in adj])]).astype(np.int32)
+    col = np.array([v for a in adj for v in a], np.int32)
+    graphs.append(((row, col), nv, 0))
+    for (row, col), nv, src in graphs:
         want, depth = oracle.bfs_full(row, col, nv, src)
         arena = DeviceArena()
         hr, hc, hl = arena.alloc("i32", nv + 1), arena.alloc("i32", col.size), arena.alloc("i32", nv)
