@@ -228,6 +228,28 @@ int bf_worker_stream(bf_runtime *rt, int32_t worker, void **stream);
 int bf_bfs_levels(bf_runtime *rt, uint32_t row, uint32_t col, uint32_t lvl,
                   int32_t nv, int32_t source, int32_t *depth);
 
+/* Sharded BFS traversal, one process per GPU (parallel.bfs_levels_sharded;
+ * SURVEY §8e "bfs: per-level frontier exchange").  A shard keeps the whole
+ * nv-bit visited bitmap and per-vertex level bytes on its device and expands
+ * only the frontier vertices of its own range [vlo, vhi).  Per level the host
+ * calls expand, all-gathers every rank's bitmap (world x words uint32 in
+ * rank order, e.g. torch.distributed.all_gather_into_tensor over NCCL) and
+ * passes it to merge (OR), then compact, which returns the number of vertices
+ * discovered in the level — the same on every rank, so the loop ends together
+ * (stop at 0).  finish writes lvl (identical on every rank; exactly the
+ * levels of bf_bfs_levels).  All calls run on worker 0's stream and return
+ * when their work is done (merge only enqueues). */
+typedef struct bf_bfs_shard bf_bfs_shard;
+int bf_bfs_shard_create(bf_runtime *rt, int32_t nv, bf_bfs_shard **out);
+int bf_bfs_shard_destroy(bf_bfs_shard *s);
+/* device pointer and length (uint32 words) of the shard's visited bitmap */
+int bf_bfs_shard_bitmap(bf_bfs_shard *s, void **dev_ptr, int64_t *words);
+int bf_bfs_shard_begin(bf_bfs_shard *s, int32_t source, int64_t vlo, int64_t vhi);
+int bf_bfs_shard_expand(bf_bfs_shard *s, uint32_t row, uint32_t col);
+int bf_bfs_shard_merge(bf_bfs_shard *s, const void *gathered_dev, int32_t world);
+int bf_bfs_shard_compact(bf_bfs_shard *s, uint32_t lvl, int64_t *fresh);
+int bf_bfs_shard_finish(bf_bfs_shard *s, uint32_t lvl, int32_t *depth);
+
 /* Rodinia's hotspot host loop fused: the result of `iterations` ping-pong
  * launches of `hotspot` (kernels/hotspot.kn) starting from buffer `a`, with
  * `b` as the other buffer — bit-identical.  tsteps = 1: one streaming pass

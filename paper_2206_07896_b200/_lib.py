@@ -38,6 +38,8 @@ EXPORTS = [
     "bf_counters_get", "bf_worker_stream",
     "bf_kernel_count", "bf_kernel_info",
     "bf_bfs_levels", "bf_hotspot_run", "bf_jit_register",
+    "bf_bfs_shard_create", "bf_bfs_shard_destroy", "bf_bfs_shard_bitmap", "bf_bfs_shard_begin",
+    "bf_bfs_shard_expand", "bf_bfs_shard_merge", "bf_bfs_shard_compact", "bf_bfs_shard_finish",
 ]
 
 
@@ -115,6 +117,14 @@ def _declare(lib) -> None:
         "bf_worker_stream": (C.c_int, [P, i32, C.POINTER(P)]),
         "bf_kernel_count": (C.c_int, [I32P]),
         "bf_bfs_levels": (C.c_int, [P, u32, u32, u32, i32, i32, I32P]),
+        "bf_bfs_shard_create": (C.c_int, [P, i32, C.POINTER(P)]),
+        "bf_bfs_shard_destroy": (C.c_int, [P]),
+        "bf_bfs_shard_bitmap": (C.c_int, [P, C.POINTER(P), I64P]),
+        "bf_bfs_shard_begin": (C.c_int, [P, i32, i64, i64]),
+        "bf_bfs_shard_expand": (C.c_int, [P, u32, u32]),
+        "bf_bfs_shard_merge": (C.c_int, [P, P, i32]),
+        "bf_bfs_shard_compact": (C.c_int, [P, u32, I64P]),
+        "bf_bfs_shard_finish": (C.c_int, [P, u32, I32P]),
         "bf_hotspot_run": (C.c_int, [P, u32, u32, u32, i32, i32, C.POINTER(dbl), i32, i32]),
         "bf_jit_register": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, i32, I32P, I32P, i32]),
         "bf_kernel_info": (C.c_int, [i32, C.c_char_p, i32, I32P, I32P, I32P, i32]),

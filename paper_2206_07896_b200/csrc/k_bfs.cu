@@ -390,6 +390,67 @@ __global__ void __launch_bounds__(256) bfs_fill_m1(int* lvl, long long nv) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) lvl[i] = -1;
 }
 
+// ---- sharded traversal (one process per GPU, parallel.bfs_levels_sharded) --
+// Every rank keeps the whole visited bitmap and the level bytes; it expands
+// only the frontier vertices of its own range [vlo, vhi); after the ranks'
+// bitmaps are OR-merged (an all-gather of the nv-bit `now`), the compaction
+// sees the same fresh set on every rank: all ranks record the same levels,
+// each enqueues only its own fresh vertices, and the global fresh count (the
+// loop condition) agrees without another collective.
+__global__ void __launch_bounds__(256) bfs_merge_or(unsigned* now, const unsigned* __restrict__ g,
+                                                    long long words, int world) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) {
+    unsigned v = now[i];
+    for (int r = 0; r < world; r++) v |= __ldcs(g + (long long)r * words + i);
+    now[i] = v;
+  }
+}
+
+// sizes: [0] own queue length, [1] next own queue length, [2] CSR error, [3] global fresh
+__global__ void __launch_bounds__(256) bfs_compact_sh(unsigned* now, unsigned* prev, long long words, int* nq,
+                                                      int* sizes, unsigned char* lv8, int* lvl, int depth,
+                                                      long long vlo, long long vhi) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const bool bytes = depth + 1 < 255;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < words; i += stride) {
+    unsigned fresh = 0, own = 0;
+    if (i < words) {
+      const unsigned nw = __ldcg(now + i);
+      fresh = nw & ~prev[i];
+      if (fresh) prev[i] = nw;
+      // bits of word i inside [vlo, vhi)
+      const long long b0 = i * 32;
+      unsigned m = 0xffffffffu;
+      if (b0 < vlo) m = vlo - b0 >= 32 ? 0u : (m << (vlo - b0));
+      if (b0 + 32 > vhi) m &= vhi <= b0 ? 0u : (0xffffffffu >> (b0 + 32 - vhi));
+      own = fresh & m;
+    }
+    const int c = __popc(own);
+    int incl = c, all = __popc(fresh);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+      all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(sizes + 1, total);
+    if (lane == 0 && all) atomicAdd(sizes + 3, all);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = base + incl - c;
+    while (fresh) {
+      const int b = __ffs(fresh) - 1;
+      const int v = (int)(i * 32 + b);
+      if (own >> b & 1) nq[pos++] = v;
+      if (bytes) lv8[v] = (unsigned char)(depth + 1);
+      else lvl[v] = depth + 1;
+      fresh &= fresh - 1;
+    }
+  }
+}
+
 // next frontier = now & ~prev, prev = now
 __global__ void __launch_bounds__(256) bfs_compact(unsigned* now, unsigned* prev, long long words,
                                                    int* nq, int* sizes, int* lvl, int depth) {
@@ -563,6 +624,196 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
     return e == cudaErrorInvalidValue ? BF_E_FAULT : BF_E_CUDA;
   }
   *depth_out = depth;
+  return BF_OK;
+}
+
+// ---- sharded traversal state (bf_bfs_* in include/bfgpu.h) ----------------
+struct BfsShard {
+  int nv = 0;
+  long long words = 0, vlo = 0, vhi = 0;
+  unsigned *now = nullptr, *prev = nullptr;
+  int *qa = nullptr, *qb = nullptr, *sizes = nullptr, *hs = nullptr, *lvl_tmp = nullptr;
+  unsigned char* lv8 = nullptr;
+  int depth = 0, qn = 0;
+  bool deep = false;
+  int* q = nullptr;
+  int* nq = nullptr;
+};
+
+extern "C" int bf_bfs_shard_destroy_impl(void* p);
+
+extern "C" int bf_bfs_shard_create_impl(int nv, void** out, char* err, int errcap) {
+  using namespace bf;
+  if (nv <= 0) {
+    snprintf(err, errcap, "bfs shard: nv must be > 0");
+    return BF_E_INVALID;
+  }
+  BfsShard* s = new BfsShard();
+  s->nv = nv;
+  s->words = ((long long)nv + 31) / 32;
+  cudaError_t e = cudaMalloc((void**)&s->now, s->words * 4);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->prev, s->words * 4);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->qa, (size_t)nv * 4);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->qb, (size_t)nv * 4);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->lv8, (size_t)nv + 16);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->sizes, 16);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&s->hs, 16);
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    bf_bfs_shard_destroy_impl(s);
+    return BF_E_CUDA;
+  }
+  *out = s;
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_destroy_impl(void* p) {
+  BfsShard* s = (BfsShard*)p;
+  if (!s) return BF_OK;
+  cudaFree(s->now);
+  cudaFree(s->prev);
+  cudaFree(s->qa);
+  cudaFree(s->qb);
+  cudaFree(s->lv8);
+  cudaFree(s->sizes);
+  if (s->hs) cudaFreeHost(s->hs);
+  delete s;
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_bitmap_impl(void* p, void** ptr, long long* words) {
+  BfsShard* s = (BfsShard*)p;
+  *ptr = s->now;
+  *words = s->words;
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_begin_impl(void* p, void* stream_v, int num_sms, int src, long long vlo, long long vhi,
+                                       char* err, int errcap) {
+  using namespace bf;
+  BfsShard* s = (BfsShard*)p;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  if (src < 0 || src >= s->nv || vlo < 0 || vhi < vlo || vhi > s->nv) {
+    snprintf(err, errcap, "bfs shard: bad source or vertex range");
+    return BF_E_INVALID;
+  }
+  s->vlo = vlo;
+  s->vhi = vhi;
+  s->depth = 0;
+  s->deep = false;
+  s->q = s->qa;
+  s->nq = s->qb;
+  const int g = stream_grid(s->nv, 256 * 4, num_sms, 8);
+  bfs_init8<<<g, 256, 0, stream>>>(s->lv8, s->now, s->prev, s->nv, s->words, src, s->qa, s->sizes);
+  bfs_seed8<<<1, 1, 0, stream>>>(s->lv8, s->now, s->prev, src);
+  s->qn = (src >= vlo && src < vhi) ? 1 : 0;
+  s->hs[0] = s->qn;
+  s->hs[1] = 0;
+  s->hs[2] = 0;
+  s->hs[3] = 0;
+  cudaMemcpyAsync(s->sizes, s->hs, 16, cudaMemcpyHostToDevice, stream);
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
+    return BF_E_CUDA;
+  }
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_expand_impl(void* p, void* stream_v, int num_sms, const int* row, long long lr,
+                                        const int* col, long long lcol, char* err, int errcap) {
+  using namespace bf;
+  BfsShard* s = (BfsShard*)p;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  if (lr < (long long)s->nv + 1) {
+    snprintf(err, errcap, "bfs shard: row shorter than nv + 1");
+    return BF_E_INVALID;
+  }
+  if (s->qn > 0) {
+    const int grid = stream_grid((s->qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
+    bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, s->now, s->nv, s->q, s->sizes);
+  }
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
+    return BF_E_CUDA;
+  }
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_merge_impl(void* p, void* stream_v, int num_sms, const void* gathered, int world,
+                                       char* err, int errcap) {
+  using namespace bf;
+  BfsShard* s = (BfsShard*)p;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  const int grid = stream_grid(s->words, 256, num_sms, 8);
+  bfs_merge_or<<<grid, 256, 0, stream>>>(s->now, (const unsigned*)gathered, s->words, world);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
+    return BF_E_CUDA;
+  }
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_compact_impl(void* p, void* stream_v, int num_sms, int* lvl, long long ll,
+                                         long long* fresh, char* err, int errcap) {
+  using namespace bf;
+  BfsShard* s = (BfsShard*)p;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  if (ll < s->nv) {
+    snprintf(err, errcap, "bfs shard: lvl shorter than nv");
+    return BF_E_INVALID;
+  }
+  if (s->depth + 1 >= 255 && !s->deep) {
+    const int g = stream_grid(s->nv, 256 * 4, num_sms, 8);
+    bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, s->nv);
+    s->deep = true;
+  }
+  const int cgrid = stream_grid(s->words, 256, num_sms, 8);
+  bfs_compact_sh<<<cgrid, 256, 0, stream>>>(s->now, s->prev, s->words, s->nq, s->sizes, s->lv8, lvl, s->depth,
+                                             s->vlo, s->vhi);
+  cudaMemcpyAsync(s->hs, s->sizes, 16, cudaMemcpyDeviceToHost, stream);
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
+    return BF_E_CUDA;
+  }
+  if (s->hs[2]) {
+    snprintf(err, errcap, "bfs_levels: CSR index out of range");
+    return BF_E_FAULT;
+  }
+  *fresh = s->hs[3];
+  s->depth++;
+  s->qn = s->hs[1];
+  s->hs[0] = s->qn;
+  s->hs[1] = 0;
+  s->hs[3] = 0;
+  cudaMemcpyAsync(s->sizes, s->hs, 16, cudaMemcpyHostToDevice, stream);
+  int* t = s->q;
+  s->q = s->nq;
+  s->nq = t;
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_finish_impl(void* p, void* stream_v, int num_sms, int* lvl, long long ll, int* depth,
+                                        char* err, int errcap) {
+  using namespace bf;
+  BfsShard* s = (BfsShard*)p;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  if (ll < s->nv) {
+    snprintf(err, errcap, "bfs shard: lvl shorter than nv");
+    return BF_E_INVALID;
+  }
+  const int g = stream_grid(s->nv, 256 * 4, num_sms, 8);
+  bfs_finish<<<g, 256, 0, stream>>>(s->lv8, lvl, s->nv, s->deep);
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
+    return BF_E_CUDA;
+  }
+  *depth = s->depth;
   return BF_OK;
 }
 

@@ -1210,6 +1210,122 @@ int bf_bfs_levels(bf_runtime* rt, uint32_t row, uint32_t col, uint32_t lvl, int3
   return BF_OK;
 }
 
+// ---- sharded BFS traversal (parallel.bfs_levels_sharded) --------------------
+extern "C" {
+int bf_bfs_shard_create_impl(int nv, void** out, char* err, int errcap);
+int bf_bfs_shard_destroy_impl(void* p);
+int bf_bfs_shard_bitmap_impl(void* p, void** ptr, long long* words);
+int bf_bfs_shard_begin_impl(void* p, void* stream, int num_sms, int src, long long vlo, long long vhi, char* err,
+                            int errcap);
+int bf_bfs_shard_expand_impl(void* p, void* stream, int num_sms, const int* row, long long lr, const int* col,
+                             long long lcol, char* err, int errcap);
+int bf_bfs_shard_merge_impl(void* p, void* stream, int num_sms, const void* gathered, int world, char* err,
+                            int errcap);
+int bf_bfs_shard_compact_impl(void* p, void* stream, int num_sms, int* lvl, long long ll, long long* fresh,
+                              char* err, int errcap);
+int bf_bfs_shard_finish_impl(void* p, void* stream, int num_sms, int* lvl, long long ll, int* depth, char* err,
+                             int errcap);
+}
+
+struct bf_bfs_shard {
+  bf_runtime* rt;
+  void* impl;
+};
+
+#define BFS_SHARD_PRE(s)                                                   \
+  if (!(s) || !(s)->rt) return fail(BF_E_INVALID, "null bfs shard");      \
+  if ((s)->rt->shut_down) return fail(BF_E_SHUTDOWN, "runtime shut down"); \
+  {                                                                        \
+    int rc_ = set_device((s)->rt->device);                                 \
+    if (rc_) return rc_;                                                   \
+  }
+
+int bf_bfs_shard_create(bf_runtime* rt, int32_t nv, bf_bfs_shard** out) {
+  if (!rt || !out) return fail(BF_E_INVALID, "null argument");
+  if (rt->shut_down) return fail(BF_E_SHUTDOWN, "runtime shut down");
+  int rc = set_device(rt->device);
+  if (rc) return rc;
+  char err[256] = {0};
+  void* impl = nullptr;
+  rc = bf_bfs_shard_create_impl(nv, &impl, err, sizeof(err));
+  if (rc) return fail(rc, err);
+  *out = new bf_bfs_shard{rt, impl};
+  return BF_OK;
+}
+
+int bf_bfs_shard_destroy(bf_bfs_shard* s) {
+  if (!s) return BF_OK;
+  if (s->rt) set_device(s->rt->device);
+  bf_bfs_shard_destroy_impl(s->impl);
+  delete s;
+  return BF_OK;
+}
+
+int bf_bfs_shard_bitmap(bf_bfs_shard* s, void** dev_ptr, int64_t* words) {
+  if (!s || !dev_ptr || !words) return fail(BF_E_INVALID, "null argument");
+  long long w = 0;
+  bf_bfs_shard_bitmap_impl(s->impl, dev_ptr, &w);
+  *words = w;
+  return BF_OK;
+}
+
+int bf_bfs_shard_begin(bf_bfs_shard* s, int32_t source, int64_t vlo, int64_t vhi) {
+  BFS_SHARD_PRE(s);
+  int rc = sync_workers(s->rt);
+  if (rc) return rc;
+  char err[256] = {0};
+  rc = bf_bfs_shard_begin_impl(s->impl, (void*)s->rt->streams[0], s->rt->num_sms, source, vlo, vhi, err,
+                               sizeof(err));
+  return rc ? fail(rc, err) : BF_OK;
+}
+
+int bf_bfs_shard_expand(bf_bfs_shard* s, uint32_t row, uint32_t col) {
+  BFS_SHARD_PRE(s);
+  Buffer* R = lookup(s->rt->arena, row);
+  Buffer* C = lookup(s->rt->arena, col);
+  if (!R || !C) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (R->scalar != BF_I32 || C->scalar != BF_I32) return fail(BF_E_TYPEFAULT, "row and col must be i32 buffers");
+  char err[256] = {0};
+  int rc = bf_bfs_shard_expand_impl(s->impl, (void*)s->rt->streams[0], s->rt->num_sms, (const int*)R->ptr,
+                                    R->length, (const int*)C->ptr, C->length, err, sizeof(err));
+  return rc ? fail(rc, err) : BF_OK;
+}
+
+int bf_bfs_shard_merge(bf_bfs_shard* s, const void* gathered, int32_t world) {
+  BFS_SHARD_PRE(s);
+  if (!gathered || world < 1) return fail(BF_E_INVALID, "bad gathered bitmaps");
+  char err[256] = {0};
+  int rc = bf_bfs_shard_merge_impl(s->impl, (void*)s->rt->streams[0], s->rt->num_sms, gathered, world, err,
+                                   sizeof(err));
+  return rc ? fail(rc, err) : BF_OK;
+}
+
+int bf_bfs_shard_compact(bf_bfs_shard* s, uint32_t lvl, int64_t* fresh) {
+  BFS_SHARD_PRE(s);
+  if (!fresh) return fail(BF_E_INVALID, "null argument");
+  Buffer* L = lookup(s->rt->arena, lvl);
+  if (!L) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (L->scalar != BF_I32) return fail(BF_E_TYPEFAULT, "lvl must be an i32 buffer");
+  char err[256] = {0};
+  long long f = 0;
+  int rc = bf_bfs_shard_compact_impl(s->impl, (void*)s->rt->streams[0], s->rt->num_sms, (int*)L->ptr, L->length,
+                                     &f, err, sizeof(err));
+  *fresh = f;
+  return rc ? fail(rc, err) : BF_OK;
+}
+
+int bf_bfs_shard_finish(bf_bfs_shard* s, uint32_t lvl, int32_t* depth) {
+  BFS_SHARD_PRE(s);
+  if (!depth) return fail(BF_E_INVALID, "null argument");
+  Buffer* L = lookup(s->rt->arena, lvl);
+  if (!L) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (L->scalar != BF_I32) return fail(BF_E_TYPEFAULT, "lvl must be an i32 buffer");
+  char err[256] = {0};
+  int rc = bf_bfs_shard_finish_impl(s->impl, (void*)s->rt->streams[0], s->rt->num_sms, (int*)L->ptr, L->length,
+                                    depth, err, sizeof(err));
+  return rc ? fail(rc, err) : BF_OK;
+}
+
 int bf_hotspot_run_impl(void* stream, int num_sms, float* a, float* b, const float* p, int rows,
                         int cols, const double* kc, int iterations, int tsteps, char* err,
                         int errcap);

@@ -22,3 +22,56 @@ def bfs_levels(rt, row: int, col: int, lvl: int, nv: int, source: int = 0) -> in
     if rc != _lib.OK:
         raise BfError(rc, _lib.last_error())
     return depth.value
+
+
+class BfsShard:
+    """One rank's share of a sharded traversal (bf_bfs_shard_*): the whole
+    visited bitmap and level bytes on this device, expansion of the frontier
+    vertices in [vlo, vhi) only.  Driven by parallel.bfs_levels_sharded."""
+
+    def __init__(self, rt, nv: int):
+        self.rt = rt
+        self.nv = nv
+        self._h = C.c_void_p()
+        self._call("bf_bfs_shard_create", rt._native, nv, C.byref(self._h))
+
+    def _call(self, fn, *args):
+        rc = getattr(_lib.lib(), fn)(*args)
+        if rc != _lib.OK:
+            raise BfError(rc, _lib.last_error())
+
+    def bitmap(self):
+        """(device pointer, uint32 word count) of the visited bitmap."""
+        ptr, words = C.c_void_p(), C.c_int64()
+        self._call("bf_bfs_shard_bitmap", self._h, C.byref(ptr), C.byref(words))
+        return ptr.value, words.value
+
+    def begin(self, source: int, vlo: int, vhi: int) -> None:
+        self._call("bf_bfs_shard_begin", self._h, source, vlo, vhi)
+
+    def expand(self, row: int, col: int) -> None:
+        self._call("bf_bfs_shard_expand", self._h, row, col)
+
+    def merge(self, gathered_ptr: int, world: int) -> None:
+        self._call("bf_bfs_shard_merge", self._h, C.c_void_p(gathered_ptr), world)
+
+    def compact(self, lvl: int) -> int:
+        fresh = C.c_int64()
+        self._call("bf_bfs_shard_compact", self._h, lvl, C.byref(fresh))
+        return fresh.value
+
+    def finish(self, lvl: int) -> int:
+        depth = C.c_int32()
+        self._call("bf_bfs_shard_finish", self._h, lvl, C.byref(depth))
+        return depth.value
+
+    def close(self) -> None:
+        if self._h:
+            _lib.lib().bf_bfs_shard_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

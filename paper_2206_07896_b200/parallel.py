@@ -15,10 +15,14 @@ data need a collective:
     NCCL point-to-point every `halo` iterations.
   * hist / hist_stride / wreduce / kmeans — per-rank partial counts or sums
     combined with one all-reduce (launch_sharded, COMBINE).
-  * vecadd / nn / fir / reduce — disjoint outputs: no exchange is needed for
+  * vecadd / nn / fir / reduce / backprop — disjoint outputs: no exchange is needed for
     the computation; launch_sharded assembles the full output on every rank
     with one all-gather when the caller wants it replicated.
   * bfs level step — monotone levels and flag: all-reduce MAX.
+  * bfs whole traversal (bfs_levels_sharded) — ranks own vertex ranges and
+    expand only their frontier; per level one all-gather of the nv-bit
+    visited bitmap (8 MB at 2^26 vertices) merged by OR, after which every
+    rank sees the same fresh set (same levels, same loop exit).
 
 Everything here is backend-agnostic torch.distributed (NCCL on GPUs, gloo in
 the CPU tests).
@@ -149,6 +153,9 @@ COMBINE = {
     "wreduce": {"out": "sum"},
     "kmeans": {"member": "owned", "sums": "sum", "counts": "sum"},
     "bfs": {"lvl": "max", "changed": "max"},
+    # backprop: blocks own disjoint weight rows (and partial-sum rows)
+    "bpnn_layerforward": {"w": "owned", "partial": "owned"},
+    "bpnn_adjust_weights": {"w": "owned", "oldw": "owned"},
 }
 
 
@@ -220,3 +227,55 @@ def launch_sharded(rt, arena, routine, grid, block, shmem: int, packed, outputs:
     comb.finish(tensors)
     torch.cuda.synchronize(device)
     return task
+
+
+# ---------------------------------------------------------------------------
+# sharded BFS traversal
+# ---------------------------------------------------------------------------
+
+def bfs_levels_sharded(shard, row: int, col: int, lvl: int, nv: int, source: int, world: int, rank: int,
+                       gather: Callable) -> int:
+    """Whole traversal over `world` ranks (per-level frontier
+    exchange).  `shard` provides begin/expand/merge/compact/finish/bitmap
+    (graph.BfsShard on a GPU); `gather(bitmap)` returns the world bitmaps in
+    rank order as one flat buffer (device pointer for the native shard).
+    Returns max level + 1; `lvl` ends identical on every rank."""
+    lo, hi = rank_range(nv, world, rank)
+    shard.begin(source, lo, hi)
+    while True:
+        shard.expand(row, col)
+        if world > 1:
+            shard.merge(gather(shard), world)
+        if shard.compact(lvl) == 0:
+            break
+    return shard.finish(lvl)
+
+
+def nccl_bitmap_gather(world: int, device):
+    """gather() for bfs_levels_sharded over torch.distributed (NCCL on GPUs):
+    all_gather_into_tensor of the shard's bitmap; returns the device pointer
+    of the gathered [world x words] buffer (kept alive by the closure)."""
+    import torch
+    import torch.distributed as dist
+    state = {}
+
+    def gather(shard):
+        ptr, words = shard.bitmap()
+        if "buf" not in state or state["buf"].numel() != world * words:
+            state["buf"] = torch.empty(world * words, dtype=torch.int32, device=device)
+        mine = _device_view(ptr, words, device)
+        dist.all_gather_into_tensor(state["buf"], mine)
+        torch.cuda.current_stream(device).synchronize()
+        return state["buf"].data_ptr()
+    return gather
+
+
+def _device_view(ptr: int, n: int, device):
+    """A torch int32 view of n device words at `ptr` (no copy)."""
+    import torch
+
+    class _CAI:
+        def __init__(self):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False),
+                                             "version": 3, "strides": None}
+    return torch.as_tensor(_CAI(), device=device)

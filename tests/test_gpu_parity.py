@@ -404,3 +404,80 @@ def test_launch_sharded_single_rank_nccl():
                     assert bit_equal(g, want[n]), (inst.kernel, n)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_bfs_shards_on_one_device_vs_oracle(world):
+    """The native shard steps (bf_bfs_shard_*) for `world` ranks, driven in
+    lockstep in one process on one device (the bitmap all-gather is a device
+    concatenation): every shard ends with the oracle's levels; the per-level
+    fresh counts agree across shards."""
+    import torch
+    import instances as I
+    from paper_2206_07896_b200 import DeviceArena, Runtime, graph
+    from paper_2206_07896_b200.parallel import _device_view, rank_range
+    dev = torch.device("cuda", 0)
+    for nv, deg, seed, src in [(20000, 8, 5, 0), (3001, 2, 6, 3000), (257, 1, 7, 9)]:
+        row, col = I.random_graph(nv, deg, seed)
+        want, depth = oracle.bfs_full(row, col, nv, src)
+        arena = DeviceArena()
+        hr, hc = arena.alloc("i32", nv + 1), arena.alloc("i32", col.size)
+        arena.upload_numpy(hr, row)
+        arena.upload_numpy(hc, col)
+        lv = [arena.alloc("i32", nv) for _ in range(world)]
+        with Runtime(arena) as rt:
+            shards = [graph.BfsShard(rt, nv) for _ in range(world)]
+            for r, s in enumerate(shards):
+                s.begin(src, *rank_range(nv, world, r))
+            while True:
+                for s in shards:
+                    s.expand(hr, hc)
+                views = [_device_view(*s.bitmap(), dev) for s in shards]
+                gathered = torch.cat(views)
+                torch.cuda.synchronize()
+                for s in shards:
+                    s.merge(gathered.data_ptr(), world)
+                fresh = [s.compact(lv[r]) for r, s in enumerate(shards)]
+                assert len(set(fresh)) == 1
+                if fresh[0] == 0:
+                    break
+            depths = [s.finish(lv[r]) for r, s in enumerate(shards)]
+            for s in shards:
+                s.close()
+        assert depths == [depth] * world
+        for h in lv:
+            assert bit_equal(arena.to_numpy(h), want)
+
+
+def test_bfs_levels_sharded_nccl_world1():
+    """parallel.bfs_levels_sharded end to end over NCCL (world of one)."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    import instances as I
+    from paper_2206_07896_b200 import DeviceArena, Runtime, graph
+    from paper_2206_07896_b200.parallel import bfs_levels_sharded, nccl_bitmap_gather
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        nv, deg = 100000, 8
+        row, col = I.random_graph(nv, deg, 11)
+        want, depth = oracle.bfs_full(row, col, nv, 5)
+        arena = DeviceArena()
+        hr, hc, hl = arena.alloc("i32", nv + 1), arena.alloc("i32", col.size), arena.alloc("i32", nv)
+        arena.upload_numpy(hr, row)
+        arena.upload_numpy(hc, col)
+        with Runtime(arena) as rt:
+            shard = graph.BfsShard(rt, nv)
+            got = bfs_levels_sharded(shard, hr, hc, hl, nv, 5, 1, 0,
+                                     nccl_bitmap_gather(1, torch.device("cuda", 0)))
+            shard.close()
+        assert got == depth
+        assert bit_equal(arena.to_numpy(hl), want)
+    finally:
+        dist.destroy_process_group()

@@ -124,7 +124,8 @@ def _shard_worker(rank, world, port, out_q):
         from paper_2206_07896_b200.parallel import COMBINE, Combiner, rank_range
         rng = _r.Random(77)
         cases = [I.vecadd(rng), I.reduce(rng), I.hist(rng), I.wreduce(rng), I.nn(3000, 128, seed=4),
-                 I.kmeans(1500, 8, 5, 128, seed=5), I.bfs(4000, 4, cur=0, seed=6, block=128)]
+                 I.kmeans(1500, 8, 5, 128, seed=5), I.bfs(4000, 4, cur=0, seed=6, block=128),
+                 I.backprop_forward(160, seed=7), I.backprop_adjust(96, seed=8)]
         results = []
         for inst in cases:
             first, hi = rank_range(inst.grid.total, world, rank)
@@ -164,7 +165,8 @@ def test_sharded_launches_match_single_launch(world):
     import oracle
     rng = _r.Random(77)
     cases = [I.vecadd(rng), I.reduce(rng), I.hist(rng), I.wreduce(rng), I.nn(3000, 128, seed=4),
-             I.kmeans(1500, 8, 5, 128, seed=5), I.bfs(4000, 4, cur=0, seed=6, block=128)]
+             I.kmeans(1500, 8, 5, 128, seed=5), I.bfs(4000, 4, cur=0, seed=6, block=128),
+                 I.backprop_forward(160, seed=7), I.backprop_adjust(96, seed=8)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -185,3 +187,97 @@ def test_sharded_launches_match_single_launch(world):
                 assert np.allclose(g, w, rtol=1e-4, atol=1e-4), inst.kernel
             else:
                 assert np.array_equal(g.view(np.uint8), w.view(np.uint8)), (inst.kernel, name)
+
+
+# ---- sharded BFS traversal (parallel.bfs_levels_sharded) --------------------
+
+class NumpyBfsShard:
+    """CPU restatement of one bf_bfs_shard (TEST INFRASTRUCTURE): whole
+    visited set and levels, expansion of the owned frontier only."""
+
+    def __init__(self, nv):
+        self.nv = nv
+
+    def begin(self, src, lo, hi):
+        self.lo, self.hi = lo, hi
+        self.now = np.zeros(self.nv, bool)
+        self.now[src] = True
+        self.prev = self.now.copy()
+        self.lv = np.full(self.nv, -1, np.int32)
+        self.lv[src] = 0
+        self.q = [src] if lo <= src < hi else []
+        self.depth = 0
+
+    def expand(self, row, col):
+        for u in self.q:
+            self.now[col[row[u]:row[u + 1]]] = True
+
+    def bitmap(self):
+        return torch.from_numpy(self.now.astype(np.uint8))
+
+    def merge(self, gathered, world):
+        self.now |= gathered.reshape(world, self.nv).any(axis=0)
+
+    def compact(self, lvl):
+        fresh = self.now & ~self.prev
+        self.prev = self.now.copy()
+        ids = np.flatnonzero(fresh)
+        self.lv[ids] = self.depth + 1
+        self.q = [int(v) for v in ids if self.lo <= v < self.hi]
+        self.depth += 1
+        return int(ids.size)
+
+    def finish(self, lvl):
+        return self.depth
+
+
+def _bfs_shard_worker(rank, world, port, out_q):
+    sys.path[:0] = [str(ROOT), str(ROOT / "oracle")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import instances as I
+        from paper_2206_07896_b200.parallel import bfs_levels_sharded
+        results = []
+        for nv, deg, seed, src in [(3000, 3, 1, 0), (5000, 8, 2, 4321), (400, 1, 3, 7)]:
+            row, col = I.random_graph(nv, deg, seed)
+            shard = NumpyBfsShard(nv)
+
+            def gather(sh):
+                mine = sh.bitmap()
+                parts = [torch.zeros_like(mine) for _ in range(world)]
+                dist.all_gather(parts, mine)
+                return torch.cat(parts).numpy().astype(bool)
+            depth = bfs_levels_sharded(shard, row, col, None, nv, src, world, rank, gather)
+            results.append((shard.lv.copy(), depth))
+        allres = [None] * world
+        dist.all_gather_object(allres, results)
+        if rank == 0:
+            out_q.put(allres)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bfs_levels_sharded_protocol(world):
+    """Vertex-range shards + per-level bitmap all-gather/OR: every rank ends
+    with exactly the single-process levels (oracle) and the same depth."""
+    import instances as I
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bfs_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allres = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for k, (nv, deg, seed, src) in enumerate([(3000, 3, 1, 0), (5000, 8, 2, 4321), (400, 1, 3, 7)]):
+        row, col = I.random_graph(nv, deg, seed)
+        want, depth = oracle.bfs_full(row, col, nv, src)
+        for r in range(world):
+            lv, d = allres[r][k]
+            assert np.array_equal(lv, want), (k, r)
+            assert d == depth, (k, r)
