@@ -528,23 +528,28 @@ __global__ void __launch_bounds__(256) fir_tile(const float* __restrict__ x,
   }
 }
 
-// taps <= 13: each thread computes 4 consecutive outputs from a window of
-// <= 16 x values read as aligned float4 (neighbouring threads' windows
-// overlap in L1); w lives in registers as doubles.
+// taps <= 13: each thread computes OPT consecutive outputs from a window of
+// OPT + taps - 1 <= 16 x values read as aligned float4 (neighbouring threads'
+// windows overlap in L1); w lives in registers as doubles.  The window is
+// converted to f64 once: (OPT + taps - 1) / OPT conversions per output (the
+// F2F conversions, not the DFMAs, bound this kernel), so taps <= 9 use
+// OPT = 8 (2 per output at 8 taps) and larger filters OPT = 4.
 constexpr int kFirRegTaps = 13;
 
+template <int OPT>
 __global__ void __launch_bounds__(256) fir_reg(const float* __restrict__ x, long long lx,
                                                float* __restrict__ y,
                                                const float* __restrict__ w, int taps,
                                                long long nout) {
-  double wd[kFirRegTaps];
+  constexpr int MAXT = 17 - OPT;  // window OPT + taps - 1 <= 16
+  double wd[MAXT];
 #pragma unroll
-  for (int i = 0; i < kFirRegTaps; i++) wd[i] = i < taps ? (double)__ldg(w + i) : 0.0;
-  const int nvec = (3 + taps + 3) / 4;  // float4 chunks covering 3 + taps floats
-  const long long groups = (nout + 3) / 4;
+  for (int i = 0; i < MAXT; i++) wd[i] = i < taps ? (double)__ldg(w + i) : 0.0;
+  const int nvec = (OPT - 1 + taps + 3) / 4;  // float4 chunks covering OPT - 1 + taps floats
+  const long long groups = (nout + OPT - 1) / OPT;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
-    const long long o = 4 * g;
+    const long long o = OPT * g;
     float xv[16];
     if (o + 4 * nvec <= lx) {
       const float4* x4 = reinterpret_cast<const float4*>(x + o);
@@ -553,29 +558,34 @@ __global__ void __launch_bounds__(256) fir_reg(const float* __restrict__ x, long
         if (j < nvec) {
           const float4 v = __ldg(x4 + j);
           xv[4 * j] = v.x; xv[4 * j + 1] = v.y; xv[4 * j + 2] = v.z; xv[4 * j + 3] = v.w;
+        } else {
+          xv[4 * j] = xv[4 * j + 1] = xv[4 * j + 2] = xv[4 * j + 3] = 0.f;
         }
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 16; j++) xv[j] = (o + j < lx) ? __ldg(x + o + j) : 0.f;
     }
-    // convert the window once (16 F2F per 4 outputs, not one per FMA)
     double xd[16];
 #pragma unroll
-    for (int j = 0; j < 16; j++) xd[j] = (j < 3 + taps) ? (double)xv[j] : 0.0;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = 0; j < 16; j++) xd[j] = (j < OPT - 1 + taps) ? (double)xv[j] : 0.0;
+    double acc[OPT];
 #pragma unroll
-    for (int i = 0; i < kFirRegTaps; i++) {
+    for (int q = 0; q < OPT; q++) acc[q] = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXT; i++) {
       if (i < taps) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) acc[q] = fma(wd[i], xd[q + i], acc[q]);
+        for (int q = 0; q < OPT; q++) acc[q] = fma(wd[i], xd[q + i], acc[q]);
       }
     }
-    if (o + 3 < nout) {
-      __stcs(reinterpret_cast<float4*>(y + o),
-             make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]));
+    if (o + OPT - 1 < nout) {
+#pragma unroll
+      for (int q = 0; q < OPT; q += 4)
+        __stcs(reinterpret_cast<float4*>(y + o + q),
+               make_float4((float)acc[q], (float)acc[q + 1], (float)acc[q + 2], (float)acc[q + 3]));
     } else {
-      for (int q = 0; q < 4; q++)
+      for (int q = 0; q < OPT; q++)
         if (o + q < nout) y[o + q] = (float)acc[q];
     }
   }
@@ -599,10 +609,17 @@ static int launch_fir(LaunchCtx& ctx) {
     ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first, "fir index out of range");
     return BF_OK;
   }
+  if (t <= 9) {
+    int grid = stream_grid((nout + 7) / 8, 256 * 2, ctx.num_sms, 8);
+    fir_reg<8><<<grid, 256, 0, ctx.stream>>>((const float*)X.ptr, X.len, (float*)Y.ptr,
+                                             (const float*)W.ptr, t, nout);
+    BF_CUDA_LAUNCH_CHECK(ctx);
+    return BF_OK;
+  }
   if (t <= kFirRegTaps) {
     int grid = stream_grid((nout + 3) / 4, 256 * 4, ctx.num_sms, 8);
-    fir_reg<<<grid, 256, 0, ctx.stream>>>((const float*)X.ptr, X.len, (float*)Y.ptr,
-                                          (const float*)W.ptr, t, nout);
+    fir_reg<4><<<grid, 256, 0, ctx.stream>>>((const float*)X.ptr, X.len, (float*)Y.ptr,
+                                             (const float*)W.ptr, t, nout);
     BF_CUDA_LAUNCH_CHECK(ctx);
     return BF_OK;
   }

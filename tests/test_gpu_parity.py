@@ -231,7 +231,8 @@ def test_large_random_corpus_vs_oracle():
         got, trap, _, _ = gpu_run(inst)
         assert trap is None and bit_equal(got["out"], want["out"]), bx
     x = rng.uniform(-1, 1, n + 16).astype(np.float32)
-    for taps, bx, m in ((8, 256, 1024), (13, 64, 999), (1, 256, 7), (20, 128, 33)):
+    for taps, bx, m in ((8, 256, 1024), (13, 64, 999), (1, 256, 7), (20, 128, 33), (9, 100, 37),
+                        (10, 33, 41), (3, 7, 5), (9, 3, 1)):
         w = rng.uniform(-1, 1, taps).astype(np.float32)
         nout = bx * m
         inst = I.Instance("fir", I.Geom(1), I.Geom(bx), 0,

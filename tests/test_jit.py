@@ -63,11 +63,13 @@ def _mk_for(reference, inst):
 def test_goldens_through_jit(need_gpu, reference, force_jit, name):
     cases = golden.load(name)
     for k, (inst, expected, trap) in enumerate(cases):
-        if inst.kernel == "reduce" and inst.block.y * inst.block.z > 1:
+        if inst.kernel in ("reduce", "bpnn_layerforward") and inst.block.z > 1 or \
+                inst.kernel == "reduce" and inst.block.y > 1:
             # duplicated threads update buf[t] in place without atomics: a
             # data race under CUDA semantics, ordered only by the reference's
             # sequential interpreter.  The hand-written reduce reproduces the
             # order (reduce_tree); generated code follows CUDA.
+            # Same for backprop's in-place column tree with duplicated z threads.
             continue
         mk = _mk_for(reference, inst)
         got, got_trap, _, _ = gpu_run(inst, routine=mk)
