@@ -104,6 +104,19 @@ inline int stream_grid(long long work_items, int items_per_cta, int num_sms,
   return (int)(need < cap ? need : cap);
 }
 
+// CTAs of `fn` resident per SM at this block size / dynamic smem (cached).
+// Grid-stride kernels size their grid with it: a grid larger than one
+// resident wave leaves a partial second wave (a tail) on every launch.
+int resident_ctas(const void* fn, int threads, size_t smem);
+
+// stream_grid capped at one resident wave of `fn`
+template <typename F>
+inline int wave_grid(F fn, int threads, size_t smem, long long work_items, int items_per_cta, int num_sms,
+                     int ctas_per_sm) {
+  const int r = resident_ctas((const void*)fn, threads, smem);
+  return stream_grid(work_items, items_per_cta, num_sms, r < ctas_per_sm ? r : ctas_per_sm);
+}
+
 // full-grid hotspot step with the streaming band kernel (k_hotspot.cu)
 int hotspot_step_full(cudaStream_t stream, int num_sms, const float* src, const float* power,
                       float* dst, int rows, int cols, const double* kc);

@@ -132,8 +132,8 @@ __device__ __forceinline__ int warp_sum(int v) {
 // the slice is read as <= MAXV int4 per lane, U blocks per iteration, every
 // load of the iteration issued before any shuffle tree (loads in flight per
 // lane: U*MAXV*16 B).  Otherwise a plain strided loop.
-template <int MAXV, int U>
-__global__ void __launch_bounds__(256) reduce_warp(const int* __restrict__ x, long long lx,
+template <int MAXV, int U, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) reduce_warp(const int* __restrict__ x, long long lx,
                                                    int* __restrict__ out, long long lout, int n,
                                                    long long x0, long long x1, KDesc k) {
   const int lane = threadIdx.x & 31;
@@ -232,14 +232,16 @@ static int launch_reduce(LaunchCtx& ctx) {
       int* op = (int*)O.ptr;
       KDesc d = ctx.desc();
       if (bx % 4 == 0 && bx <= 128) {
-        int grid = stream_grid(nx, 8 * 8, ctx.num_sms, 8);
-        reduce_warp<1, 8><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
+        int grid = wave_grid(reduce_warp<1, 8, 4>, 256, 0, nx, 8 * 8, ctx.num_sms, 8);
+        reduce_warp<1, 8, 4><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
       } else if (bx % 4 == 0 && bx <= 256) {
-        int grid = stream_grid(nx, 8 * 4, ctx.num_sms, 8);
-        reduce_warp<2, 4><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
+        // (2 int4 per lane per block, 4 blocks per warp step; 6 CTAs/SM:
+        // 0.88 of HBM vs 0.48 with the register-unbounded build)
+        int grid = wave_grid(reduce_warp<2, 4, 6>, 256, 0, nx, 8 * 4, ctx.num_sms, 8);
+        reduce_warp<2, 4, 6><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
       } else {
-        int grid = stream_grid(nx, 8, ctx.num_sms, 8);
-        reduce_warp<0, 1><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
+        int grid = wave_grid(reduce_warp<0, 1, 8>, 256, 0, nx, 8, ctx.num_sms, 8);
+        reduce_warp<0, 1, 8><<<grid, 256, 0, ctx.stream>>>(xp, X.len, op, O.len, n, xi.first, xi.second, d);
       }
     } else {
       int grid = (int)std::min<long long>(nx, (long long)ctx.num_sms * 8);
@@ -318,6 +320,37 @@ __device__ __forceinline__ void hist_add(unsigned* sh, unsigned* mine, int* coun
   }
 }
 
+// four pixels: with a power-of-two bin count and all four non-negative, the
+// bins are plain masks and cannot trap (one branch per 4 pixels)
+template <int MODE, bool POW2, bool SAFE>
+__device__ __forceinline__ void hist_add4(unsigned* sh, unsigned* mine, int* counts, long long lc, int4 v,
+                                          const FastMod& fm, unsigned copies, bool& bad) {
+  if (POW2 && SAFE && (v.x | v.y | v.z | v.w) >= 0) {
+    const int m = (int)(fm.d - 1);
+    if (MODE == 0) {
+      mine[(v.x & m) * 32] += copies;
+      mine[(v.y & m) * 32] += copies;
+      mine[(v.z & m) * 32] += copies;
+      mine[(v.w & m) * 32] += copies;
+    } else if (MODE == 1) {
+      atomicAdd(sh + (v.x & m), copies);
+      atomicAdd(sh + (v.y & m), copies);
+      atomicAdd(sh + (v.z & m), copies);
+      atomicAdd(sh + (v.w & m), copies);
+    } else {
+      atomicAdd((unsigned*)counts + (v.x & m), copies);
+      atomicAdd((unsigned*)counts + (v.y & m), copies);
+      atomicAdd((unsigned*)counts + (v.z & m), copies);
+      atomicAdd((unsigned*)counts + (v.w & m), copies);
+    }
+    return;
+  }
+  hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.x, fm), copies, bad);
+  hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.y, fm), copies, bad);
+  hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.z, fm), copies, bad);
+  hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.w, fm), copies, bad);
+}
+
 template <int MODE, bool POW2, bool SAFE>
 __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, int* counts,
                                                   long long lc, long long lo, long long hi,
@@ -351,20 +384,9 @@ __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, i
 #pragma unroll
     for (int u = 0; u < 4; u++) v[u] = __ldcs(p4 + g + u * stride);
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].x, fm), copies, bad);
-      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].y, fm), copies, bad);
-      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].z, fm), copies, bad);
-      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v[u].w, fm), copies, bad);
-    }
+    for (int u = 0; u < 4; u++) hist_add4<MODE, POW2, SAFE>(sh, mine, counts, lc, v[u], fm, copies, bad);
   }
-  for (; g < end; g += stride) {
-    const int4 v = __ldcs(p4 + g);
-    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.x, fm), copies, bad);
-    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.y, fm), copies, bad);
-    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.z, fm), copies, bad);
-    hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(v.w, fm), copies, bad);
-  }
+  for (; g < end; g += stride) hist_add4<MODE, POW2, SAFE>(sh, mine, counts, lc, __ldcs(p4 + g), fm, copies, bad);
   if (bad) {
     // exact block of the first bad pixel is not tracked on this path: the
     // fetch's first block whose range holds one is reported (kind is exact)
@@ -610,14 +632,14 @@ static int launch_fir(LaunchCtx& ctx) {
     return BF_OK;
   }
   if (t <= 9) {
-    int grid = stream_grid((nout + 7) / 8, 256 * 2, ctx.num_sms, 8);
+    int grid = wave_grid(fir_reg<8>, 256, 0, (nout + 7) / 8, 256 * 2, ctx.num_sms, 8);
     fir_reg<8><<<grid, 256, 0, ctx.stream>>>((const float*)X.ptr, X.len, (float*)Y.ptr,
                                              (const float*)W.ptr, t, nout);
     BF_CUDA_LAUNCH_CHECK(ctx);
     return BF_OK;
   }
   if (t <= kFirRegTaps) {
-    int grid = stream_grid((nout + 3) / 4, 256 * 4, ctx.num_sms, 8);
+    int grid = wave_grid(fir_reg<4>, 256, 0, (nout + 3) / 4, 256 * 4, ctx.num_sms, 8);
     fir_reg<4><<<grid, 256, 0, ctx.stream>>>((const float*)X.ptr, X.len, (float*)Y.ptr,
                                              (const float*)W.ptr, t, nout);
     BF_CUDA_LAUNCH_CHECK(ctx);

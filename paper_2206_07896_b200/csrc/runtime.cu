@@ -33,6 +33,26 @@
 #include "bf_internal.h"
 #include "common.cuh"
 
+// ---- occupancy cache ----------------------------------------------------------
+namespace bf {
+int resident_ctas(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(fn, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache[key] = n;
+  return n;
+}
+}  // namespace bf
+
+
 namespace bf {
 
 static thread_local std::string g_last_error;
