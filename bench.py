@@ -520,6 +520,84 @@ def run_sweep(args) -> None:
         dist.destroy_process_group()
 
 
+def run_reorder(args) -> None:
+    """the reference's grid-stride reordering study
+    (bench.run_reorder_experiment, transform.reorder_grid_stride) on the B200.
+    The reference rewrites `base + j*blockDim.x` into `base*K + j` so that a
+    CPU thread walks a contiguous chunk (fewer simulated LLC misses); on the
+    GPU the same rewrite turns every warp access into 32 scattered sectors.
+    Both versions of hist_stride and fir run through the JIT (codegen + NVRTC,
+    one CTA per logical block, exactly the DSL semantics) on the same inputs;
+    the outputs must agree; reported: device time per launch, and the sectors
+    per warp request when run under ncu (profiles/r1_reorder_sectors.csv)."""
+    import torch
+
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "blockfuse").exists():
+        ref = Path("/root/reference/pkg/src")
+    sys.path.append(str(ref))
+    from blockfuse.bench import CORPUS
+    from blockfuse.transform import reorder_grid_stride
+
+    from paper_2206_07896_b200 import ArgSlot, DeviceArena, Dim3, PackedArgs, Runtime, routines
+    torch.cuda.set_device(0)
+    device = torch.device("cuda", 0)
+    arena = DeviceArena(0)
+    rows = []
+    routines.FORCE_JIT = True
+    try:
+        for name in ("hist_stride", "fir"):
+            orig = CORPUS[name].compiled()
+            reord = reorder_grid_stride(orig)
+            bx, k = 256, args.reorder_k
+            if name == "hist_stride":
+                n = bx * k
+                x, out = arena.alloc("i32", n), arena.alloc("i32", 16)
+                torch.as_tensor(arena.cuda_array(x), device=device).random_(0, 1 << 16)
+                pk = PackedArgs([ArgSlot("handle", x), ArgSlot("handle", out), ArgSlot("i32", k), ArgSlot("i32", 16)])
+                nbytes = 4 * n
+            else:
+                n, taps = bx * k, 4
+                x, out, w = arena.alloc("f32", n + taps), arena.alloc("f32", n), arena.alloc("f32", taps)
+                torch.as_tensor(arena.cuda_array(x), device=device).uniform_(-1, 1)
+                torch.as_tensor(arena.cuda_array(w), device=device).uniform_(-1, 1)
+                pk = PackedArgs([ArgSlot("handle", x), ArgSlot("handle", out), ArgSlot("handle", w),
+                                 ArgSlot("i32", taps), ArgSlot("i32", k)])
+                nbytes = 8 * n
+            res = {}
+            for label, mk in (("original", orig), ("reordered", reord)):
+                with Runtime(arena) as rt:
+                    ot = torch.as_tensor(arena.cuda_array(out), device=device)
+                    stream = torch.cuda.ExternalStream(rt.worker_stream(0))
+                    ts = []
+                    for rep in range(args.warmup + args.steps):
+                        ot.zero_()
+                        torch.cuda.synchronize()
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record(stream)
+                        rt.launch(mk, Dim3(1), Dim3(bx), 0, pk)
+                        b.record(stream)
+                        rt.device_synchronize()
+                        b.synchronize()
+                        if rep >= args.warmup:
+                            ts.append(a.elapsed_time(b) * 1e-3)
+                    res[label] = (statistics.median(ts), ot.clone())
+            same = bool(torch.equal(res["original"][1], res["reordered"][1]))
+            rows.append({"kernel": name, "elements": n, "grid": "1 x 256 (one logical block: one CTA)",
+                         "original_ms": round(res["original"][0] * 1e3, 4),
+                         "reordered_ms": round(res["reordered"][0] * 1e3, 4),
+                         "original_gbs": round(nbytes / res["original"][0] / 1e9, 2),
+                         "reordered_gbs": round(nbytes / res["reordered"][0] / 1e9, 2),
+                         "slowdown_x": round(res["reordered"][0] / res["original"][0], 2),
+                         "outputs_equal": same})
+    finally:
+        routines.FORCE_JIT = False
+    print(json.dumps({"metric": "grid-stride reordering study on the GPU (reference transform.reorder_grid_stride)",
+                      "value": None, "unit": "ms", "n_gpus": 1,
+                      "config": {"workload": f"hist_stride / fir, 256 threads x {args.reorder_k} strides, JIT"},
+                      "reorder": rows}), flush=True)
+
+
 def run_grain(args) -> None:
     """the paper's grain-size study on the GPU runtime.
     A fetch of `grain` logical blocks is one grid launch on a worker stream,
@@ -617,7 +695,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["hotspot", "sweep", "grain"], default="hotspot")
+    ap.add_argument("--workload", choices=["hotspot", "sweep", "grain", "reorder"], default="hotspot")
+    ap.add_argument("--reorder-k", type=int, default=1 << 16, help="strides per thread (reorder study)")
     ap.add_argument("--size", type=int, default=8192)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--halo", type=int, default=8)
@@ -635,6 +714,8 @@ def main() -> None:
         run_reference_arm(args)
     elif args.workload == "sweep":
         run_sweep(args)
+    elif args.workload == "reorder":
+        run_reorder(args)
     elif args.workload == "grain":
         run_grain(args)
     else:
