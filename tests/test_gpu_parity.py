@@ -482,3 +482,50 @@ def test_bfs_levels_sharded_nccl_world1():
         assert bit_equal(arena.to_numpy(hl), want)
     finally:
         dist.destroy_process_group()
+
+
+_KMEANS_VARIANT_SCRIPT = r"""
+import sys
+sys.path[:0] = [{root!r}, {root!r} + '/oracle', {root!r} + '/tests']
+import numpy as np
+import instances as I
+import oracle
+from gpu_helpers import bit_equal, gpu_run
+cases = [I.kmeans(3000, 32, 16, 256, seed=11), I.kmeans(999, 16, 16, 96, seed=14, dup=True),
+         I.kmeans(4096, 32, 16, 256, seed=16, dup=True), I.kmeans(3001, 32, 7, 256, seed=19, dup=True),
+         I.kmeans(20000, 32, 16, 256, seed=21), I.kmeans(1024, 16, 5, 128, seed=22)]
+edge = I.kmeans(2048, 32, 16, 256, seed=20)
+fe = np.asarray(edge.buffer("f").values).copy().reshape(32, 2048)
+fe[3, 7] = np.nan
+fe[:, 11] = np.float32(3e38)
+fe[:, 100:140] *= np.float32(1e-30)
+edge.buffer("f").values = fe.reshape(-1)
+cases.append(edge)
+for k, inst in enumerate(cases):
+    want, _ = oracle.run(inst)
+    got, trap, _, _ = gpu_run(inst)
+    assert trap is None, k
+    assert bit_equal(got["member"], want["member"]), k
+    assert bit_equal(got["counts"], want["counts"]), k
+    w, g = want["sums"].astype(np.float64), got["sums"].astype(np.float64)
+    fin = np.isfinite(w)
+    assert np.array_equal(np.isnan(w), np.isnan(g)), k
+    assert np.all(np.abs(w[fin] - g[fin]) <= 1e-4 * np.maximum(np.maximum(abs(w[fin]), abs(g[fin])), 1.0)), k
+print("ok", len(cases))
+"""
+
+
+@pytest.mark.parametrize("variant", [2, 5])
+def test_kmeans_opt_in_variants_vs_oracle(variant):
+    """The opt-in kmeans kernels (BF_KMEANS_V: 2 register-blocked FFMA
+    screen, 5 tcgen05 distance GEMM) stay bit-exact in membership; run in a
+    subprocess because the variant is read once when the library loads."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ, BF_KMEANS_V=str(variant))
+    r = subprocess.run([sys.executable, "-c", _KMEANS_VARIANT_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().startswith("ok"), r.stderr[-2000:]
