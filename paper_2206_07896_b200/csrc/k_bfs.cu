@@ -106,6 +106,159 @@ __global__ void __launch_bounds__(256) bfs_step(const int* __restrict__ row, lon
   }
 }
 
+// Two-phase level step (a launch whose fetch covers the whole grid):
+//   scan    one pass over lvl[0, ll) builds an "unvisited" bitmap (lvl == -1,
+//           8 MB at 2^26 vertices, L2-resident) and appends the frontier
+//           (lvl == cur, u in [lo, hi)) to a queue;
+//   expand  frontier vertices relax their out-edges against the bitmap; the
+//           first thread to clear a target's bit (atomicAnd) writes
+//           lvl[v] = cur + 1 once.
+// Same result as bfs_step (frontier = lvl == cur at launch start, targets =
+// lvl == -1 at launch start, every write is cur + 1), but the per-edge test is
+// an L2 hit instead of a random DRAM read of the 256 MB lvl array.
+__global__ void __launch_bounds__(256) bfs_scan(const int* __restrict__ lvl, long long ll, unsigned* unv,
+                                                long long words, int* q, int* qn, long long lo, long long hi,
+                                                int cur) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w - lane < words; w += stride) {
+    unsigned um = 0, fm = 0;
+    if (w < words) {
+      const long long v0 = w * 32;
+      if (v0 + 32 <= ll) {
+        const int4* l4 = reinterpret_cast<const int4*>(lvl + v0);
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int4 x = __ldcs(l4 + j);
+          um |= (x.x == -1 ? 1u : 0u) << (4 * j) | (x.y == -1 ? 1u : 0u) << (4 * j + 1) |
+                (x.z == -1 ? 1u : 0u) << (4 * j + 2) | (x.w == -1 ? 1u : 0u) << (4 * j + 3);
+          fm |= (x.x == cur ? 1u : 0u) << (4 * j) | (x.y == cur ? 1u : 0u) << (4 * j + 1) |
+                (x.z == cur ? 1u : 0u) << (4 * j + 2) | (x.w == cur ? 1u : 0u) << (4 * j + 3);
+        }
+      } else {
+        for (int j = 0; j < 32 && v0 + j < ll; j++) {
+          const int x = lvl[v0 + j];
+          um |= (x == -1 ? 1u : 0u) << j;
+          fm |= (x == cur ? 1u : 0u) << j;
+        }
+      }
+      unv[w] = um;
+      // frontier restricted to the fetch's vertices [lo, hi)
+      if (v0 < lo) fm &= lo - v0 >= 32 ? 0u : (0xffffffffu << (lo - v0));
+      if (v0 + 32 > hi) fm &= hi <= v0 ? 0u : (0xffffffffu >> (v0 + 32 - hi));
+    }
+    const int c = __popc(fm);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(qn, total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = base + incl - c;
+    for (; fm; fm &= fm - 1) q[pos++] = (int)(w * 32 + __ffs(fm) - 1);
+  }
+}
+
+__global__ void __launch_bounds__(256) bfs_relax(const int* __restrict__ row, long long lr,
+                                                 const int* __restrict__ col, long long lcol, int* lvl,
+                                                 long long ll, unsigned* unv, const int* __restrict__ q,
+                                                 const int* qn, int* changed, long long lch, int cur, int bx,
+                                                 KDesc k) {
+  const int n = *qn;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool any = false;
+  long long bad_u = -1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int u = __ldg(q + i);
+    if ((long long)u + 1 >= lr) {
+      if (bad_u < 0) bad_u = u;
+      continue;
+    }
+    const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
+    for (int e = e0; e < e1; e += 8) {
+      int v[8];
+      unsigned wv[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        v[j] = -1;
+        if (e + j < e1) {
+          if (e + j < 0 || e + j >= lcol) bad_u = bad_u < 0 ? u : bad_u;
+          else v[j] = __ldg(col + e + j);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        wv[j] = 0u;
+        if (e + j < e1 && e + j >= 0 && e + j < lcol) {
+          if (v[j] < 0 || v[j] >= ll) bad_u = bad_u < 0 ? u : bad_u;
+          else wv[j] = __ldcg(unv + (v[j] >> 5));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const unsigned bit = 1u << (v[j] & 31);
+        if (wv[j] & bit) {
+          const unsigned old = atomicAnd(unv + (v[j] >> 5), ~bit);
+          if (old & bit) {
+            lvl[v[j]] = (int)((unsigned)cur + 1u);
+            any = true;
+          }
+        }
+      }
+      if (bad_u >= 0) break;
+    }
+  }
+  if (bad_u >= 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, bad_u / bx));
+  if (__syncthreads_or(any) && threadIdx.x == 0) {
+    if (lch < 1) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, k.first);
+    else changed[0] = 1;
+  }
+}
+
+// per-device scratch of the two-phase step (grow-only)
+struct BfsStepScratch {
+  long long cap_words = 0, cap_q = 0;
+  unsigned* unv = nullptr;
+  int* q = nullptr;
+  int* qn = nullptr;
+};
+
+static int launch_bfs_two_phase(LaunchCtx& ctx, const ArgVal& R, const ArgVal& Co, const ArgVal& L,
+                                const ArgVal& Ch, long long lo, long long hi, int cur, long long bx) {
+  static BfsStepScratch sc[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BfsStepScratch& S = sc[dev & 63];
+  const long long ll = L.len, words = (ll + 31) / 32, nq = hi - lo;
+  if (S.cap_words < words || S.cap_q < nq || !S.qn) {
+    cudaStreamSynchronize(ctx.stream);
+    cudaFree(S.unv);
+    cudaFree(S.q);
+    cudaFree(S.qn);
+    S = BfsStepScratch();
+    if (cudaMalloc((void**)&S.unv, words * 4) != cudaSuccess || cudaMalloc((void**)&S.q, nq * 4) != cudaSuccess ||
+        cudaMalloc((void**)&S.qn, 4) != cudaSuccess) {
+      *ctx.error = "bfs: scratch allocation failed";
+      cudaGetLastError();
+      return BF_E_CUDA;
+    }
+    S.cap_words = words;
+    S.cap_q = nq;
+  }
+  cudaMemsetAsync(S.qn, 0, 4, ctx.stream);
+  const int g1 = wave_grid(bfs_scan, 256, 0, words, 256, ctx.num_sms, 8);
+  bfs_scan<<<g1, 256, 0, ctx.stream>>>((const int*)L.ptr, ll, S.unv, words, S.q, S.qn, lo, hi, cur);
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  const int g2 = wave_grid(bfs_relax, 256, 0, nq, 256, ctx.num_sms, 8);
+  bfs_relax<<<g2, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len, (int*)L.ptr, ll,
+                                        S.unv, S.q, S.qn, (int*)Ch.ptr, Ch.len, cur, (int)bx, ctx.desc());
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  return BF_OK;
+}
+
 static int launch_bfs(LaunchCtx& ctx) {
   const ArgVal& R = ctx.args[0];
   const ArgVal& Co = ctx.args[1];
@@ -124,9 +277,21 @@ static int launch_bfs(LaunchCtx& ctx) {
     *ctx.error = "bfs: vertex id beyond i32";
     return BF_E_UNSUPPORTED;
   }
+  static int step_v = -1;
+  if (step_v < 0) {
+    const char* e = getenv("BF_BFS_STEP_V");
+    step_v = e ? atoi(e) : 2;
+  }
+  const bool whole = ctx.first == 0 && ctx.count == (long long)ctx.grid[0];
   for (auto& xi : ctx.x_intervals()) {
     long long lo = xi.first * bx, hi = std::min(xi.second * bx, nv);
     if (lo >= hi) continue;
+    if (step_v == 2 && whole && hi <= L.len) {
+      // the fetch covers the whole grid: one lvl pass builds the visited bitmap
+      int rc = launch_bfs_two_phase(ctx, R, Co, L, Ch, lo, hi, cur, bx);
+      if (rc) return rc;
+      continue;
+    }
     int grid = stream_grid((hi - lo + 3) / 4, 256, ctx.num_sms, 8);
     bfs_step<<<grid, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len,
                                            (int*)L.ptr, L.len, (int*)Ch.ptr, Ch.len, lo, hi, cur,
