@@ -187,6 +187,33 @@ def build_cases(arena, torch, device, scale: int = 28) -> list:
                       check=lambda: int(tkn.long().sum().item()) == npts, reset=km_reset,
                       note="16M x 32 f32, k=16: one assignment + accumulation pass; f64 distances"))
 
+    # --- kmeans host loop: 10 passes of assignment + centroid update (cluster.py)
+    from paper_2206_07896_b200.cluster import KmeansDriver
+    kc2 = alloc("f32", k * nf)
+    km2 = alloc("i32", npts)
+    tkc2 = _t(arena, kc2, torch, device)
+    passes = 10
+    state = {}
+
+    def km_loop(rt, stream):
+        if "drv" not in state:
+            state["drv"] = KmeansDriver(rt, arena, kf, kc2, km2, npts, nf, k)
+        d = state["drv"]
+        for _ in range(passes):
+            d.assign()
+            d.update()
+        return 2 * passes
+
+    def km_loop_reset():
+        tkc2.copy_(tkc)
+        if "drv" in state:
+            arena.fill_value(state["drv"].prev, -1)
+    cases.append(Case("kmeans_loop", "kmeans_assign", passes * npts * (4 * nf + 4), passes * npts, "point",
+                      [], host_loop=km_loop, reset=km_loop_reset,
+                      check=lambda: bool(torch.isfinite(tkc2).all().item()),
+                      note=f"Rodinia kmeans host loop, {passes} passes (assignment + centroid update + delta "
+                           "through cluster.KmeansDriver); per pass one host sync (delta)"))
+
     # --- backprop: Rodinia's two device kernels, 2^(scale-4) input units x 16 hidden
     nin, hid = 1 << (scale - 4), 16
     nb = nin // 16

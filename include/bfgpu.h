@@ -228,6 +228,19 @@ int bf_worker_stream(bf_runtime *rt, int32_t worker, void **stream);
 int bf_bfs_levels(bf_runtime *rt, uint32_t row, uint32_t col, uint32_t lvl,
                   int32_t nv, int32_t source, int32_t *depth);
 
+/* One pass of Rodinia's kmeans host loop after an assignment launch of
+ * kernels/kmeans.kn (kmeans_clustering.c's do/while): cent[c][l] =
+ * sums[c][l] / counts[c] in f32 for clusters with members (others keep
+ * their centroid), sums and counts zeroed for the next pass, and *delta =
+ * number of points p in [p_lo, p_hi) with member[p] != prev_member[p]
+ * (Rodinia's delta), after which prev_member = member on that range.  With
+ * several ranks the caller all-reduces sums and counts before and delta
+ * after (cluster.kmeans_iterate).  Runs on worker 0's stream after draining
+ * every worker; returns when done. */
+int bf_kmeans_update(bf_runtime *rt, uint32_t cent, uint32_t sums, uint32_t counts,
+                     int32_t nf, int32_t k, uint32_t member, uint32_t prev_member,
+                     int64_t p_lo, int64_t p_hi, int64_t *delta);
+
 /* Sharded BFS traversal, one process per GPU (parallel.bfs_levels_sharded;
  * SURVEY §8e "bfs: per-level frontier exchange").  A shard keeps the whole
  * nv-bit visited bitmap and per-vertex level bytes on its device and expands

@@ -40,6 +40,7 @@ EXPORTS = [
     "bf_bfs_levels", "bf_hotspot_run", "bf_jit_register",
     "bf_bfs_shard_create", "bf_bfs_shard_destroy", "bf_bfs_shard_bitmap", "bf_bfs_shard_begin",
     "bf_bfs_shard_expand", "bf_bfs_shard_merge", "bf_bfs_shard_compact", "bf_bfs_shard_finish",
+    "bf_kmeans_update",
 ]
 
 
@@ -125,6 +126,7 @@ def _declare(lib) -> None:
         "bf_bfs_shard_merge": (C.c_int, [P, P, i32]),
         "bf_bfs_shard_compact": (C.c_int, [P, u32, I64P]),
         "bf_bfs_shard_finish": (C.c_int, [P, u32, I32P]),
+        "bf_kmeans_update": (C.c_int, [P, u32, u32, u32, i32, i32, u32, u32, i64, i64, I64P]),
         "bf_hotspot_run": (C.c_int, [P, u32, u32, u32, i32, i32, C.POINTER(dbl), i32, i32]),
         "bf_jit_register": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, i32, I32P, I32P, i32]),
         "bf_kernel_info": (C.c_int, [i32, C.c_char_p, i32, I32P, I32P, I32P, i32]),

@@ -1302,3 +1302,64 @@ static Registrar reg_kmeans("kmeans",
                             launch_kmeans);
 
 }  // namespace bf
+
+// ---- Rodinia kmeans host loop, device part (cluster.kmeans_iterate) -------
+// After an assignment launch (and, across ranks, the all-reduce of sums and
+// counts): new centroid = sums / counts in f32 where the count is non-zero
+// (kmeans_clustering.c: clusters[i][j] = new_centers[i][j] /
+// new_centers_len[i]), sums and counts cleared for the next pass, and the
+// number of points in [p_lo, p_hi) whose membership changed since the
+// previous pass (Rodinia's delta), with prev := member.
+namespace bf {
+__global__ void kmeans_centroids(float* cent, float* sums, int* counts, int nf, int k) {
+  for (int i = threadIdx.x; i < k * nf; i += blockDim.x) {
+    const int c = i / nf, n = counts[c];
+    if (n > 0) cent[i] = __fdiv_rn(sums[i], (float)n);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k * nf; i += blockDim.x) sums[i] = 0.f;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) counts[i] = 0;
+}
+
+__global__ void __launch_bounds__(256) kmeans_delta(const int* __restrict__ member, int* prev, long long lo,
+                                                    long long hi, unsigned long long* delta) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned c = 0;
+  for (long long p = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += stride) {
+    const int m = member[p];
+    c += m != prev[p];
+    prev[p] = m;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(delta, (unsigned long long)c);
+}
+}  // namespace bf
+
+extern "C" int bf_kmeans_update_impl(void* stream_v, int num_sms, float* cent, float* sums, int* counts, int nf,
+                                     int k, const int* member, int* prev, long long p_lo, long long p_hi,
+                                     long long* delta, char* err, int errcap) {
+  using namespace bf;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  static unsigned long long* d = nullptr;
+  static unsigned long long* h = nullptr;
+  if (!d) {
+    if (cudaMalloc((void**)&d, 8) != cudaSuccess || cudaMallocHost((void**)&h, 8) != cudaSuccess) {
+      snprintf(err, errcap, "kmeans_update: scratch allocation failed");
+      return BF_E_CUDA;
+    }
+  }
+  kmeans_centroids<<<1, 512, 0, stream>>>(cent, sums, counts, nf, k);
+  cudaMemsetAsync(d, 0, 8, stream);
+  if (p_hi > p_lo) {
+    const int grid = stream_grid(p_hi - p_lo, 256 * 4, num_sms, 8);
+    kmeans_delta<<<grid, 256, 0, stream>>>(member, prev, p_lo, p_hi, d);
+  }
+  cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, stream);
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "kmeans_update: %s", cudaGetErrorString(e));
+    return BF_E_CUDA;
+  }
+  *delta = (long long)*h;
+  return BF_OK;
+}

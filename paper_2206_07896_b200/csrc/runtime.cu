@@ -1382,6 +1382,39 @@ int bf_hotspot_run(bf_runtime* rt, uint32_t a, uint32_t power, uint32_t b, int32
   return BF_OK;
 }
 
+int bf_kmeans_update_impl(void* stream, int num_sms, float* cent, float* sums, int* counts, int nf, int k,
+                          const int* member, int* prev, long long p_lo, long long p_hi, long long* delta,
+                          char* err, int errcap);
+
+int bf_kmeans_update(bf_runtime* rt, uint32_t cent, uint32_t sums, uint32_t counts, int32_t nf, int32_t k,
+                     uint32_t member, uint32_t prev_member, int64_t p_lo, int64_t p_hi, int64_t* delta) {
+  if (!rt || !delta) return fail(BF_E_INVALID, "null argument");
+  if (rt->shut_down) return fail(BF_E_SHUTDOWN, "launch after shutdown");
+  Buffer* Ce = lookup(rt->arena, cent);
+  Buffer* S = lookup(rt->arena, sums);
+  Buffer* Cn = lookup(rt->arena, counts);
+  Buffer* M = lookup(rt->arena, member);
+  Buffer* P = lookup(rt->arena, prev_member);
+  if (!Ce || !S || !Cn || !M || !P) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (Ce->scalar != BF_F32 || S->scalar != BF_F32 || Cn->scalar != BF_I32 || M->scalar != BF_I32 ||
+      P->scalar != BF_I32)
+    return fail(BF_E_TYPEFAULT, "kmeans_update: cent/sums f32, counts/member/prev i32");
+  if (nf <= 0 || k <= 0 || Ce->length < (long long)k * nf || S->length < (long long)k * nf || Cn->length < k ||
+      p_lo < 0 || p_hi < p_lo || M->length < p_hi || P->length < p_hi)
+    return fail(BF_E_INVALID, "kmeans_update: buffer shorter than k*nf / k / point range");
+  int rc = set_device(rt->device);
+  if (rc) return rc;
+  rc = sync_workers(rt);
+  if (rc) return rc;
+  char err[256] = {0};
+  long long d = 0;
+  rc = bf_kmeans_update_impl((void*)rt->streams[0], rt->num_sms, (float*)Ce->ptr, (float*)S->ptr, (int*)Cn->ptr,
+                             nf, k, (const int*)M->ptr, (int*)P->ptr, p_lo, p_hi, &d, err, sizeof(err));
+  if (rc) return fail(rc, err);
+  *delta = d;
+  return BF_OK;
+}
+
 // ---- JIT kernels ---------------------------------------------------------------
 
 int bf_jit_register_impl(const char* key, const char* source, const char* entry, int32_t nparams,

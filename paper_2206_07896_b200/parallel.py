@@ -279,3 +279,22 @@ def _device_view(ptr: int, n: int, device):
             self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False),
                                              "version": 3, "strides": None}
     return torch.as_tensor(_CAI(), device=device)
+
+
+def nccl_allreduce(arena, device):
+    """allreduce() for cluster.kmeans_iterate over torch.distributed: a list
+    of arena handles is summed in place (zero-copy views); an int is summed
+    and returned."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(x):
+        if isinstance(x, int):
+            t = torch.tensor([x], dtype=torch.int64, device=device)
+            dist.all_reduce(t)
+            return int(t.item())
+        for h in x:
+            dist.all_reduce(torch.as_tensor(arena.cuda_array(h), device=device))
+        torch.cuda.current_stream(device).synchronize()
+        return None
+    return allreduce

@@ -529,3 +529,98 @@ def test_kmeans_opt_in_variants_vs_oracle(variant):
     r = subprocess.run([sys.executable, "-c", _KMEANS_VARIANT_SCRIPT.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().startswith("ok"), r.stderr[-2000:]
+
+
+def _km_assign_oracle(fv, cent, npts, nf, k):
+    import instances as I
+    inst = I.kmeans(npts, nf, k, 256, seed=0)
+    inst.buffer("f").values = fv
+    inst.buffer("cent").values = cent
+    want, trap = oracle.run(inst)
+    assert trap is None
+    return want
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_kmeans_iterate_passes_exact(world):
+    """Rodinia's host loop (cluster.KmeansDriver) for `world` ranks driven in
+    lockstep on one device (sums/counts all-reduced by a device add): every
+    pass's membership is exactly the reference assignment under the
+    centroids that pass used, counts exact, sums within 1e-4; all ranks hold
+    identical centroids; the loop reaches delta == 0."""
+    import torch
+    import instances as I
+    from paper_2206_07896_b200 import DeviceArena, Runtime
+    from paper_2206_07896_b200.cluster import KmeansDriver
+    dev = torch.device("cuda", 0)
+    npts, nf, k = 6000, 8, 5
+    fv = I.kmeans_inputs(npts, nf, seed=31)
+    cent0 = np.ascontiguousarray(fv.reshape(nf, npts)[:, :k].T).reshape(-1)
+    arena = DeviceArena()
+    hf = arena.alloc("f32", npts * nf)
+    arena.upload_numpy(hf, fv)
+    hm = arena.alloc("i32", npts)
+    cents = [arena.alloc("f32", k * nf) for _ in range(world)]
+    for h in cents:
+        arena.upload_numpy(h, cent0)
+    view = lambda h: torch.as_tensor(arena.cuda_array(h), device=dev)  # noqa: E731
+    with Runtime(arena) as rt:
+        drv = [KmeansDriver(rt, arena, hf, cents[r], hm, npts, nf, k, world, r) for r in range(world)]
+        for p in range(60):
+            used = arena.to_numpy(cents[0]).copy()
+            for r in range(1, world):
+                assert np.array_equal(arena.to_numpy(cents[r]).view(np.uint32), used.view(np.uint32))
+            for d in drv:
+                d.assign()
+            s = sum(view(d.sums) for d in drv)
+            c = sum(view(d.counts) for d in drv)
+            for d in drv:
+                view(d.sums).copy_(s)
+                view(d.counts).copy_(c)
+            torch.cuda.synchronize()
+            want = _km_assign_oracle(fv, used, npts, nf, k)
+            assert bit_equal(arena.to_numpy(hm), want["member"]), p
+            assert bit_equal(arena.to_numpy(drv[0].counts), want["counts"]), p
+            w, g = want["sums"].astype(np.float64), arena.to_numpy(drv[0].sums).astype(np.float64)
+            assert np.all(np.abs(w - g) <= 1e-4 * np.maximum(np.maximum(abs(w), abs(g)), 1.0)), p
+            delta = sum(d.update() for d in drv)
+            if delta == 0:
+                break
+        assert p > 1 and delta == 0
+
+
+def test_kmeans_iterate_nccl_world1():
+    """cluster.kmeans_iterate end to end (world of one over NCCL helpers)."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    import instances as I
+    from paper_2206_07896_b200 import DeviceArena, Runtime
+    from paper_2206_07896_b200.cluster import kmeans_iterate
+    from paper_2206_07896_b200.parallel import nccl_allreduce
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        npts, nf, k = 50000, 32, 16
+        fv = I.kmeans_inputs(npts, nf, seed=33)
+        arena = DeviceArena()
+        hf, hc, hm = arena.alloc("f32", npts * nf), arena.alloc("f32", k * nf), arena.alloc("i32", npts)
+        arena.upload_numpy(hf, fv)
+        arena.upload_numpy(hc, np.ascontiguousarray(fv.reshape(nf, npts)[:, :k].T).reshape(-1))
+        with Runtime(arena) as rt:
+            passes, delta = kmeans_iterate(rt, arena, hf, hc, hm, npts, nf, k, max_iter=500, world=1, rank=0,
+                                           allreduce=nccl_allreduce(arena, torch.device("cuda", 0)))
+        assert passes > 2 and delta == 0
+        cent = arena.to_numpy(hc).astype(np.float64).reshape(k, nf)
+        mem = arena.to_numpy(hm)
+        f = fv.reshape(nf, npts).T.astype(np.float64)
+        for c in range(k):  # converged: every centroid is the mean of its members
+            if (mem == c).any():
+                assert np.allclose(cent[c], f[mem == c].mean(0), rtol=1e-4, atol=1e-5)
+    finally:
+        dist.destroy_process_group()
