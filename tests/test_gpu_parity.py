@@ -624,3 +624,56 @@ def test_kmeans_iterate_nccl_world1():
                 assert np.allclose(cent[c], f[mem == c].mean(0), rtol=1e-4, atol=1e-5)
     finally:
         dist.destroy_process_group()
+
+
+def test_benchmark_configs_full_size_vs_oracle():
+    """The BASELINE configs at their full sizes, checked against the oracle
+    where it finishes in seconds (OpenMP over host cores): hotspot 8192^2
+    (3 chained launches through Runtime.launch, bit-exact), nn 2^24 records
+    (bit-exact), BFS 2^24 vertices x 8 through the fused driver (levels
+    bit-exact), kmeans 2^20 points x 32, k = 16 (membership/counts bit-exact)."""
+    import os
+    import instances as I
+    from gpu_helpers import materialize
+    from paper_2206_07896_b200 import DeviceArena, Dim3, Runtime, graph, routines
+    threads = max(1, len(os.sched_getaffinity(0)))
+    # hotspot: 3 ping-pong launches of the full grid
+    n, iters = 8192, 3
+    temp, power = I.hotspot_inputs(n, n, 0)
+    params = I.hotspot_params(n, n)
+    want = oracle.hotspot_iterate(temp, power, n, n, params, iters, nthreads=threads)
+    inst = I.hotspot(n, n, 16, 16, seed=0)
+    arena = DeviceArena()
+    packed, h = materialize(inst, arena)
+    from paper_2206_07896_b200 import ArgSlot, PackedArgs
+    sl = list(packed.slots)
+    sl2 = [ArgSlot("handle", h["dst"]), sl[1], ArgSlot("handle", h["src"])] + sl[3:]
+    with Runtime(arena) as rt:
+        for it in range(iters):
+            rt.launch(routines.get("hotspot"), Dim3(n // 16, n // 16), Dim3(16, 16), 0,
+                      packed if it % 2 == 0 else PackedArgs(sl2))
+        rt.device_synchronize()
+    got = arena.to_numpy(h["dst"] if iters % 2 == 1 else h["src"])
+    assert bit_equal(got, want)
+    # nn 2^24 records
+    nn = I.nn(1 << 24, 256, seed=5)
+    want, trap = oracle.run(nn, nthreads=threads)
+    got, got_trap, _, _ = gpu_run(nn)
+    assert trap is None and got_trap is None and bit_equal(got["d"], want["d"])
+    # BFS 2^24 x 8, fused traversal
+    nv = 1 << 24
+    row, col = I.random_graph(nv, 8, 7)
+    lv, depth = oracle.bfs_full(row, col, nv, 0)
+    arena = DeviceArena()
+    hr, hc, hl = arena.alloc("i32", nv + 1), arena.alloc("i32", col.size), arena.alloc("i32", nv)
+    arena.upload_numpy(hr, row)
+    arena.upload_numpy(hc, col)
+    with Runtime(arena) as rt:
+        assert graph.bfs_levels(rt, hr, hc, hl, nv, 0) == depth
+    assert bit_equal(arena.to_numpy(hl), lv)
+    # kmeans 2^20 x 32, k = 16 (one assignment pass)
+    km = I.kmeans(1 << 20, 32, 16, 256, seed=9)
+    want, trap = oracle.run(km)
+    got, got_trap, _, _ = gpu_run(km)
+    assert trap is None and got_trap is None
+    assert bit_equal(got["member"], want["member"]) and bit_equal(got["counts"], want["counts"])
