@@ -404,17 +404,17 @@ __global__ void __launch_bounds__(256) bfs_expand(const int* __restrict__ row,
 // default caching), anything else edge by edge.  All 16 targets' bitmap
 // words are loaded before any RED is issued.
 constexpr int kBfsV2 = 2;
-template <bool TEST>
+template <bool TEST, int V = kBfsV2>
 __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
                                                     const int* __restrict__ col, long long ne,
                                                     unsigned* now, long long nv,
                                                     const int* __restrict__ q, int* sizes) {
   const int qn = sizes[0];
-  const long long stride = (long long)gridDim.x * blockDim.x * kBfsV2;
-  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kBfsV2; i0 < qn; i0 += stride) {
-    int e0[kBfsV2], e1[kBfsV2];
+  const long long stride = (long long)gridDim.x * blockDim.x * V;
+  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * V; i0 < qn; i0 += stride) {
+    int e0[V], e1[V];
 #pragma unroll
-    for (int a = 0; a < kBfsV2; a++) {
+    for (int a = 0; a < V; a++) {
       e0[a] = e1[a] = 0;
       if (i0 + a < qn) {
         const int u = __ldg(q + i0 + a);
@@ -428,11 +428,13 @@ __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
         }
       }
     }
-    const int maxd = max(e1[0] - e0[0], e1[1] - e0[1]);
-    for (int j = 0; j < maxd; j += 8) {
-      int v[kBfsV2][8];
+    int maxd = 0;
 #pragma unroll
-      for (int a = 0; a < kBfsV2; a++) {
+    for (int a = 0; a < V; a++) maxd = max(maxd, e1[a] - e0[a]);
+    for (int j = 0; j < maxd; j += 8) {
+      int v[V][8];
+#pragma unroll
+      for (int a = 0; a < V; a++) {
         const int b = e0[a] + j;
         if (b + 8 <= e1[a] && (b & 3) == 0) {
           const int4 x = __ldg(reinterpret_cast<const int4*>(col + b));
@@ -444,9 +446,9 @@ __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
           for (int t = 0; t < 8; t++) v[a][t] = b + t < e1[a] ? __ldg(col + b + t) : -1;
         }
       }
-      unsigned w[kBfsV2][8];
+      unsigned w[V][8];
 #pragma unroll
-      for (int a = 0; a < kBfsV2; a++)
+      for (int a = 0; a < V; a++)
 #pragma unroll
         for (int t = 0; t < 8; t++) {
           w[a][t] = 0xffffffffu;
@@ -456,7 +458,7 @@ __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
           }
         }
 #pragma unroll
-      for (int a = 0; a < kBfsV2; a++)
+      for (int a = 0; a < V; a++)
 #pragma unroll
         for (int t = 0; t < 8; t++) {
           const unsigned bit = 1u << (v[a][t] & 31);
@@ -750,11 +752,16 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
           bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, nv);
           deep = true;
         }
-        int grid = stream_grid((qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
-        if (variant == 3)
+        if (variant == 4) {  // four frontier vertices per thread (32 probes in flight)
+          int grid = wave_grid(bfs_expand_v<true, 4>, 256, 0, (qn + 3) / 4, 256, num_sms, 8);
+          bfs_expand_v<true, 4><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
+        } else if (variant == 3) {
+          int grid = wave_grid(bfs_expand_v<false>, 256, 0, (qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
           bfs_expand_v<false><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
-        else
+        } else {
+          int grid = wave_grid(bfs_expand_v<true>, 256, 0, (qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
           bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
+        }
         bfs_compact8<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lv8, lvl, depth);
       }
       cudaMemcpyAsync(hs, sizes, 12, cudaMemcpyDeviceToHost, stream);
