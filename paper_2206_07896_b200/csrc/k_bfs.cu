@@ -292,7 +292,7 @@ static int launch_bfs(LaunchCtx& ctx) {
       if (rc) return rc;
       continue;
     }
-    int grid = stream_grid((hi - lo + 3) / 4, 256, ctx.num_sms, 8);
+    int grid = wave_grid(bfs_step, 256, 0, (hi - lo + 3) / 4, 256, ctx.num_sms, 8);
     bfs_step<<<grid, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len,
                                            (int*)L.ptr, L.len, (int*)Ch.ptr, Ch.len, lo, hi, cur,
                                            (int)bx, ctx.desc());

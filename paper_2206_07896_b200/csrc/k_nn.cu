@@ -127,12 +127,13 @@ static int launch_nn(LaunchCtx& ctx) {
       hi = bad;
     }
     if (lo >= hi) continue;
-    int grid = stream_grid((hi - lo + 3) / 4, 256, ctx.num_sms, 8);
     static int emu = -1;
     if (emu < 0) {
       const char* e = getenv("BF_NN_SQRT_EMU");
       emu = e ? atoi(e) : 0;
     }
+    const int grid = emu ? wave_grid(nn_stream<true>, 256, 0, (hi - lo + 3) / 4, 256, ctx.num_sms, 8)
+                         : wave_grid(nn_stream<false>, 256, 0, (hi - lo + 3) / 4, 256, ctx.num_sms, 8);
     if (emu)
       nn_stream<true><<<grid, 256, 0, ctx.stream>>>((const float*)L.ptr, (float*)D.ptr, lo, hi, x, y);
     else

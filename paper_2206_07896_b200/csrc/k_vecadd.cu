@@ -75,7 +75,7 @@ static int launch_vecadd(LaunchCtx& ctx) {
       hi = minlen;
     }
     if (lo >= hi) continue;
-    int grid = stream_grid((hi - lo + 3) / 4, 256 * 2, ctx.num_sms, 8);
+    int grid = wave_grid(vecadd_stream, 256, 0, (hi - lo + 3) / 4, 256 * 2, ctx.num_sms, 8);
     vecadd_stream<<<grid, 256, 0, ctx.stream>>>((const float*)A.ptr, (const float*)B.ptr,
                                                 (float*)C.ptr, lo, hi);
     BF_CUDA_LAUNCH_CHECK(ctx);
