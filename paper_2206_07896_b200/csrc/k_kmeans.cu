@@ -520,6 +520,18 @@ __device__ __forceinline__ double km_dist_tile(const float* T, int col, const fl
   return dist;
 }
 
+// f32 distance in the difference form (second-stage screen)
+template <int NF>
+__device__ __forceinline__ float km_dist_f32(const float* T, int col, const float* cc) {
+  float acc = 0.f;
+#pragma unroll 8
+  for (int l = 0; l < NF; l++) {
+    const float d = __fsub_rn(T[l * kTcStride + col], cc[l]);
+    acc = fmaf(d, d, acc);
+  }
+  return acc;
+}
+
 template <int NF>
 __global__ void __launch_bounds__(32 * (kTcWarps + 1), KM_TC_MINB) kmeans_tc(const float* __restrict__ f,
                                                                    const float* __restrict__ cent,
@@ -693,13 +705,49 @@ __global__ void __launch_bounds__(32 * (kTcWarps + 1), KM_TC_MINB) kmeans_tc(con
               if (need[r]) best[r] = e;
               continue;
             }
+            // stage 2: the candidates' distances in f32 in the difference
+            // form sum (x - c)^2, whose error is relative to the distance
+            // itself: |d32 - d| <= (nf + 4) 2^-24 d (+ subnormal slack).
+            // A single survivor of that screen is the answer; otherwise the
+            // exact f64 recurrence decides among the survivors.
+            bool sv[4];
+            int nsv = 0;
+            {
+              float d32[4], u2 = INFINITY;
+              const float e2 = (float)(NF + 4) * 5.9604645e-08f * 1.01f;
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const int c = 8 * (j >> 1) + 2 * t + (j & 1);
+                sv[j] = need[r] && fin[r] && tv[r][j] <= thr[r];
+                d32[j] = sv[j] ? km_dist_f32<NF>(T, cr, cf + c * NF) : INFINITY;
+                u2 = fminf(u2, fmaf(d32[j], e2, d32[j]) + 1e-40f);
+              }
+              u2 = fminf(u2, __shfl_xor_sync(0xffffffffu, u2, 1));
+              u2 = fminf(u2, __shfl_xor_sync(0xffffffffu, u2, 2));
+              int lowc = 16;
+#pragma unroll
+              for (int j = 3; j >= 0; j--) {
+                sv[j] = sv[j] && fmaf(-d32[j], e2, d32[j]) - 1e-40f <= u2;
+                nsv += sv[j];
+                if (sv[j]) lowc = 8 * (j >> 1) + 2 * t + (j & 1);
+              }
+              nsv += __shfl_xor_sync(0xffffffffu, nsv, 1);
+              lowc = min(lowc, __shfl_xor_sync(0xffffffffu, lowc, 1));
+              nsv += __shfl_xor_sync(0xffffffffu, nsv, 2);
+              lowc = min(lowc, __shfl_xor_sync(0xffffffffu, lowc, 2));
+              if (need[r] && fin[r] && nsv == 1) {
+                best[r] = lowc;
+                need[r] = false;
+              }
+            }
+            if (!__any_sync(0xffffffffu, need[r])) continue;
             double bd = INFINITY;
             int bi = 16;
             if (need[r] && fin[r]) {
 #pragma unroll
               for (int j = 0; j < 4; j++) {
                 const int c = 8 * (j >> 1) + 2 * t + (j & 1);
-                if (tv[r][j] <= thr[r]) {
+                if (sv[j]) {
                   const double dist = km_dist_tile<NF>(T, cr, cf + c * NF);
                   if (dist < bd || (dist == bd && c < bi)) {
                     bd = dist;
