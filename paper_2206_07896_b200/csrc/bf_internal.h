@@ -104,6 +104,17 @@ inline int stream_grid(long long work_items, int items_per_cta, int num_sms,
   return (int)(need < cap ? need : cap);
 }
 
+// True the first time it is called for the current device with this flag
+// array (function attributes such as the dynamic shared-memory limit are set
+// per device).
+inline bool first_on_device(bool (&done)[64]) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done[dev & 63]) return false;
+  done[dev & 63] = true;
+  return true;
+}
+
 // CTAs of `fn` resident per SM at this block size / dynamic smem (cached).
 // Grid-stride kernels size their grid with it: a grid larger than one
 // resident wave leaves a partial second wave (a tail) on every launch.

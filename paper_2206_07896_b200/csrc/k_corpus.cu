@@ -100,11 +100,10 @@ static int launch_reverse(LaunchCtx& ctx) {
     *ctx.error = "reverse: dynamic shared memory above 200 KiB";
     return BF_E_UNSUPPORTED;
   }
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(reverse_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaGetLastError();
-    attr = true;
   }
   long long B = (long long)ctx.block[0] * ctx.block[1] * ctx.block[2];
   int threads = (int)std::min<long long>(1024, ((B + 31) / 32) * 32);
@@ -414,12 +413,11 @@ template <int MODE, bool POW2, bool SAFE>
 static void hist_go(LaunchCtx& ctx, int grid, size_t smem, const ArgVal& P, const ArgVal& Cn,
                     long long lo, long long hi, const FastMod& fm, unsigned copies, long long xbase,
                     int bx_div) {
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
+  static bool attr[64] = {};
+  if ((smem > 48 * 1024) && first_on_device(attr)) {
     cudaFuncSetAttribute(hist_range<MODE, POW2, SAFE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cudaGetLastError();
-    attr = true;
   }
   hist_range<MODE, POW2, SAFE><<<grid, 256, smem, ctx.stream>>>(
       (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, fm, copies, ctx.desc(), xbase, bx_div);

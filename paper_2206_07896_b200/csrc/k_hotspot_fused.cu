@@ -289,10 +289,9 @@ static int run_passes(cudaStream_t stream, float* a, float* b, const float* p, i
                       const HsConstF& k, int iterations, float** result) {
   constexpr int RH = kTbH + 2 * T, RW = kTbW + 2 * T;
   const size_t smem = (size_t)3 * RH * RW * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(hotspot_tb<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
   }
   dim3 grid((cols + kTbW - 1) / kTbW, (rows + kTbH - 1) / kTbH);
   float* cur = a;

@@ -1235,14 +1235,13 @@ static int launch_kmeans(LaunchCtx& ctx) {
       const long long main_hi = lo + (hi - lo) / 4 * 4;
       auto fn = nf == 32 ? kmeans_umma<32> : kmeans_umma<16>;
       const size_t smem = nf == 32 ? kmeans_umma_smem<32>() : kmeans_umma_smem<16>();
-      static bool attr = false;
-      if (!attr) {
+      static bool attr[64] = {};
+      if (first_on_device(attr)) {
         cudaFuncSetAttribute(kmeans_umma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_umma_smem<32>());
         cudaFuncSetAttribute(kmeans_umma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_umma_smem<16>());
         cudaFuncSetAttribute(kmeans_umma<32>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(kmeans_umma<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaGetLastError();
-        attr = true;
       }
       const int grid = stream_grid(main_hi - lo, kTcPts, ctx.num_sms, KM_UM_MINB);  // CTAs per SM (smem, registers)
       fn<<<grid, 160, smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr, (float*)S.ptr,
@@ -1257,14 +1256,13 @@ static int launch_kmeans(LaunchCtx& ctx) {
       auto fn = nf == 32 ? kmeans_tc<32> : nf == 24 ? kmeans_tc<24> : nf == 16 ? kmeans_tc<16> : kmeans_tc<8>;
       const size_t smem = nf == 32 ? kmeans_tc_smem<32>() : nf == 24 ? kmeans_tc_smem<24>()
                         : nf == 16 ? kmeans_tc_smem<16>() : kmeans_tc_smem<8>();
-      static bool attr = false;
-      if (!attr) {
+      static bool attr[64] = {};
+      if (first_on_device(attr)) {
         cudaFuncSetAttribute(kmeans_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_tc_smem<32>());
         cudaFuncSetAttribute(kmeans_tc<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_tc_smem<24>());
         cudaFuncSetAttribute(kmeans_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_tc_smem<16>());
         cudaFuncSetAttribute(kmeans_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_tc_smem<8>());
         cudaGetLastError();
-        attr = true;
       }
       const int grid = stream_grid(main_hi - lo, kTcPts, ctx.num_sms, KM_TC_MINB);
       fn<<<grid, 32 * (kTcWarps + 1), smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr,
@@ -1281,12 +1279,11 @@ static int launch_kmeans(LaunchCtx& ctx) {
       const bool one = kmeans_variant() == 3;
       auto fn = nf == 32 ? (one ? kmeans_rb<32, 1> : kmeans_rb<32, 2>) : nf == 16 ? kmeans_rb<16, 2>
               : nf == 8 ? kmeans_rb<8, 2> : kmeans_rb<4, 2>;
-      static bool attr = false;
-      if (!attr) {
+      static bool attr[64] = {};
+      if (first_on_device(attr)) {
         for (auto g : {kmeans_rb<32, 1>, kmeans_rb<32, 2>, kmeans_rb<16, 2>, kmeans_rb<8, 2>, kmeans_rb<4, 2>})
           cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         cudaGetLastError();
-        attr = true;
       }
       int grid = stream_grid(hi - lo, 256 * 2, ctx.num_sms, 2);
       fn<<<grid, 256, smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr,
@@ -1299,12 +1296,11 @@ static int launch_kmeans(LaunchCtx& ctx) {
                                      (size_t)kKmWarps * kc * nf) + sizeof(int) * kc;
       auto fn = nf == 32 ? kmeans_fast<32> : nf == 16 ? kmeans_fast<16> : nf == 8 ? kmeans_fast<8>
               : nf == 4 ? kmeans_fast<4> : kmeans_fast<0>;
-      static bool attr = false;
-      if (!attr) {
+      static bool attr[64] = {};
+      if (first_on_device(attr)) {
         for (auto g : {kmeans_fast<32>, kmeans_fast<16>, kmeans_fast<8>, kmeans_fast<4>, kmeans_fast<0>})
           cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaGetLastError();
-        attr = true;
       }
       int grid = stream_grid(hi - lo, 256 * 4, ctx.num_sms, 4);
       fn<<<grid, 256, smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr,
@@ -1315,19 +1311,17 @@ static int launch_kmeans(LaunchCtx& ctx) {
     size_t smem = (size_t)kc * nf * (sizeof(double) + sizeof(float)) + kc * sizeof(int);
     int grid = stream_grid(hi - lo, 256 * 4, ctx.num_sms, 4);
     if (nf <= kKmMaxF) {
-      static bool attr = false;
-      if (!attr) {
+      static bool attr[64] = {};
+      if (first_on_device(attr)) {
         cudaFuncSetAttribute(kmeans_assign<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        attr = true;
       }
       kmeans_assign<true><<<grid, 256, smem, ctx.stream>>>(
           (const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr, (float*)S.ptr, (int*)Cn.ptr,
           (int)npts, nf, k, lo, hi);
     } else {
-      static bool attr = false;
-      if (!attr) {
+      static bool attr[64] = {};
+      if (first_on_device(attr)) {
         cudaFuncSetAttribute(kmeans_assign<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        attr = true;
       }
       kmeans_assign<false><<<grid, 256, smem, ctx.stream>>>(
           (const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr, (float*)S.ptr, (int*)Cn.ptr,
@@ -1388,11 +1382,17 @@ extern "C" int bf_kmeans_update_impl(void* stream_v, int num_sms, float* cent, f
                                      long long* delta, char* err, int errcap) {
   using namespace bf;
   cudaStream_t stream = (cudaStream_t)stream_v;
-  static unsigned long long* d = nullptr;
-  static unsigned long long* h = nullptr;
+  static unsigned long long* dd[64] = {};  // per-device scratch counter + pinned read-back
+  static unsigned long long* hh[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  unsigned long long*& d = dd[dev & 63];
+  unsigned long long*& h = hh[dev & 63];
   if (!d) {
     if (cudaMalloc((void**)&d, 8) != cudaSuccess || cudaMallocHost((void**)&h, 8) != cudaSuccess) {
       snprintf(err, errcap, "kmeans_update: scratch allocation failed");
+      cudaGetLastError();
+      d = nullptr;
       return BF_E_CUDA;
     }
   }
