@@ -419,6 +419,8 @@ static void hist_go(LaunchCtx& ctx, int grid, size_t smem, const ArgVal& P, cons
                          (int)smem);
     cudaGetLastError();
   }
+  // one resident wave (registers / shared memory bound the CTAs per SM)
+  grid = std::min(grid, wave_grid(hist_range<MODE, POW2, SAFE>, 256, smem, hi - lo, 256 * 16, ctx.num_sms, 8));
   hist_range<MODE, POW2, SAFE><<<grid, 256, smem, ctx.stream>>>(
       (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, fm, copies, ctx.desc(), xbase, bx_div);
 }
