@@ -98,8 +98,28 @@ _SLOT_FMT = {"i32": (struct.Struct("<iii4x"), 0), "i64": (struct.Struct("<iiq"),
 def pack_slots(packed) -> tuple[C.Array, int]:
     """Reference PackedArgs (or any object with .slots of (kind, value)) ->
     contiguous bf_slot array (16 B per slot).  f32 slots keep the unrounded
-    double."""
+    double.  The packed array is cached on the PackedArgs object and reused
+    while its (kind, value) signature is unchanged (slots are mutable), which
+    takes the packing off the launch path of host loops that relaunch the
+    same arguments (hotspot's ping-pong, the BFS level loop)."""
     slots = packed.slots if packed is not None else ()
+    try:
+        sig = tuple([(s.kind, s.value) for s in slots])
+    except AttributeError:
+        sig = None
+    cached = getattr(packed, "_bf_packed", None) if sig is not None else None
+    if cached is not None and cached[0] == sig:
+        return cached[1], cached[2]
+    arr, n = _pack_slots(slots)
+    if sig is not None:
+        try:
+            packed._bf_packed = (sig, arr, n)
+        except AttributeError:  # __slots__ objects: no cache
+            pass
+    return arr, n
+
+
+def _pack_slots(slots) -> tuple[C.Array, int]:
     n = len(slots)
     buf = bytearray(16 * max(n, 1))
     i = -1
