@@ -1373,7 +1373,14 @@ __global__ void __launch_bounds__(256) kmeans_delta(const int* __restrict__ memb
     prev[p] = m;
   }
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(delta, (unsigned long long)c);
+  __shared__ unsigned wsum[8];  // one atomic per CTA, not per warp (a single hot address)
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += wsum[w];
+    if (t) atomicAdd(delta, t);
+  }
 }
 }  // namespace bf
 
