@@ -106,6 +106,43 @@ __global__ void __launch_bounds__(256) bfs_step(const int* __restrict__ row, lon
   }
 }
 
+// CTA-wide queue append: every thread contributes c items and gets its first
+// slot; one atomicAdd per CTA (the counter is a single hot address: per-warp
+// atomics serialise at the L2 on the largest levels).  Must be called by all
+// threads of the CTA (CTA-uniform loops).
+__device__ __forceinline__ int cta_append(int c, int* counter, int* extra_total = nullptr, int extra = 0) {
+  __shared__ int wtot[32], wext[32];
+  __shared__ int cbase;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int ex = extra;
+  for (int o = 16; o > 0; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
+  if (lane == 31) {
+    wtot[warp] = incl;
+    wext[warp] = ex;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0, et = 0;
+    for (int w = 0; w < nw; w++) {
+      const int t = wtot[w];
+      wtot[w] = run;
+      run += t;
+      et += wext[w];
+    }
+    cbase = run ? atomicAdd(counter, run) : 0;
+    if (extra_total && et) atomicAdd(extra_total, et);
+  }
+  __syncthreads();
+  const int base = cbase + wtot[warp] + incl - c;
+  __syncthreads();  // wtot / cbase are rewritten by the next call
+  return base;
+}
+
 // Two-phase level step (a launch whose fetch covers the whole grid):
 //   scan    one pass over lvl[0, ll) builds an "unvisited" bitmap (lvl == -1,
 //           8 MB at 2^26 vertices, L2-resident) and appends the frontier
@@ -120,8 +157,8 @@ __global__ void __launch_bounds__(256) bfs_scan(const int* __restrict__ lvl, lon
                                                 long long words, int* q, int* qn, long long lo, long long hi,
                                                 int cur) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
-  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w - lane < words; w += stride) {
+  for (long long w0 = (long long)blockIdx.x * blockDim.x; w0 < words; w0 += stride) {  // CTA-uniform
+    const long long w = w0 + threadIdx.x;
     unsigned um = 0, fm = 0;
     if (w < words) {
       const long long v0 = w * 32;
@@ -147,17 +184,7 @@ __global__ void __launch_bounds__(256) bfs_scan(const int* __restrict__ lvl, lon
       if (v0 < lo) fm &= lo - v0 >= 32 ? 0u : (0xffffffffu << (lo - v0));
       if (v0 + 32 > hi) fm &= hi <= v0 ? 0u : (0xffffffffu >> (v0 + 32 - hi));
     }
-    const int c = __popc(fm);
-    int incl = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int base = 0;
-    if (lane == 31 && total) base = atomicAdd(qn, total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int pos = base + incl - c;
+    int pos = cta_append(__popc(fm), qn);
     for (; fm; fm &= fm - 1) q[pos++] = (int)(w * 32 + __ffs(fm) - 1);
   }
 }
@@ -475,26 +502,16 @@ __global__ void __launch_bounds__(256) bfs_compact8(unsigned* now, unsigned* pre
                                                     int* nq, int* sizes, unsigned char* lv8, int* lvl,
                                                     int depth) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
   const bool bytes = depth + 1 < 255;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < words; i += stride) {
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < words; i0 += stride) {  // CTA-uniform
+    const long long i = i0 + threadIdx.x;
     unsigned fresh = 0;
     if (i < words) {
       const unsigned nw = __ldcg(now + i);
       fresh = nw & ~prev[i];
       if (fresh) prev[i] = nw;
     }
-    const int c = __popc(fresh);
-    int incl = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int base = 0;
-    if (lane == 31 && total) base = atomicAdd(sizes + 1, total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int pos = base + incl - c;
+    int pos = cta_append(__popc(fresh), sizes + 1);
     while (fresh) {
       const int b = __ffs(fresh) - 1;
       const int v = (int)(i * 32 + b);
@@ -579,9 +596,9 @@ __global__ void __launch_bounds__(256) bfs_compact_sh(unsigned* now, unsigned* p
                                                       int* sizes, unsigned char* lv8, int* lvl, int depth,
                                                       long long vlo, long long vhi) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
   const bool bytes = depth + 1 < 255;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < words; i += stride) {
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < words; i0 += stride) {  // CTA-uniform
+    const long long i = i0 + threadIdx.x;
     unsigned fresh = 0, own = 0;
     if (i < words) {
       const unsigned nw = __ldcg(now + i);
@@ -594,19 +611,7 @@ __global__ void __launch_bounds__(256) bfs_compact_sh(unsigned* now, unsigned* p
       if (b0 + 32 > vhi) m &= vhi <= b0 ? 0u : (0xffffffffu >> (b0 + 32 - vhi));
       own = fresh & m;
     }
-    const int c = __popc(own);
-    int incl = c, all = __popc(fresh);
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-      all += __shfl_xor_sync(0xffffffffu, all, o);
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int base = 0;
-    if (lane == 31 && total) base = atomicAdd(sizes + 1, total);
-    if (lane == 0 && all) atomicAdd(sizes + 3, all);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int pos = base + incl - c;
+    int pos = cta_append(__popc(own), sizes + 1, sizes + 3, __popc(fresh));
     while (fresh) {
       const int b = __ffs(fresh) - 1;
       const int v = (int)(i * 32 + b);
