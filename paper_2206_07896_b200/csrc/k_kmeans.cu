@@ -14,6 +14,8 @@
 // of one feature are coalesced; each thread keeps its point's <= 32 features
 // in registers; centroids live in shared memory as doubles (broadcast reads).
 // Bound: FP64 (3 DP ops per point x cluster x feature), see DESIGN.md.
+#include <cuda_bf16.h>
+
 #include <climits>
 
 #include "bf_internal.h"
@@ -439,7 +441,8 @@ __global__ void __launch_bounds__(256, MINB) kmeans_rb(const float* __restrict__
 // operand x = hi + lo, hi = x rounded to TF32 (integer add + mask), lo = x - hi
 // (exact in f32) truncated to TF32 by a mask (|x - hi - lo| <= 2^-21 |x|):
 //   dot ~ hi.hi + hi.lo + lo.hi   (3 MMAs)
-//   sums = F_hi^T onehot + F_lo^T onehot   (onehot is exact)
+// The sums use bf16 pairs on m16n8k16 (x = hi + lo, |x - hi - lo| <= 2^-18 |x|;
+// the one-hot is exact): sums = F_hi^T onehot + F_lo^T onehot, 16 points per MMA.
 // Screen bound, with S = sum_l |f_l c_l| <= |f||c|: split residue
 // (lo.lo plus the two truncated cross terms) <= 5.01 2^-22 S; hi.hi
 // accumulates alone over nf/8 <= 4 MMAs of 8 exact products each, every
@@ -484,6 +487,21 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// (x0, x1) -> bf16x2 pairs hi = RN(x), lo = RN(x - hi) (element 0 in the low half)
+__device__ __forceinline__ void split_bf16x2(float2 x, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x.x, x.y);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x.x - __low2float(h), x.y - __high2float(h));
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -781,32 +799,42 @@ __global__ void __launch_bounds__(32 * (kTcWarps + 1), KM_TC_MINB) kmeans_tc(con
                 for (int l = 0; l < NF; l++) atomicAdd(ssum + best[r] * NF + l, T[l * kTcStride + col + 8 * r]);
             }
         }
-        // ---- sums GEMM: acc[features x clusters] += F^T[features x 8 points] onehot[8 points x clusters]
-        // (point q of this k-step contributes iff it is valid and finite)
-#pragma unroll
-        for (int ks = 0; ks < 2; ks++) {
-          const int pc = warp * 32 + mt * 16 + 8 * ks;  // first point column of this k-step
-          const int src = (ok[ks] && fin[ks]) ? best[ks] : -1;
-          const int q0 = __shfl_sync(0xffffffffu, src, 4 * t);
-          const int q1 = __shfl_sync(0xffffffffu, src, 4 * (t + 4));
-          const float* Tp = T + pc + t;
+        // ---- sums GEMM: acc[features x clusters] += F^T[features x 16 points] onehot, on
+        // bf16 pairs (m16n8k16): x = hi + lo with hi, lo bf16 (|x - hi - lo| <= 2^-18 |x|,
+        // far inside the sums tolerance), the one-hot exact in bf16; points that are not
+        // valid and finite contribute zeros
+        {
+          const int bs0 = (ok[0] && fin[0]) ? best[0] : -1;  // point g of the m-tile
+          const int bs1 = (ok[1] && fin[1]) ? best[1] : -1;  // point g + 8
+          const int qa = __shfl_sync(0xffffffffu, bs0, 8 * t), qb = __shfl_sync(0xffffffffu, bs0, 8 * t + 4);
+          const int qc = __shfl_sync(0xffffffffu, bs1, 8 * t), qd = __shfl_sync(0xffffffffu, bs1, 8 * t + 4);
+          const float* Tp = T + warp * 32 + mt * 16 + 2 * t;  // points 2t, 2t+1 (and +8) of the m-tile
 #pragma unroll
           for (int ms = 0; ms < MS; ms++) {
             const int r0 = 16 * ms + g, r1 = r0 + 8;
-            const float y0 = q0 >= 0 ? Tp[r0 * kTcStride] : 0.f;
-            const float y2 = q1 >= 0 ? Tp[r0 * kTcStride + 4] : 0.f;
-            const float y1 = (r1 < NF && q0 >= 0) ? Tp[r1 * kTcStride] : 0.f;
-            const float y3 = (r1 < NF && q1 >= 0) ? Tp[r1 * kTcStride + 4] : 0.f;
-            uint32_t yh[4], yl[4];
-            split_tf32(y0, yh[0], yl[0]);
-            split_tf32(y1, yh[1], yl[1]);
-            split_tf32(y2, yh[2], yl[2]);
-            split_tf32(y3, yh[3], yl[3]);
+            float2 xa = *reinterpret_cast<const float2*>(Tp + r0 * kTcStride);
+            float2 xb = *reinterpret_cast<const float2*>(Tp + r0 * kTcStride + 8);
+            float2 xc = make_float2(0.f, 0.f), xd = xc;
+            if (r1 < NF) {
+              xc = *reinterpret_cast<const float2*>(Tp + r1 * kTcStride);
+              xd = *reinterpret_cast<const float2*>(Tp + r1 * kTcStride + 8);
+            }
+            if (qa < 0) xa.x = xc.x = 0.f;
+            if (qb < 0) xa.y = xc.y = 0.f;
+            if (qc < 0) xb.x = xd.x = 0.f;
+            if (qd < 0) xb.y = xd.y = 0.f;
+            uint32_t ah[4], al[4];
+            split_bf16x2(xa, ah[0], al[0]);
+            split_bf16x2(xc, ah[1], al[1]);
+            split_bf16x2(xb, ah[2], al[2]);
+            split_bf16x2(xd, ah[3], al[3]);
 #pragma unroll
             for (int nt = 0; nt < 2; nt++) {
-              const uint32_t o0 = q0 == 8 * nt + g ? one : 0u, o1 = q1 == 8 * nt + g ? one : 0u;
-              mma_tf32(acc[ms][nt], yl, o0, o1);
-              mma_tf32(acc[ms][nt], yh, o0, o1);
+              const int cl = 8 * nt + g;
+              const uint32_t b0 = (qa == cl ? 0x3F80u : 0u) | (qb == cl ? 0x3F800000u : 0u);
+              const uint32_t b1 = (qc == cl ? 0x3F80u : 0u) | (qd == cl ? 0x3F800000u : 0u);
+              mma_bf16(acc[ms][nt], al, b0, b1);
+              mma_bf16(acc[ms][nt], ah, b0, b1);
             }
           }
         }
