@@ -260,6 +260,13 @@ def test_bfs_levels_fused_vs_oracle():
     row = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
     col = g.integers(0, nv, int(row[-1])).astype(np.int32)
     graphs.append(((row, col), nv, 3))
+    # large enough for the bucketed levels (> 2 slices of 2^18 vertices),
+    # variable degrees 0..16
+    nv = 1 << 20
+    degs = g.integers(0, 17, nv)
+    row = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
+    col = g.integers(0, nv, int(row[-1])).astype(np.int32)
+    graphs.append(((row, col), nv, 12345))
     nv = 1400
     adj = [[i + 1] if i < 699 else [] for i in range(nv)]
     for i in range(0, 700, 7):
@@ -677,3 +684,41 @@ def test_benchmark_configs_full_size_vs_oracle():
     got, got_trap, _, _ = gpu_run(km)
     assert trap is None and got_trap is None
     assert bit_equal(got["member"], want["member"]) and bit_equal(got["counts"], want["counts"])
+
+
+def test_bfs_bucketed_levels_opt_in_vs_oracle():
+    """The opt-in bucketed large levels (BF_BFS_BUCKET=1) stay bit-exact;
+    run in a subprocess because the switch is read when the library loads."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    script = f"""
+import sys
+sys.path[:0] = [{root!r}, {root!r} + '/oracle', {root!r} + '/tests']
+import numpy as np
+import instances as I
+import oracle
+from gpu_helpers import bit_equal
+from paper_2206_07896_b200 import DeviceArena, Runtime, graph
+g = np.random.default_rng(4)
+nv = 1 << 20
+degs = g.integers(0, 17, nv)
+row = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
+col = g.integers(0, nv, int(row[-1])).astype(np.int32)
+for (r, c), src in [((row, col), 7), (I.random_graph(1 << 21, 8, 3), 0)]:
+    n = r.size - 1
+    want, depth = oracle.bfs_full(r, c, n, src)
+    arena = DeviceArena()
+    hr, hc, hl = arena.alloc("i32", n + 1), arena.alloc("i32", c.size), arena.alloc("i32", n)
+    arena.upload_numpy(hr, r)
+    arena.upload_numpy(hc, c)
+    with Runtime(arena) as rt:
+        assert graph.bfs_levels(rt, hr, hc, hl, n, src) == depth
+    assert bit_equal(arena.to_numpy(hl), want)
+print("ok")
+"""
+    env = dict(os.environ, BF_BFS_BUCKET="1")
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
