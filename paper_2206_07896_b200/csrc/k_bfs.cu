@@ -435,8 +435,13 @@ template <bool TEST, int V = kBfsV2>
 __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
                                                     const int* __restrict__ col, long long ne,
                                                     unsigned* now, long long nv,
-                                                    const int* __restrict__ q, int* sizes) {
+                                                    const int* __restrict__ q, int* sizes,
+                                                    int* zero_p, int* hist) {
   const int qn = sizes[0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // pipelined loop: next-next level's counter, qn record
+    if (zero_p) *zero_p = 0;
+    if (hist) *(volatile int*)hist = qn;
+  }
   const long long stride = (long long)gridDim.x * blockDim.x * V;
   for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * V; i0 < qn; i0 += stride) {
     int e0[V], e1[V];
@@ -519,6 +524,163 @@ __global__ void __launch_bounds__(256) bfs_compact8(unsigned* now, unsigned* pre
       if (bytes) lv8[v] = (unsigned char)(depth + 1);
       else lvl[v] = depth + 1;
       fresh &= fresh - 1;
+    }
+  }
+}
+
+// Compaction with coalesced writes (depth + 1 < 255): the CTA's new
+// vertices are staged in shared memory and leave as one contiguous queue run,
+// and a word's 32 level bytes (one 32 B sector of lv8) are merged in
+// registers and stored as two 16 B vectors instead of one byte store per new
+// vertex.  Same queue contents and order as bfs_compact8.
+__device__ __forceinline__ unsigned lv8_merge(unsigned x, unsigned fresh, int sh, unsigned lb) {
+  const unsigned m4 = (fresh >> sh) & 0xFu;
+  const unsigned bm = ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu;  // bit j -> byte j
+  return (x & ~bm) | (lb & bm);
+}
+
+__global__ void __launch_bounds__(256) bfs_compact8s(unsigned* now, unsigned* prev, long long words,
+                                                     int* nq, const int* qn_p, int* out_cnt,
+                                                     unsigned char* lv8, int* lvl, int depth) {
+  __shared__ int stage[256 * 32];
+  __shared__ int wtot[8];
+  __shared__ int cbase, ctot;
+  if (*qn_p == 0) return;  // nothing was expanded: nothing is fresh
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool bytes = depth + 1 < 255;
+  const unsigned lb = (unsigned)(depth + 1) * 0x01010101u;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < words; i0 += stride) {  // CTA-uniform
+    const long long i = i0 + threadIdx.x;
+    unsigned fresh = 0;
+    if (i < words) {
+      const unsigned nw = __ldcg(now + i);
+      fresh = nw & ~prev[i];
+      if (fresh && !bytes) {  // levels beyond a byte: lvl written directly
+        prev[i] = nw;
+        for (unsigned f = fresh; f; f &= f - 1) lvl[i * 32 + __ffs(f) - 1] = depth + 1;
+      } else if (fresh) {
+        prev[i] = nw;
+        uint4* p = reinterpret_cast<uint4*>(lv8 + i * 32);
+        uint4 a = p[0], b = p[1];
+        a.x = lv8_merge(a.x, fresh, 0, lb);
+        a.y = lv8_merge(a.y, fresh, 4, lb);
+        a.z = lv8_merge(a.z, fresh, 8, lb);
+        a.w = lv8_merge(a.w, fresh, 12, lb);
+        b.x = lv8_merge(b.x, fresh, 16, lb);
+        b.y = lv8_merge(b.y, fresh, 20, lb);
+        b.z = lv8_merge(b.z, fresh, 24, lb);
+        b.w = lv8_merge(b.w, fresh, 28, lb);
+        p[0] = a;
+        p[1] = b;
+      }
+    }
+    const int c = __popc(fresh);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int w = 0; w < 8; w++) {
+        const int t = wtot[w];
+        wtot[w] = run;
+        run += t;
+      }
+      ctot = run;
+      cbase = run ? atomicAdd(out_cnt, run) : 0;
+    }
+    __syncthreads();
+    int pos = wtot[warp] + incl - c;
+    for (unsigned f = fresh; f; f &= f - 1) stage[pos++] = (int)(i * 32 + __ffs(f) - 1);
+    __syncthreads();
+    const int tot = ctot, base = cbase;
+    for (int j = threadIdx.x; j < tot; j += blockDim.x) nq[base + j] = stage[j];
+    __syncthreads();
+  }
+}
+
+// Small levels: expansion and compaction in one pass.  atomicOr returns the
+// bitmap word, so the one thread that sets a target's bit owns the target: it
+// appends it to the next queue (one atomicAdd per warp and chunk), records its
+// level and sets the bit in prev as well, so a later sweep (bfs_compact8s)
+// sees it as old.  Loops are warp-uniform (warp-wide appends).
+template <int V>
+__global__ void __launch_bounds__(256) bfs_expand_app(const int* __restrict__ row, const int* __restrict__ col,
+                                                      long long ne, unsigned* now, unsigned* prev, long long nv,
+                                                      const int* __restrict__ q, int* sizes, int* nq,
+                                                      unsigned char* lv8, int* lvl, int depth, bool deep) {
+  const int qn = sizes[0];
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x * V;
+  for (long long b0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * V; b0 < qn; b0 += stride) {
+    const long long i0 = b0 + (long long)lane * V;
+    int e0[V], e1[V];
+#pragma unroll
+    for (int a = 0; a < V; a++) {
+      e0[a] = e1[a] = 0;
+      if (i0 + a < qn) {
+        const int u = __ldg(q + i0 + a);
+        e0[a] = __ldg(row + u);
+        e1[a] = __ldg(row + u + 1);
+        if (e0[a] < 0 || e1[a] > ne || e1[a] < e0[a]) {
+          sizes[2] = 1;
+          e1[a] = e0[a];
+        }
+      }
+    }
+    int maxd = 0;
+#pragma unroll
+    for (int a = 0; a < V; a++) maxd = max(maxd, e1[a] - e0[a]);
+    maxd = __reduce_max_sync(0xffffffffu, maxd);
+    for (int j = 0; j < maxd; j += 8) {
+      int v[V][8];
+#pragma unroll
+      for (int a = 0; a < V; a++)
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+          v[a][t] = e0[a] + j + t < e1[a] ? __ldg(col + e0[a] + j + t) : -1;
+          if (v[a][t] >= nv) {
+            sizes[2] = 1;
+            v[a][t] = -1;
+          }
+        }
+      unsigned mine = 0;
+#pragma unroll
+      for (int a = 0; a < V; a++)
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+          if (v[a][t] >= 0) {
+            const unsigned bit = 1u << (v[a][t] & 31);
+            if (!(__ldcg(now + (v[a][t] >> 5)) & bit) && !(atomicOr(now + (v[a][t] >> 5), bit) & bit))
+              mine |= 1u << (a * 8 + t);
+          }
+      const int c = __popc(mine);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int base = 0;
+      if (lane == 31 && incl) base = atomicAdd(sizes + 1, incl);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      int pos = base + incl - c;
+#pragma unroll
+      for (int a = 0; a < V; a++)
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+          if (mine & (1u << (a * 8 + t))) {
+            const int x = v[a][t];
+            nq[pos++] = x;
+            if (deep) lvl[x] = depth + 1;
+            else lv8[x] = (unsigned char)(depth + 1);
+            atomicOr(prev + (x >> 5), 1u << (x & 31));
+          }
     }
   }
 }
@@ -847,6 +1009,10 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
     long long *offsets = nullptr, *cursors = nullptr;
     int* buckets = nullptr;
     long long cap_buckets = 0;
+    // pipelined loop: rotating level counters, host-mapped qn record, events
+    int* ctr = nullptr;
+    int *hist = nullptr, *hist_d = nullptr;
+    cudaEvent_t evx[4] = {};
   };
   static Scratch sc[64];
   int dev = 0;
@@ -868,7 +1034,7 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.prev, words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.qa, (size_t)nv * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.qb, (size_t)nv * 4);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&S.lv8, (size_t)nv + 16);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.lv8, (size_t)words * 32 + 16);  // whole sectors (bfs_compact8s)
     if (e == cudaSuccess) {
       S.cap_v = nv;
       S.cap_words = words;
@@ -876,6 +1042,12 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   }
   if (e == cudaSuccess && !S.sizes) e = cudaMalloc((void**)&S.sizes, 16);
   if (e == cudaSuccess && !S.hs) e = cudaMallocHost((void**)&S.hs, 16);
+  if (e == cudaSuccess && !S.ctr) e = cudaMalloc((void**)&S.ctr, 12 * sizeof(int));
+  if (e == cudaSuccess && !S.hist) {
+    e = cudaHostAlloc((void**)&S.hist, 64 * sizeof(int), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&S.hist_d, S.hist, 0);
+    for (int i = 0; i < 4 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&S.evx[i], cudaEventDisableTiming);
+  }
   unsigned *now = S.now, *prev = S.prev;
   int *qa = S.qa, *qb = S.qb, *sizes = S.sizes, *hs = S.hs;
   unsigned char* lv8 = S.lv8;
@@ -888,6 +1060,17 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   if (bucket_on < 0) {
     const char* be = getenv("BF_BFS_BUCKET");
     bucket_on = be ? atoi(be) : 0;
+  }
+  // small levels (qn * BF_BFS_APP <= nv) expand and append in one pass; 0: off
+  static int app_div = -1;
+  if (app_div < 0) {
+    const char* ae = getenv("BF_BFS_APP");
+    app_div = ae ? atoi(ae) : 0;
+  }
+  static int cs_on = -1;  // coalesced compaction (bfs_compact8s), BF_BFS_CS
+  if (cs_on < 0) {
+    const char* ce = getenv("BF_BFS_CS");
+    cs_on = ce ? atoi(ce) : 1;
   }
   bool deep = false;
   int depth = 0;
@@ -923,6 +1106,57 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
     int* q = qa;
     int* nq = qb;
     const int cgrid = stream_grid(words, 256, num_sms, 8);
+    // Default path, pipelined: the host enqueues level d + 2 as soon as level
+    // d + 1's expansion has recorded its frontier size (host-mapped), so the
+    // device never waits for a host round trip between levels.  Three
+    // rotating counters: level L expands ctr[4(L%3)] vertices, its compaction
+    // appends into ctr[4((L+1)%3)], and its expansion zeroes ctr[4((L+2)%3)]
+    // (that level's input was consumed by level L - 1); [+2] error flags.
+    const bool piped = variant == 2 && !bucket_on && app_div <= 0 && cs_on;
+    if (piped) {
+      const int xgrid = wave_grid(bfs_expand_v<true>, 256, 0, ((long long)nv + 1) / 2, 256, num_sms, 8);
+      const int sgrid = wave_grid(bfs_compact8s, 256, 0, words, 256, num_sms, 8);
+      auto enqueue = [&](int L) {
+        int* B = S.ctr + 4 * (L % 3);
+        int* Bn = S.ctr + 4 * ((L + 1) % 3);
+        int* Bz = S.ctr + 4 * ((L + 2) % 3);
+        int* qL = (L & 1) ? qb : qa;
+        int* nqL = (L & 1) ? qa : qb;
+        if (L + 1 >= 255 && !deep) {  // levels beyond a byte: lvl written directly from here on
+          bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, nv);
+          deep = true;
+        }
+        bfs_expand_v<true><<<xgrid, 256, 0, stream>>>(row, col, lcol, now, nv, qL, B, Bz, S.hist_d + (L & 63));
+        cudaEventRecord(S.evx[L & 3], stream);
+        bfs_compact8s<<<sgrid, 256, 0, stream>>>(now, prev, words, nqL, B, Bn, lv8, lvl, L);
+      };
+      cudaMemsetAsync(S.ctr, 0, 12 * sizeof(int), stream);
+      bfs_init8<<<g, 256, 0, stream>>>(lv8, now, prev, nv, words, src, qa, S.ctr);
+      bfs_seed8<<<1, 1, 0, stream>>>(lv8, now, prev, src);
+      enqueue(0);
+      enqueue(1);
+      for (int d = 0;; d++) {
+        e = cudaEventSynchronize(S.evx[(d + 1) & 3]);
+        if (e != cudaSuccess) break;
+        const int qn1 = ((volatile int*)S.hist)[(d + 1) & 63];
+        if (qn1 == 0) {
+          depth = d + 1;
+          break;
+        }
+        enqueue(d + 2);
+      }
+      if (e == cudaSuccess) {
+        int c[12];
+        cudaMemcpyAsync(c, S.ctr, sizeof(c), cudaMemcpyDeviceToHost, stream);
+        e = cudaStreamSynchronize(stream);
+        if (e == cudaSuccess && (c[2] | c[6] | c[10])) {
+          snprintf(err, errcap, "bfs_levels: CSR index out of range");
+          e = cudaErrorInvalidValue;
+        }
+      }
+      qn = 0;
+    }
+    // per-level host loop (other variants)
     while (qn > 0) {
       if (variant == 1) {
         int grid = stream_grid((qn + kBfsVPT - 1) / kBfsVPT, 256, num_sms, 8);
@@ -933,6 +1167,7 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
           bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, nv);
           deep = true;
         }
+        bool appended = false;
         const int nslices = (int)((nv + (1 << kSliceLog) - 1) >> kSliceLog);
         bool bucketed = bucket_on && nslices <= kMaxSlices && (long long)qn * 32 >= nv && nslices >= 2;
         if (bucketed && (!S.counts || S.cap_buckets < lcol)) {
@@ -966,15 +1201,26 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
                                                         depth, nslices);
         } else if (variant == 4) {  // four frontier vertices per thread (32 probes in flight)
           int grid = wave_grid(bfs_expand_v<true, 4>, 256, 0, (qn + 3) / 4, 256, num_sms, 8);
-          bfs_expand_v<true, 4><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
+          bfs_expand_v<true, 4><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes, nullptr, nullptr);
         } else if (variant == 3) {
           int grid = wave_grid(bfs_expand_v<false>, 256, 0, (qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
-          bfs_expand_v<false><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
+          bfs_expand_v<false><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes, nullptr, nullptr);
+        } else if (app_div > 0 && (long long)qn * app_div <= nv) {  // small level: fused append
+          int grid = wave_grid(bfs_expand_app<2>, 256, 0, (qn + 1) / 2, 256, num_sms, 8);
+          bfs_expand_app<2><<<grid, 256, 0, stream>>>(row, col, lcol, now, prev, nv, q, sizes, nq, lv8, lvl,
+                                                      depth, deep);
+          appended = true;
         } else {
           int grid = wave_grid(bfs_expand_v<true>, 256, 0, (qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
-          bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes);
+          bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes, nullptr, nullptr);
         }
-        if (!bucketed) bfs_compact8<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lv8, lvl, depth);
+        if (appended) {
+        } else if (!bucketed && cs_on && !deep && depth + 1 < 255) {
+          const int sgrid = wave_grid(bfs_compact8s, 256, 0, words, 256, num_sms, 8);
+          bfs_compact8s<<<sgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, sizes + 1, lv8, lvl, depth);
+        } else if (!bucketed) {
+          bfs_compact8<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lv8, lvl, depth);
+        }
       }
       cudaMemcpyAsync(hs, sizes, 12, cudaMemcpyDeviceToHost, stream);
       e = cudaStreamSynchronize(stream);
@@ -1116,7 +1362,7 @@ extern "C" int bf_bfs_shard_expand_impl(void* p, void* stream_v, int num_sms, co
   }
   if (s->qn > 0) {
     const int grid = stream_grid((s->qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
-    bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, s->now, s->nv, s->q, s->sizes);
+    bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, s->now, s->nv, s->q, s->sizes, nullptr, nullptr);
   }
   cudaError_t e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) {

@@ -686,9 +686,14 @@ def test_benchmark_configs_full_size_vs_oracle():
     assert bit_equal(got["member"], want["member"]) and bit_equal(got["counts"], want["counts"])
 
 
-def test_bfs_bucketed_levels_opt_in_vs_oracle():
-    """The opt-in bucketed large levels (BF_BFS_BUCKET=1) stay bit-exact;
-    run in a subprocess because the switch is read when the library loads."""
+@pytest.mark.parametrize("switch", [{"BF_BFS_BUCKET": "1"}, {"BF_BFS_CS": "0"}, {"BF_BFS_APP": "256"},
+                                    {"BF_BFS_APP": "1"}, {"BF_BFS_V": "4"}])
+def test_bfs_opt_in_levels_vs_oracle(switch):
+    """The opt-in traversal variants stay bit-exact: bucketed large levels
+    (BF_BFS_BUCKET=1), the per-level host loop with byte-store compaction
+    (BF_BFS_CS=0), fused expand-and-append for small levels (BF_BFS_APP),
+    four vertices per thread (BF_BFS_V=4); a chain graph takes each past 255
+    levels.  Run in a subprocess: the switches are read when the library loads."""
     import os
     import subprocess
     import sys
@@ -707,7 +712,14 @@ nv = 1 << 20
 degs = g.integers(0, 17, nv)
 row = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
 col = g.integers(0, nv, int(row[-1])).astype(np.int32)
-for (r, c), src in [((row, col), 7), (I.random_graph(1 << 21, 8, 3), 0)]:
+n = 1400
+adj = [[i + 1] if i < 699 else [] for i in range(n)]
+for i in range(0, 700, 7):
+    adj[i].append(700 + i % 700)
+    adj[700 + i % 700].append(700 + (i + 350) % 700)
+chain = (np.concatenate([[0], np.cumsum([len(a) for a in adj])]).astype(np.int32),
+         np.array([v for a in adj for v in a], np.int32))
+for (r, c), src in [((row, col), 7), (I.random_graph(1 << 21, 8, 3), 0), (chain, 0)]:
     n = r.size - 1
     want, depth = oracle.bfs_full(r, c, n, src)
     arena = DeviceArena()
@@ -719,6 +731,6 @@ for (r, c), src in [((row, col), 7), (I.random_graph(1 << 21, 8, 3), 0)]:
     assert bit_equal(arena.to_numpy(hl), want)
 print("ok")
 """
-    env = dict(os.environ, BF_BFS_BUCKET="1")
+    env = dict(os.environ, **switch)
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
