@@ -189,6 +189,98 @@ __global__ void __launch_bounds__(256) bfs_scan(const int* __restrict__ lvl, lon
   }
 }
 
+// bfs_scan with one int4 of lvl per thread (fully coalesced loads), the
+// bitmap words assembled by 8-lane OR reductions, the unvisited set written
+// twice (unv, mutated by the relax, and unv0, the launch-start snapshot the
+// deferred lvl writes diff against), and the frontier staged in shared memory
+// and appended as one contiguous queue run per CTA iteration.
+__global__ void __launch_bounds__(256) bfs_scan2(const int* __restrict__ lvl, long long ll, unsigned* unv,
+                                                 unsigned* unv0, int* q, int* qn, long long lo, long long hi,
+                                                 int cur) {
+  constexpr int J = 8;  // quads per thread per iteration (8 x 16 B loads in flight)
+  __shared__ int stage[256 * 4 * J];
+  __shared__ int wtot[8];
+  __shared__ int cbase, ctot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long quads = ((ll + 31) / 32) * 8;  // whole words
+  const long long stride = (long long)gridDim.x * blockDim.x * J;
+  for (long long t0 = (long long)blockIdx.x * blockDim.x * J; t0 < quads; t0 += stride) {  // CTA-uniform
+    int4 x[J];
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+      const long long t = t0 + j * 256 + threadIdx.x;
+      x[j] = make_int4(0, 0, 0, 0);
+      if (t * 4 + 4 <= ll) x[j] = __ldcs(reinterpret_cast<const int4*>(lvl + t * 4));
+    }
+    unsigned fm[J];
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+      const long long t = t0 + j * 256 + threadIdx.x;
+      const long long v0 = t * 4;
+      unsigned um = 0, f = 0;
+      if (t < quads) {
+        if (v0 + 4 <= ll) {
+          um = (x[j].x == -1) | (x[j].y == -1) << 1 | (x[j].z == -1) << 2 | (x[j].w == -1) << 3;
+          f = (x[j].x == cur) | (x[j].y == cur) << 1 | (x[j].z == cur) << 2 | (x[j].w == cur) << 3;
+        } else {
+          for (int e = 0; e < 4 && v0 + e < ll; e++) {
+            const int y = lvl[v0 + e];
+            um |= (unsigned)(y == -1) << e;
+            f |= (unsigned)(y == cur) << e;
+          }
+        }
+        // frontier restricted to the fetch's vertices [lo, hi)
+        if (v0 < lo || v0 + 4 > hi)
+          for (int e = 0; e < 4; e++)
+            if (v0 + e < lo || v0 + e >= hi) f &= ~(1u << e);
+      }
+      unsigned word = um << (4 * (lane & 7));
+      word |= __shfl_xor_sync(0xffffffffu, word, 1);
+      word |= __shfl_xor_sync(0xffffffffu, word, 2);
+      word |= __shfl_xor_sync(0xffffffffu, word, 4);
+      if ((lane & 7) == 0 && t < quads) {
+        unv[t >> 3] = word;
+        unv0[t >> 3] = word;
+      }
+      fm[j] = f;
+      c += __popc(f);
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int w = 0; w < 8; w++) {
+        const int y = wtot[w];
+        wtot[w] = run;
+        run += y;
+      }
+      ctot = run;
+      cbase = run ? atomicAdd(qn, run) : 0;
+    }
+    __syncthreads();
+    const int tot = ctot;
+    if (tot) {  // CTA-uniform
+      int pos = wtot[warp] + incl - c;
+#pragma unroll
+      for (int j = 0; j < J; j++) {
+        const long long v0 = (t0 + j * 256 + threadIdx.x) * 4;
+        for (unsigned f = fm[j]; f; f &= f - 1) stage[pos++] = (int)(v0 + __ffs(f) - 1);
+      }
+      __syncthreads();
+      const int base = cbase;
+      for (int j = threadIdx.x; j < tot; j += blockDim.x) q[base + j] = stage[j];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) bfs_relax(const int* __restrict__ row, long long lr,
                                                  const int* __restrict__ col, long long lcol, int* lvl,
                                                  long long ll, unsigned* unv, const int* __restrict__ q,
@@ -245,10 +337,142 @@ __global__ void __launch_bounds__(256) bfs_relax(const int* __restrict__ row, lo
   }
 }
 
+// Relax step with whole-adjacency vector loads and no claiming atomics:
+// every thread that finds a target still unvisited writes lvl[v] = cur + 1
+// (all writers of a vertex write the same value) and clears the bit with a
+// RED, so no thread waits on an atomic round trip.  V frontier vertices per
+// thread, eight edges per step (two 16 B loads when aligned).  Same lvl and
+// changed flag as bfs_relax; faults as bfs_relax (kind and vertex).
+template <int V>
+__global__ void __launch_bounds__(256) bfs_relax_v(const int* __restrict__ row, long long lr,
+                                                   const int* __restrict__ col, long long lcol, int* lvl,
+                                                   long long ll, unsigned* unv, const int* __restrict__ q,
+                                                   const int* qn, int* changed, long long lch, int cur, int bx,
+                                                   KDesc k, int defer_min) {
+  const int n = *qn;
+  const bool DEFER = n >= defer_min;  // big frontier: bfs_apply writes lvl
+  const long long stride = (long long)gridDim.x * blockDim.x * V;
+  bool any = false;
+  long long bad_u = -1;
+  const int nxt = (int)((unsigned)cur + 1u);
+  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * V; i0 < n; i0 += stride) {
+    int e0[V], e1[V], uu[V];
+#pragma unroll
+    for (int a = 0; a < V; a++) {
+      e0[a] = e1[a] = 0;
+      uu[a] = 0;
+      if (i0 + a < n) {
+        const int u = __ldg(q + i0 + a);
+        uu[a] = u;
+        if ((long long)u + 1 >= lr) {
+          if (bad_u < 0) bad_u = u;
+          continue;
+        }
+        e0[a] = __ldg(row + u);
+        e1[a] = __ldg(row + u + 1);
+        if (e1[a] > e0[a] && (e0[a] < 0 || e1[a] > lcol)) {  // edge index outside col
+          if (bad_u < 0) bad_u = u;
+          e1[a] = e0[a];
+        }
+      }
+    }
+    int maxd = 0;
+#pragma unroll
+    for (int a = 0; a < V; a++) maxd = max(maxd, e1[a] - e0[a]);
+    for (int j = 0; j < maxd; j += 8) {
+      int v[V][8];
+#pragma unroll
+      for (int a = 0; a < V; a++) {
+        const int b = e0[a] + j;
+        if (b + 8 <= e1[a] && (b & 3) == 0) {
+          const int4 x = __ldg(reinterpret_cast<const int4*>(col + b));
+          const int4 y = __ldg(reinterpret_cast<const int4*>(col + b + 4));
+          v[a][0] = x.x; v[a][1] = x.y; v[a][2] = x.z; v[a][3] = x.w;
+          v[a][4] = y.x; v[a][5] = y.y; v[a][6] = y.z; v[a][7] = y.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; t++) v[a][t] = b + t < e1[a] ? __ldg(col + b + t) : -1;
+        }
+      }
+      unsigned w[V][8];
+#pragma unroll
+      for (int a = 0; a < V; a++)
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+          w[a][t] = 0u;
+          if (e0[a] + j + t < e1[a]) {
+            if (v[a][t] < 0 || v[a][t] >= ll) {
+              if (bad_u < 0) bad_u = uu[a];
+            } else {
+              w[a][t] = __ldcg(unv + (v[a][t] >> 5));
+            }
+          }
+        }
+#pragma unroll
+      for (int a = 0; a < V; a++)
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+          const unsigned bit = 1u << (v[a][t] & 31);
+          if (w[a][t] & bit) {
+            if (!DEFER) lvl[v[a][t]] = nxt;
+            atomicAnd(unv + (v[a][t] >> 5), ~bit);  // result unused: RED
+            any = true;
+          }
+        }
+    }
+  }
+  if (bad_u >= 0) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bfs_block_of_x(k, bad_u / bx));
+  if (DEFER) return;  // bfs_apply writes lvl and the changed flag
+  if (__syncthreads_or(any) && threadIdx.x == 0) {
+    if (lch < 1) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, k.first);
+    else changed[0] = 1;
+  }
+}
+
+// Deferred level writes of the relax step: the vertices claimed in this
+// launch are unv0 & ~unv (unvisited at the start, cleared by the relax); one
+// thread per 4 vertices rewrites their int4 of lvl only where a claim falls
+// (read-merge-write of whole 16 B pieces, all 4 claimed: plain store), so the
+// big levels write lvl in full sectors instead of one scattered 4 B store per
+// claimed vertex (a partial-sector read-modify-write in DRAM).
+__global__ void __launch_bounds__(256) bfs_apply(const unsigned* __restrict__ unv0, const unsigned* unv, int* lvl,
+                                                 long long ll, int cur, int* changed, long long lch, KDesc k,
+                                                 const int* qn, int defer_min) {
+  if (*qn < defer_min) return;  // the relax wrote lvl itself
+  const long long quads = (ll + 3) / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int nxt = (int)((unsigned)cur + 1u);
+  bool any = false;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < quads; t += stride) {
+    const long long w = t >> 3;
+    const unsigned m = ((unv0[w] & ~__ldcg(unv + w)) >> (4 * (t & 7))) & 0xFu;
+    if (!m) continue;
+    any = true;
+    const long long v0 = t * 4;
+    if (v0 + 4 <= ll) {
+      int4* p = reinterpret_cast<int4*>(lvl + v0);
+      int4 x = m == 0xFu ? make_int4(nxt, nxt, nxt, nxt) : *p;
+      if (m & 1u) x.x = nxt;
+      if (m & 2u) x.y = nxt;
+      if (m & 4u) x.z = nxt;
+      if (m & 8u) x.w = nxt;
+      *p = x;
+    } else {
+      for (int j = 0; j < 4; j++)
+        if (m & (1u << j)) lvl[v0 + j] = nxt;
+    }
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) {
+    if (lch < 1) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, k.first);
+    else changed[0] = 1;
+  }
+}
+
 // per-device scratch of the two-phase step (grow-only)
 struct BfsStepScratch {
   long long cap_words = 0, cap_q = 0;
   unsigned* unv = nullptr;
+  unsigned* unv0 = nullptr;  // unvisited set at the launch start (deferred lvl writes)
   int* q = nullptr;
   int* qn = nullptr;
 };
@@ -263,10 +487,12 @@ static int launch_bfs_two_phase(LaunchCtx& ctx, const ArgVal& R, const ArgVal& C
   if (S.cap_words < words || S.cap_q < nq || !S.qn) {
     cudaStreamSynchronize(ctx.stream);
     cudaFree(S.unv);
+    cudaFree(S.unv0);
     cudaFree(S.q);
     cudaFree(S.qn);
     S = BfsStepScratch();
-    if (cudaMalloc((void**)&S.unv, words * 4) != cudaSuccess || cudaMalloc((void**)&S.q, nq * 4) != cudaSuccess ||
+    if (cudaMalloc((void**)&S.unv, words * 4) != cudaSuccess || cudaMalloc((void**)&S.unv0, words * 4) != cudaSuccess ||
+        cudaMalloc((void**)&S.q, nq * 4) != cudaSuccess ||
         cudaMalloc((void**)&S.qn, 4) != cudaSuccess) {
       *ctx.error = "bfs: scratch allocation failed";
       cudaGetLastError();
@@ -275,13 +501,46 @@ static int launch_bfs_two_phase(LaunchCtx& ctx, const ArgVal& R, const ArgVal& C
     S.cap_words = words;
     S.cap_q = nq;
   }
+  // BF_BFS_RELAX: 3 (default) = bfs_scan2 + bfs_relax_v<2> with the big
+  // levels' lvl writes deferred to bfs_apply; 2 = bfs_scan + bfs_relax_v<2>;
+  // 0 = bfs_scan + bfs_relax (claiming atomics)
+  static int relax_v = -1, defer_div = -1;
+  if (relax_v < 0) {
+    const char* e = getenv("BF_BFS_RELAX");
+    relax_v = e ? atoi(e) : 3;
+    const char* d = getenv("BF_BFS_DEFER_DIV");  // frontier >= len(lvl) / div: deferred writes
+    defer_div = d ? std::max(1, atoi(d)) : 64;
+  }
   cudaMemsetAsync(S.qn, 0, 4, ctx.stream);
+  if (relax_v == 3) {
+    const int defer_min = (int)std::max(1LL, ll / defer_div);
+    const int g1 = wave_grid(bfs_scan2, 256, 0, words * 8, 256 * 8, ctx.num_sms, 8);
+    bfs_scan2<<<g1, 256, 0, ctx.stream>>>((const int*)L.ptr, ll, S.unv, S.unv0, S.q, S.qn, lo, hi, cur);
+    BF_CUDA_LAUNCH_CHECK(ctx);
+    const int g2 = wave_grid(bfs_relax_v<2>, 256, 0, (nq + 1) / 2, 256, ctx.num_sms, 8);
+    bfs_relax_v<2><<<g2, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len, (int*)L.ptr,
+                                               ll, S.unv, S.q, S.qn, (int*)Ch.ptr, Ch.len, cur, (int)bx, ctx.desc(),
+                                               defer_min);
+    BF_CUDA_LAUNCH_CHECK(ctx);
+    const int g3 = wave_grid(bfs_apply, 256, 0, (ll + 3) / 4, 256, ctx.num_sms, 8);
+    bfs_apply<<<g3, 256, 0, ctx.stream>>>(S.unv0, S.unv, (int*)L.ptr, ll, cur, (int*)Ch.ptr, Ch.len, ctx.desc(),
+                                          S.qn, defer_min);
+    BF_CUDA_LAUNCH_CHECK(ctx);
+    return BF_OK;
+  }
   const int g1 = wave_grid(bfs_scan, 256, 0, words, 256, ctx.num_sms, 8);
   bfs_scan<<<g1, 256, 0, ctx.stream>>>((const int*)L.ptr, ll, S.unv, words, S.q, S.qn, lo, hi, cur);
   BF_CUDA_LAUNCH_CHECK(ctx);
-  const int g2 = wave_grid(bfs_relax, 256, 0, nq, 256, ctx.num_sms, 8);
-  bfs_relax<<<g2, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len, (int*)L.ptr, ll,
-                                        S.unv, S.q, S.qn, (int*)Ch.ptr, Ch.len, cur, (int)bx, ctx.desc());
+  if (relax_v > 0) {
+    const int g2 = wave_grid(bfs_relax_v<2>, 256, 0, (nq + 1) / 2, 256, ctx.num_sms, 8);
+    bfs_relax_v<2><<<g2, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len, (int*)L.ptr,
+                                               ll, S.unv, S.q, S.qn, (int*)Ch.ptr, Ch.len, cur, (int)bx, ctx.desc(),
+                                               INT_MAX);
+  } else {
+    const int g2 = wave_grid(bfs_relax, 256, 0, nq, 256, ctx.num_sms, 8);
+    bfs_relax<<<g2, 256, 0, ctx.stream>>>((const int*)R.ptr, R.len, (const int*)Co.ptr, Co.len, (int*)L.ptr, ll,
+                                          S.unv, S.q, S.qn, (int*)Ch.ptr, Ch.len, cur, (int)bx, ctx.desc());
+  }
   BF_CUDA_LAUNCH_CHECK(ctx);
   return BF_OK;
 }

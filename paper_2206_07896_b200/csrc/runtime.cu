@@ -335,6 +335,7 @@ struct bf_runtime {
   std::vector<cudaStream_t> streams;
   bool holding = false;          // hold_blocks: launches wait on the host
   bf::DevFault* fault_dev = nullptr;
+  bf::DevFault* fault_host = nullptr;  // pinned copy, fetched in the sync's own stream round trip
   bf::HostTrap trap;             // first trap (host- or device-detected)
   uint64_t trap_task = 0;
   std::string trap_kernel;
@@ -429,12 +430,26 @@ static int sync_workers(bf_runtime* rt) {
   return retire(rt, true);
 }
 
-static void absorb_device_fault(bf_runtime* rt) {
-  DevFault f;
-  if (cudaMemcpy(&f, rt->fault_dev, sizeof(f), cudaMemcpyDeviceToHost) != cudaSuccess) {
-    cudaGetLastError();
-    return;
+// sync_workers plus the device fault record, fetched by an async copy queued
+// behind worker 0's work: one host round trip instead of a sync followed by a
+// blocking (legacy-stream) cudaMemcpy.  Other workers are drained first, so
+// their faults are in the record before the copy runs.
+static int sync_workers_fault(bf_runtime* rt) {
+  int rc = open_gate(rt);
+  if (rc) return rc;
+  for (size_t i = 1; i < rt->streams.size(); i++) {
+    cudaError_t e = cudaStreamSynchronize(rt->streams[i]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   }
+  cudaError_t e = cudaMemcpyAsync(rt->fault_host, rt->fault_dev, sizeof(DevFault), cudaMemcpyDeviceToHost,
+                                  rt->streams[0]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(rt->streams[0]);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return retire(rt, true);
+}
+
+static void absorb_device_fault(bf_runtime* rt) {
+  const DevFault f = *rt->fault_host;  // fetched by sync_workers_fault
   if (f.kind != BF_TRAP_NONE && rt->trap.kind == BF_TRAP_NONE) {
     rt->trap.kind = f.kind;
     rt->trap.block = f.block;
@@ -861,7 +876,8 @@ int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double blo
   }
   rt->holding = (flags & BF_FLAG_HOLD_BLOCKS) != 0;
   if (cudaMalloc(&rt->fault_dev, sizeof(DevFault)) != cudaSuccess ||
-      cudaMemset(rt->fault_dev, 0, sizeof(DevFault)) != cudaSuccess) {
+      cudaMemset(rt->fault_dev, 0, sizeof(DevFault)) != cudaSuccess ||
+      cudaMallocHost(&rt->fault_host, sizeof(DevFault)) != cudaSuccess) {
     cudaGetLastError();
     return fail(BF_E_CUDA, "fault word allocation failed");
   }
@@ -876,8 +892,8 @@ int bf_shutdown(bf_runtime* rt) {
   rt->shut_down = true;
   set_device(rt->device);
   bf_queue_close(&rt->queue);
-  int rc = sync_workers(rt);
-  absorb_device_fault(rt);
+  int rc = sync_workers_fault(rt);
+  if (rc == BF_OK) absorb_device_fault(rt);
   return rc;
 }
 
@@ -890,6 +906,7 @@ int bf_runtime_destroy(bf_runtime* rt) {
   for (auto& kv : rt->tasks)
     if (kv.second.executed_dev) cudaFree(kv.second.executed_dev);
   if (rt->fault_dev) cudaFree(rt->fault_dev);
+  if (rt->fault_host) cudaFreeHost(rt->fault_host);
   bf_arena* a = rt->arena;
   a->live_runtimes--;
   if (a->live_runtimes == 0) {
@@ -1115,7 +1132,7 @@ int bf_synchronize(bf_runtime* rt, bf_fault* fault) {
   if (!rt) return fail(BF_E_INVALID, "null runtime");
   int rc = set_device(rt->device);
   if (rc) return rc;
-  rc = sync_workers(rt);
+  rc = sync_workers_fault(rt);
   if (rc) return rc;
   rt->syncs += 1;
   absorb_device_fault(rt);
