@@ -613,8 +613,14 @@ def test_kmeans_iterate_nccl_world1():
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
+        # 16 well-separated blobs (point p in blob p % 16): the loop converges
+        # in a few passes (uniform data needs hundreds, and the order of the
+        # f32 centroid-sum atomics makes that count vary run to run)
         npts, nf, k = 50000, 32, 16
-        fv = I.kmeans_inputs(npts, nf, seed=33)
+        g = np.random.default_rng(33)
+        centers = g.uniform(0.0, 1.0, (k, nf))
+        pts = centers[np.arange(npts) % k] + g.normal(0.0, 0.02, (npts, nf))
+        fv = np.ascontiguousarray(pts.T.astype(np.float32)).reshape(-1)  # feature-major
         arena = DeviceArena()
         hf, hc, hm = arena.alloc("f32", npts * nf), arena.alloc("f32", k * nf), arena.alloc("i32", npts)
         arena.upload_numpy(hf, fv)
@@ -622,7 +628,7 @@ def test_kmeans_iterate_nccl_world1():
         with Runtime(arena) as rt:
             passes, delta = kmeans_iterate(rt, arena, hf, hc, hm, npts, nf, k, max_iter=500, world=1, rank=0,
                                            allreduce=nccl_allreduce(arena, torch.device("cuda", 0)))
-        assert passes > 2 and delta == 0
+        assert passes >= 2 and delta == 0
         cent = arena.to_numpy(hc).astype(np.float64).reshape(k, nf)
         mem = arena.to_numpy(hm)
         f = fv.reshape(nf, npts).T.astype(np.float64)
