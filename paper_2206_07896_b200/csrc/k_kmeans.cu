@@ -1394,8 +1394,36 @@ __global__ void kmeans_centroids(float* cent, float* sums, int* counts, int nf, 
 __global__ void __launch_bounds__(256) kmeans_delta(const int* __restrict__ member, int* prev, long long lo,
                                                     long long hi, unsigned long long* delta) {
   const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned c = 0;
-  for (long long p = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += stride) {
+  // 16 B vectors over the 4-aligned middle (two in flight per thread), prev
+  // rewritten only where a membership changed; scalar head and tail
+  const long long a0 = (lo + 3) & ~3LL, a1 = hi & ~3LL;
+  if (a0 < a1) {
+    const int4* m4 = reinterpret_cast<const int4*>(member + a0);
+    int4* p4 = reinterpret_cast<int4*>(prev + a0);
+    const long long nv4 = (a1 - a0) / 4;
+    for (long long i = tid; i < nv4; i += 2 * stride) {
+      const bool two = i + stride < nv4;
+      const int4 m = __ldcs(m4 + i), q = p4[i];
+      int4 m2 = make_int4(0, 0, 0, 0), q2 = m2;
+      if (two) {
+        m2 = __ldcs(m4 + i + stride);
+        q2 = p4[i + stride];
+      }
+      const unsigned d = (m.x != q.x) + (m.y != q.y) + (m.z != q.z) + (m.w != q.w);
+      const unsigned d2 = (m2.x != q2.x) + (m2.y != q2.y) + (m2.z != q2.z) + (m2.w != q2.w);
+      if (d) p4[i] = m;
+      if (d2) p4[i + stride] = m2;
+      c += d + d2;
+    }
+  }
+  for (long long p = lo + tid; p < hi && p < a0; p += stride) {
+    const int m = member[p];
+    c += m != prev[p];
+    prev[p] = m;
+  }
+  for (long long p = (a1 > a0 ? a1 : a0) + tid; p < hi; p += stride) {
     const int m = member[p];
     c += m != prev[p];
     prev[p] = m;
@@ -1434,7 +1462,7 @@ extern "C" int bf_kmeans_update_impl(void* stream_v, int num_sms, float* cent, f
   kmeans_centroids<<<1, 512, 0, stream>>>(cent, sums, counts, nf, k);
   cudaMemsetAsync(d, 0, 8, stream);
   if (p_hi > p_lo) {
-    const int grid = stream_grid(p_hi - p_lo, 256 * 4, num_sms, 8);
+    const int grid = wave_grid(kmeans_delta, 256, 0, (p_hi - p_lo + 7) / 8, 256, num_sms, 8);
     kmeans_delta<<<grid, 256, 0, stream>>>(member, prev, p_lo, p_hi, d);
   }
   cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, stream);
