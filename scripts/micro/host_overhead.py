@@ -45,3 +45,29 @@ with Runtime(arena) as rt:
         rt.device_synchronize()
         return int(arena.to_numpy(chg)[0])
     t("full level (fill, launch, sync, read)", level)
+
+# vecadd PR1 launch costs: through Runtime.launch, and the bare C ABI call
+import ctypes as C
+from paper_2206_07896_b200 import _lib
+from paper_2206_07896_b200.runtime import pack_slots
+n = 1 << 20
+h = [arena.alloc("f32", n) for _ in range(3)]
+pk = PackedArgs([ArgSlot("handle", h[0]), ArgSlot("handle", h[1]), ArgSlot("handle", h[2]), ArgSlot("i32", n)])
+va = routines.get("vecadd")
+with Runtime(arena) as rt:
+    t("vecadd launch (Runtime.launch, no sync)", lambda: rt.launch(va, Dim3(4096), Dim3(256), 0, pk))
+    rt.device_synchronize()
+    slots, ns = pack_slots(pk)
+    g = (C.c_int32 * 3)(4096, 1, 1); b = (C.c_int32 * 3)(256, 1, 1); tid = C.c_uint64()
+    L = _lib.lib()
+    t("vecadd launch (bf_launch via ctypes)", lambda: L.bf_launch(rt._native, b"vecadd", g, b, 0, slots, ns, 32, 4096, C.byref(tid)))
+    rt.device_synchronize()
+    t("vecadd launch + sync", lambda: (rt.launch(va, Dim3(4096), Dim3(256), 0, pk), rt.device_synchronize()))
+    torch.cuda.synchronize()
+    s = torch.cuda.ExternalStream(rt.worker_stream(0))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for rep in range(3):
+        ev[0].record(s)
+        for _ in range(200): rt.launch(va, Dim3(4096), Dim3(256), 0, pk)
+        ev[1].record(s); rt.device_synchronize(); ev[1].synchronize()
+        print("200 back-to-back vecadd PR1 launches: device us per launch", ev[0].elapsed_time(ev[1]) * 1e3 / 200)
