@@ -378,12 +378,26 @@ __global__ void __launch_bounds__(256) hist_range(const int* __restrict__ pix, i
   const int4* p4 = reinterpret_cast<const int4*>(pix);
   const long long end = vhi / 4;
   long long g = vlo / 4 + tid;
-  for (; g + 3 * stride < end; g += 4 * stride) {
+  // software-pipelined: the next group's four 16 B loads are in flight while
+  // this group's 16 pixels update the counters (shared-memory RMW chains)
+  if (g + 3 * stride < end) {
     int4 v[4];
 #pragma unroll
     for (int u = 0; u < 4; u++) v[u] = __ldcs(p4 + g + u * stride);
+    for (;;) {
+      const bool more = g + 7 * stride < end;
+      int4 nx[4];
+      if (more) {
 #pragma unroll
-    for (int u = 0; u < 4; u++) hist_add4<MODE, POW2, SAFE>(sh, mine, counts, lc, v[u], fm, copies, bad);
+        for (int u = 0; u < 4; u++) nx[u] = __ldcs(p4 + g + (4 + u) * stride);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) hist_add4<MODE, POW2, SAFE>(sh, mine, counts, lc, v[u], fm, copies, bad);
+      g += 4 * stride;
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < 4; u++) v[u] = nx[u];
+    }
   }
   for (; g < end; g += stride) hist_add4<MODE, POW2, SAFE>(sh, mine, counts, lc, __ldcs(p4 + g), fm, copies, bad);
   if (bad) {

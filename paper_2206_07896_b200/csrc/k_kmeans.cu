@@ -471,7 +471,10 @@ __global__ void __launch_bounds__(256, MINB) kmeans_rb(const float* __restrict__
 // A fragments).  HBM is read exactly once.
 constexpr int kTcPts = 128;
 constexpr int kTcStride = kTcPts + 8;
-constexpr int kTcStages = 3;
+#ifndef KM_TC_STAGES
+#define KM_TC_STAGES 3
+#endif
+constexpr int kTcStages = KM_TC_STAGES;
 constexpr int kTcWarps = 4;
 #ifndef KM_TC_MINB
 #define KM_TC_MINB 3
