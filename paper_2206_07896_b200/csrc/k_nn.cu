@@ -88,13 +88,32 @@ __global__ void __launch_bounds__(256) nn_stream(const float* __restrict__ ll,
   float4* d4 = reinterpret_cast<float4*>(d);
   long long g = vlo / 4 + tid;
   const long long end = vhi / 4;
-  for (; g + stride < end; g += 2 * stride) {  // 4 x 16 B loads in flight
-    const float4 p0 = __ldcs(l4 + 2 * g), q0 = __ldcs(l4 + 2 * g + 1);
-    const float4 p1 = __ldcs(l4 + 2 * (g + stride)), q1 = __ldcs(l4 + 2 * (g + stride) + 1);
-    __stcs(d4 + g, make_float4(nn_dist<EMU>(p0.x, p0.y, x, y), nn_dist<EMU>(p0.z, p0.w, x, y),
-                               nn_dist<EMU>(q0.x, q0.y, x, y), nn_dist<EMU>(q0.z, q0.w, x, y)));
-    __stcs(d4 + g + stride, make_float4(nn_dist<EMU>(p1.x, p1.y, x, y), nn_dist<EMU>(p1.z, p1.w, x, y),
-                                        nn_dist<EMU>(q1.x, q1.y, x, y), nn_dist<EMU>(q1.z, q1.w, x, y)));
+  // 4 x 16 B loads per step, software-pipelined: the next step's loads are
+  // in flight while this step's eight f64 distances (DSQRT) are computed
+  if (g + stride < end) {
+    float4 p0 = __ldcs(l4 + 2 * g), q0 = __ldcs(l4 + 2 * g + 1);
+    float4 p1 = __ldcs(l4 + 2 * (g + stride)), q1 = __ldcs(l4 + 2 * (g + stride) + 1);
+    for (;;) {
+      const long long gn = g + 2 * stride;
+      const bool more = gn + stride < end;
+      float4 np0, nq0, np1, nq1;
+      if (more) {
+        np0 = __ldcs(l4 + 2 * gn);
+        nq0 = __ldcs(l4 + 2 * gn + 1);
+        np1 = __ldcs(l4 + 2 * (gn + stride));
+        nq1 = __ldcs(l4 + 2 * (gn + stride) + 1);
+      }
+      __stcs(d4 + g, make_float4(nn_dist<EMU>(p0.x, p0.y, x, y), nn_dist<EMU>(p0.z, p0.w, x, y),
+                                 nn_dist<EMU>(q0.x, q0.y, x, y), nn_dist<EMU>(q0.z, q0.w, x, y)));
+      __stcs(d4 + g + stride, make_float4(nn_dist<EMU>(p1.x, p1.y, x, y), nn_dist<EMU>(p1.z, p1.w, x, y),
+                                          nn_dist<EMU>(q1.x, q1.y, x, y), nn_dist<EMU>(q1.z, q1.w, x, y)));
+      g = gn;
+      if (!more) break;
+      p0 = np0;
+      q0 = nq0;
+      p1 = np1;
+      q1 = nq1;
+    }
   }
   if (g < end) {
     const float4 p = __ldcs(l4 + 2 * g), q = __ldcs(l4 + 2 * g + 1);
