@@ -740,3 +740,40 @@ print("ok")
     env = dict(os.environ, **switch)
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("switch", [{"BF_BFS_RELAX": "0"}, {"BF_BFS_RELAX": "2"}, {"BF_BFS_DEFER_DIV": "1"},
+                                    {"BF_BFS_DEFER_DIV": "1000000000"}])
+def test_bfs_level_variants_vs_oracle(switch):
+    """Per-level launch variants stay bit-exact on every level (levels and the
+    changed flag): the claiming relax (BF_BFS_RELAX=0), the RED relax without
+    deferred writes (2), the default with every level deferred to bfs_apply
+    (BF_BFS_DEFER_DIV=1) and with none deferred.  Subprocess: the switches
+    are read when the library loads."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    script = f"""
+import sys
+sys.path[:0] = [{root!r}, {root!r} + '/oracle', {root!r} + '/tests']
+import instances as I
+import oracle
+from gpu_helpers import bit_equal, gpu_run
+for nv, deg, seed in [(5000, 4, 1), (20000, 8, 2), (777, 1, 3), (3000, 13, 4), (100003, 6, 5)]:
+    lvl = None
+    for cur in range(200):
+        inst = I.bfs(nv, deg, cur=cur, seed=seed, block=256, lvl=lvl)
+        want, _ = oracle.run(inst)
+        got, trap, _, _ = gpu_run(inst)
+        assert trap is None
+        assert bit_equal(got["lvl"], want["lvl"]) and bit_equal(got["changed"], want["changed"]), (nv, cur)
+        lvl = want["lvl"]
+        if want["changed"][0] == 0:
+            break
+print("ok")
+"""
+    env = dict(os.environ, **switch)
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
