@@ -52,6 +52,11 @@ __global__ void __launch_bounds__(128) hotspot_band(const float* __restrict__ sr
                                                     float* __restrict__ dst, int rows, int cols,
                                                     int r_lo, int r_hi, int c_lo, int c_hi,
                                                     int groups, int bands, HsConst k) {
+  // programmatic dependent launch (hotspot_pdl): this grid may be scheduled
+  // while the previous kernel in the stream drains; wait for it (and its
+  // memory) before the first load, and let the next launch get scheduled
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (w >= groups * bands) return;  // warp-uniform
@@ -268,6 +273,35 @@ static HsBandFn hotspot_band_fn(int pf) {
   }
 }
 
+// BF_HOTSPOT_PDL (default 1): band launches carry the programmatic stream
+// serialization attribute, so a launch's CTAs are scheduled as the previous
+// launch's CTAs retire (launch latency hidden) and wait in-kernel for its
+// completion (griddepcontrol.wait) before reading.
+static bool hotspot_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BF_HOTSPOT_PDL");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+static void hotspot_band_launch(HsBandFn fn, int grid, cudaStream_t stream, const float* src, const float* power,
+                                float* dst, int rows, int cols, int r_lo, int r_hi, int c_lo, int c_hi, int groups,
+                                int bands, HsConst k) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = hotspot_pdl() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, fn, src, power, dst, rows, cols, r_lo, r_hi, c_lo, c_hi, groups, bands, k);
+}
+
 static int hotspot_resident_warps(int num_sms, int pf) {
   static int per_sm[5] = {0, 0, 0, 0, 0};
   if (per_sm[pf] == 0) {
@@ -320,8 +354,8 @@ int hotspot_step_full(cudaStream_t stream, int num_sms, const float* src, const 
     int bands = std::max(1, warps / groups);
     if (bands > rows) bands = rows;
     const int grid = (groups * bands + 3) / 4;
-    hotspot_band_fn(pf)<<<grid, 128, 0, stream>>>(src, power, dst, rows, cols, 0, rows, 0, cols,
-                                                  groups, bands, k);
+    hotspot_band_launch(hotspot_band_fn(pf), grid, stream, src, power, dst, rows, cols, 0, rows, 0, cols, groups,
+                        bands, k);
   } else {
     KDesc d{};
     int grid = stream_grid((long long)rows * cols, 256, num_sms, 8);
@@ -365,9 +399,8 @@ static int launch_hotspot(LaunchCtx& ctx) {
       int bands = std::max(1, warps / groups);
       if (bands > r_hi - r_lo) bands = (int)(r_hi - r_lo);
       const int grid = (groups * bands + 3) / 4;
-      hotspot_band_fn(pf)<<<grid, 128, 0, ctx.stream>>>((const float*)S.ptr, (const float*)P.ptr,
-                                                 (float*)D.ptr, rows, cols, (int)r_lo, (int)r_hi,
-                                                 (int)c_lo, (int)c_hi, groups, bands, k);
+      hotspot_band_launch(hotspot_band_fn(pf), grid, ctx.stream, (const float*)S.ptr, (const float*)P.ptr,
+                          (float*)D.ptr, rows, cols, (int)r_lo, (int)r_hi, (int)c_lo, (int)c_hi, groups, bands, k);
     } else {
       long long zb = zbase;
       if (zb + (rc.y0 * ctx.grid[0] + rc.x0) < ctx.first) zb += plane;
