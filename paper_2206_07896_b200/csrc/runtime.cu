@@ -369,7 +369,11 @@ static cudaEvent_t get_event(bf_runtime* rt) {
 static int retire(bf_runtime* rt, bool wait) {
   while (!rt->inflight.empty()) {
     FetchRecord& f = rt->inflight.front();
-    if (wait) {
+    if (!f.done) {
+      // untracked fetch (fetch events off): complete only once the workers
+      // were synchronized
+      if (!wait) return BF_OK;
+    } else if (wait) {
       cudaError_t e = cudaEventSynchronize(f.done);
       if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
     } else {
@@ -378,7 +382,7 @@ static int retire(bf_runtime* rt, bool wait) {
         // fetches on other workers may have finished; keep FIFO simple and
         // scan the rest without blocking
         for (auto it = rt->inflight.begin() + 1; it != rt->inflight.end();) {
-          if (cudaEventQuery(it->done) == cudaSuccess) {
+          if (it->done && cudaEventQuery(it->done) == cudaSuccess) {
             TaskRec& t = rt->tasks[it->task];
             t.completed += it->count;
             t.done_ranges.push_back({it->first, it->count});
@@ -400,7 +404,7 @@ static int retire(bf_runtime* rt, bool wait) {
     t.done_ranges.push_back({f.first, f.count});
     rt->blocks_executed += f.count;
     rt->busy[f.worker] += f.count;
-    rt->event_pool.push_back(f.done);
+    if (f.done) rt->event_pool.push_back(f.done);
     rt->inflight.pop_front();
   }
   return BF_OK;
@@ -976,8 +980,19 @@ static int issue_fetch(bf_runtime* rt, Fetch& f) {
   fr.worker = f.worker;
   fr.first = f.first;
   fr.count = f.count;
-  fr.done = get_event(rt);
-  CK(cudaEventRecord(fr.done, s));
+  // per-fetch completion events keep task.remaining live between
+  // synchronizations; BF_FETCH_EVENTS=0 drops them (no stream operation
+  // between consecutive kernels; tasks complete at the next synchronize)
+  static int fetch_events = -1;
+  if (fetch_events < 0) {
+    const char* e = getenv("BF_FETCH_EVENTS");
+    fetch_events = e ? atoi(e) : 1;
+  }
+  fr.done = nullptr;
+  if (fetch_events) {
+    fr.done = get_event(rt);
+    CK(cudaEventRecord(fr.done, s));
+  }
   rt->inflight.push_back(fr);
   return BF_OK;
 }
