@@ -42,7 +42,7 @@ L = ["# Round 1 profile summary (B200, sm_100a)", "",
      f"| roofline | {rf['kernel']} avg launch {rf['avg_launch_us']} us, {rf['achieved']} GB/s of {rf['peak']} measured = {rf['frac']} |",
      f"| DRAM traffic per launch (ncu) | {rf['traffic']} B (algorithmic 805,306,368) |",
      f"| e2e (pinned host buffers, H2D + 100 launches + D2H per step) | {e2e['value']} GB/s pipelined, {e2e.get('serial_value')} GB/s serial |",
-     f"| fused driver (bf_hotspot_run) | {bench.get('hotspot_fused', {}).get('value', bench.get('hotspot_fused'))} |",
+     f"| fused driver (bf_hotspot_run, register-wavefront temporal blocking) | {bench.get('hotspot_fused', {}).get('value', bench.get('hotspot_fused'))} GB/s algorithmic |",
      f"| CPU port (oracle.c, OpenMP, host cores) | {bench['cpu_baseline']['value']} {bench['cpu_baseline']['unit']} |",
      f"| clocks | {bench['clocks']} |", "",
      f"## Launch list shares (`profiles/r1_launches.csv`)", "",
