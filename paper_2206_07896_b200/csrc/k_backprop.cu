@@ -278,11 +278,7 @@ static int launch_bp_forward(LaunchCtx& ctx) {
     b1 = bad;
   }
   if (b0 >= b1) return BF_OK;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bp_forward, 256, 0);
-    per_sm = std::max(per_sm, 1);
-  }
+  const int per_sm = resident_ctas((const void*)bp_forward, 256, 0);
   const int grid = stream_grid(b1 - b0, kBpChunk, ctx.num_sms, per_sm);
   bp_forward<<<grid, 256, 0, ctx.stream>>>((const float*)In.ptr, (float*)W.ptr, (float*)P.ptr, b0, b1);
   BF_CUDA_LAUNCH_CHECK(ctx);
@@ -307,11 +303,7 @@ static int launch_bp_adjust(LaunchCtx& ctx) {
   }
   if (b0 >= b1) return BF_OK;
   const bool bias = b0 == 0;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bp_adjust, 256, 0);
-    per_sm = std::max(per_sm, 1);
-  }
+  const int per_sm = resident_ctas((const void*)bp_adjust, 256, 0);
   const int grid = stream_grid(b1 - b0, kBpChunkA, ctx.num_sms, per_sm);
   bp_adjust<<<grid, 256, 0, ctx.stream>>>((const float*)D.ptr, (const float*)L.ptr, (float*)W.ptr, (float*)O.ptr,
                                           b0, b1, bias);

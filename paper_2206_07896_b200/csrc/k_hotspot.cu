@@ -303,14 +303,7 @@ static void hotspot_band_launch(HsBandFn fn, int grid, cudaStream_t stream, cons
 }
 
 static int hotspot_resident_warps(int num_sms, int pf) {
-  static int per_sm[5] = {0, 0, 0, 0, 0};
-  if (per_sm[pf] == 0) {
-    int ctas = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, hotspot_band_fn(pf), 128, 0);
-    cudaGetLastError();
-    per_sm[pf] = ctas > 0 ? ctas * 4 : 16;
-  }
-  return per_sm[pf] * num_sms;
+  return resident_ctas((const void*)hotspot_band_fn(pf), 128, 0) * 4 * num_sms;
 }
 
 // Generic path: any geometry or alignment; one thread per cell of the cell

@@ -248,13 +248,7 @@ __global__ void __launch_bounds__(128) hotspot_wave(const float* __restrict__ sr
 template <int T>
 static int wave_pass(cudaStream_t stream, int num_sms, const float* a, const float* p, float* b,
                      int rows, int cols, const HsConstF& k) {
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    int ctas = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, hotspot_wave<T>, 128, 0);
-    cudaGetLastError();
-    per_sm = ctas > 0 ? ctas * 4 : 8;
-  }
+  const int per_sm = resident_ctas((const void*)hotspot_wave<T>, 128, 0) * 4;  // warps
   const int strips = (cols + kWaveOut - 1) / kWaveOut;
   int bands = std::max(1, per_sm * num_sms / strips);
   if (bands > rows) bands = rows;
