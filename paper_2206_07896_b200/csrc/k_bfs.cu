@@ -809,12 +809,27 @@ __global__ void __launch_bounds__(256) bfs_compact8s(unsigned* now, unsigned* pr
   const bool bytes = depth + 1 < 255;
   const unsigned lb = (unsigned)(depth + 1) * 0x01010101u;
   const long long stride = (long long)gridDim.x * blockDim.x;
+  // the next iteration's bitmap words are loaded one iteration ahead, and an
+  // iteration whose 256 words hold no new vertex (most of them on small
+  // levels) costs one barrier
+  unsigned cn = 0, cp = 0;
+  {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < words) {
+      cn = __ldcg(now + i);
+      cp = prev[i];
+    }
+  }
   for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < words; i0 += stride) {  // CTA-uniform
     const long long i = i0 + threadIdx.x;
-    unsigned fresh = 0;
+    const unsigned nw = cn, pw = cp;
+    if (i + stride < words) {
+      cn = __ldcg(now + i + stride);
+      cp = prev[i + stride];
+    }
+    unsigned fresh = i < words ? nw & ~pw : 0u;
+    if (!__syncthreads_or(fresh != 0)) continue;
     if (i < words) {
-      const unsigned nw = __ldcg(now + i);
-      fresh = nw & ~prev[i];
       if (fresh && !bytes) {  // levels beyond a byte: lvl written directly
         prev[i] = nw;
         for (unsigned f = fresh; f; f &= f - 1) lvl[i * 32 + __ffs(f) - 1] = depth + 1;
