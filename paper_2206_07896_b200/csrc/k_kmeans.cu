@@ -469,13 +469,16 @@ __global__ void __launch_bounds__(256, MINB) kmeans_rb(const float* __restrict__
 // ring guarded by full/empty mbarriers; four consumer warps (32 points each)
 // read their MMA fragments from the tile (row stride 136 floats: conflict-free
 // A fragments).  HBM is read exactly once.
-constexpr int kTcPts = 128;
+#ifndef KM_TC_WARPS
+#define KM_TC_WARPS 4  // consumer warps per CTA (32 points each); kmeans_umma needs 4 (M = 128)
+#endif
+constexpr int kTcPts = 32 * KM_TC_WARPS;
 constexpr int kTcStride = kTcPts + 8;
 #ifndef KM_TC_STAGES
 #define KM_TC_STAGES 3
 #endif
 constexpr int kTcStages = KM_TC_STAGES;
-constexpr int kTcWarps = 4;
+constexpr int kTcWarps = KM_TC_WARPS;
 #ifndef KM_TC_MINB
 #define KM_TC_MINB 3
 #endif
