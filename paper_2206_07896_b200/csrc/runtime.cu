@@ -298,6 +298,7 @@ struct FetchRecord {
   int worker;
   long long first, count;
   cudaEvent_t done;
+  bool owns = true;  // returns `done` to the pool when retired (lazy cover events are shared)
 };
 
 struct TaskRec {
@@ -365,8 +366,44 @@ static cudaEvent_t get_event(bf_runtime* rt) {
   return e;
 }
 
+static int fetch_event_mode() {
+  // BF_FETCH_EVENTS: 1 = an event after every fetch; 2 (default) = lazy: no
+  // stream operation between launches, a query covers every worker's
+  // untracked tail with one event (stream order: when it completes, so did
+  // every fetch before it), so task.remaining still falls without a
+  // synchronize; 0 = untracked until the next synchronize
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("BF_FETCH_EVENTS");
+    m = e ? atoi(e) : 2;
+  }
+  return m;
+}
+
+// lazy mode: one event per worker stream covers its fetches without one
+static void cover_untracked(bf_runtime* rt) {
+  for (size_t w = 0; w < rt->streams.size(); w++) {
+    FetchRecord* last = nullptr;
+    for (auto& f : rt->inflight)
+      if (f.worker == (int)w && !f.done) last = &f;
+    if (!last) continue;
+    cudaEvent_t ev = get_event(rt);
+    if (cudaEventRecord(ev, rt->streams[w]) != cudaSuccess) {
+      cudaGetLastError();
+      rt->event_pool.push_back(ev);
+      continue;
+    }
+    for (auto& f : rt->inflight)
+      if (f.worker == (int)w && !f.done) {
+        f.done = ev;
+        f.owns = &f == last;  // the stream's last covered fetch retires last
+      }
+  }
+}
+
 // Retire completed fetches (all of them when `wait`).
 static int retire(bf_runtime* rt, bool wait) {
+  if (!wait && fetch_event_mode() == 2) cover_untracked(rt);
   while (!rt->inflight.empty()) {
     FetchRecord& f = rt->inflight.front();
     if (!f.done) {
@@ -388,7 +425,7 @@ static int retire(bf_runtime* rt, bool wait) {
             t.done_ranges.push_back({it->first, it->count});
             rt->blocks_executed += it->count;
             rt->busy[it->worker] += it->count;
-            rt->event_pool.push_back(it->done);
+            if (it->owns) rt->event_pool.push_back(it->done);
             it = rt->inflight.erase(it);
           } else {
             cudaGetLastError();
@@ -404,7 +441,7 @@ static int retire(bf_runtime* rt, bool wait) {
     t.done_ranges.push_back({f.first, f.count});
     rt->blocks_executed += f.count;
     rt->busy[f.worker] += f.count;
-    if (f.done) rt->event_pool.push_back(f.done);
+    if (f.done && f.owns) rt->event_pool.push_back(f.done);
     rt->inflight.pop_front();
   }
   return BF_OK;
@@ -980,16 +1017,10 @@ static int issue_fetch(bf_runtime* rt, Fetch& f) {
   fr.worker = f.worker;
   fr.first = f.first;
   fr.count = f.count;
-  // per-fetch completion events keep task.remaining live between
-  // synchronizations; BF_FETCH_EVENTS=0 drops them (no stream operation
-  // between consecutive kernels; tasks complete at the next synchronize)
-  static int fetch_events = -1;
-  if (fetch_events < 0) {
-    const char* e = getenv("BF_FETCH_EVENTS");
-    fetch_events = e ? atoi(e) : 1;
-  }
+  // completion tracking (fetch_event_mode): an event after the fetch only in
+  // mode 1; by default a query covers the untracked tail lazily
   fr.done = nullptr;
-  if (fetch_events) {
+  if (fetch_event_mode() == 1) {
     fr.done = get_event(rt);
     CK(cudaEventRecord(fr.done, s));
   }

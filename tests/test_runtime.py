@@ -228,6 +228,26 @@ def test_launch_does_not_wait_for_workers(need_gpu):  # test_runtime.py:167-178
 
 
 @gpu
+def test_remaining_falls_without_synchronize(need_gpu):
+    """task.remaining reaches 0 by polling alone (no device_synchronize), as a
+    host spinning on the reference's counters would: completion is tracked
+    lazily by an event that covers every fetch issued before the query."""
+    import time
+    inst = I.vecadd(random.Random(12))
+    arena = DeviceArena()
+    packed, handles = materialize(inst, arena)
+    with Runtime(arena, pool_size=2) as rt:
+        tasks = [rt.launch(routines.get("vecadd"), Dim3(inst.grid.x), Dim3(inst.block.x), 0, packed)
+                 for _ in range(5)]
+        deadline = time.time() + 30
+        while any(t.remaining for t in tasks) and time.time() < deadline:
+            time.sleep(0.001)
+        assert [t.remaining for t in tasks] == [0] * 5
+        assert rt.unfinished_tasks() == []
+        assert rt.counters.blocks_executed == 5 * inst.grid.total
+
+
+@gpu
 def test_hold_new_blocks_rearms_the_gate(need_gpu):
     inst = I.vecadd(random.Random(11))
     arena = DeviceArena()
