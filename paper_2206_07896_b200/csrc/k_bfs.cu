@@ -1048,12 +1048,26 @@ __global__ void __launch_bounds__(256) bfs_compact_sh(unsigned* now, unsigned* p
       own = fresh & m;
     }
     int pos = cta_append(__popc(own), sizes + 1, sizes + 3, __popc(fresh));
+    if (fresh && bytes) {  // the word's 32 level bytes: one merged 32 B sector store
+      const unsigned lb = (unsigned)(depth + 1) * 0x01010101u;
+      uint4* p = reinterpret_cast<uint4*>(lv8 + i * 32);
+      uint4 a = p[0], c = p[1];
+      a.x = lv8_merge(a.x, fresh, 0, lb);
+      a.y = lv8_merge(a.y, fresh, 4, lb);
+      a.z = lv8_merge(a.z, fresh, 8, lb);
+      a.w = lv8_merge(a.w, fresh, 12, lb);
+      c.x = lv8_merge(c.x, fresh, 16, lb);
+      c.y = lv8_merge(c.y, fresh, 20, lb);
+      c.z = lv8_merge(c.z, fresh, 24, lb);
+      c.w = lv8_merge(c.w, fresh, 28, lb);
+      p[0] = a;
+      p[1] = c;
+    }
     while (fresh) {
       const int b = __ffs(fresh) - 1;
       const int v = (int)(i * 32 + b);
       if (own >> b & 1) nq[pos++] = v;
-      if (bytes) lv8[v] = (unsigned char)(depth + 1);
-      else lvl[v] = depth + 1;
+      if (!bytes) lvl[v] = depth + 1;
       fresh &= fresh - 1;
     }
   }
@@ -1559,7 +1573,7 @@ extern "C" int bf_bfs_shard_create_impl(int nv, void** out, char* err, int errca
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->prev, s->words * 4);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->qa, (size_t)nv * 4);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->qb, (size_t)nv * 4);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&s->lv8, (size_t)nv + 16);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->lv8, (size_t)s->words * 32 + 16);  // whole sectors
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->sizes, 16);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&s->hs, 16);
   if (e != cudaSuccess) {
