@@ -68,7 +68,12 @@ struct BfJitGeom {
 };
 struct BfJitArgs { long long w[%(nw)d]; };
 
-__device__ __forceinline__ void bf_trap(const BfJitGeom& G, int kind, long long blk) {
+// a trap records the first fault and stops the trapping thread's side
+// effects (stores, atomics, loops): the reference aborts the block at the
+// raise (runtime.py:335-343); the CTA leaves its block loop at the next
+// block boundary (__syncthreads_or of the flags)
+__device__ __forceinline__ void bf_trap(const BfJitGeom& G, int kind, long long blk, bool& t) {
+  t = true;
   if (atomicCAS(G.fault, 0, kind) == 0) {
     *reinterpret_cast<long long*>(G.fault + 2) = blk;
     *reinterpret_cast<unsigned long long*>(G.fault + 4) = G.task;
@@ -86,25 +91,25 @@ __device__ __forceinline__ long long bf_neg64(long long a) { return (long long)(
 
 HELPERS = r"""
 #define BF_DIV_INT(T, NEG)                                                        \
-  __device__ __forceinline__ T bf_div_##T(T a, T b, const BfJitGeom& G, long long blk) { \
-    if (b == 0) { bf_trap(G, 2, blk); return 0; }                                 \
+  __device__ __forceinline__ T bf_div_##T(T a, T b, const BfJitGeom& G, long long blk, bool& t) { \
+    if (b == 0) { bf_trap(G, 2, blk, t); return 0; }                                 \
     if (b == -1) return NEG(a);                                                   \
     return a / b;                                                                 \
   }                                                                               \
-  __device__ __forceinline__ T bf_mod_##T(T a, T b, const BfJitGeom& G, long long blk) { \
-    if (b == 0) { bf_trap(G, 2, blk); return 0; }                                 \
+  __device__ __forceinline__ T bf_mod_##T(T a, T b, const BfJitGeom& G, long long blk, bool& t) { \
+    if (b == 0) { bf_trap(G, 2, blk, t); return 0; }                                 \
     if (b == -1) return 0;                                                        \
     return a % b;                                                                 \
   }
 typedef long long ll;
 BF_DIV_INT(int, bf_neg32)
 BF_DIV_INT(ll, bf_neg64)
-__device__ __forceinline__ double bf_fdiv(double a, double b, const BfJitGeom& G, long long blk) {
-  if (b == 0.0) { bf_trap(G, 2, blk); return 0.0; }
+__device__ __forceinline__ double bf_fdiv(double a, double b, const BfJitGeom& G, long long blk, bool& t) {
+  if (b == 0.0) { bf_trap(G, 2, blk, t); return 0.0; }
   return a / b;
 }
-__device__ __forceinline__ double bf_sqrt(double a, const BfJitGeom& G, long long blk) {
-  if (a < 0.0) { bf_trap(G, 3, blk); return 0.0; }
+__device__ __forceinline__ double bf_sqrt(double a, const BfJitGeom& G, long long blk, bool& t) {
+  if (a < 0.0) { bf_trap(G, 3, blk, t); return 0.0; }
   return sqrt(a);
 }
 __device__ __forceinline__ int bf_abs32(int a) { return a < 0 ? bf_neg32(a) : a; }
@@ -202,7 +207,7 @@ class _Gen:
             t = self.new_tmp()
             out.append(f"long long {t}_i = (long long)({idx});")
             out.append(f"{_CTYPE[ety]} {t} = 0;")
-            out.append(f"if ({t}_i < 0 || {t}_i >= (long long)({ln})) bf_trap(G, 1, blk); "
+            out.append(f"if ({t}_i < 0 || {t}_i >= (long long)({ln})) bf_trap(G, 1, blk, bf_t); "
                        f"else {t} = ({_CTYPE[ety]}){ptr}[{t}_i];")
             return t, ety
         if k == "Binary":
@@ -239,7 +244,7 @@ class _Gen:
                     return f"bf_abs64({a})", ty
                 return f"fabs({a})", ty
             if e.func == "sqrt":
-                return f"bf_sqrt((double)({args[0][0]}), G, blk)", ty if ty in ("f32", "f64") else "f64"
+                return f"bf_sqrt((double)({args[0][0]}), G, blk, bf_t)", ty if ty in ("f32", "f64") else "f64"
             raise CodegenError(f"unknown intrinsic {e.func!r}")
         raise CodegenError(f"unknown expression node {k}")
 
@@ -270,16 +275,16 @@ class _Gen:
             if op == "*":
                 return f"bf_mul{w}({lv}, {rv})", ty
             if op == "/":
-                return f"bf_div_{c}({lv}, {rv}, G, blk)", ty
+                return f"bf_div_{c}({lv}, {rv}, G, blk, bf_t)", ty
             if op == "%":
-                return f"bf_mod_{c}({lv}, {rv}, G, blk)", ty
+                return f"bf_mod_{c}({lv}, {rv}, G, blk, bf_t)", ty
         else:
             if op in ("+", "-", "*"):
                 return f"((double)({lv}) {op} (double)({rv}))", ty
             if op == "/":
-                return f"bf_fdiv((double)({lv}), (double)({rv}), G, blk)", ty
+                return f"bf_fdiv((double)({lv}), (double)({rv}), G, blk, bf_t)", ty
             if op == "%":
-                out.append("bf_trap(G, 3, blk);")
+                out.append("bf_trap(G, 3, blk, bf_t);")
                 return "0.0", ty
         raise CodegenError(f"unknown operator {op!r}")
 
@@ -386,7 +391,7 @@ class _Gen:
         subst: dict = {}
         if self.warp_mode and k in ("LocalDecl", "Assign", "AtomicStmt") and self.has_warp(s):
             if in_if:  # interp.py:325-327
-                lines.append(f"{ind}bf_trap(G, 4, blk);")
+                lines.append(f"{ind}bf_trap(G, 4, blk, bf_t);")
                 return
             subst = self.lockstep(s, lines, subst, ind)
         out: list = []
@@ -408,7 +413,7 @@ class _Gen:
                 lines.extend(ind + x for x in out)
                 t = self.new_tmp()
                 lines.append(f"{ind}{{ long long {t} = (long long)({idx}); "
-                             f"if ({t} < 0 || {t} >= (long long)({ln})) bf_trap(G, 1, blk); "
+                             f"if ({t} < 0 || {t} >= (long long)({ln})) bf_trap(G, 1, blk, bf_t); "
                              f"else {ptr}[{t}] = ({_MTYPE[ety]})({self.coerce(v, ty, ety)}); }}")
         elif k == "If":
             c, _ = self.expr(s.cond, out, subst)
@@ -427,7 +432,7 @@ class _Gen:
             hout: list = []
             hi, hty = self.expr(s.hi, hout, {})
             lines.extend(ind + "  " + x for x in hout)
-            lines.append(f"{ind}  if (!(v_{s.var} < ({hi}))) break;")
+            lines.append(f"{ind}  if (!(v_{s.var} < ({hi})) || bf_t) break;")
             self.stmts(s.body, lines, ind + "  ", in_if)
             sout: list = []
             st, sty = self.expr(s.step, sout, {})
@@ -437,7 +442,7 @@ class _Gen:
         elif k == "AtomicStmt":
             space, ety, ptr, ln = self.arrays[s.target.name]
             if s.target.index is None:
-                lines.append(f"{ind}bf_trap(G, 3, blk);")
+                lines.append(f"{ind}bf_trap(G, 3, blk, bf_t);")
                 return
             idx, _ = self.expr(s.target.index, out, subst)
             opv, oty = self.expr(s.operand, out, subst)
@@ -447,7 +452,7 @@ class _Gen:
             lines.extend(ind + x for x in out)
             t = self.new_tmp()
             lines.append(f"{ind}{{ long long {t} = (long long)({idx});")
-            lines.append(f"{ind}  if ({t} < 0 || {t} >= (long long)({ln})) bf_trap(G, 1, blk); else {{")
+            lines.append(f"{ind}  if ({t} < 0 || {t} >= (long long)({ln})) bf_trap(G, 1, blk, bf_t); else if (!bf_t) {{")
             a = f"&{ptr}[{t}]"
             if s.kind == "add":
                 if ety == "i32":
@@ -503,7 +508,7 @@ class _Gen:
                 st, sty = self.expr(sec.step, sout, {})
                 body.extend(ind + "  " + x for x in sout)
                 body.append(f"{ind}  v_{sec.var} = bf_add32(v_{sec.var}, {self.coerce(st, sty, 'i32')});")
-                body.append(f"{ind}  __syncthreads();")
+                body.append(f"{ind}  if (__syncthreads_or(bf_t)) break;")
                 body.append(f"{ind}}}")
             if si in getattr(self.mk, "barrier_boundaries", set()):
                 body.append(f"{ind}__syncthreads();")
@@ -548,6 +553,7 @@ class _Gen:
         src.append("  const int wcount = (B - wbase) < ws ? (B - wbase) : ws;")
         src.append("  const long long wlim = wcount;")
         src.append("  (void)wlane; (void)wlim; (void)B;")
+        src.append("  bool bf_t = false;  // this thread trapped")
         src.append("  for (long long blk = G.first + blockIdx.x; blk < G.first + G.count; blk += gridDim.x) {")
         src.append("    const int blockIdx_x = (int)(blk % G.gx), blockIdx_y = (int)((blk / G.gx) % G.gy), "
                    "blockIdx_z = (int)(blk / ((long long)G.gx * G.gy));")
@@ -561,7 +567,7 @@ class _Gen:
             src.append(f"    v_{name} = 0;")
         src.append("    __syncthreads();")
         src.extend(body)
-        src.append("    __syncthreads();")
+        src.append("    if (__syncthreads_or(bf_t)) break;")
         src.append("  }")
         src.append("}")
         return "\n".join(src) + "\n"

@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <deque>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -127,6 +129,28 @@ inline int wave_grid(F fn, int threads, size_t smem, long long work_items, int i
   const int r = resident_ctas((const void*)fn, threads, smem);
   return stream_grid(work_items, items_per_cta, num_sms, r < ctas_per_sm ? r : ctas_per_sm);
 }
+
+// Per-stream device scratch.  Kernels that keep scratch across the launches
+// of one fetch (the bfs level step, the fused traversal) key it by the
+// stream the fetch runs on, so concurrent fetches on different worker
+// streams (pool_size > 1) or runtimes never share it; growing it only has
+// to order against that stream.  The runtime releases a stream's scratch
+// when it destroys the stream (bf_runtime_destroy).
+struct StreamScratch {
+  virtual ~StreamScratch() {}
+};
+std::mutex& stream_scratch_mutex();
+std::unique_ptr<StreamScratch>& stream_scratch_slot(cudaStream_t s, int kind);
+void release_stream_scratch(cudaStream_t s);
+
+template <class T>
+T& scratch_for(cudaStream_t s, int kind) {
+  std::lock_guard<std::mutex> lk(stream_scratch_mutex());
+  std::unique_ptr<StreamScratch>& slot = stream_scratch_slot(s, kind);
+  if (!slot) slot.reset(new T());
+  return *static_cast<T*>(slot.get());
+}
+enum { SCRATCH_BFS_STEP = 1, SCRATCH_BFS_LEVELS = 2, SCRATCH_NN_TOPK = 3 };
 
 // full-grid hotspot step with the streaming band kernel (k_hotspot.cu)
 int hotspot_step_full(cudaStream_t stream, int num_sms, const float* src, const float* power,

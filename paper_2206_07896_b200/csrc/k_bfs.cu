@@ -468,29 +468,34 @@ __global__ void __launch_bounds__(256) bfs_apply(const unsigned* __restrict__ un
   }
 }
 
-// per-device scratch of the two-phase step (grow-only)
-struct BfsStepScratch {
+// per-stream scratch of the two-phase step (grow-only)
+struct BfsStepScratch : StreamScratch {
   long long cap_words = 0, cap_q = 0;
   unsigned* unv = nullptr;
   unsigned* unv0 = nullptr;  // unvisited set at the launch start (deferred lvl writes)
   int* q = nullptr;
   int* qn = nullptr;
+  void release() {
+    cudaFree(unv);
+    cudaFree(unv0);
+    cudaFree(q);
+    cudaFree(qn);
+    unv = unv0 = nullptr;
+    q = qn = nullptr;
+    cap_words = cap_q = 0;
+  }
+  ~BfsStepScratch() override { release(); }
 };
 
 static int launch_bfs_two_phase(LaunchCtx& ctx, const ArgVal& R, const ArgVal& Co, const ArgVal& L,
                                 const ArgVal& Ch, long long lo, long long hi, int cur, long long bx) {
-  static BfsStepScratch sc[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  BfsStepScratch& S = sc[dev & 63];
+  // keyed by the fetch's stream: fetches on other worker streams may run
+  // concurrently and have their own; growing orders against this stream only
+  BfsStepScratch& S = scratch_for<BfsStepScratch>(ctx.stream, SCRATCH_BFS_STEP);
   const long long ll = L.len, words = (ll + 31) / 32, nq = hi - lo;
   if (S.cap_words < words || S.cap_q < nq || !S.qn) {
     cudaStreamSynchronize(ctx.stream);
-    cudaFree(S.unv);
-    cudaFree(S.unv0);
-    cudaFree(S.q);
-    cudaFree(S.qn);
-    S = BfsStepScratch();
+    S.release();
     if (cudaMalloc((void**)&S.unv, words * 4) != cudaSuccess || cudaMalloc((void**)&S.unv0, words * 4) != cudaSuccess ||
         cudaMalloc((void**)&S.q, nq * 4) != cudaSuccess ||
         cudaMalloc((void**)&S.qn, 4) != cudaSuccess) {
@@ -1287,7 +1292,8 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   const long long words = ((long long)nv + 31) / 32;
   // scratch (bitmaps, two frontier queues, counters) is kept per device and
   // only grows: a traversal does no allocation after the first
-  struct Scratch {
+  struct Scratch : StreamScratch {
+    std::mutex busy;  // a traversal is a synchronous host loop: one caller at a time per stream
     long long cap_words = 0, cap_v = 0;
     unsigned *now = nullptr, *prev = nullptr;
     int *qa = nullptr, *qb = nullptr, *sizes = nullptr, *hs = nullptr;
@@ -1301,11 +1307,26 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
     int* ctr = nullptr;
     int *hist = nullptr, *hist_d = nullptr;
     cudaEvent_t evx[4] = {};
+    ~Scratch() override {
+      cudaFree(now);
+      cudaFree(prev);
+      cudaFree(qa);
+      cudaFree(qb);
+      cudaFree(lv8);
+      cudaFree(sizes);
+      cudaFree(counts);
+      cudaFree(offsets);
+      cudaFree(cursors);
+      cudaFree(buckets);
+      cudaFree(ctr);
+      if (hs) cudaFreeHost(hs);
+      if (hist) cudaFreeHost(hist);
+      for (auto& e : evx)
+        if (e) cudaEventDestroy(e);
+    }
   };
-  static Scratch sc[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  Scratch& S = sc[dev & 63];
+  Scratch& S = scratch_for<Scratch>(stream, SCRATCH_BFS_LEVELS);
+  std::lock_guard<std::mutex> busy(S.busy);
   cudaError_t e = cudaSuccess;
   if (S.cap_v < nv) {
     cudaStreamSynchronize(stream);

@@ -35,6 +35,34 @@
 
 // ---- occupancy cache ----------------------------------------------------------
 namespace bf {
+static std::map<std::pair<cudaStream_t, int>, std::unique_ptr<StreamScratch>>& scratch_map() {
+  static std::map<std::pair<cudaStream_t, int>, std::unique_ptr<StreamScratch>> m;
+  return m;
+}
+std::mutex& stream_scratch_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+std::unique_ptr<StreamScratch>& stream_scratch_slot(cudaStream_t s, int kind) {
+  return scratch_map()[std::make_pair(s, kind)];
+}
+void release_stream_scratch(cudaStream_t s) {
+  std::vector<std::unique_ptr<StreamScratch>> dead;
+  {
+    std::lock_guard<std::mutex> lk(stream_scratch_mutex());
+    auto& m = scratch_map();
+    for (auto it = m.begin(); it != m.end();) {
+      if (it->first.first == s) {
+        dead.push_back(std::move(it->second));
+        it = m.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  dead.clear();  // destructors free the device memory outside the lock
+}
+
 int resident_ctas(const void* fn, int threads, size_t smem) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, size_t>, int> cache;
@@ -297,8 +325,7 @@ struct FetchRecord {
   uint64_t task;
   int worker;
   long long first, count;
-  cudaEvent_t done;
-  bool owns = true;  // returns `done` to the pool when retired (lazy cover events are shared)
+  cudaEvent_t done;  // shared by the fetches a lazy cover event covers (event_refs)
 };
 
 struct TaskRec {
@@ -345,6 +372,7 @@ struct bf_runtime {
   std::deque<bf::FetchRecord> inflight;
   std::deque<bf::Fetch> deferred;  // held launches (hold_blocks)
   std::vector<cudaEvent_t> event_pool;
+  std::map<cudaEvent_t, int> event_refs;  // fetch records still pointing at each in-use event
   uint64_t next_task = 1;
   uint64_t rr = 0;               // round-robin worker cursor
   // counters
@@ -380,6 +408,17 @@ static int fetch_event_mode() {
   return m;
 }
 
+// A fetch record retires: its event returns to the pool when no other
+// record still points at it (a lazy cover event is shared by every fetch it
+// covers, and they may retire out of order across workers).
+static void drop_event_ref(bf_runtime* rt, cudaEvent_t ev) {
+  auto it = rt->event_refs.find(ev);
+  if (it == rt->event_refs.end() || --it->second <= 0) {
+    if (it != rt->event_refs.end()) rt->event_refs.erase(it);
+    rt->event_pool.push_back(ev);
+  }
+}
+
 // lazy mode: one event per worker stream covers its fetches without one
 static void cover_untracked(bf_runtime* rt) {
   for (size_t w = 0; w < rt->streams.size(); w++) {
@@ -393,11 +432,13 @@ static void cover_untracked(bf_runtime* rt) {
       rt->event_pool.push_back(ev);
       continue;
     }
+    int n = 0;
     for (auto& f : rt->inflight)
       if (f.worker == (int)w && !f.done) {
         f.done = ev;
-        f.owns = &f == last;  // the stream's last covered fetch retires last
+        n++;
       }
+    rt->event_refs[ev] = n;  // back to the pool once the last of them retires
   }
 }
 
@@ -425,7 +466,7 @@ static int retire(bf_runtime* rt, bool wait) {
             t.done_ranges.push_back({it->first, it->count});
             rt->blocks_executed += it->count;
             rt->busy[it->worker] += it->count;
-            if (it->owns) rt->event_pool.push_back(it->done);
+            drop_event_ref(rt, it->done);
             it = rt->inflight.erase(it);
           } else {
             cudaGetLastError();
@@ -441,7 +482,7 @@ static int retire(bf_runtime* rt, bool wait) {
     t.done_ranges.push_back({f.first, f.count});
     rt->blocks_executed += f.count;
     rt->busy[f.worker] += f.count;
-    if (f.done && f.owns) rt->event_pool.push_back(f.done);
+    if (f.done) drop_event_ref(rt, f.done);
     rt->inflight.pop_front();
   }
   return BF_OK;
@@ -942,7 +983,10 @@ int bf_runtime_destroy(bf_runtime* rt) {
   if (!rt) return BF_OK;
   bf_shutdown(rt);
   set_device(rt->device);
-  for (auto s : rt->streams) cudaStreamDestroy(s);
+  for (auto s : rt->streams) {
+    release_stream_scratch(s);
+    cudaStreamDestroy(s);
+  }
   for (auto e : rt->event_pool) cudaEventDestroy(e);
   for (auto& kv : rt->tasks)
     if (kv.second.executed_dev) cudaFree(kv.second.executed_dev);

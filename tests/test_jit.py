@@ -176,6 +176,15 @@ EXECUTOR_CASES = [
      (3,), (64,), [("i32", list(range(192))), ("i32", [0] * 9)], [], False, 32, 0),
     ("f32_atomics", "kernel fa(s: global f32[], x: global f32[]) {\n  atomic_add(s[threadIdx.x % 2], x[threadIdx.x]);\n}\n",
      (1,), (1,), [("f32", [0.0, 0.0]), ("f32", [0.1])], [], False, 32, 0),
+    # a trapping loop step (0 after the trap) must end the loop, not hang:
+    # the reference raises DivByZero at the first step
+    ("trap_step_loop", "kernel k(a: global i32[], n: i32, d: i32) {\n"
+     "  for (i = 0; i < n; i += n / d) { a[0] = a[0] + 1; }\n}\n",
+     (1,), (4,), [("i32", [0])], [("i32", 10), ("i32", 0)], False, 32, 0),
+    # the same inside a barrier loop (a LoopSection)
+    ("trap_step_barrier_loop", "kernel k(a: global i32[], n: i32, d: i32) {\n  shared i32 s[4];\n"
+     "  for (i = 0; i < n; i += n / d) { s[threadIdx.x] = i; barrier; a[threadIdx.x] = s[0]; barrier; }\n}\n",
+     (2,), (4,), [("i32", [0] * 4)], [("i32", 10), ("i32", 0)], False, 32, 0),
 ]
 
 
