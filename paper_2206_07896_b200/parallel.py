@@ -58,6 +58,12 @@ class HotspotBands:
 
     def __post_init__(self):
         self.own = rank_range(self.rows, self.world, self.rank)
+        last = rank_range(self.rows, self.world, self.world - 1)
+        if last[0] >= last[1]:
+            # a rank without rows would leave its neighbours' halo sends
+            # unmatched (the exchange would hang)
+            raise ValueError(f"{self.rows} rows cannot give each of {self.world} ranks a band "
+                             f"(ceil(rows / world) = {average_grain(self.rows, self.world)})")
         if self.world > 1:
             if self.halo < 1:
                 raise ValueError("multi-rank hotspot needs halo >= 1")

@@ -104,7 +104,9 @@ def pack_slots(packed) -> tuple[C.Array, int]:
     same arguments (hotspot's ping-pong, the BFS level loop)."""
     slots = packed.slots if packed is not None else ()
     try:
-        sig = tuple([(s.kind, s.value) for s in slots])
+        # floats by bit pattern: 0.0 == -0.0 in Python, but they pack (and
+        # compute) differently
+        sig = tuple([(s.kind, s.value.hex() if s.value.__class__ is float else s.value) for s in slots])
     except AttributeError:
         sig = None
     cached = getattr(packed, "_bf_packed", None) if sig is not None else None

@@ -108,6 +108,8 @@ def test_band_validation():
         HotspotBands(16, 16, 2, 0, halo=0)
     with pytest.raises(ValueError):
         HotspotBands(16, 16, 4, 0, halo=8)  # bands of 4 rows < halo
+    with pytest.raises(ValueError):
+        HotspotBands(9, 16, 4, 0, halo=1)  # ceil(9/4) = 3: rank 3 would own no rows
     b = HotspotBands(100, 8, 4, 1, halo=5)
     assert b.own == (25, 50) and b.local_rows == (20, 55) and b.up == 0 and b.down == 2
 

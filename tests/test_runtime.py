@@ -427,3 +427,17 @@ def test_arena_surface(need_gpu):  # arena.py:75-152
     assert a.alloc("i32", 0) == 4  # never reused
     with pytest.raises(ValueError):
         a.alloc("i32", -1)
+
+
+def test_packed_cache_distinguishes_negative_zero():
+    """the packed-slot cache must not reuse 0.0's packing for -0.0."""
+    import struct
+
+    from paper_2206_07896_b200 import ArgSlot, PackedArgs
+    from paper_2206_07896_b200.runtime import pack_slots
+    pk = PackedArgs([ArgSlot("f32", 0.0)])
+    arr, n = pack_slots(pk)
+    assert bytes(arr)[8:16] == struct.pack("<d", 0.0)
+    pk.slots[0] = ArgSlot("f32", -0.0)
+    arr, n = pack_slots(pk)
+    assert bytes(arr)[8:16] == struct.pack("<d", -0.0)
