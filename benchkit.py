@@ -93,6 +93,20 @@ def build_cases(arena, torch, device, scale: int = 28) -> list:
     cases.append(Case("nn", "nn_stream", 12 * n, n, "record",
                       [(routines.get("nn"), Dim3(n // 256), Dim3(256), 0, pk)], check=nn_check))
 
+    # --- nn top-k indices: the 5 nearest of the 2^28 distances --------------
+    tk = 5
+    ti, tdist = alloc("i32", tk), alloc("f32", tk)
+    pk = PackedArgs([ArgSlot("handle", d), ArgSlot("handle", ti), ArgSlot("handle", tdist),
+                     ArgSlot("i32", n), ArgSlot("i32", tk)])
+
+    def topk_check():
+        order = torch.sort(td, stable=True).indices[:tk]
+        return bool(torch.equal(_t(arena, ti, torch, device).long(), order))
+    cases.append(Case("nn_topk", "nn_topk_pass", 4 * n, n, "record",
+                      [(routines.get("nn_topk"), Dim3(1), Dim3(1), 0, pk)], check=topk_check,
+                      note="Rodinia nn's k-nearest selection (k=5) over the nn case's 2^28 distances; "
+                           "4 B per record; indices checked against a stable sort"))
+
     # --- hist, 2^28 pixels, 16 bins -----------------------------------------
     pix = alloc("i32", n)
     cnt = alloc("i32", 16)

@@ -193,6 +193,7 @@ def northstar_sets() -> None:
     pack(hs, GOLDEN / "hotspot.npz")
     nn = [I.nn(1000, 128, seed=1), I.nn(777, 64, seed=2, target=(-12.25, 170.5)), I.nn(0, 32, seed=3)]
     pack(nn, GOLDEN / "nn.npz")
+    pack(topk_set(), GOLDEN / "nn_topk.npz")
     km = [I.kmeans(700, 8, 5, 128, seed=1), I.kmeans(300, 32, 16, 64, seed=2),
           I.kmeans(257, 4, 3, 32, seed=3, dup=True)]
     pack(km, GOLDEN / "kmeans.npz")
@@ -209,6 +210,26 @@ def northstar_sets() -> None:
         if outs["changed"][0] == 0:
             break
     pack(bf, GOLDEN / "bfs.npz")
+
+
+def topk_set() -> list:
+    """nn_topk (Rodinia nn's k-nearest selection): ties, NaN/inf/signed
+    zeros, k beyond n, n = 0, distances from an nn launch, multi-block and
+    multi-thread geometries (only blockIdx.x == 0 / threadIdx.x == 0 act),
+    and out-of-range traps."""
+    out = [I.nn_topk(500, 5, seed=1), I.nn_topk(400, 16, seed=2, special=True),
+           I.nn_topk(40, 32, seed=3, special=True), I.nn_topk(7, 12, seed=4),
+           I.nn_topk(0, 3, seed=5), I.nn_topk(300, 1, seed=6, special=True),
+           I.nn_topk(200, 8, seed=7, grid=(3, 2), block=(4, 2))]
+    nn = I.nn(1000, 128, seed=1)
+    outs, _ = run_ref(nn)
+    out.append(I.nn_topk(1000, 10, d=outs["d"]))
+    out.append(I.nn_topk(100, 6, seed=8, idx_len=4))     # idx too short: OutOfBounds
+    out.append(I.nn_topk(100, 6, seed=9, dist_len=5))    # dist too short: OutOfBounds
+    t = I.nn_topk(100, 6, seed=10)                       # n beyond d: OutOfBounds
+    t.args[3] = ("i32", 120)
+    out.append(t)
+    return out
 
 
 def backprop_set() -> list:
@@ -260,5 +281,7 @@ if __name__ == "__main__":
         pack(trap_set(), GOLDEN / "traps.npz")
     if "northstar" in which:
         northstar_sets()
+    if "topk" in which:
+        pack(topk_set(), GOLDEN / "nn_topk.npz")
     if "backprop" in which or "northstar" in which:
         pack(backprop_set(), GOLDEN / "backprop.npz")

@@ -238,6 +238,32 @@ def nn(n: int, block: int = 256, seed: int = 0, target=NN_TARGET) -> Instance:
                     ["d"])
 
 
+def topk_distances(n: int, seed: int = 0, special: bool = False) -> np.ndarray:
+    """Distance-like f32 values with many exact ties (one decimal); with
+    `special`, also NaN, +inf, -0.0, 0.0 and negative values."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    d = np.round(g.uniform(0.0, 50.0, n), 1).astype(np.float32)
+    if special and n:
+        picks = g.integers(0, n, size=min(n, 12))
+        vals = [np.nan, np.inf, -0.0, 0.0, -1.5, np.nan, 0.0, -0.0, 3.0, -np.inf, np.nan, 0.1]
+        for p, v in zip(picks, vals):
+            d[p] = v
+    return d
+
+
+def nn_topk(n: int, k: int, seed: int = 0, special: bool = False, grid=(1,), block=(1,),
+            idx_len=None, dist_len=None, d=None) -> Instance:
+    d = topk_distances(n, seed, special) if d is None else np.asarray(d, np.float32)
+    li = max(k, 1) if idx_len is None else idx_len
+    ls = max(k, 1) if dist_len is None else dist_len
+    return Instance("nn_topk", Geom(*grid), Geom(*block), 0,
+                    [Buf("d", "f32", max(d.size, 1), d if d.size else np.zeros(1, np.float32)),
+                     Buf("idx", "i32", li, np.full(li, 7, np.int32)),
+                     Buf("dist", "f32", ls, np.full(ls, 9.0, np.float32))],
+                    [("buf", "d"), ("buf", "idx"), ("buf", "dist"), ("i32", n), ("i32", k)],
+                    ["idx", "dist"])
+
+
 def kmeans_inputs(npts: int, nf: int, seed: int = 0) -> np.ndarray:
     g = np.random.Generator(np.random.PCG64(seed))
     return g.uniform(0.0, 1.0, npts * nf).astype(np.float32)  # feature-major f[l*npts + p]

@@ -170,4 +170,256 @@ static Registrar reg_nn("nn",
                          {BF_SLOT_F32, BF_F32, "y"}},
                         launch_nn);
 
+// ---------------------------------------------------------------------------
+// nn_topk — paper_2206_07896_b200/kernels/nn_topk.kn (Rodinia nn's selection
+// of the k nearest records).  The DSL kernel's k passes each pick the least
+// record after the previous pick in (distance, index) order, NaN distances
+// last: that is the first k entries of a stable sort of d.  On the device the
+// order is a 64-bit key (monotone f32 key << 32 | index; NaN -> all ones,
+// -0.0 -> +0.0, which compare equal in the DSL), so picks are unique.
+//
+// One pass over d (4 B per record): every thread keeps the K smallest keys
+// of its grid-stride share in registers (sorted; a key is inserted by one
+// compare-exchange sweep, and the fast reject compares only the high word),
+// each CTA merges its threads' lists into its k smallest (k rounds of a
+// block-wide min; the owner pops), writes them to scratch, and the last CTA
+// to finish (ticket) merges the grid's candidates the same way and writes
+// idx / dist (dist re-read from d, so a -0.0 keeps its sign).  k > 32 runs
+// in rounds of 32 picks, each round taking keys above the previous round's
+// last pick (kept on the device).
+__device__ __forceinline__ unsigned long long topk_key(float v, unsigned i) {
+  unsigned b = __float_as_uint(v);
+  if (v != v) b = 0xffffffffu;  // NaN after every number
+  else {
+    if (v == 0.0f) b = 0u;  // -0.0 == +0.0
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  }
+  return ((unsigned long long)b << 32) | i;
+}
+
+template <int K>
+struct TopList {
+  unsigned long long l[K];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int j = 0; j < K; j++) l[j] = ~0ull;
+  }
+  __device__ __forceinline__ void insert(unsigned long long key) {
+    if (key >= l[K - 1]) return;
+#pragma unroll
+    for (int j = 0; j < K; j++) {  // sorted insert as one min/max sweep
+      const unsigned long long lo = key < l[j] ? key : l[j];
+      key = key < l[j] ? l[j] : key;
+      l[j] = lo;
+    }
+  }
+  __device__ __forceinline__ void pop() {
+#pragma unroll
+    for (int j = 0; j < K - 1; j++) l[j] = l[j + 1];
+    l[K - 1] = ~0ull;
+  }
+};
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// The `cnt` smallest keys of the union of the block's lists -> out[0..cnt)
+// (every thread of the block calls it; out may be shared or global).
+template <int K>
+__device__ void block_merge(TopList<K>& t, int cnt, unsigned long long* out) {
+  __shared__ unsigned long long wmin[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int r = 0; r < cnt; r++) {
+    const unsigned long long m = warp_min_u64(t.l[0]);
+    if (lane == 0) wmin[warp] = m;
+    __syncthreads();
+    unsigned long long bm = wmin[0];
+    for (int w = 1; w < nw; w++) bm = wmin[w] < bm ? wmin[w] : bm;
+    if (bm != ~0ull && t.l[0] == bm) t.pop();  // keys are unique: one owner
+    if (threadIdx.x == 0) out[r] = bm;
+    __syncthreads();
+  }
+}
+
+struct TopkArgs {
+  const float* d;
+  long long n;
+  int* idx;
+  float* dist;
+  int base;                  // first output slot of this round
+  int cnt;                   // picks this round (<= K)
+  int kw_idx, kw_dist;       // slots [0, kw) of idx / dist may be written
+  unsigned long long* cand;  // [gridDim.x][K] scratch
+  unsigned* ticket;
+  unsigned long long* lo;    // keys must exceed *lo (the previous round's last pick)
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
+  const unsigned long long lo = *a.lo;
+  TopList<K> t;
+  t.init();
+  const long long n4 = a.n >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const float4* d4 = reinterpret_cast<const float4*>(a.d);
+  unsigned thr = 0xffffffffu;  // high word of the list's last key: fast reject
+  auto offer = [&](float v, long long i) {
+    const unsigned long long key = topk_key(v, (unsigned)i);
+    if ((unsigned)(key >> 32) > thr || key <= lo) return;
+    t.insert(key);
+    thr = (unsigned)(t.l[K - 1] >> 32);
+  };
+  // four 16 B loads in flight per thread before any key work
+  for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < n4; j0 += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if (j0 + u * stride < n4) v[u] = __ldcs(d4 + j0 + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const long long j = j0 + u * stride;
+      if (j < n4) {
+        offer(v[u].x, 4 * j);
+        offer(v[u].y, 4 * j + 1);
+        offer(v[u].z, 4 * j + 2);
+        offer(v[u].w, 4 * j + 3);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (int)(a.n & 3)) offer(a.d[4 * n4 + threadIdx.x], 4 * n4 + threadIdx.x);
+  block_merge<K>(t, a.cnt, a.cand + (long long)blockIdx.x * K);
+  // last CTA merges every CTA's candidates
+  __shared__ bool last;
+  __threadfence();
+  if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  t.init();
+  const long long total = (long long)gridDim.x * K;
+  for (long long j = threadIdx.x; j < total; j += blockDim.x) {
+    const long long c = j / K, r = j % K;
+    if (r < a.cnt) t.insert(__ldcg(a.cand + c * K + r));
+  }
+  __shared__ unsigned long long fin[K];
+  block_merge<K>(t, a.cnt, fin);
+  if (threadIdx.x == 0) {
+    unsigned long long lastkey = ~0ull;
+    for (int r = 0; r < a.cnt; r++) {
+      const int slot = a.base + r;
+      const unsigned long long key = fin[r];
+      const int i = key == ~0ull ? -1 : (int)(key & 0xffffffffu);
+      if (slot < a.kw_idx) a.idx[slot] = i;
+      if (i >= 0 && slot < a.kw_dist) a.dist[slot] = a.d[i];
+      if (i >= 0) lastkey = key;
+    }
+    // the next round starts after this round's last pick (all of them when
+    // the records ran out)
+    *a.lo = fin[a.cnt - 1] == ~0ull ? ~0ull : lastkey;
+    *a.ticket = 0;
+  }
+}
+
+// a round with no records left: the remaining slots get -1
+__global__ void nn_topk_fill(int* idx, int from, int to) {
+  for (int j = from + threadIdx.x; j < to; j += blockDim.x) idx[j] = -1;
+}
+
+struct TopkScratch : StreamScratch {
+  unsigned long long* cand = nullptr;
+  unsigned* ticket = nullptr;
+  unsigned long long* lo = nullptr;
+  long long cap = 0;
+  ~TopkScratch() override {
+    cudaFree(cand);
+    cudaFree(ticket);
+    cudaFree(lo);
+  }
+};
+
+static int launch_nn_topk(LaunchCtx& ctx) {
+  const ArgVal& D = ctx.args[0];
+  const ArgVal& I = ctx.args[1];
+  const ArgVal& O = ctx.args[2];
+  const long long n = std::max(0, ctx.args[3].i32);
+  const long long k = ctx.args[4].i32;
+  // only logical blocks with blockIdx.x == 0 select (thread 0 of each; all
+  // of them write the same values): one selection if the fetch holds one
+  bool any = false;
+  for (auto& xi : ctx.x_intervals())
+    if (xi.first == 0) any = true;
+  if (!any || k <= 0) return BF_OK;
+  const long long blk = ctx.first_block_with_x(0);
+  const long long ld = D.len, li = I.len, lo_ = O.len;
+  if (n > ld) {  // pass 0 reads d[len(d)]
+    ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, blk, "nn_topk: n beyond len(d)");
+    return BF_OK;
+  }
+  // pass j writes idx[j], then dist[j] when a record was picked (j < n)
+  long long kw_idx = k, kw_dist = std::min(k, n);
+  long long jt = LLONG_MAX;
+  if (k > li) jt = li;
+  if (std::min(k, n) > lo_) jt = std::min(jt, lo_);
+  if (jt != LLONG_MAX) {
+    ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, blk, "nn_topk: output index out of range");
+    kw_idx = std::min(kw_idx, jt < li ? jt + 1 : jt);  // idx[jt] is written before dist[jt] traps
+    kw_idx = std::min(kw_idx, li);
+    kw_dist = std::min(kw_dist, jt);
+  }
+  const bool small = k <= 8;
+  const int K = small ? 8 : 32;
+  const int grid = small ? wave_grid(nn_topk_pass<8>, 256, 0, std::max(1LL, n / 4), 256 * 8, ctx.num_sms, 4)
+                         : wave_grid(nn_topk_pass<32>, 256, 0, std::max(1LL, n / 4), 256 * 8, ctx.num_sms, 4);
+  TopkScratch& S = scratch_for<TopkScratch>(ctx.stream, SCRATCH_NN_TOPK);
+  if (S.cap < (long long)grid * K) {
+    cudaStreamSynchronize(ctx.stream);
+    cudaFree(S.cand);
+    S.cand = nullptr;
+    S.cap = 0;
+    if (cudaMalloc((void**)&S.cand, (size_t)grid * K * 8) != cudaSuccess) {
+      cudaGetLastError();
+      *ctx.error = "nn_topk: scratch allocation failed";
+      return BF_E_CUDA;
+    }
+    S.cap = (long long)grid * K;
+  }
+  if (!S.ticket) {
+    if (cudaMalloc((void**)&S.ticket, 4) != cudaSuccess || cudaMalloc((void**)&S.lo, 8) != cudaSuccess) {
+      cudaGetLastError();
+      *ctx.error = "nn_topk: scratch allocation failed";
+      return BF_E_CUDA;
+    }
+    cudaMemsetAsync(S.ticket, 0, 4, ctx.stream);
+  }
+  cudaMemsetAsync(S.lo, 0, 8, ctx.stream);  // every key exceeds 0
+  for (long long base = 0; base < k; base += K) {
+    TopkArgs a{(const float*)D.ptr, n, (int*)I.ptr, (float*)O.ptr, (int)base, (int)std::min<long long>(K, k - base),
+               (int)kw_idx, (int)kw_dist, S.cand, S.ticket, S.lo};
+    if (base >= n) {  // no records left: -1 for the rest
+      const int to = (int)std::min(k, kw_idx);
+      if (base < to) nn_topk_fill<<<1, 256, 0, ctx.stream>>>((int*)I.ptr, (int)base, to);
+      BF_CUDA_LAUNCH_CHECK(ctx);
+      break;
+    }
+    if (small) nn_topk_pass<8><<<grid, 256, 0, ctx.stream>>>(a);
+    else nn_topk_pass<32><<<grid, 256, 0, ctx.stream>>>(a);
+    BF_CUDA_LAUNCH_CHECK(ctx);
+  }
+  return BF_OK;
+}
+
+static Registrar reg_nn_topk("nn_topk",
+                             {{BF_SLOT_HANDLE, BF_F32, "d"},
+                              {BF_SLOT_HANDLE, BF_I32, "idx"},
+                              {BF_SLOT_HANDLE, BF_F32, "dist"},
+                              {BF_SLOT_I32, BF_I32, "n"},
+                              {BF_SLOT_I32, BF_I32, "k"}},
+                             launch_nn_topk);
+
 }  // namespace bf

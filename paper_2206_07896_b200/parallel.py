@@ -15,6 +15,9 @@ data need a collective:
     NCCL point-to-point every `halo` iterations.
   * hist / hist_stride / wreduce / kmeans — per-rank partial counts or sums
     combined with one all-reduce (launch_sharded, COMBINE).
+  * nn top-k (nn_topk_sharded) — each rank selects its k nearest records,
+    one all-gather of k (index, distance) pairs, merged in (distance, index)
+    order.
   * vecadd / nn / fir / reduce / backprop — disjoint outputs: no exchange is needed for
     the computation; launch_sharded assembles the full output on every rank
     with one all-gather when the caller wants it replicated.
@@ -233,6 +236,84 @@ def launch_sharded(rt, arena, routine, grid, block, shmem: int, packed, outputs:
     comb.finish(tensors)
     torch.cuda.synchronize(device)
     return task
+
+
+# ---------------------------------------------------------------------------
+# sharded nn search: records split in contiguous ranges, each rank selects
+# its k nearest (nn_topk on its own distances), one all-gather of k
+# (index, distance) pairs per rank, merged by the same (distance, index)
+# order — the g x k candidate merge of SURVEY §8e.
+# ---------------------------------------------------------------------------
+
+def topk_merge(idx_lists, dist_lists, k: int):
+    """First k of the candidates in (distance, index) order, NaN distances
+    last, -0.0 == 0.0 (kernels/nn_topk.kn); idx -1 entries are empty.
+    Returns (idx int32[k] with -1 padding, dist float32[<= k])."""
+    import numpy as np
+    idx = np.concatenate([np.asarray(x, np.int64) for x in idx_lists]) if idx_lists else np.zeros(0, np.int64)
+    dist = np.concatenate([np.asarray(x, np.float32) for x in dist_lists]) if dist_lists else np.zeros(0, np.float32)
+    keep = idx >= 0
+    idx, dist = idx[keep], dist[keep]
+    order = np.lexsort((idx, dist))  # stable; NaN sorts last; -0.0 ties 0.0
+    sel = order[:max(k, 0)]
+    out = np.full(max(k, 0), -1, np.int32)
+    out[:sel.size] = idx[sel]
+    return out, dist[sel]
+
+
+def nn_topk_sharded(local_select: Callable, n_local: int, offset: int, k: int, world: int, rank: int,
+                    gather: Callable):
+    """Global k nearest from per-rank picks.  local_select(k) -> (idx, dist)
+    of this rank's records (local indices, -1 padded; e.g. an nn_topk launch
+    on the rank's own distances); gather(idx int64[k], dist f32[k]) ->
+    (world lists of both) in rank order.  Identical result on every rank."""
+    import numpy as np
+    idx, dist = local_select(k) if n_local > 0 else (np.full(k, -1, np.int32), np.zeros(k, np.float32))
+    idx = np.asarray(idx, np.int64)
+    gidx = np.where(idx >= 0, idx + offset, -1)
+    d = np.zeros(k, np.float32)
+    d[:np.asarray(dist).size] = np.asarray(dist, np.float32)[:k]
+    if world > 1:
+        il, dl = gather(gidx, d)
+    else:
+        il, dl = [gidx], [d]
+    return topk_merge(il, dl, k)
+
+
+def dist_topk_gather(device=None):
+    """gather() for nn_topk_sharded over torch.distributed (NCCL tensors on
+    `device`, or CPU tensors for gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    def gather(gidx, d):
+        world = dist.get_world_size()
+        ti = torch.as_tensor(gidx, dtype=torch.int64, device=device)
+        td = torch.as_tensor(d, dtype=torch.float32, device=device)
+        oi = [torch.empty_like(ti) for _ in range(world)]
+        od = [torch.empty_like(td) for _ in range(world)]
+        dist.all_gather(oi, ti)
+        dist.all_gather(od, td)
+        return [x.cpu().numpy() for x in oi], [x.cpu().numpy() for x in od]
+    return gather
+
+
+def gpu_topk_select(rt, arena, d_handle: int, n_local: int):
+    """local_select() for nn_topk_sharded: one nn_topk launch over this
+    rank's distance buffer."""
+    from . import ArgSlot, Dim3, PackedArgs, routines
+
+    def select(k):
+        idx, dist = arena.alloc("i32", max(k, 1)), arena.alloc("f32", max(k, 1))
+        rt.launch(routines.get("nn_topk"), Dim3(1), Dim3(1), 0,
+                  PackedArgs([ArgSlot("handle", d_handle), ArgSlot("handle", idx), ArgSlot("handle", dist),
+                              ArgSlot("i32", n_local), ArgSlot("i32", k)]))
+        rt.device_synchronize()
+        out = arena.to_numpy(idx)[:k], arena.to_numpy(dist)[:k]
+        arena.free(idx)
+        arena.free(dist)
+        return out
+    return select
 
 
 # ---------------------------------------------------------------------------

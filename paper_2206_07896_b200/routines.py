@@ -77,6 +77,8 @@ _TABLE = {
                    ("rz1", "f32"), ("amb", "f32")), False, 14, False, "hotspot.kn"),
     "nn": (_p(("ll", "global f32[]"), ("d", "global f32[]"), ("n", "i32"), ("x", "f32"), ("y", "f32")),
            False, 5, False, "nn.kn"),
+    "nn_topk": (_p(("d", "global f32[]"), ("idx", "global i32[]"), ("dist", "global f32[]"), ("n", "i32"),
+                   ("k", "i32")), False, 31, False, "nn_topk.kn"),
     "kmeans": (_p(("f", "global f32[]"), ("cent", "global f32[]"), ("member", "global i32[]"),
                   ("sums", "global f32[]"), ("counts", "global i32[]"), ("npts", "i32"), ("nf", "i32"),
                   ("k", "i32")), True, 16, False, "kmeans.kn"),

@@ -47,4 +47,4 @@ def load(name: str):
     return out
 
 
-SETS = ["corpus_sweep", "corpus_extra", "geometry", "traps", "hotspot", "nn", "kmeans", "bfs", "backprop"]
+SETS = ["corpus_sweep", "corpus_extra", "geometry", "traps", "hotspot", "nn", "nn_topk", "kmeans", "bfs", "backprop"]

@@ -283,3 +283,59 @@ def test_bfs_levels_sharded_protocol(world):
             lv, d = allres[r][k]
             assert np.array_equal(lv, want), (k, r)
             assert d == depth, (k, r)
+
+
+def _topk_worker(rank, world, port, out_q):
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2206_07896_b200.parallel import dist_topk_gather, nn_topk_sharded, rank_range
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(11)
+        n = 10007
+        d = np.round(rng.uniform(0, 30, n), 1).astype(np.float32)  # many ties across ranks
+        d[rng.integers(0, n, 20)] = np.nan
+        d[rng.integers(0, n, 20)] = -0.0
+        lo, hi = rank_range(n, world, rank)
+        loc = d[lo:hi]
+
+        def select(k):  # the device kernel's contract: stable order of the local records
+            o = np.argsort(loc, kind="stable")[:k]
+            idx = np.full(k, -1, np.int32)
+            idx[:o.size] = o
+            return idx, loc[o]
+        res = {}
+        for k in (1, 5, 37, 3000):
+            idx, dd = nn_topk_sharded(select, hi - lo, lo, k, world, rank, dist_topk_gather())
+            res[k] = (idx.tolist(), dd.view(np.uint32).tolist())
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nn_topk_sharded_merge(world):
+    """g x k candidate merge over gloo == the single-device selection (a
+    stable sort of all distances), identical on every rank."""
+    import numpy as np
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_topk_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    rng = np.random.default_rng(11)
+    n = 10007
+    d = np.round(rng.uniform(0, 30, n), 1).astype(np.float32)
+    d[rng.integers(0, n, 20)] = np.nan
+    d[rng.integers(0, n, 20)] = -0.0
+    for k in (1, 5, 37, 3000):
+        want = np.argsort(d, kind="stable")[:k]
+        for r in range(world):
+            idx, bits = got[r][k]
+            assert idx == want.tolist(), (world, r, k)
+            assert bits == d[want].view(np.uint32).tolist()
