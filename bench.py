@@ -173,7 +173,7 @@ def run_reference_arm(args) -> None:
     cells_iter = args.size * args.size * args.iters
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": BYTES_PER_CELL_ITER * cells_iter / (value * 1e9) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
@@ -318,15 +318,22 @@ def run_ours(args) -> None:
     # end-to-end through the public API with host buffers (pinned): every
     # step uploads its inputs (temp + power) and downloads its result.
     # serial: upload, 100 launches, sync, download — nothing overlaps.
-    # pipelined (the reported e2e): two resident buffer sets; launches are
+    # pipelined (the reported e2e): three resident buffer sets; launches are
     # asynchronous (Runtime.launch returns at issue), so while step k runs on
-    # one set the host downloads step k-1's result and uploads step k+1's
-    # inputs into the other set (uploads on the arena's copy stream, the
-    # download concurrently on its D2H stream).  Every step's copies are
-    # inside the timed region.
+    # set k%3 the host downloads step k-1's result from set (k-1)%3 and
+    # uploads step k+1's inputs into set (k+1)%3 (uploads on the arena's copy
+    # stream, the download concurrently on its D2H stream from a helper
+    # thread).  Three sets keep the download source, the upload target and
+    # the running step disjoint.  Every step's copies are inside the timed
+    # region, and every step's downloaded grid is compared bit for bit with
+    # the resident-path result after the region.
     h_temp = torch.from_numpy(temp[r0 * size:r1 * size].copy()).pin_memory().numpy()
     h_power = torch.from_numpy(power[r0 * size:r1 * size].copy()).pin_memory().numpy()
-    h_out = torch.empty(cells, dtype=torch.float32).pin_memory().numpy()
+    expect = arena.to_numpy(step())  # the resident path's result on these inputs
+    rt.device_synchronize()
+    n_outs = min(args.steps, 16)
+    h_outs = [torch.empty(cells, dtype=torch.float32).pin_memory().numpy() for _ in range(n_outs)]
+    h_out = h_outs[0]
     serial = []
     for k in range(args.warmup + args.steps):
         barrier(world)
@@ -340,8 +347,9 @@ def run_ours(args) -> None:
         if k >= args.warmup:
             serial.append(max_over_ranks(dt, world))
     serial_s = statistics.median(serial)
+    e2e_checked = bool(np.array_equal(h_out.view(np.uint32), expect.view(np.uint32)))
 
-    if len(sets) == 1:
+    while len(sets) < 3:
         sets.append(BufferSet())
 
     def pipelined(nsteps: int) -> float:
@@ -351,40 +359,45 @@ def run_ours(args) -> None:
         arena.upload_numpy(sets[0].pow, h_power)
         prev = None
         for k in range(nsteps):
-            res = sets[k % 2].step()
+            res = sets[k % 3].step()
             pending = None
-            if prev is not None:  # D2H on its own stream, from a helper thread
-                pending = copier.submit(arena.download_into, prev, h_out)
+            if prev is not None:  # D2H of step k-1 on its own stream, from a helper thread
+                pending = copier.submit(arena.download_into, prev, h_outs[(k - 1) % n_outs])
             if k + 1 < nsteps:
-                nxt = sets[(k + 1) % 2]
+                nxt = sets[(k + 1) % 3]
                 arena.upload_numpy(nxt.src, h_temp)
                 arena.upload_numpy(nxt.pow, h_power)
             if pending is not None:
                 pending.result()
             rt.device_synchronize()
             prev = res
-        arena.download_into(prev, h_out)
+        arena.download_into(prev, h_outs[(nsteps - 1) % n_outs])
         return max_over_ranks(time.perf_counter() - t0, world)
 
     import concurrent.futures as cf
     copier = cf.ThreadPoolExecutor(max_workers=1)
 
     pipelined(max(2, args.warmup))
+    for h in h_outs:
+        h.fill(np.nan)
     e2e_s = pipelined(args.steps) / args.steps
     e2e_value = BYTES_PER_CELL_ITER * size * size * iters / e2e_s / 1e9
     copier.shutdown()
+    for h in h_outs:  # every timed step's delivered result (the last 16 if steps > 16)
+        e2e_checked &= bool(np.array_equal(h.view(np.uint32), expect.view(np.uint32)))
+    e2e_checked = bool(max_over_ranks(0.0 if e2e_checked else 1.0, world) == 0.0)
+    del h_outs, h_out
+    launch = launch_latency(arena, rt, torch, stream) if rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_hotspot(size, iters, args.cpu_budget, len(os.sched_getaffinity(0)))
-        pyref = None
-        try:
-            import benchkit
-            pyref = benchkit.python_reference_sample()
-        except Exception as e:  # reported, not hidden
-            pyref = {"error": repr(e)}
-        if pyref is not None:
-            cpu["python_reference_vecadd"] = pyref
+        import benchkit
+        ref = benchkit.reference_runtime_pair("hotspot", benchkit.REF_LOG_BENCH, len(os.sched_getaffinity(0)))
+        cpu["reference_runtime"] = ref  # the unmodified blockfuse.Runtime on a sample of the same kernel
+        best = max((v["elem_per_s"] for v in ref.values() if isinstance(v, dict)), default=None)
+        if best:
+            cpu["speedup_vs_reference_runtime"] = round(total_cells / (dev_ms * 1e-3) / best, 1)
 
     kernels = None
     kernel_launches = 0
@@ -414,10 +427,13 @@ def run_ours(args) -> None:
                          "kernel": "hotspot_rows", "avg_launch_us": round(avg_launch_ms * 1e3, 3)},
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": 2 * cells * 4 * world, "d2h_bytes_per_step": cells * 4 * world,
-                    "ms_per_step": round(e2e_s * 1e3, 3), "mode": "pipelined (2 buffer sets)",
+                    "ms_per_step": round(e2e_s * 1e3, 3), "mode": "pipelined (3 buffer sets)",
+                    "checked": e2e_checked,
+                    "check": "every timed step's downloaded grid == the resident-path result, bit for bit",
                     "serial_value": round(BYTES_PER_CELL_ITER * size * size * iters / serial_s / 1e9, 3),
                     "serial_ms_per_step": round(serial_s * 1e3, 3)},
             "gpu_launches": iters * args.steps,
+            "launch_latency": launch,
             "clocks": clocks.summary(),
         }
         if cpu is not None:
@@ -522,6 +538,107 @@ def run_sweep(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def run_kmeans(args) -> None:
+    """BASELINE configs[2] across ranks: Rodinia's kmeans host loop (16M
+    points x 32 features, k = 16) for --passes passes per step.  Each rank
+    assigns its contiguous range of logical blocks (rank_range: the average
+    grain with ranks as workers) through Runtime.launch_range; per pass the
+    k x nf sums and k counts are all-reduced over NCCL (~2.1 KB) and every
+    rank applies the same centroid update (cluster.KmeansDriver).  value =
+    points assigned per second over the whole job (strong scaling)."""
+    import torch
+
+    from paper_2206_07896_b200 import DeviceArena, Runtime
+    from paper_2206_07896_b200.cluster import KmeansDriver
+    from paper_2206_07896_b200.parallel import nccl_allreduce
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    npts, nf, k, passes = args.kmeans_points, 32, 16, args.passes
+    arena = DeviceArena(local)
+    rt = Runtime(arena)
+    stream = torch.cuda.ExternalStream(rt.worker_stream(0), device=device)
+    f, cent, member = arena.alloc("f32", npts * nf), arena.alloc("f32", k * nf), arena.alloc("i32", npts)
+    g = torch.Generator(device=device)
+    g.manual_seed(0)  # the same points on every rank
+    tf = torch.as_tensor(arena.cuda_array(f), device=device)
+    tf.uniform_(0, 1, generator=g)
+    tc = torch.as_tensor(arena.cuda_array(cent), device=device)
+    c0 = tf.view(nf, npts)[:, :k].t().contiguous().view(-1).clone()
+    allreduce = nccl_allreduce(arena, device) if world > 1 else None
+    drv = KmeansDriver(rt, arena, f, cent, member, npts, nf, k, world, rank)
+
+    def step():
+        tc.copy_(c0)
+        arena.fill_value(drv.prev, -1)
+        torch.cuda.synchronize()
+        for _ in range(passes):
+            drv.assign()
+            if world > 1:
+                allreduce([drv.sums, drv.counts])
+            d = drv.update()
+            if world > 1:
+                allreduce(d)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    with ClockSampler(local) as clocks:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            step()
+        b.record(stream)
+        rt.device_synchronize()
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
+    cent_sum = float(tc.double().sum().item())
+    if rank == 0:
+        pts = npts * passes
+        print(json.dumps({
+            "metric": METRIC, "value": round(pts * (4 * nf + 4) / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
+            "data": "synthetic",
+            "config": {"workload": f"kmeans {npts} x {nf} f32, k={k}, {passes} passes per step (Rodinia host loop)",
+                       "parallelism": f"point ranges x{world}, per-pass all-reduce of sums/counts",
+                       "bytes_per_point_pass": 4 * nf + 4},
+            "elem_per_s": pts / (ms * 1e-3), "centroid_checksum": cent_sum,
+            "clocks": clocks.summary()}), flush=True)
+    rt.shutdown()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_cpu_runtime(args) -> None:
+    """SURVEY §8d "CPU timing (reference path)": the unmodified reference
+    runtime (blockfuse.Runtime) per kernel at the survey's sizes, pool =
+    host cores and pool = 1, each result checked against the oracle; beside
+    it the C port (oracle/oracle.c) on all host cores.  Host-only (no GPU)."""
+    import benchkit
+    threads = len(os.sched_getaffinity(0))
+    rows = {}
+    for name, log_n in benchkit.REF_LOG_SURVEY.items():
+        ent = benchkit.reference_runtime_pair(name, benchkit.REF_LOG_SURVEY, threads)
+        try:
+            ent = dict(ent, port=benchkit.cpu_sample(name, threads))
+        except Exception as e:
+            ent = dict(ent, port={"error": repr(e)})
+        rows[name] = ent
+        print(json.dumps({"kernel": name, **ent}), file=sys.stderr, flush=True)
+    print(json.dumps({"metric": "reference CPU runtime per kernel (blockfuse.Runtime) and the C port",
+                      "value": None, "unit": "elem/s", "n_gpus": 0, "host_threads": threads,
+                      "config": {"workload": "SURVEY §8d CPU sample sizes (log2)", "sizes": benchkit.REF_LOG_SURVEY},
+                      "kernels": rows}), flush=True)
 
 
 def run_reorder(args) -> None:
@@ -653,6 +770,52 @@ def run_grain(args) -> None:
                       "grain": rows}), flush=True)
 
 
+def launch_latency(arena, rt, torch, stream, reps: int = 2000) -> dict:
+    """BASELINE configs[0] / SURVEY §8d C1: vecAdd 2^20 f32, grid 4096 x 256
+    (PR1), through Runtime.launch.  launch_us: host time of one
+    Runtime.launch call (non-blocking); launch_sync_us: one launch followed
+    by device_synchronize, wall clock (the reference measures 59.5 us for
+    this pair on its thread pool, runtime.py:255-278); device_us: device time
+    per launch back to back (CUDA events on the worker stream)."""
+    from paper_2206_07896_b200 import ArgSlot, Dim3, PackedArgs, routines
+    n = 1 << 20
+    hs = [arena.alloc("f32", n) for _ in range(3)]
+    dev = torch.device("cuda", arena.device)
+    for h in hs[:2]:
+        torch.as_tensor(arena.cuda_array(h), device=dev).uniform_(-1, 1)
+    torch.cuda.synchronize()
+    pk = PackedArgs([ArgSlot("handle", hs[0]), ArgSlot("handle", hs[1]), ArgSlot("handle", hs[2]),
+                     ArgSlot("i32", n)])
+    va, g, b = routines.get("vecadd"), Dim3(4096), Dim3(256)
+    for _ in range(100):
+        rt.launch(va, g, b, 0, pk)
+    rt.device_synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rt.launch(va, g, b, 0, pk)
+    launch_us = (time.perf_counter() - t0) / reps * 1e6
+    rt.device_synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rt.launch(va, g, b, 0, pk)
+        rt.device_synchronize()
+    sync_us = (time.perf_counter() - t0) / reps * 1e6
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        rt.launch(va, g, b, 0, pk)
+    e1.record(stream)
+    rt.device_synchronize()
+    e1.synchronize()
+    dev_us = e0.elapsed_time(e1) * 1e3 / reps
+    for h in hs:
+        arena.free(h)
+    return {"workload": "vecadd 2^20 f32, grid 4096 x 256 (PR1)", "launch_us": round(launch_us, 3),
+            "launch_sync_us": round(sync_us, 3), "device_us_per_launch": round(dev_us, 3),
+            "device_gbs": round(12 * n / (dev_us * 1e-6) / 1e9, 1), "reps": reps,
+            "reference_launch_sync_us": 59.5}
+
+
 def per_kernel_table(arena, rt, torch, stream, args) -> tuple[dict, int]:
     """Every other kernel of the path at full size (benchkit.py), N=1."""
     import benchkit
@@ -689,8 +852,36 @@ def per_kernel_table(arena, rt, torch, stream, args) -> tuple[dict, int]:
                 ent["cpu_baseline"] = cpu
                 if "elem_per_s" in cpu:
                     ent["speedup_vs_cpu_port"] = round(c.elems_per_step / r["dev_s"] / cpu["elem_per_s"], 1)
+            ref = benchkit.reference_runtime_pair(c.name, benchkit.REF_LOG_BENCH, threads)
+            if ref is not None:
+                ent["reference_runtime"] = ref
+                best = max((v["elem_per_s"] for v in ref.values() if isinstance(v, dict)), default=None)
+                if best:
+                    ent["speedup_vs_reference_runtime"] = round(c.elems_per_step / r["dev_s"] / best, 1)
         table[c.name] = ent
     return table, launches
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a launcher: re-exec this script under torchrun, one
+    process per GPU (RANK / LOCAL_RANK / WORLD_SIZE from the environment),
+    rendezvous on 127.0.0.1.  Fails loudly when fewer than N GPUs are
+    visible (the reference arm needs no GPU: its ranks > 0 exit at once)."""
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) visible",
+                  file=sys.stderr, flush=True)
+            return 1
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main() -> None:
@@ -699,9 +890,11 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["hotspot", "sweep", "grain", "reorder"], default="hotspot")
+    ap.add_argument("--workload", choices=["hotspot", "sweep", "grain", "reorder", "kmeans", "cpu-runtime"], default="hotspot")
     ap.add_argument("--reorder-k", type=int, default=1 << 16, help="strides per thread (reorder study)")
     ap.add_argument("--size", type=int, default=8192)
+    ap.add_argument("--kmeans-points", type=int, default=1 << 24)
+    ap.add_argument("--passes", type=int, default=10, help="kmeans host-loop passes per step")
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--halo", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -717,12 +910,23 @@ def main() -> None:
     ap.add_argument("--bfs-log-v", type=int, default=26)
     ap.add_argument("--cases", default="", help="comma list: only these per-kernel cases")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: one process per GPU expected")
     if args.impl == "reference":
         run_reference_arm(args)
     elif args.workload == "sweep":
         run_sweep(args)
     elif args.workload == "reorder":
         run_reorder(args)
+    elif args.workload == "kmeans":
+        run_kmeans(args)
+    elif args.workload == "cpu-runtime":
+        run_cpu_runtime(args)
     elif args.workload == "grain":
         run_grain(args)
     else:

@@ -403,122 +403,239 @@ def time_case(case: Case, rt, torch, stream, reps: int, warmup: int) -> dict:
     return {"dev_s": dev, "wall_s": wall, "launches": nlaunch, "checked": ok}
 
 
-def cpu_sample(name: str, threads: int, budget: float = 0.5) -> Optional[dict]:
-    """Oracle port (oracle/oracle.c) throughput on a bounded sample of the
-    same kernel, in elements/s; one thread unless the kernel's blocks are
-    independent (nn, hotspot use OpenMP)."""
+def sample_instance(name: str, log_n: int):
+    """A seeded oracle.instances.Instance of one bench case at 2^log_n
+    elements (points for kmeans, input units for backprop, cells for
+    hotspot) -> (instance, elements).  bfs returns its graph instead
+    (see bfs_sample)."""
     sys.path.insert(0, str(ROOT / "oracle"))
-    import random
-
     import instances as I
     import numpy as np
-    import oracle
 
-    rng = random.Random(5)
+    n = 1 << log_n
     if name in ("vecadd", "vecadd_pr1"):
-        n = 1 << 22
-        inst = I.vecadd(rng)
-        inst.grid, inst.block = I.Geom(n // 256), I.Geom(256)
         a = np.random.default_rng(1).uniform(-1, 1, n).astype(np.float32)
-        inst.buffers = [I.Buf("a", "f32", n, a), I.Buf("b", "f32", n, a), I.Buf("c", "f32", n, np.zeros(n, np.float32))]
-        inst.args[3] = ("i32", n)
-        elems, nt = n, 1
-    elif name == "nn":
-        n = 1 << 22
-        inst = I.nn(n, 256)
-        elems, nt = n, threads
-    elif name in ("hist", "hist_stride", "reduce", "wreduce"):
-        n = 1 << 22
-        pix = np.random.default_rng(2).integers(0, 1 << 16, n).astype(np.int32)
-        if name == "hist":
-            inst = I.Instance("hist", I.Geom(n // 256), I.Geom(256), 0,
-                              [I.Buf("pix", "i32", n, pix), I.Buf("counts", "i32", 16, np.zeros(16, np.int32))],
-                              [("buf", "pix"), ("buf", "counts"), ("i32", n), ("i32", 16)], ["counts"])
-        elif name == "hist_stride":
-            inst = I.Instance("hist_stride", I.Geom(1), I.Geom(256), 0,
-                              [I.Buf("pix", "i32", n, pix), I.Buf("counts", "i32", 16, np.zeros(16, np.int32))],
-                              [("buf", "pix"), ("buf", "counts"), ("i32", n // 256), ("i32", 16)], ["counts"])
-        elif name == "reduce":
-            inst = I.Instance("reduce", I.Geom(n // 256), I.Geom(256), 0,
-                              [I.Buf("x", "i32", n, pix), I.Buf("out", "i32", n // 256, np.zeros(n // 256, np.int32))],
-                              [("buf", "x"), ("buf", "out"), ("i32", n)], ["out"])
-        else:
-            inst = I.Instance("wreduce", I.Geom(n // 256), I.Geom(256), 0,
-                              [I.Buf("x", "i32", n, pix), I.Buf("out", "i32", 1, np.zeros(1, np.int32))],
-                              [("buf", "x"), ("buf", "out"), ("i32", n)], ["out"])
-        elems, nt = n, 1
-    elif name == "fir":
-        m = 1 << 14
+        b = np.random.default_rng(2).uniform(-1, 1, n).astype(np.float32)
+        inst = I.Instance("vecadd", I.Geom(max(1, n // 256)), I.Geom(256), 0,
+                          [I.Buf("a", "f32", n, a), I.Buf("b", "f32", n, b),
+                           I.Buf("c", "f32", n, np.zeros(n, np.float32))],
+                          [("buf", "a"), ("buf", "b"), ("buf", "c"), ("i32", n)], ["c"])
+        return inst, n
+    if name == "nn":
+        return I.nn(n, 256), n
+    if name == "hotspot":
+        side = 1 << (log_n // 2)
+        return I.hotspot(side, side, 16, 16, seed=0), side * side
+    pix = np.random.default_rng(2).integers(0, 1 << 16, n).astype(np.int32)
+    if name == "hist":
+        return I.Instance("hist", I.Geom(max(1, n // 256)), I.Geom(256), 0,
+                          [I.Buf("pix", "i32", n, pix), I.Buf("counts", "i32", 16, np.zeros(16, np.int32))],
+                          [("buf", "pix"), ("buf", "counts"), ("i32", n), ("i32", 16)], ["counts"]), n
+    if name == "hist_stride":
+        return I.Instance("hist_stride", I.Geom(1), I.Geom(256), 0,
+                          [I.Buf("pix", "i32", n, pix), I.Buf("counts", "i32", 16, np.zeros(16, np.int32))],
+                          [("buf", "pix"), ("buf", "counts"), ("i32", max(1, n // 256)), ("i32", 16)],
+                          ["counts"]), n
+    if name == "reduce":
+        return I.Instance("reduce", I.Geom(max(1, n // 256)), I.Geom(256), 0,
+                          [I.Buf("x", "i32", n, pix),
+                           I.Buf("out", "i32", max(1, n // 256), np.zeros(max(1, n // 256), np.int32))],
+                          [("buf", "x"), ("buf", "out"), ("i32", n)], ["out"]), n
+    if name == "wreduce":
+        return I.Instance("wreduce", I.Geom(max(1, n // 256)), I.Geom(256), 0,
+                          [I.Buf("x", "i32", n, pix), I.Buf("out", "i32", 1, np.zeros(1, np.int32))],
+                          [("buf", "x"), ("buf", "out"), ("i32", n)], ["out"]), n
+    if name == "fir":
+        m = max(1, n // 256)
         x = np.random.default_rng(3).uniform(-1, 1, m * 256 + 8).astype(np.float32)
         w = np.random.default_rng(4).uniform(-1, 1, 8).astype(np.float32)
-        inst = I.Instance("fir", I.Geom(1), I.Geom(256), 0,
-                          [I.Buf("x", "f32", x.size, x), I.Buf("y", "f32", m * 256, np.zeros(m * 256, np.float32)),
-                           I.Buf("w", "f32", 8, w)],
-                          [("buf", "x"), ("buf", "y"), ("buf", "w"), ("i32", 8), ("i32", m)], ["y"])
-        elems, nt = m * 256, 1
-    elif name == "kmeans":
-        inst = I.kmeans(1 << 15, 32, 16, 256)
-        elems, nt = 1 << 15, 1
-    elif name == "bp_forward":
-        inst = I.backprop_forward(1 << 18, seed=1)
-        elems, nt = 1 << 18, 1
-    elif name == "bp_adjust":
-        inst = I.backprop_adjust(1 << 18, seed=1)
-        elems, nt = 1 << 18, 1
-    elif name == "bfs":
-        nv = 1 << 20
+        return I.Instance("fir", I.Geom(1), I.Geom(256), 0,
+                          [I.Buf("x", "f32", x.size, x),
+                           I.Buf("y", "f32", m * 256, np.zeros(m * 256, np.float32)), I.Buf("w", "f32", 8, w)],
+                          [("buf", "x"), ("buf", "y"), ("buf", "w"), ("i32", 8), ("i32", m)], ["y"]), m * 256
+    if name in ("kmeans", "kmeans_loop"):
+        return I.kmeans(n, 32, 16, 256), n
+    if name == "bp_forward":
+        return I.backprop_forward(n, seed=1), n
+    if name == "bp_adjust":
+        return I.backprop_adjust(n, seed=1), n
+    return None, 0
+
+
+# bench-run sample sizes (log2): the C port, all host cores, ~0.5 s each
+PORT_LOG = {"vecadd": 24, "vecadd_pr1": 20, "nn": 22, "hist": 24, "hist_stride": 22, "reduce": 24,
+            "wreduce": 24, "fir": 20, "kmeans": 16, "kmeans_loop": 16, "bp_forward": 18,
+            "bp_adjust": 18, "bfs": 22, "bfs_fused": 22, "hotspot": 22}
+# the reference runtime (pure Python): SURVEY §8d sizes for the study
+# (--workload cpu-runtime), and ~1 s samples for the default bench line
+REF_LOG_SURVEY = {"vecadd_pr1": 20, "vecadd": 20, "hotspot": 16, "kmeans": 10, "bfs": 14, "nn": 20,
+                  "hist": 16, "hist_stride": 16, "reduce": 16, "wreduce": 16, "fir": 16,
+                  "bp_forward": 12, "bp_adjust": 12}
+REF_LOG_BENCH = {"vecadd_pr1": 14, "vecadd": 14, "hotspot": 12, "kmeans": 7, "bfs": 11, "nn": 14,
+                 "hist": 13, "hist_stride": 13, "reduce": 13, "wreduce": 13, "fir": 13,
+                 "bp_forward": 9, "bp_adjust": 9}
+
+
+def cpu_sample(name: str, threads: int, budget: float = 0.5) -> Optional[dict]:
+    """Oracle port (oracle/oracle.c) throughput on a bounded sample of the
+    same kernel, in elements/s, on all host threads: the launch's logical
+    blocks split into one contiguous range per thread (oracle.run_par, the
+    reference pool's average grain).  Single-block launches (fir and
+    hist_stride are grid 1 in the corpus) run on one thread."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import instances as I
+    import oracle
+
+    if name in ("bfs", "bfs_fused"):
+        nv = 1 << PORT_LOG["bfs"]
         row, col = I.random_graph(nv, 8, 1)
         t0 = time.perf_counter()
         oracle.bfs_full(row, col, nv, 0)
         dt = time.perf_counter() - t0
         return {"elem_per_s": col.size / dt, "cores": 1, "kind": "port",
-                "sample": f"bfs 2^20 vertices x 8, frontier-queue restatement, {dt:.2f} s"}
-    else:
+                "sample": f"bfs 2^{PORT_LOG['bfs']} vertices x 8, frontier-queue restatement, {dt:.2f} s"}
+    if name not in PORT_LOG:
         return None
+    inst, elems = sample_instance(name, PORT_LOG[name])
+    nt = threads if inst.grid.total > 1 else 1
     t0 = time.perf_counter()
     reps = 0
     while True:
-        oracle.run(inst, nthreads=nt)
+        oracle.run_par(inst, nt)
         reps += 1
         if time.perf_counter() - t0 > budget:
             break
     dt = (time.perf_counter() - t0) / reps
     return {"elem_per_s": elems / dt, "cores": nt, "kind": "port",
-            "sample": f"{name} {elems} elements, oracle/oracle.c, {reps} run(s) of {dt:.3f} s"}
+            "sample": f"{name} {elems} elements, oracle/oracle.c over {nt} thread(s), {reps} run(s) of {dt:.3f} s"}
 
 
-def python_reference_sample(budget_elems: int = 1 << 14) -> Optional[dict]:
-    """The unmodified reference runtime (blockfuse, pure Python thread pool)
-    on vecadd 2^14 elements, pool = host cores: the CPU runtime itself."""
-    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
-        if (p / "blockfuse" / "__init__.py").exists() and str(p) not in sys.path:
-            sys.path.append(str(p))
-            break
-    try:
-        import random
+REF_NAME = {"kmeans_loop": "kmeans", "bfs_fused": "bfs"}
+_REF_CACHE: dict = {}
 
-        from blockfuse.bench import CORPUS, materialize
-        from blockfuse.runtime import Runtime
-        from blockfuse.arena import DeviceArena
-        from blockfuse.syntax import Dim3
-    except Exception:
+
+def reference_runtime_pair(name: str, sizes: dict, threads: int) -> Optional[dict]:
+    """reference_runtime_sample at pool = host cores and pool = 1 (the GIL
+    makes them about equal), cached per kernel for one bench run."""
+    key = REF_NAME.get(name, name)
+    if key not in sizes:
         return None
-    case = CORPUS["vecadd"]
-    inst = case.random_instance(random.Random(1))
-    n = budget_elems
-    inst.grid, inst.block = Dim3(n // 256), Dim3(256)
+    if (key, sizes[key]) not in _REF_CACHE:
+        try:
+            _REF_CACHE[(key, sizes[key])] = {
+                "pool_cores": reference_runtime_sample(key, threads, sizes[key]),
+                "pool_1": reference_runtime_sample(key, 1, sizes[key])}
+        except Exception as e:  # reported, never hidden
+            _REF_CACHE[(key, sizes[key])] = {"error": repr(e)}
+    return _REF_CACHE[(key, sizes[key])]
+
+
+def _reference_modules():
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "blockfuse" / "__init__.py").exists():
+            if str(p) not in sys.path:
+                sys.path.append(str(p))
+            break
+    import blockfuse.arena as A
+    import blockfuse.bench as B
+    import blockfuse.executor as E
+    import blockfuse.hostprog as H
+    import blockfuse.parser as P
+    import blockfuse.runtime as R
+    import blockfuse.syntax as S
+    from blockfuse.transform import transform as T
+    return A, B, E, H, P, R, S, T
+
+
+_REF_KERNELS: dict = {}
+
+
+def _reference_kernel(name: str, warp_size: int = 32):
+    """The reference's compiled MpmdKernel of a corpus kernel, or of one of
+    our north-star kernels (paper_2206_07896_b200/kernels/*.kn) parsed and
+    transformed by the reference's own front end."""
+    A, B, E, H, P, R, S, T = _reference_modules()
+    if name not in _REF_KERNELS:
+        if name in B.CORPUS:
+            _REF_KERNELS[name] = B.CORPUS[name].compiled(warp_size)
+        else:
+            for f in (ROOT / "paper_2206_07896_b200" / "kernels").glob("*.kn"):
+                for kname, prog in P.parse_unit(f.read_text()).items():
+                    if kname == name:
+                        _REF_KERNELS[name] = T(prog, warp_mode=False, warp_size=warp_size)
+    return _REF_KERNELS[name]
+
+
+def reference_runtime_sample(name: str, pool: int, log_n: int) -> Optional[dict]:
+    """The unmodified reference runtime (blockfuse.Runtime: task queue +
+    Python thread pool, runtime.py:216-350) running one launch of the case
+    (bfs: Rodinia's per-level host loop to the end of the traversal) on a
+    2^log_n sample; wall time of launch + device_synchronize.  The result is
+    compared with the oracle (`matches_oracle`)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import instances as I
+    import numpy as np
+    import oracle
+    A, B, E, H, P, R, S, T = _reference_modules()
+    if name in ("bfs", "bfs_fused"):
+        nv = 1 << log_n
+        row, col = I.random_graph(nv, 8, 1)
+        want, depth = oracle.bfs_full(row, col, nv, 0)
+        arena = A.DeviceArena()
+        hr, hc, hl, hch = (arena.alloc("i32", nv + 1), arena.alloc("i32", col.size), arena.alloc("i32", nv),
+                           arena.alloc("i32", 1))
+        arena.fill(hr, row.tolist())
+        arena.fill(hc, col.tolist())
+        init = [-1] * nv
+        init[0] = 0
+        arena.fill(hl, init)
+        mk = _reference_kernel("bfs")
+        t0 = time.perf_counter()
+        with R.Runtime(arena, pool_size=pool) as rt:
+            cur = 0
+            while True:
+                arena.fill(hch, [0])
+                pk = H.PackedArgs([E.ArgSlot("handle", hr), E.ArgSlot("handle", hc), E.ArgSlot("handle", hl),
+                                   E.ArgSlot("handle", hch), E.ArgSlot("i32", nv), E.ArgSlot("i32", cur)])
+                rt.launch(mk, S.Dim3(-(-nv // 256)), S.Dim3(256), 0, pk)
+                rt.device_synchronize()
+                if arena.to_list(hch)[0] == 0:
+                    break
+                cur += 1
+        dt = time.perf_counter() - t0
+        ok = bool(np.array_equal(np.array(arena.to_list(hl), np.int32), want))
+        return {"elem_per_s": col.size / dt, "unit_elem": "edge", "seconds": round(dt, 3), "pool": pool,
+                "kind": "reference", "matches_oracle": ok,
+                "sample": f"blockfuse Runtime, bfs 2^{log_n} x 8 full traversal ({cur + 1} level launches), "
+                          f"pool {pool}"}
+    inst, elems = sample_instance(name, log_n)
+    if inst is None:
+        return None
+    want, _ = oracle.run(inst)
+    arena = A.DeviceArena()
+    handles = {}
     for b in inst.buffers:
-        b.length = n
-        b.values = [0.5] * n
-    inst.args[3] = ("i32", n)
-    arena = DeviceArena()
-    packed, _ = materialize(inst, arena)
-    pool = len(os.sched_getaffinity(0))
-    mk = case.compiled()
+        h = arena.alloc(b.scalar, b.length)
+        arena.fill(h, np.asarray(b.values).reshape(-1)[: b.length].tolist())
+        handles[b.name] = h
+    pk = H.PackedArgs([E.ArgSlot("handle", handles[a[1]]) if a[0] == "buf" else E.ArgSlot(a[0], a[1])
+                       for a in inst.args])
+    mk = _reference_kernel(inst.kernel)
+    g = S.Dim3(inst.grid.x, inst.grid.y, inst.grid.z)
+    bl = S.Dim3(inst.block.x, inst.block.y, inst.block.z)
     t0 = time.perf_counter()
-    with Runtime(arena, pool_size=pool) as rt:
-        rt.launch(mk, inst.grid, inst.block, 0, packed)
+    with R.Runtime(arena, pool_size=pool) as rt:
+        rt.launch(mk, g, bl, inst.shmem, pk)
         rt.device_synchronize()
     dt = time.perf_counter() - t0
-    return {"elem_per_s": n / dt, "gbs": 12 * n / dt / 1e9, "cores": pool, "kind": "reference",
-            "sample": f"blockfuse Runtime, vecadd {n} elements, pool {pool}, {dt:.2f} s"}
+    ok = True
+    for o in inst.outputs:
+        got = np.array(arena.to_list(handles[o]), dtype=want[o].dtype)
+        if inst.kernel == "kmeans" and o == "sums":
+            ok &= bool(np.allclose(got, want[o], rtol=1e-4, atol=1e-4))
+        else:
+            ok &= bool(np.array_equal(got.view(np.uint8), want[o].view(np.uint8)))
+    return {"elem_per_s": elems / dt, "seconds": round(dt, 3), "pool": pool, "kind": "reference",
+            "matches_oracle": ok,
+            "sample": f"blockfuse Runtime, {name} 2^{log_n} ({elems} elements), grid "
+                      f"{inst.grid.x}x{inst.grid.y} x block {inst.block.x}x{inst.block.y}, pool {pool}"}

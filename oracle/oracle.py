@@ -86,6 +86,9 @@ def run(inst, nthreads: int = 1, block_range=None):
     k = inst.kernel
     fn = getattr(L, "or_" + k)
     extra = []
+    if k == "kmeans" and nthreads > 1:  # membership/counts exact, sums within rounding
+        fn = L.or_kmeans_mt
+        extra = [C.c_int(nthreads)]
     if k == "reverse":
         extra = [C.c_longlong(inst.shmem)]
     elif k == "wreduce":
@@ -95,6 +98,73 @@ def run(inst, nthreads: int = 1, block_range=None):
     fn(g, *argv, *extra, C.byref(t))
     trap = None if t.kind == 0 else (TRAP_NAMES.get(t.kind, "?"), t.block)
     return bufs, trap
+
+
+# buffers that several blocks accumulate into (atomic adds / flag stores):
+# each host thread of run_par gets a private zeroed copy, summed afterwards
+ACCUMULATE = {"hist": ("counts",), "wreduce": ("out",), "kmeans": ("sums", "counts"), "bfs": ("changed",)}
+
+
+def run_par(inst, nthreads: int):
+    """The launch split into `nthreads` contiguous logical-block ranges run
+    concurrently on host threads (the reference's own worker-pool execution,
+    runtime.py:305-350, with the average grain): ctypes releases the GIL, the
+    block range is thread-local in oracle.c.  Disjoint outputs are shared;
+    accumulated buffers (ACCUMULATE) are private per thread and added in
+    thread order (integers: exact; kmeans f32 sums: within rounding); the
+    bfs `changed` flag is OR-ed.  Returns (outputs, trap) like run()."""
+    import concurrent.futures as cf
+    G = inst.grid.x * inst.grid.y * inst.grid.z
+    nthreads = max(1, min(nthreads, G))
+    if nthreads == 1:
+        return run(inst)
+    L = lib()
+    bufs = {b.name: _arr(b) for b in inst.buffers}
+    acc = ACCUMULATE.get(inst.kernel, ())
+    g = Geom(inst.grid.x, inst.grid.y, inst.grid.z, inst.block.x, inst.block.y, inst.block.z)
+    fn = getattr(L, "or_" + inst.kernel)
+    extra = []
+    if inst.kernel == "reverse":
+        extra = [C.c_longlong(inst.shmem)]
+    elif inst.kernel == "wreduce":
+        extra = [C.c_int(inst.warp_size)]
+    elif inst.kernel in ("hotspot", "nn"):
+        extra = [C.c_int(1)]
+    cuts = [G * i // nthreads for i in range(nthreads + 1)]
+    priv = [{name: np.zeros_like(bufs[name]) for name in acc} for _ in range(nthreads)]
+
+    def work(i):
+        L.or_set_range(C.c_longlong(cuts[i]), C.c_longlong(cuts[i + 1] - cuts[i]))
+        argv = []
+        for a in inst.args:
+            if a[0] == "buf":
+                arr = priv[i][a[1]] if a[1] in acc else bufs[a[1]]
+                argv += [_ptr(arr), C.c_longlong(arr.size)]
+            elif a[0] == "i32":
+                argv.append(C.c_int(int(a[1])))
+            elif a[0] == "i64":
+                argv.append(C.c_longlong(int(a[1])))
+            else:
+                argv.append(C.c_double(float(a[1])))
+        t = OTrap()
+        fn(g, *argv, *extra, C.byref(t))
+        L.or_set_range(C.c_longlong(0), C.c_longlong(-1))
+        return None if t.kind == 0 else (TRAP_NAMES.get(t.kind, "?"), t.block)
+
+    with cf.ThreadPoolExecutor(nthreads) as ex:
+        traps = list(ex.map(work, range(nthreads)))
+    for name in acc:
+        base = bufs[name]
+        if inst.kernel == "bfs":
+            base |= np.bitwise_or.reduce([p[name] for p in priv])
+        elif base.dtype == np.float32:
+            for p in priv:
+                base[:] = (base.astype(np.float64) + p[name]).astype(np.float32)
+        else:
+            tot = base.astype(np.int64) + sum(p[name].astype(np.int64) for p in priv)
+            base[:] = ((tot + 2**31) % 2**32 - 2**31).astype(base.dtype)
+    hit = [t for t in traps if t is not None]
+    return bufs, (min(hit, key=lambda t: t[1]) if hit else None)
 
 
 def bfs_full(row: np.ndarray, col: np.ndarray, nv: int, source: int = 0) -> tuple[np.ndarray, int]:

@@ -34,6 +34,24 @@ def test_reference_arm_contract():
     assert d["value"] > 0 and d["config"]["workload"].startswith("hotspot")
 
 
+def test_gpus_n_spawns_ranks():
+    """`--gpus 2` without a launcher re-execs under torchrun: two ranks run
+    (the reference arm prints once, from rank 0, with n_gpus = the world)."""
+    d = _run(["--impl", "reference", "--gpus", "2", "--size", "128", "--iters", "2", "--steps", "1",
+              "--warmup", "0", "--cpu-budget", "0.1"], timeout=300)
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_gpus_n_fails_loudly_without_gpus():
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("enough GPUs here")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=str(ROOT))
+    assert r.returncode != 0 and "requested but only" in r.stderr
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
 @pytest.mark.gpu
 def test_our_arm_contract_small():
     if not has_gpu():
@@ -46,3 +64,5 @@ def test_our_arm_contract_small():
     assert d["gpu_launches"] == 30 and d["value"] > 0 and 0 < d["roofline"]["frac"] < 1.5
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
+    assert d["e2e"]["checked"] is True
+    assert d["launch_latency"]["launch_sync_us"] > 0
