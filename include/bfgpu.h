@@ -127,6 +127,12 @@ int bf_arena_destroy(bf_arena *arena);
 int bf_alloc(bf_arena *arena, int32_t scalar, int64_t length, uint32_t *handle);
 /* DeviceArena.free (arena.py:86-87); orders after launches in flight. */
 int bf_free(bf_arena *arena, uint32_t handle);
+/* An element-range view [first, first + length) of a buffer under a new
+ * handle (no copy; the reference has no views — this is the multi-GPU
+ * partitioner's way to hand one rank's element range of a grid-stride
+ * launch to the unchanged kernel, parallel.py).  The offset must be 16 B
+ * aligned; the parent cannot be freed while views of it are live. */
+int bf_view(bf_arena *arena, uint32_t handle, int64_t first, int64_t length, uint32_t *view);
 /* DeviceArena.scalar_type / length (arena.py:95-99) plus the device pointer. */
 int bf_buffer_info(bf_arena *arena, uint32_t handle, int32_t *scalar,
                    int64_t *length, uint64_t *device_ptr);
@@ -260,6 +266,11 @@ int bf_bfs_shard_bitmap(bf_bfs_shard *s, void **dev_ptr, int64_t *words);
 int bf_bfs_shard_begin(bf_bfs_shard *s, int32_t source, int64_t vlo, int64_t vhi);
 int bf_bfs_shard_expand(bf_bfs_shard *s, uint32_t row, uint32_t col);
 int bf_bfs_shard_merge(bf_bfs_shard *s, const void *gathered_dev, int32_t world);
+/* One rank's bitmap slice after an all-to-all of the world bitmaps:
+ * now[first + i] = OR over r < world of recv[r * count + i] (the visited
+ * bitmap has 64 zero words of padding past `words`). */
+int bf_bfs_shard_merge_slice(bf_bfs_shard *s, const void *recv_dev, int32_t world, int64_t first,
+                             int64_t count);
 int bf_bfs_shard_compact(bf_bfs_shard *s, uint32_t lvl, int64_t *fresh);
 int bf_bfs_shard_finish(bf_bfs_shard *s, uint32_t lvl, int32_t *depth);
 

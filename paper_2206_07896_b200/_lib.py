@@ -28,7 +28,7 @@ FLAG_INSTRUMENT = 0x2
 
 EXPORTS = [
     "bf_abi_version", "bf_last_error", "bf_device_count",
-    "bf_arena_create", "bf_arena_destroy", "bf_alloc", "bf_free", "bf_buffer_info",
+    "bf_arena_create", "bf_arena_destroy", "bf_alloc", "bf_free", "bf_view", "bf_buffer_info",
     "bf_upload", "bf_download", "bf_fill32", "bf_copy",
     "bf_queue_create", "bf_queue_destroy", "bf_queue_push", "bf_queue_fetch",
     "bf_queue_close", "bf_queue_is_empty", "bf_queue_task", "bf_queue_counters",
@@ -39,7 +39,7 @@ EXPORTS = [
     "bf_kernel_count", "bf_kernel_info",
     "bf_bfs_levels", "bf_hotspot_run", "bf_jit_register",
     "bf_bfs_shard_create", "bf_bfs_shard_destroy", "bf_bfs_shard_bitmap", "bf_bfs_shard_begin",
-    "bf_bfs_shard_expand", "bf_bfs_shard_merge", "bf_bfs_shard_compact", "bf_bfs_shard_finish",
+    "bf_bfs_shard_expand", "bf_bfs_shard_merge", "bf_bfs_shard_merge_slice", "bf_bfs_shard_compact", "bf_bfs_shard_finish",
     "bf_kmeans_update",
 ]
 
@@ -90,6 +90,7 @@ def _declare(lib) -> None:
         "bf_arena_destroy": (C.c_int, [P]),
         "bf_alloc": (C.c_int, [P, i32, i64, U32P]),
         "bf_free": (C.c_int, [P, u32]),
+        "bf_view": (C.c_int, [P, u32, i64, i64, C.POINTER(u32)]),
         "bf_buffer_info": (C.c_int, [P, u32, I32P, I64P, U64P]),
         "bf_upload": (C.c_int, [P, u32, P, i64, i64]),
         "bf_download": (C.c_int, [P, u32, P, i64, i64]),
@@ -124,6 +125,7 @@ def _declare(lib) -> None:
         "bf_bfs_shard_begin": (C.c_int, [P, i32, i64, i64]),
         "bf_bfs_shard_expand": (C.c_int, [P, u32, u32]),
         "bf_bfs_shard_merge": (C.c_int, [P, P, i32]),
+        "bf_bfs_shard_merge_slice": (C.c_int, [P, P, i32, i64, i64]),
         "bf_bfs_shard_compact": (C.c_int, [P, u32, I64P]),
         "bf_bfs_shard_finish": (C.c_int, [P, u32, I32P]),
         "bf_kmeans_update": (C.c_int, [P, u32, u32, u32, i32, i32, u32, u32, i64, i64, I64P]),

@@ -99,6 +99,16 @@ class DeviceArena:
         check(_lib.lib().bf_free(self._ptr, handle))
         del self._meta[handle]
 
+    def view(self, handle: int, first: int, length: int) -> int:
+        """A new handle aliasing elements [first, first + length) of `handle`
+        (bf_view: no copy, 16 B-aligned offset); freed with free()."""
+        scalar, _ = self._buf(handle)
+        h = C.c_uint32()
+        check(_lib.lib().bf_view(self._ptr, handle, first, length, C.byref(h)))
+        self._meta[h.value] = (scalar, length)
+        self._bases[h.value] = self._bases[handle] + first * SCALAR_SIZE[scalar]
+        return h.value
+
     def _buf(self, handle: int) -> tuple[str, int]:
         m = self._meta.get(handle)
         if m is None:

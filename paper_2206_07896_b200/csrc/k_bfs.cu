@@ -1032,6 +1032,18 @@ __global__ void __launch_bounds__(256) bfs_merge_or(unsigned* now, const unsigne
   }
 }
 
+// one rank's slice of the visited bitmap after an all-to-all: recv holds the
+// world ranks' copies of words [first, first + count) back to back
+__global__ void __launch_bounds__(256) bfs_merge_slice(unsigned* now, const unsigned* __restrict__ recv,
+                                                       long long count, int world) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    unsigned v = 0;
+    for (int r = 0; r < world; r++) v |= __ldcs(recv + (long long)r * count + i);
+    now[i] = v;
+  }
+}
+
 // sizes: [0] own queue length, [1] next own queue length, [2] CSR error, [3] global fresh
 __global__ void __launch_bounds__(256) bfs_compact_sh(unsigned* now, unsigned* prev, long long words, int* nq,
                                                       int* sizes, unsigned char* lv8, int* lvl, int depth,
@@ -1590,7 +1602,10 @@ extern "C" int bf_bfs_shard_create_impl(int nv, void** out, char* err, int errca
   BfsShard* s = new BfsShard();
   s->nv = nv;
   s->words = ((long long)nv + 31) / 32;
-  cudaError_t e = cudaMalloc((void**)&s->now, s->words * 4);
+  // `now` carries 64 zero words of padding so an exchange can treat it as
+  // world x ceil(words / world) words for any world <= 64 (parallel.py)
+  cudaError_t e = cudaMalloc((void**)&s->now, (s->words + 64) * 4);
+  if (e == cudaSuccess) e = cudaMemset(s->now, 0, (s->words + 64) * 4);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->prev, s->words * 4);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->qa, (size_t)nv * 4);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->qb, (size_t)nv * 4);
@@ -1689,6 +1704,27 @@ extern "C" int bf_bfs_shard_merge_impl(void* p, void* stream_v, int num_sms, con
   const int grid = stream_grid(s->words, 256, num_sms, 8);
   bfs_merge_or<<<grid, 256, 0, stream>>>(s->now, (const unsigned*)gathered, s->words, world);
   cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
+    return BF_E_CUDA;
+  }
+  return BF_OK;
+}
+
+extern "C" int bf_bfs_shard_merge_slice_impl(void* p, void* stream_v, int num_sms, const void* recv, int world,
+                                             long long first, long long count, char* err, int errcap) {
+  using namespace bf;
+  BfsShard* s = (BfsShard*)p;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  if (first < 0 || count < 0 || first + count > s->words + 64) {
+    snprintf(err, errcap, "bfs shard: slice outside the bitmap");
+    return BF_E_INVALID;
+  }
+  if (count > 0) {
+    const int grid = stream_grid(count, 256, num_sms, 8);
+    bfs_merge_slice<<<grid, 256, 0, stream>>>(s->now + first, (const unsigned*)recv, count, world);
+  }
+  cudaError_t e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) {
     snprintf(err, errcap, "bfs shard: %s", cudaGetErrorString(e));
     return BF_E_CUDA;

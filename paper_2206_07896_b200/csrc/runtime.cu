@@ -214,6 +214,8 @@ struct Buffer {
   int32_t scalar;
   int64_t length;
   void* ptr;
+  uint32_t parent = 0;  // != 0: an element-range view of that buffer (owns no memory)
+  int32_t views = 0;    // live views of this buffer
 };
 
 }  // namespace bf
@@ -614,7 +616,8 @@ int bf_arena_destroy(bf_arena* a) {
 static void arena_free(bf_arena* a) {
   set_device(a->device);
   cudaDeviceSynchronize();
-  for (auto& kv : a->buffers) cudaFree(kv.second.ptr);
+  for (auto& kv : a->buffers)
+    if (!kv.second.parent) cudaFree(kv.second.ptr);
   release_zombies(a);
   for (int i = 0; i < 2; i++) {
     if (a->staging[i]) cudaFreeHost(a->staging[i]);
@@ -656,6 +659,15 @@ int bf_free(bf_arena* a, uint32_t h) {
     auto it = a->buffers.find(h);
     if (it == a->buffers.end())
       return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+    if (it->second.views > 0)
+      return fail(BF_E_INVALID, "buffer " + std::to_string(h) + " still has " +
+                                    std::to_string(it->second.views) + " live view(s)");
+    if (it->second.parent) {  // a view: the parent keeps the memory
+      auto p = a->buffers.find(it->second.parent);
+      if (p != a->buffers.end()) p->second.views--;
+      a->buffers.erase(it);
+      return BF_OK;
+    }
     a->zombies.push_back(it->second.ptr);
     a->buffers.erase(it);
   }
@@ -664,6 +676,26 @@ int bf_free(bf_arena* a, uint32_t h) {
     cudaDeviceSynchronize();
     release_zombies(a);
   }
+  return BF_OK;
+}
+
+int bf_view(bf_arena* a, uint32_t h, int64_t first, int64_t length, uint32_t* handle) {
+  if (!a || !handle) return fail(BF_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(a->mu);
+  auto it = a->buffers.find(h);
+  if (it == a->buffers.end()) return fail(BF_E_DANGLING, "dangling buffer handle " + std::to_string(h));
+  Buffer& b = it->second;
+  if (first < 0 || length < 0 || first + length > b.length)
+    return fail(BF_E_INVALID, "view [" + std::to_string(first) + ", " + std::to_string(first + length) +
+                                  ") outside buffer of " + std::to_string(b.length) + " elements");
+  const int64_t off = first * kScalarSize[b.scalar];
+  if (off % 16)
+    return fail(BF_E_INVALID, "view offset of " + std::to_string(off) + " bytes is not 16 B aligned");
+  const uint32_t root = b.parent ? b.parent : h;
+  uint32_t v = a->next_handle++;
+  a->buffers[v] = Buffer{b.scalar, length, (char*)b.ptr + off, root, 0};
+  a->buffers[root].views++;
+  *handle = v;
   return BF_OK;
 }
 
@@ -1348,6 +1380,8 @@ int bf_bfs_shard_expand_impl(void* p, void* stream, int num_sms, const int* row,
                              long long lcol, char* err, int errcap);
 int bf_bfs_shard_merge_impl(void* p, void* stream, int num_sms, const void* gathered, int world, char* err,
                             int errcap);
+int bf_bfs_shard_merge_slice_impl(void* p, void* stream, int num_sms, const void* recv, int world, long long first,
+                                  long long count, char* err, int errcap);
 int bf_bfs_shard_compact_impl(void* p, void* stream, int num_sms, int* lvl, long long ll, long long* fresh,
                               char* err, int errcap);
 int bf_bfs_shard_finish_impl(void* p, void* stream, int num_sms, int* lvl, long long ll, int* depth, char* err,
@@ -1424,6 +1458,15 @@ int bf_bfs_shard_merge(bf_bfs_shard* s, const void* gathered, int32_t world) {
   char err[256] = {0};
   int rc = bf_bfs_shard_merge_impl(s->impl, (void*)s->rt->streams[0], s->rt->num_sms, gathered, world, err,
                                    sizeof(err));
+  return rc ? fail(rc, err) : BF_OK;
+}
+
+int bf_bfs_shard_merge_slice(bf_bfs_shard* s, const void* recv, int32_t world, int64_t first, int64_t count) {
+  BFS_SHARD_PRE(s);
+  if (!recv || world < 1) return fail(BF_E_INVALID, "bad received slices");
+  char err[256] = {0};
+  int rc = bf_bfs_shard_merge_slice_impl(s->impl, (void*)s->rt->streams[0], s->rt->num_sms, recv, world, first,
+                                         count, err, sizeof(err));
   return rc ? fail(rc, err) : BF_OK;
 }
 

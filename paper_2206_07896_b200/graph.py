@@ -55,6 +55,22 @@ class BfsShard:
     def merge(self, gathered_ptr: int, world: int) -> None:
         self._call("bf_bfs_shard_merge", self._h, C.c_void_p(gathered_ptr), world)
 
+    def bitmap_tensor(self, world: int):
+        """The visited bitmap as a torch int32 device view of world x
+        ceil(words / world) words (the shard pads it with 64 zero words)."""
+        import torch
+
+        from .parallel import _device_view, bitmap_slices
+        if world > 64:
+            raise ValueError("the bitmap padding covers at most 64 ranks")
+        ptr, words = self.bitmap()
+        return _device_view(ptr, world * bitmap_slices(words, world),
+                            torch.device("cuda", self.rt.arena.device))
+
+    def merge_slice(self, recv, world: int, first: int, count: int) -> None:
+        """now[first + i] = OR over r of recv[r * count + i] (device tensor)."""
+        self._call("bf_bfs_shard_merge_slice", self._h, C.c_void_p(recv.data_ptr()), world, first, count)
+
     def compact(self, lvl: int) -> int:
         fresh = C.c_int64()
         self._call("bf_bfs_shard_compact", self._h, lvl, C.byref(fresh))

@@ -23,9 +23,10 @@ data need a collective:
     with one all-gather when the caller wants it replicated.
   * bfs level step — monotone levels and flag: all-reduce MAX.
   * bfs whole traversal (bfs_levels_sharded) — ranks own vertex ranges and
-    expand only their frontier; per level one all-gather of the nv-bit
-    visited bitmap (8 MB at 2^26 vertices) merged by OR, after which every
-    rank sees the same fresh set (same levels, same loop exit).
+    expand only their frontier; per level the nv-bit visited bitmap (8 MB at
+    2^26 vertices) is OR-reduced by an all-to-all of slices, a per-slice OR
+    and an all-gather (~2 bitmaps received per rank), after which every rank
+    sees the same fresh set (same levels, same loop exit).
 
 Everything here is backend-agnostic torch.distributed (NCCL on GPUs, gloo in
 the CPU tests).
@@ -147,9 +148,14 @@ class _null:
 #             reference's own atomics);
 #   "max"   — monotone flags/levels (bfs: lvl only moves -1 -> cur+1, changed
 #             0 -> 1): all-reduce MAX;
-#   "owned" — disjoint writes: every rank keeps the values it changed, merged
-#             by an all-gather of (changed mask, values) — generic over any
-#             kernel whose blocks write disjoint elements.
+#   "owned" — disjoint writes.  Where the kernel's index map sends a block
+#             range to a contiguous element range (owned_ranges: 1-D launches
+#             of vecadd / nn / kmeans / reduce, Rodinia's 1 x n/16 backprop
+#             grid), every rank contributes exactly its range and one
+#             all-gather of ceil-padded ranges assembles the buffer: each
+#             rank receives about one buffer's worth, not world copies.  Other
+#             geometries (duplicated threads, 2-D grids) fall back to a
+#             generic all-gather of (changed mask, values).
 # ---------------------------------------------------------------------------
 
 COMBINE = {
@@ -168,14 +174,89 @@ COMBINE = {
 }
 
 
+def _block_span(kernel: str, buf: str, grid, block, scalars: dict, b0: int, b1: int):
+    """[lo, hi) bounding every element that logical blocks [b0, b1) can
+    write in `buf` (before clipping), or None when the index map is not a
+    contiguous function of the block id for this geometry."""
+    one_d = grid.y == 1 and grid.z == 1
+    if b1 <= b0:
+        return (0, 0)
+    if kernel in ("vecadd", "nn", "kmeans") and buf in ("c", "d", "member"):
+        # id = blockIdx.x * blockDim.x + threadIdx.x  (corpus/vecadd.kn, kernels/nn.kn, kmeans.kn)
+        if one_d and block.y == 1 and block.z == 1:
+            return b0 * block.x, b1 * block.x
+        return None
+    if kernel == "reduce" and buf == "out" and one_d:
+        return b0, b1  # out[blockIdx.x] (corpus/reduce.kn)
+    if kernel in ("bpnn_layerforward", "bpnn_adjust_weights") and grid.x == 1 and grid.z == 1 \
+            and block.z == 1 and block.x <= 16 and block.y <= 16:
+        hid = scalars["hid"]
+        if hid < 0:
+            return None
+        if buf in ("w", "oldw"):
+            # index = (hid+1)*(16*by + ty + 1) + tx + 1 (kernels/backprop.kn); adjust's block 0
+            # also writes the bias row w[1..16]
+            lo = (hid + 1) * (16 * b0 + 1) + 1
+            if b0 == 0 and kernel == "bpnn_adjust_weights":
+                lo = 1
+            hi = (hid + 1) * (16 * (b1 - 1) + block.y) + block.x + 1
+            return lo, hi
+        if buf == "partial":
+            return b0 * hid, (b1 - 1) * hid + block.y  # partial[by*hid + ty]
+    return None
+
+
+def owned_ranges(kernel: str, buf: str, grid, block, scalars: dict, length: int, world: int):
+    """Per-rank [lo, hi) element ranges of an "owned" buffer under the
+    rank_range block split, clipped to the buffer; None when the map is not
+    contiguous or the ranks' ranges would overlap (then the masked combine
+    is used)."""
+    total = grid.x * grid.y * grid.z
+    out = []
+    for r in range(world):
+        b0, b1 = rank_range(total, world, r)
+        span = _block_span(kernel, buf, grid, block, scalars, b0, b1)
+        if span is None:
+            return None
+        lo, hi = max(0, min(span[0], length)), max(0, min(span[1], length))
+        out.append((lo, max(lo, hi)))
+    nonempty = sorted(x for x in out if x[1] > x[0])
+    if any(a[1] > b[0] for a, b in zip(nonempty, nonempty[1:])):
+        return None
+    return out
+
+
+def gather_ranges(t, ranges, rank: int) -> None:
+    """Replicate a 1-D tensor whose ranks each hold the final values of
+    their own disjoint [lo, hi): one all-gather of ceil-padded pieces, then
+    every rank writes the others' pieces in place.  Received bytes per rank
+    = world x the largest piece (~ the buffer), not world x the buffer."""
+    import torch
+    import torch.distributed as dist
+    world = len(ranges)
+    width = max((hi - lo for lo, hi in ranges), default=0)
+    if width == 0:
+        return
+    lo, hi = ranges[rank]
+    send = torch.zeros(width, dtype=t.dtype, device=t.device)
+    send[:hi - lo] = t[lo:hi]
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send)
+    for q, (a, b) in enumerate(ranges):
+        if q != rank and b > a:
+            t[a:b] = parts[q][:b - a]
+
+
 class Combiner:
     """Prepare (before the rank's launch) and combine (after it) the output
-    buffers of one sharded launch; tensors are 1-D torch views."""
+    buffers of one sharded launch; tensors are 1-D torch views.  `ranges`
+    maps owned buffers to their per-rank element ranges (owned_ranges)."""
 
-    def __init__(self, spec: dict, world: int, rank: int):
+    def __init__(self, spec: dict, world: int, rank: int, ranges: dict | None = None):
         self.spec = spec
         self.world = world
         self.rank = rank
+        self.ranges = ranges or {}
         self.before: dict = {}
 
     def prepare(self, tensors: dict) -> None:
@@ -183,7 +264,7 @@ class Combiner:
             t = tensors[name]
             if op == "sum" and self.rank != 0:
                 t.zero_()
-            elif op == "owned":
+            elif op == "owned" and self.ranges.get(name) is None:
                 self.before[name] = t.clone()
 
     def finish(self, tensors: dict) -> None:
@@ -196,6 +277,8 @@ class Combiner:
                 dist.all_reduce(t, op=dist.ReduceOp.SUM)
             elif op == "max":
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            elif self.ranges.get(name) is not None:
+                gather_ranges(t, self.ranges[name], self.rank)
             else:
                 b = self.before.pop(name)
                 changed = (t.view(torch.uint8).view(-1, t.element_size()) !=
@@ -210,21 +293,33 @@ class Combiner:
                 t.copy_(out)
 
 
+def _scalars(routine, packed) -> dict:
+    params = getattr(routine, "params", None) or ()
+    names = [p[0] if isinstance(p, tuple) else getattr(p, "name", "") for p in params]
+    return {n: s.value for n, s in zip(names, packed.slots) if s.kind != "handle"}
+
+
 def launch_sharded(rt, arena, routine, grid, block, shmem: int, packed, outputs: dict,
                    world: int, rank: int):
     """Run this rank's share of a launch and combine the outputs.
 
     outputs: {param name: buffer handle} of the buffers the kernel writes.
-    Returns the rank's KernelTask."""
+    Grid-1 grid-stride kernels (fir, hist_stride) are split by element
+    ranges instead (launch_sharded_strides).  Returns the rank's KernelTask."""
     import torch
     name = getattr(routine, "name", "")
+    if name in STRIDE_SPLIT and grid.x * grid.y * grid.z == 1:
+        return launch_sharded_strides(rt, arena, routine, block, packed, outputs, world, rank)
     spec = {p: op for p, op in COMBINE.get(name, {}).items() if p in outputs}
     if set(spec) != set(outputs):
         missing = set(outputs) - set(spec)
         raise ValueError(f"no combine rule for {name}: {sorted(missing)}")
     device = torch.device("cuda", arena.device)
     tensors = {p: torch.as_tensor(arena.cuda_array(h), device=device) for p, h in outputs.items()}
-    comb = Combiner(spec, world, rank)
+    sc = _scalars(routine, packed)
+    ranges = {p: owned_ranges(name, p, grid, block, sc, arena.length(outputs[p]), world)
+              for p, op in spec.items() if op == "owned"}
+    comb = Combiner(spec, world, rank, ranges)
     torch.cuda.synchronize(device)
     comb.prepare(tensors)
     torch.cuda.synchronize(device)
@@ -233,6 +328,98 @@ def launch_sharded(rt, arena, routine, grid, block, shmem: int, packed, outputs:
     if hi > first:
         task = rt.launch_range(routine, grid, block, shmem, packed, first, hi - first)
     rt.device_synchronize()
+    comb.finish(tensors)
+    torch.cuda.synchronize(device)
+    return task
+
+
+# ---------------------------------------------------------------------------
+# grid-1 grid-stride kernels (corpus fir.kn, hist_stride.kn): the single
+# logical block's loop `for j < m: ... t + j*blockDim.x ...` is split into
+# contiguous j ranges (output ranges with the (taps-1) read-only
+# halo for fir, element ranges + all-reduce for hist_stride).  Each rank
+# runs the unchanged kernel on element-range views of the buffers
+# (DeviceArena.view -> bf_view): fir reads x[j0*B, j1*B + taps - 1) and
+# writes y[j0*B, j1*B); hist_stride reads pix[j0*B, j1*B) and counts into its
+# own partial histogram, all-reduced.
+# ---------------------------------------------------------------------------
+
+# kernel -> (strided count param, {read/write buffer: halo elements}, combine)
+STRIDE_SPLIT = {
+    "fir": ("m", {"x": "taps-1", "y": 0}, {"y": "owned"}),
+    "hist_stride": ("k", {"pix": 0}, {"counts": "sum"}),
+}
+
+
+def stride_plan(kernel: str, bx: int, scalars: dict, lengths: dict, world: int, rank: int):
+    """This rank's j range and the element-range views it needs:
+    -> (j0, j1, {buffer: (first, length)}, {owned buffer: per-rank ranges}).
+    j ranges are whole multiples of `step` strides so that every view starts
+    16 B aligned (4-byte elements: j0 * bx % 4 == 0)."""
+    import math
+    count_param, views, combine = STRIDE_SPLIT[kernel]
+    m = max(0, scalars[count_param])
+    step = 4 // math.gcd(bx, 4)
+    units = -(-m // step)
+
+    def jr(r):
+        if units == 0:
+            return 0, 0
+        a, b = rank_range(units, world, r)
+        return min(a * step, m), min(b * step, m)
+    j0, j1 = jr(rank)
+    plan = {}
+    for buf, halo in views.items():
+        h = max(0, scalars["taps"] - 1) if halo == "taps-1" else 0
+        first = min(j0 * bx, lengths[buf])
+        plan[buf] = (first, max(0, min(j1 * bx + h, lengths[buf]) - first))
+    owned = {}
+    for buf, op in combine.items():
+        if op == "owned":
+            owned[buf] = [(min(a * bx, lengths[buf]), min(b * bx, lengths[buf]))
+                          for a, b in (jr(r) for r in range(world))]
+    return j0, j1, plan, owned
+
+
+def launch_sharded_strides(rt, arena, routine, block, packed, outputs: dict, world: int, rank: int):
+    """Element-range shard of a grid-1 grid-stride launch (fir, hist_stride)."""
+    import torch
+
+    from . import ArgSlot, Dim3, PackedArgs
+    name = routine.name
+    params = [p[0] for p in routine.params]
+    count_param, views, combine = STRIDE_SPLIT[name]
+    if set(outputs) != set(combine):
+        raise ValueError(f"{name}: outputs must be {sorted(combine)}")
+    handles = {n: s.value for n, s in zip(params, packed.slots) if s.kind == "handle"}
+    sc = _scalars(routine, packed)
+    lengths = {n: arena.length(h) for n, h in handles.items()}
+    j0, j1, plan, owned = stride_plan(name, block.x, sc, lengths, world, rank)
+    device = torch.device("cuda", arena.device)
+    tensors = {p: torch.as_tensor(arena.cuda_array(h), device=device) for p, h in outputs.items()}
+    comb = Combiner(combine, world, rank, owned)
+    torch.cuda.synchronize(device)
+    comb.prepare(tensors)
+    torch.cuda.synchronize(device)
+    task = None
+    made = []
+    try:
+        if j1 > j0:
+            slots = []
+            for pname, s in zip(params, packed.slots):
+                if pname in plan:
+                    v = arena.view(handles[pname], *plan[pname])
+                    made.append(v)
+                    slots.append(ArgSlot("handle", v))
+                elif pname == count_param:
+                    slots.append(ArgSlot(s.kind, j1 - j0))
+                else:
+                    slots.append(s)
+            task = rt.launch(routine, Dim3(1), block, 0, PackedArgs(slots))
+        rt.device_synchronize()
+    finally:
+        for v in made:
+            arena.free(v)
     comb.finish(tensors)
     torch.cuda.synchronize(device)
     return task
@@ -321,40 +508,65 @@ def gpu_topk_select(rt, arena, d_handle: int, n_local: int):
 # ---------------------------------------------------------------------------
 
 def bfs_levels_sharded(shard, row: int, col: int, lvl: int, nv: int, source: int, world: int, rank: int,
-                       gather: Callable) -> int:
+                       exchange: Callable) -> int:
     """Whole traversal over `world` ranks (per-level frontier
-    exchange).  `shard` provides begin/expand/merge/compact/finish/bitmap
-    (graph.BfsShard on a GPU); `gather(bitmap)` returns the world bitmaps in
-    rank order as one flat buffer (device pointer for the native shard).
-    Returns max level + 1; `lvl` ends identical on every rank."""
+    exchange).  `shard` provides begin/expand/compact/finish (graph.BfsShard
+    on a GPU); `exchange(shard)` leaves the shard's visited bitmap equal to
+    the OR of all ranks' bitmaps (bitmap_exchange: all-to-all of
+    bitmap slices, OR per owned slice, all-gather).  Returns max level + 1;
+    `lvl` ends identical on every rank."""
     lo, hi = rank_range(nv, world, rank)
     shard.begin(source, lo, hi)
     while True:
         shard.expand(row, col)
         if world > 1:
-            shard.merge(gather(shard), world)
+            exchange(shard)
         if shard.compact(lvl) == 0:
             break
     return shard.finish(lvl)
 
 
-def nccl_bitmap_gather(world: int, device):
-    """gather() for bfs_levels_sharded over torch.distributed (NCCL on GPUs):
-    all_gather_into_tensor of the shard's bitmap; returns the device pointer
-    of the gathered [world x words] buffer (kept alive by the closure)."""
+def bitmap_slices(words: int, world: int) -> int:
+    """Words per rank slice of the exchange: ceil(words / world) (the
+    bitmap is padded to world x slice words)."""
+    return -(-words // world)
+
+
+def bitmap_exchange(world: int, rank: int, stream=None):
+    """exchange() for bfs_levels_sharded over torch.distributed (NCCL on
+    GPUs; gloo with the CPU test shard).  The shard exposes its visited
+    bitmap as world x g words, g = ceil(words / world) (bitmap_tensor), and
+    rank r owns words [r*g, (r+1)*g):
+      1. all_to_all_single: rank r receives every rank's copy of its slice;
+      2. shard.merge_slice ORs them into its own slice (on the device:
+         bf_bfs_shard_merge_slice);
+      3. all-gather of the slices (in place on NCCL): every rank gets all.
+    Bytes received per rank and level: 2 x (world-1)/world x the bitmap
+    (8 MB at 2^26 vertices), where an all-gather of whole bitmaps would
+    move (world-1) x the bitmap."""
     import torch
     import torch.distributed as dist
-    state = {}
 
-    def gather(shard):
-        ptr, words = shard.bitmap()
-        if "buf" not in state or state["buf"].numel() != world * words:
-            state["buf"] = torch.empty(world * words, dtype=torch.int32, device=device)
-        mine = _device_view(ptr, words, device)
-        dist.all_gather_into_tensor(state["buf"], mine)
-        torch.cuda.current_stream(device).synchronize()
-        return state["buf"].data_ptr()
-    return gather
+    def exchange(shard):
+        now = shard.bitmap_tensor(world)
+        g = now.numel() // world
+        recv = torch.empty_like(now)
+        ctx = torch.cuda.stream(stream) if (stream is not None and now.is_cuda) else _null()
+        with ctx:
+            dist.all_to_all_single(recv, now)
+            if now.is_cuda:
+                torch.cuda.current_stream(now.device).synchronize()
+        shard.merge_slice(recv, world, rank * g, g)
+        with ctx:
+            mine = now[rank * g:(rank + 1) * g]
+            if now.is_cuda:
+                dist.all_gather_into_tensor(now, mine)
+                torch.cuda.current_stream(now.device).synchronize()
+            else:
+                parts = [torch.empty_like(mine) for _ in range(world)]
+                dist.all_gather(parts, mine.clone())
+                shard.set_bitmap(torch.cat(parts))
+    return exchange
 
 
 def _device_view(ptr: int, n: int, device):

@@ -377,6 +377,41 @@ def test_launch_range_covers_grid():
             assert bit_equal(arena.to_numpy(handles[buf]), want[buf]), inst.kernel
 
 
+def test_arena_views():
+    """DeviceArena.view (bf_view): an aliasing element range under a new
+    handle; kernels launched on views see exactly that range; 16 B offsets
+    only; a parent with live views cannot be freed."""
+    from paper_2206_07896_b200 import ArgSlot, DeviceArena, Dim3, PackedArgs, Runtime, routines
+    from paper_2206_07896_b200._lib import BfError
+    arena = DeviceArena()
+    n = 4096
+    a, b, c = (arena.alloc("f32", n) for _ in range(3))
+    x = np.arange(n, dtype=np.float32)
+    arena.upload_numpy(a, x)
+    arena.upload_numpy(b, 2 * x)
+    va, vb, vc = (arena.view(h, 1024, 512) for h in (a, b, c))
+    assert arena.length(va) == 512 and arena.scalar_type(va) == "f32"
+    assert bit_equal(arena.to_numpy(va), x[1024:1536])
+    with Runtime(arena) as rt:
+        rt.launch(routines.get("vecadd"), Dim3(2), Dim3(256), 0,
+                  PackedArgs([ArgSlot("handle", va), ArgSlot("handle", vb), ArgSlot("handle", vc),
+                              ArgSlot("i32", 512)]))
+        rt.device_synchronize()
+    got = arena.to_numpy(c)
+    want = np.zeros(n, np.float32)
+    want[1024:1536] = 3 * x[1024:1536]
+    assert bit_equal(got, want)
+    with pytest.raises(BfError):
+        arena.view(a, 1, 8)  # 4 B offset: not 16 B aligned
+    with pytest.raises(BfError):
+        arena.view(a, n - 4, 8)  # past the end
+    with pytest.raises(BfError):
+        arena.free(a)  # live view
+    for v in (va, vb, vc):
+        arena.free(v)
+    arena.free(a)
+
+
 def test_launch_sharded_single_rank_nccl():
     """parallel.launch_sharded end to end on the device (world of one, NCCL)."""
     import os
@@ -396,14 +431,18 @@ def test_launch_sharded_single_rank_nccl():
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
         rng = random.Random(41)
-        for inst in [I.vecadd(rng), I.hist(rng), I.kmeans(1000, 8, 4, 128, seed=2)]:
+        cases = [I.vecadd(rng), I.hist(rng), I.kmeans(1000, 8, 4, 128, seed=2), I.reduce(rng),
+                 I.backprop_adjust(96, seed=3)]
+        cases += [c for c in (I.fir(rng) for _ in range(6)) if oracle.run(c)[1] is None][:2]
+        cases += [I.hist_stride(rng) for _ in range(2)]
+        for inst in cases:
             want, _ = oracle.run(inst)
             arena = DeviceArena()
             packed, handles = materialize(inst, arena)
             outs = {n: handles[n] for n in COMBINE[inst.kernel]}
             with Runtime(arena) as rt:
-                launch_sharded(rt, arena, routines.get(inst.kernel), Dim3(inst.grid.x), Dim3(inst.block.x),
-                               0, packed, outs, 1, 0)
+                launch_sharded(rt, arena, routines.get(inst.kernel), Dim3(inst.grid.x, inst.grid.y, inst.grid.z),
+                               Dim3(inst.block.x, inst.block.y, inst.block.z), 0, packed, outs, 1, 0)
             for n in outs:
                 g = arena.to_numpy(handles[n])
                 if n == "sums":
@@ -423,8 +462,7 @@ def test_bfs_shards_on_one_device_vs_oracle(world):
     import torch
     import instances as I
     from paper_2206_07896_b200 import DeviceArena, Runtime, graph
-    from paper_2206_07896_b200.parallel import _device_view, rank_range
-    dev = torch.device("cuda", 0)
+    from paper_2206_07896_b200.parallel import rank_range
     for nv, deg, seed, src in [(20000, 8, 5, 0), (3001, 2, 6, 3000), (257, 1, 7, 9)]:
         row, col = I.random_graph(nv, deg, seed)
         want, depth = oracle.bfs_full(row, col, nv, src)
@@ -440,11 +478,19 @@ def test_bfs_shards_on_one_device_vs_oracle(world):
             while True:
                 for s in shards:
                     s.expand(hr, hc)
-                views = [_device_view(*s.bitmap(), dev) for s in shards]
-                gathered = torch.cat(views)
+                # the bitmap exchange (parallel.bitmap_exchange) emulated on one
+                # device: all-to-all of slices, per-slice OR, all-gather
+                views = [s.bitmap_tensor(world) for s in shards]
+                g = views[0].numel() // world
                 torch.cuda.synchronize()
-                for s in shards:
-                    s.merge(gathered.data_ptr(), world)
+                for r, s in enumerate(shards):
+                    recv = torch.cat([v[r * g:(r + 1) * g] for v in views])
+                    s.merge_slice(recv, world, r * g, g)
+                for r in range(world):
+                    for q in range(world):
+                        if q != r:
+                            views[q][r * g:(r + 1) * g] = views[r][r * g:(r + 1) * g]
+                torch.cuda.synchronize()
                 fresh = [s.compact(lv[r]) for r, s in enumerate(shards)]
                 assert len(set(fresh)) == 1
                 if fresh[0] == 0:
@@ -465,7 +511,7 @@ def test_bfs_levels_sharded_nccl_world1():
     import torch.distributed as dist
     import instances as I
     from paper_2206_07896_b200 import DeviceArena, Runtime, graph
-    from paper_2206_07896_b200.parallel import bfs_levels_sharded, nccl_bitmap_gather
+    from paper_2206_07896_b200.parallel import bitmap_exchange, bfs_levels_sharded
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -482,10 +528,20 @@ def test_bfs_levels_sharded_nccl_world1():
         arena.upload_numpy(hc, col)
         with Runtime(arena) as rt:
             shard = graph.BfsShard(rt, nv)
-            got = bfs_levels_sharded(shard, hr, hc, hl, nv, 5, 1, 0,
-                                     nccl_bitmap_gather(1, torch.device("cuda", 0)))
+            got = bfs_levels_sharded(shard, hr, hc, hl, nv, 5, 1, 0, None)
+            assert got == depth
+            assert bit_equal(arena.to_numpy(hl), want)
+            # the NCCL exchange itself (all-to-all, slice OR, in-place all-gather)
+            # driven at every level: a world of one must leave the bitmap unchanged
+            ex = bitmap_exchange(1, 0)
+            shard.begin(5, 0, nv)
+            while True:
+                shard.expand(hr, hc)
+                ex(shard)
+                if shard.compact(hl) == 0:
+                    break
+            assert shard.finish(hl) == depth
             shard.close()
-        assert got == depth
         assert bit_equal(arena.to_numpy(hl), want)
     finally:
         dist.destroy_process_group()

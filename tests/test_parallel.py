@@ -123,7 +123,7 @@ def _shard_worker(rank, world, port, out_q):
 
         import instances as I
         import oracle
-        from paper_2206_07896_b200.parallel import COMBINE, Combiner, rank_range
+        from paper_2206_07896_b200.parallel import COMBINE, Combiner, owned_ranges, rank_range
         rng = _r.Random(77)
         cases = [I.vecadd(rng), I.reduce(rng), I.hist(rng), I.wreduce(rng), I.nn(3000, 128, seed=4),
                  I.kmeans(1500, 8, 5, 128, seed=5), I.bfs(4000, 4, cur=0, seed=6, block=128),
@@ -135,7 +135,14 @@ def _shard_worker(rank, world, port, out_q):
             # this rank's buffers start from the instance's initial values
             init = {b.name: torch.from_numpy(np.array(b.values, dtype=oracle._NP[b.scalar]).reshape(-1)[: b.length].copy())
                     for b in inst.buffers}
-            comb = Combiner(spec, world, rank)
+            from paper_2206_07896_b200 import routines as _routines
+            pnames = [p[0] for p in _routines.get(inst.kernel).params]
+            scal = {pn: a[1] for pn, a in zip(pnames, inst.args) if a[0] != "buf"}
+            ranges = {n: owned_ranges(inst.kernel, n, inst.grid, inst.block, scal, init[n].numel(), world)
+                      for n, op in spec.items() if op == "owned"}
+            # the contiguous owned-range combine covers every 1-D case here
+            assert all(r is not None for r in ranges.values()), (inst.kernel, ranges)
+            comb = Combiner(spec, world, rank, ranges)
             tens = {n: init[n] for n in spec}
             comb.prepare(tens)
             for b in inst.buffers:  # feed prepared values to the oracle run
@@ -191,38 +198,155 @@ def test_sharded_launches_match_single_launch(world):
                 assert np.array_equal(g.view(np.uint8), w.view(np.uint8)), (inst.kernel, name)
 
 
+def _stride_worker(rank, world, port, out_q):
+    """fir / hist_stride split by element ranges (parallel.stride_plan): the
+    rank runs the unchanged kernel (oracle) on its views, then the owned-y
+    gather or the counts all-reduce (Combiner)."""
+    sys.path[:0] = [str(ROOT), str(ROOT / "oracle")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import instances as I
+        import oracle
+        from paper_2206_07896_b200 import routines
+        from paper_2206_07896_b200.parallel import STRIDE_SPLIT, Combiner, stride_plan
+        results, worked = [], []
+        for inst in _stride_cases(I):
+            pnames = [p[0] for p in routines.get(inst.kernel).params]
+            scal = {pn: a[1] for pn, a in zip(pnames, inst.args) if a[0] != "buf"}
+            arrays = {b.name: np.array(b.values, dtype=oracle._NP[b.scalar]).reshape(-1)[:b.length].copy()
+                      for b in inst.buffers}
+            lengths = {n: a.size for n, a in arrays.items()}
+            bx = inst.block.x
+            j0, j1, plan, owned = stride_plan(inst.kernel, bx, scal, lengths, world, rank)
+            count_param, _, combine = STRIDE_SPLIT[inst.kernel]
+            tens = {n: torch.from_numpy(arrays[n]) for n in combine}
+            comb = Combiner(combine, world, rank, owned)
+            comb.prepare(tens)
+            worked.append(j1 - j0)
+            if j1 > j0:
+                sub = I.Instance(inst.kernel, inst.grid, inst.block, inst.shmem, [], [], inst.outputs)
+                for b in inst.buffers:
+                    if b.name in plan:
+                        f, ln = plan[b.name]
+                        sub.buffers.append(I.Buf(b.name, b.scalar, ln, arrays[b.name][f:f + ln].copy()))
+                    else:
+                        sub.buffers.append(I.Buf(b.name, b.scalar, b.length, arrays[b.name].copy()))
+                sub.args = [("i32", j1 - j0) if (a[0] != "buf" and pn == count_param) else a
+                            for pn, a in zip(pnames, inst.args)]
+                out, trap = oracle.run(sub)
+                assert trap is None
+                for n in combine:
+                    if n in plan:
+                        f, ln = plan[n]
+                        arrays[n][f:f + ln] = out[n]
+                    else:
+                        arrays[n][:] = out[n]
+            comb.finish(tens)
+            results.append({n: arrays[n].copy() for n in combine})
+        out_q.put((rank, results, worked))
+    finally:
+        dist.destroy_process_group()
+
+
+def _stride_cases(I):
+    import random as _r
+    rng = _r.Random(91)
+    cases = [I.fir(rng) for _ in range(4)] + [I.hist_stride(rng) for _ in range(4)]
+    # ragged block widths (views must stay 16 B aligned) and a long loop
+    n = 37 * 41
+    x = np.random.default_rng(5).uniform(-1, 1, n + 7).astype(np.float32)
+    w = np.random.default_rng(6).uniform(-1, 1, 8).astype(np.float32)
+    cases.append(I.Instance("fir", I.Geom(1), I.Geom(37), 0,
+                            [I.Buf("x", "f32", x.size, x), I.Buf("y", "f32", n, np.zeros(n, np.float32)),
+                             I.Buf("w", "f32", 8, w)],
+                            [("buf", "x"), ("buf", "y"), ("buf", "w"), ("i32", 8), ("i32", 41)], ["y"]))
+    pix = np.random.default_rng(7).integers(0, 1 << 16, 64 * 300).astype(np.int32)
+    cases.append(I.Instance("hist_stride", I.Geom(1), I.Geom(64), 0,
+                            [I.Buf("pix", "i32", pix.size, pix), I.Buf("counts", "i32", 13, np.zeros(13, np.int32))],
+                            [("buf", "pix"), ("buf", "counts"), ("i32", 300), ("i32", 13)], ["counts"]))
+    return cases
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_stride_sharded_fir_hist_stride(world):
+    """Grid-1 grid-stride kernels split by element ranges across ranks equal
+    the single launch bit for bit, and ranks > 0 do part of the work."""
+    import instances as I
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stride_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict((r, (res, wk)) for r, res, wk in (q.get(timeout=120) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cases = _stride_cases(I)
+    for k, inst in enumerate(cases):
+        want, trap = oracle.run(inst)
+        if trap is not None:
+            continue
+        for r in range(world):
+            for n, arr in got[r][0][k].items():
+                assert np.array_equal(arr.view(np.uint8), want[n].view(np.uint8)), (k, r, inst.kernel, n)
+    assert sum(got[r][1][k] for r in range(1, world) for k in range(len(cases))) > 0
+
+
 # ---- sharded BFS traversal (parallel.bfs_levels_sharded) --------------------
 
 class NumpyBfsShard:
     """CPU restatement of one bf_bfs_shard (TEST INFRASTRUCTURE): whole
-    visited set and levels, expansion of the owned frontier only."""
+    visited bitmap (uint32 words, bit i of word w = vertex 32w + i, 64 words
+    of zero padding) and levels, expansion of the owned frontier only."""
 
     def __init__(self, nv):
         self.nv = nv
+        self.words = (nv + 31) // 32
+
+    def _bits(self):
+        return np.unpackbits(self.now.view(np.uint8), bitorder="little")[:self.nv].astype(bool)
+
+    def _set_bits(self, b):
+        packed = np.packbits(b.astype(np.uint8), bitorder="little")
+        self.now[:] = 0
+        self.now.view(np.uint8)[:packed.size] = packed
 
     def begin(self, src, lo, hi):
         self.lo, self.hi = lo, hi
-        self.now = np.zeros(self.nv, bool)
-        self.now[src] = True
-        self.prev = self.now.copy()
+        self.now = np.zeros(self.words + 64, np.uint32)
+        b = np.zeros(self.nv, bool)
+        b[src] = True
+        self._set_bits(b)
+        self.prev = b.copy()
         self.lv = np.full(self.nv, -1, np.int32)
         self.lv[src] = 0
         self.q = [src] if lo <= src < hi else []
         self.depth = 0
 
     def expand(self, row, col):
+        b = self._bits()
         for u in self.q:
-            self.now[col[row[u]:row[u + 1]]] = True
+            b[col[row[u]:row[u + 1]]] = True
+        self._set_bits(b)
 
-    def bitmap(self):
-        return torch.from_numpy(self.now.astype(np.uint8))
+    def bitmap_tensor(self, world):
+        from paper_2206_07896_b200.parallel import bitmap_slices
+        return torch.from_numpy(self.now[:world * bitmap_slices(self.words, world)].view(np.int32))
 
-    def merge(self, gathered, world):
-        self.now |= gathered.reshape(world, self.nv).any(axis=0)
+    def merge_slice(self, recv, world, first, count):
+        r = recv.numpy().view(np.uint32).reshape(world, count)
+        self.now[first:first + count] = np.bitwise_or.reduce(r, axis=0)
+
+    def set_bitmap(self, t):
+        self.now[:t.numel()] = t.numpy().view(np.uint32)
 
     def compact(self, lvl):
-        fresh = self.now & ~self.prev
-        self.prev = self.now.copy()
+        b = self._bits()
+        fresh = b & ~self.prev
+        self.prev = b.copy()
         ids = np.flatnonzero(fresh)
         self.lv[ids] = self.depth + 1
         self.q = [int(v) for v in ids if self.lo <= v < self.hi]
@@ -239,18 +363,12 @@ def _bfs_shard_worker(rank, world, port, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import instances as I
-        from paper_2206_07896_b200.parallel import bfs_levels_sharded
+        from paper_2206_07896_b200.parallel import bfs_levels_sharded, bitmap_exchange
         results = []
         for nv, deg, seed, src in [(3000, 3, 1, 0), (5000, 8, 2, 4321), (400, 1, 3, 7)]:
             row, col = I.random_graph(nv, deg, seed)
             shard = NumpyBfsShard(nv)
-
-            def gather(sh):
-                mine = sh.bitmap()
-                parts = [torch.zeros_like(mine) for _ in range(world)]
-                dist.all_gather(parts, mine)
-                return torch.cat(parts).numpy().astype(bool)
-            depth = bfs_levels_sharded(shard, row, col, None, nv, src, world, rank, gather)
+            depth = bfs_levels_sharded(shard, row, col, None, nv, src, world, rank, bitmap_exchange(world, rank))
             results.append((shard.lv.copy(), depth))
         allres = [None] * world
         dist.all_gather_object(allres, results)
@@ -262,7 +380,8 @@ def _bfs_shard_worker(rank, world, port, out_q):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_bfs_levels_sharded_protocol(world):
-    """Vertex-range shards + per-level bitmap all-gather/OR: every rank ends
+    """Vertex-range shards + per-level bitmap exchange (all-to-all of slices,
+    OR, all-gather: parallel.bitmap_exchange): every rank ends
     with exactly the single-process levels (oracle) and the same depth."""
     import instances as I
     import oracle
