@@ -329,9 +329,11 @@ def run_ours(args) -> None:
     # the resident-path result after the region.
     h_temp = torch.from_numpy(temp[r0 * size:r1 * size].copy()).pin_memory().numpy()
     h_power = torch.from_numpy(power[r0 * size:r1 * size].copy()).pin_memory().numpy()
+    arena.upload_numpy(h_src, h_temp)  # the timed steps above evolved the resident grid
+    arena.upload_numpy(h_pow, h_power)
     res = step()
     rt.device_synchronize()
-    expect = arena.to_numpy(res)  # the resident path's result on these inputs
+    expect = arena.to_numpy(res)  # the resident path's result on the step's inputs
     n_outs = min(args.steps, 16)
     h_outs = [torch.empty(cells, dtype=torch.float32).pin_memory().numpy() for _ in range(n_outs)]
     h_out = h_outs[0]
