@@ -204,6 +204,32 @@ int bf_launch_range(bf_runtime *rt, const char *kernel, const int32_t grid[3],
                     const int32_t block[3], int64_t shmem_bytes, const bf_slot *slots,
                     int32_t nslots, int32_t warp_size, int64_t first, int64_t count,
                     int64_t grain, uint64_t *task_id);
+/* Runtime.launch / launch_range through one descriptor (the Python binding
+ * keeps one per (routine, geometry, PackedArgs) and passes a single pointer:
+ * a 10-argument foreign call costs more than the launch itself).
+ * `fingerprint` (nullable) is the sha256 of the routine's MpmdKernel.to_dict()
+ * (routines.fingerprint_of); when the kernel has a registered fingerprint
+ * (bf_kernel_set_fingerprint) a mismatch fails with BF_E_UNKNOWN_KERNEL, so
+ * a caller cannot run the hand-written kernel for a different body under a
+ * registered name.  count < 0 launches the whole grid. */
+typedef struct bf_launch_desc {
+  const char *kernel;
+  const uint8_t *fingerprint;  /* 32 bytes or NULL */
+  int32_t grid[3];
+  int32_t block[3];
+  int64_t shmem_bytes;
+  const bf_slot *slots;
+  int32_t nslots;
+  int32_t warp_size;
+  int64_t first;
+  int64_t count;
+  int64_t grain;
+} bf_launch_desc;
+int bf_launch_described(bf_runtime *rt, const bf_launch_desc *desc, uint64_t *task_id);
+/* Register the expected body fingerprint of a hand-written kernel
+ * (paper_2206_07896_b200/fingerprints.json, made from the reference's own
+ * transform() by oracle/gen_golden.py). */
+int bf_kernel_set_fingerprint(const char *kernel, const uint8_t fingerprint[32]);
 /* Runtime.device_synchronize (runtime.py:269-278): releases a hold, waits for
  * every worker, increments syncs, and returns BF_E_FAULT with *fault filled
  * if any launch trapped (now or earlier). */

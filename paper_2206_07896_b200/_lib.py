@@ -33,7 +33,8 @@ EXPORTS = [
     "bf_queue_create", "bf_queue_destroy", "bf_queue_push", "bf_queue_fetch",
     "bf_queue_close", "bf_queue_is_empty", "bf_queue_task", "bf_queue_counters",
     "bf_resolve_grain",
-    "bf_runtime_create", "bf_shutdown", "bf_runtime_destroy", "bf_launch", "bf_launch_range",
+    "bf_runtime_create", "bf_shutdown", "bf_runtime_destroy", "bf_launch", "bf_launch_range", "bf_launch_described",
+    "bf_kernel_set_fingerprint",
     "bf_synchronize", "bf_hold_new_blocks", "bf_task_get", "bf_task_executed",
     "bf_counters_get", "bf_worker_stream",
     "bf_kernel_count", "bf_kernel_info",
@@ -55,6 +56,13 @@ class Slot(C.Structure):
 class Fault(C.Structure):
     _fields_ = [("kind", C.c_int32), ("_pad", C.c_int32), ("block_id", C.c_int64),
                 ("task_id", C.c_uint64), ("kernel", C.c_char * 32), ("message", C.c_char * 160)]
+
+
+class LaunchDesc(C.Structure):
+    _fields_ = [("kernel", C.c_char_p), ("fingerprint", C.c_void_p), ("grid", C.c_int32 * 3),
+                ("block", C.c_int32 * 3), ("shmem_bytes", C.c_int64), ("slots", C.c_void_p),
+                ("nslots", C.c_int32), ("warp_size", C.c_int32), ("first", C.c_int64), ("count", C.c_int64),
+                ("grain", C.c_int64)]
 
 
 class TaskInfo(C.Structure):
@@ -111,6 +119,8 @@ def _declare(lib) -> None:
         "bf_launch": (C.c_int, [P, C.c_char_p, I32P, I32P, i64, C.POINTER(Slot), i32, i32, i64, U64P]),
         "bf_launch_range": (C.c_int, [P, C.c_char_p, I32P, I32P, i64, C.POINTER(Slot), i32, i32, i64, i64,
                                       i64, U64P]),
+        "bf_launch_described": (C.c_int, [P, P, P]),
+        "bf_kernel_set_fingerprint": (C.c_int, [C.c_char_p, C.c_char_p]),
         "bf_synchronize": (C.c_int, [P, C.POINTER(Fault)]),
         "bf_hold_new_blocks": (C.c_int, [P]),
         "bf_task_get": (C.c_int, [P, u64, C.POINTER(TaskInfo)]),
@@ -149,7 +159,21 @@ def lib():
                 "(there is no CPU fallback)")
         _lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | C.RTLD_GLOBAL)
         _declare(_lib)
+        _register_fingerprints(_lib)
     return _lib
+
+
+def _register_fingerprints(L) -> None:
+    """Expected body fingerprints of the hand-written kernels -> the C ABI
+    (bf_kernel_set_fingerprint), so bf_launch_desc checks them natively."""
+    import json
+    fp_file = Path(__file__).resolve().parent / "fingerprints.json"
+    if not fp_file.exists():
+        return
+    for name, hexfp in json.loads(fp_file.read_text()).items():
+        raw = bytes.fromhex(hexfp)
+        if len(raw) == 32:
+            L.bf_kernel_set_fingerprint(name.encode(), raw)  # unknown names: ignored
 
 
 def last_error() -> str:

@@ -62,7 +62,7 @@ struct BfJitGeom {
   int gx, gy, gz, bx, by, bz;
   long long first, count;
   long long dyn_elems;
-  int* fault;  // {kind, pad, block(lo, hi), task}
+  int* fault;  // {kind, pad, block(lo, hi), task(lo, hi), host flag pointer}
   unsigned long long task;
   int warp_size;
 };
@@ -77,6 +77,9 @@ __device__ __forceinline__ void bf_trap(const BfJitGeom& G, int kind, long long 
   if (atomicCAS(G.fault, 0, kind) == 0) {
     *reinterpret_cast<long long*>(G.fault + 2) = blk;
     *reinterpret_cast<unsigned long long*>(G.fault + 4) = G.task;
+    __threadfence_system();
+    int* hf = *reinterpret_cast<int* const*>(G.fault + 6);
+    if (hf) *(volatile int*)hf = 1;
   }
 }
 __device__ __forceinline__ int bf_add32(int a, int b) { return (int)((unsigned)a + (unsigned)b); }

@@ -83,6 +83,8 @@ struct KernelEntry {
   std::vector<ParamSpec> params;
   LauncherFn launch;
   const void* user = nullptr;
+  bool has_fp = false;     // expected MpmdKernel body fingerprint (bf_kernel_set_fingerprint)
+  uint8_t fp[32] = {0};
 };
 
 // Registry (static registrars in each k_*.cu file, plus JIT kernels added at

@@ -19,6 +19,8 @@ struct DevFault {
   int pad;
   long long block;
   unsigned long long task;
+  int* host_flag;  // host-mapped pinned word set after a fault: a synchronize
+                   // copies the record only when it is set
 };
 
 // Logical launch descriptor passed by value to every kernel.
@@ -35,6 +37,8 @@ __device__ __forceinline__ void record_fault(const KDesc& d, int kind, long long
   if (atomicCAS(&d.fault->kind, 0, kind) == 0) {
     d.fault->block = block;
     d.fault->task = d.task;
+    __threadfence_system();
+    if (d.fault->host_flag) *(volatile int*)d.fault->host_flag = 1;
   }
 }
 

@@ -365,7 +365,8 @@ struct bf_runtime {
   std::vector<cudaStream_t> streams;
   bool holding = false;          // hold_blocks: launches wait on the host
   bf::DevFault* fault_dev = nullptr;
-  bf::DevFault* fault_host = nullptr;  // pinned copy, fetched in the sync's own stream round trip
+  bf::DevFault* fault_host = nullptr;  // pinned copy, fetched only after the flag is seen
+  int* fault_flag = nullptr;           // host-mapped: a kernel's first fault sets it
   bf::HostTrap trap;             // first trap (host- or device-detected)
   uint64_t trap_task = 0;
   std::string trap_kernel;
@@ -514,21 +515,23 @@ static int sync_workers(bf_runtime* rt) {
   return retire(rt, true);
 }
 
-// sync_workers plus the device fault record, fetched by an async copy queued
-// behind worker 0's work: one host round trip instead of a sync followed by a
-// blocking (legacy-stream) cudaMemcpy.  Other workers are drained first, so
-// their faults are in the record before the copy runs.
+// sync_workers plus the device fault record.  A fault also sets a
+// host-mapped flag (record_fault), so the common no-fault synchronize is one
+// stream synchronize per worker; the record is copied only when the flag is
+// set (the first fault stays in it: later syncs re-raise it).
 static int sync_workers_fault(bf_runtime* rt) {
   int rc = open_gate(rt);
   if (rc) return rc;
-  for (size_t i = 1; i < rt->streams.size(); i++) {
+  for (size_t i = 0; i < rt->streams.size(); i++) {
     cudaError_t e = cudaStreamSynchronize(rt->streams[i]);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   }
-  cudaError_t e = cudaMemcpyAsync(rt->fault_host, rt->fault_dev, sizeof(DevFault), cudaMemcpyDeviceToHost,
-                                  rt->streams[0]);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(rt->streams[0]);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  if (*(volatile int*)rt->fault_flag && rt->fault_host->kind == BF_TRAP_NONE) {
+    int* keep = rt->fault_host->host_flag;
+    cudaError_t e = cudaMemcpy(rt->fault_host, rt->fault_dev, sizeof(DevFault), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy fault record");
+    rt->fault_host->host_flag = keep;
+  }
   return retire(rt, true);
 }
 
@@ -990,10 +993,24 @@ int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double blo
   }
   rt->holding = (flags & BF_FLAG_HOLD_BLOCKS) != 0;
   if (cudaMalloc(&rt->fault_dev, sizeof(DevFault)) != cudaSuccess ||
-      cudaMemset(rt->fault_dev, 0, sizeof(DevFault)) != cudaSuccess ||
-      cudaMallocHost(&rt->fault_host, sizeof(DevFault)) != cudaSuccess) {
+      cudaMallocHost(&rt->fault_host, sizeof(DevFault)) != cudaSuccess ||
+      cudaHostAlloc((void**)&rt->fault_flag, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
     return fail(BF_E_CUDA, "fault word allocation failed");
+  }
+  {
+    int* flag_dev = nullptr;
+    *rt->fault_flag = 0;
+    std::memset(rt->fault_host, 0, sizeof(DevFault));
+    if (cudaHostGetDevicePointer((void**)&flag_dev, rt->fault_flag, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(BF_E_CUDA, "fault flag mapping failed");
+    }
+    rt->fault_host->host_flag = flag_dev;
+    if (cudaMemcpy(rt->fault_dev, rt->fault_host, sizeof(DevFault), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(BF_E_CUDA, "fault word initialisation failed");
+    }
   }
   a->live_runtimes++;
   *out = rt;
@@ -1024,6 +1041,7 @@ int bf_runtime_destroy(bf_runtime* rt) {
     if (kv.second.executed_dev) cudaFree(kv.second.executed_dev);
   if (rt->fault_dev) cudaFree(rt->fault_dev);
   if (rt->fault_host) cudaFreeHost(rt->fault_host);
+  if (rt->fault_flag) cudaFreeHost(rt->fault_flag);
   bf_arena* a = rt->arena;
   a->live_runtimes--;
   if (a->live_runtimes == 0) {
@@ -1240,6 +1258,29 @@ int bf_launch(bf_runtime* rt, const char* kernel, const int32_t grid[3], const i
               int64_t grain, uint64_t* task_id) {
   return launch_impl(rt, kernel, grid, block, shmem_bytes, slots, nslots, warp_size, 0, -1, grain,
                      task_id);
+}
+
+int bf_launch_described(bf_runtime* rt, const bf_launch_desc* d, uint64_t* task_id) {
+  if (!d || !d->kernel) return fail(BF_E_INVALID, "null launch descriptor");
+  if (d->fingerprint) {
+    const KernelEntry* ke = find_kernel(d->kernel);
+    if (ke && ke->has_fp && std::memcmp(ke->fp, d->fingerprint, 32) != 0)
+      return fail(BF_E_UNKNOWN_KERNEL, std::string("kernel '") + d->kernel +
+                                           "': body fingerprint differs from the registered sm_100a kernel");
+  }
+  return launch_impl(rt, d->kernel, d->grid, d->block, d->shmem_bytes, d->slots, d->nslots, d->warp_size,
+                     d->count < 0 ? 0 : d->first, d->count, d->grain, task_id);
+}
+
+int bf_kernel_set_fingerprint(const char* kernel, const uint8_t fingerprint[32]) {
+  if (!kernel || !fingerprint) return fail(BF_E_INVALID, "null argument");
+  for (auto& k : registry())
+    if (std::strcmp(k.name, kernel) == 0) {
+      std::memcpy(k.fp, fingerprint, 32);
+      k.has_fp = true;
+      return BF_OK;
+    }
+  return fail(BF_E_UNKNOWN_KERNEL, std::string("no sm_100a kernel registered for '") + kernel + "'");
 }
 
 int bf_launch_range(bf_runtime* rt, const char* kernel, const int32_t grid[3],

@@ -99,25 +99,24 @@ def pack_slots(packed) -> tuple[C.Array, int]:
     """Reference PackedArgs (or any object with .slots of (kind, value)) ->
     contiguous bf_slot array (16 B per slot).  f32 slots keep the unrounded
     double.  The packed array is cached on the PackedArgs object and reused
-    while its (kind, value) signature is unchanged (slots are mutable), which
-    takes the packing off the launch path of host loops that relaunch the
-    same arguments (hotspot's ping-pong, the BFS level loop)."""
+    while every slot is the same object holding the same kind and value
+    objects (slots are mutable; the cache keeps the value objects alive, so
+    identity implies the same value — 0.0 and -0.0 are different objects),
+    which takes the packing off the launch path of host loops that relaunch
+    the same arguments (hotspot's ping-pong, the BFS level loop)."""
     slots = packed.slots if packed is not None else ()
-    try:
-        # floats by bit pattern: 0.0 == -0.0 in Python, but they pack (and
-        # compute) differently
-        sig = tuple([(s.kind, s.value.hex() if s.value.__class__ is float else s.value) for s in slots])
-    except AttributeError:
-        sig = None
-    cached = getattr(packed, "_bf_packed", None) if sig is not None else None
-    if cached is not None and cached[0] == sig:
-        return cached[1], cached[2]
+    cached = getattr(packed, "_bf_packed", None)
+    if cached is not None and len(cached[0]) == len(slots):
+        for (so, k, v), s in zip(cached[0], slots):
+            if s is not so or s.kind is not k or s.value is not v:
+                break
+        else:
+            return cached[1], cached[2]
     arr, n = _pack_slots(slots)
-    if sig is not None:
-        try:
-            packed._bf_packed = (sig, arr, n)
-        except AttributeError:  # __slots__ objects: no cache
-            pass
+    try:
+        packed._bf_packed = ([(s, s.kind, s.value) for s in slots], arr, n)
+    except AttributeError:  # __slots__ objects (or no .kind/.value): no cache
+        pass
     return arr, n
 
 
@@ -418,12 +417,16 @@ class Runtime:
         # weak: a task keeps its runtime alive (it reads the native record),
         # the runtime must not keep its tasks alive (no reference cycle, so
         # runtime -> arena teardown order stays refcount-driven)
-        self._tasks: "weakref.WeakSet[KernelTask]" = weakref.WeakSet()
+        self._tasks: list = []  # weakref.ref per launched task (pruned as it grows)
+        self._tasks_prune_at = 1024
         self._shut_down = False
         # reusable launch scratch (the reference is driven by one host thread)
-        self._g = (C.c_int32 * 3)()
-        self._b = (C.c_int32 * 3)()
         self._tid = C.c_uint64()
+        self._tid_addr = C.addressof(self._tid)
+        # routine -> (routine, encoded registry key, warp size, fingerprint), by
+        # identity: resolve (fingerprinting a reference MpmdKernel) runs once
+        self._rcache: dict = {}
+        self._bf_launch_desc = _lib.lib().bf_launch_described
 
     # -- host API ---------------------------------------------------------------
     def launch(self, routine, grid, block, shmem_bytes: int, packed) -> KernelTask:
@@ -437,32 +440,67 @@ class Runtime:
         blocks; its executed[] is indexed from `first`."""
         return self._launch(routine, grid, block, shmem_bytes, packed, (first, count))
 
+    def _resolved(self, routine):
+        ent = self._rcache.get(id(routine))
+        if ent is None or ent[0] is not routine or routines.FORCE_JIT:
+            name, _, warp_size = routines.resolve(routine)
+            fp = None
+            if not name.startswith("jit:") and hasattr(routine, "to_dict"):
+                fp = C.create_string_buffer(bytes.fromhex(routines.fingerprint_of(routine.to_dict())), 32)
+            ent = (routine, name.encode(), warp_size, fp)
+            if len(self._rcache) > 256:
+                self._rcache.clear()
+            self._rcache[id(routine)] = ent  # holds the routine: its id stays unique
+        return ent
+
     def _launch(self, routine, grid, block, shmem_bytes, packed, rng) -> KernelTask:
         if self._shut_down:
             raise PoolShutdown("launch after shutdown")
-        name, warp_mode, warp_size = routines.resolve(routine)
+        ent = self._resolved(routine)
         total = grid.x * grid.y * grid.z if rng is None else rng[1]
-        grain = resolve_grain(self.policy, total, self.pool_size, routine)
+        if self.policy.__class__.__name__ == "Average":
+            if total < 1:
+                raise ValueError("grid_size and pool_size must be >= 1")
+            grain = -(-total // self.pool_size)  # runtime.py:83, the native law's hot path
+        else:
+            grain = resolve_grain(self.policy, total, self.pool_size, routine)
         task = KernelTask(routine, packed, grid, block, shmem_bytes, totalBlocks=total,
                           block_per_fetch=grain)
         slots, n = pack_slots(packed)
-        g, b, tid = self._g, self._b, self._tid
-        g[0], g[1], g[2] = grid.x, grid.y, grid.z
-        b[0], b[1], b[2] = block.x, block.y, block.z
-        if rng is None:
-            rc = _lib.lib().bf_launch(self._native, name.encode(), g, b, int(shmem_bytes), slots, n,
-                                      warp_size, grain, C.byref(tid))
+        # one cached launch descriptor per (routine, geometry, grain, range) on
+        # the PackedArgs: a single pointer crosses ctypes per launch
+        dkey = (ent[1], grid.x, grid.y, grid.z, block.x, block.y, block.z, shmem_bytes, grain, rng)
+        cached = getattr(packed, "_bf_desc", None)
+        if cached is not None and cached[0] == dkey and cached[2] is slots:
+            d = cached[1]
         else:
-            rc = _lib.lib().bf_launch_range(self._native, name.encode(), g, b, int(shmem_bytes), slots,
-                                            n, warp_size, int(rng[0]), int(rng[1]), grain, C.byref(tid))
+            d = _lib.LaunchDesc()
+            d.kernel = ent[1]
+            d.fingerprint = C.addressof(ent[3]) if ent[3] is not None else None
+            d.grid[0], d.grid[1], d.grid[2] = grid.x, grid.y, grid.z
+            d.block[0], d.block[1], d.block[2] = block.x, block.y, block.z
+            d.shmem_bytes = int(shmem_bytes)
+            d.slots = C.addressof(slots)
+            d.nslots = n
+            d.warp_size = ent[2]
+            d.first, d.count = (0, -1) if rng is None else (int(rng[0]), int(rng[1]))
+            d.grain = grain
+            try:
+                packed._bf_desc = (dkey, d, slots, ent)  # keeps the slots and fingerprint alive
+            except AttributeError:
+                self._last_desc = (d, slots, ent)
+        rc = self._bf_launch_desc(self._native, C.addressof(d), self._tid_addr)
         if rc == _lib.E_SHUTDOWN:
             raise PoolShutdown("launch after shutdown")
         if rc == _lib.E_UNKNOWN_KERNEL:
             raise routines.KernelNotImplemented(_lib.last_error())
         check(rc)
         task._rt = self
-        task._id = tid.value
-        self._tasks.add(task)
+        task._id = self._tid.value
+        self._tasks.append(weakref.ref(task))
+        if len(self._tasks) > self._tasks_prune_at:
+            self._tasks = [r for r in self._tasks if r() is not None]
+            self._tasks_prune_at = max(1024, 2 * len(self._tasks))
         return task
 
     def device_synchronize(self) -> None:
@@ -477,7 +515,8 @@ class Runtime:
         check(rc)
 
     def unfinished_tasks(self) -> list:
-        return sorted((t for t in self._tasks if t.remaining > 0), key=lambda t: t._id)
+        live = [r() for r in self._tasks]
+        return sorted((t for t in live if t is not None and t.remaining > 0), key=lambda t: t._id)
 
     def hold_new_blocks(self) -> None:
         check(_lib.lib().bf_hold_new_blocks(self._native))

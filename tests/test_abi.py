@@ -44,3 +44,15 @@ def test_registry_matches_routine_table():
                 assert kind == "handle" and ptype == f"global {scalar}[]", (name, pname)
             else:
                 assert kind == ptype, (name, pname)
+
+
+def test_fingerprints_registered_natively():
+    """fingerprints.json reaches the C ABI at load (bf_kernel_set_fingerprint),
+    so bf_launch_described rejects a different body under a registered name
+    without the Python layer; unknown names are refused."""
+    import json
+    L = _lib.lib()
+    fps = json.loads((ROOT / "paper_2206_07896_b200" / "fingerprints.json").read_text())
+    assert {"vecadd", "hotspot", "kmeans", "bfs", "nn"} <= set(fps)
+    assert L.bf_kernel_set_fingerprint(b"vecadd", bytes.fromhex(fps["vecadd"])) == _lib.OK
+    assert L.bf_kernel_set_fingerprint(b"no_such_kernel", bytes(32)) == _lib.E_UNKNOWN_KERNEL

@@ -441,3 +441,38 @@ def test_packed_cache_distinguishes_negative_zero():
     pk.slots[0] = ArgSlot("f32", -0.0)
     arr, n = pack_slots(pk)
     assert bytes(arr)[8:16] == struct.pack("<d", -0.0)
+
+
+@pytest.mark.gpu
+def test_launch_described_checks_fingerprint():
+    """The C ABI's descriptor launch runs a registered kernel when the body
+    fingerprint matches and refuses a different body under the same name."""
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+    import ctypes as C
+    import json
+    from pathlib import Path
+    from paper_2206_07896_b200 import ArgSlot, DeviceArena, PackedArgs, Runtime, _lib
+    from paper_2206_07896_b200.runtime import pack_slots
+    fps = json.loads((Path(__file__).resolve().parents[1] / "paper_2206_07896_b200" / "fingerprints.json").read_text())
+    arena = DeviceArena()
+    n = 1000
+    a, b, c = (arena.alloc("f32", n) for _ in range(3))
+    arena.upload_numpy(a, np.arange(n, dtype=np.float32))
+    arena.upload_numpy(b, np.ones(n, np.float32))
+    slots, ns = pack_slots(PackedArgs([ArgSlot("handle", a), ArgSlot("handle", b), ArgSlot("handle", c),
+                                       ArgSlot("i32", n)]))
+    with Runtime(arena) as rt:
+        good = C.create_string_buffer(bytes.fromhex(fps["vecadd"]), 32)
+        bad = C.create_string_buffer(bytes(32), 32)
+        tid = C.c_uint64()
+        for fp, want in ((good, _lib.OK), (bad, _lib.E_UNKNOWN_KERNEL), (None, _lib.OK)):
+            d = _lib.LaunchDesc()
+            d.kernel = b"vecadd"
+            d.fingerprint = C.addressof(fp) if fp is not None else None
+            d.grid[:] = (4, 1, 1)
+            d.block[:] = (256, 1, 1)
+            d.slots, d.nslots, d.warp_size, d.first, d.count, d.grain = C.addressof(slots), ns, 0, 0, -1, 4
+            assert _lib.lib().bf_launch_described(rt._native, C.addressof(d), C.addressof(tid)) == want
+        rt.device_synchronize()
+    assert np.array_equal(arena.to_numpy(c), np.arange(n, dtype=np.float32) + 1)
