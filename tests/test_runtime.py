@@ -5,6 +5,8 @@ package's native runtime.  Queue and grain tests need no GPU."""
 
 import random
 
+import numpy as np
+
 import pytest
 from hypothesis import given, settings
 from hypothesis import strategies as st
