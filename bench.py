@@ -846,6 +846,8 @@ def per_kernel_table(arena, rt, torch, stream, args) -> tuple[dict, int]:
             ent["note"] = c.note
         if hasattr(c, "levels"):
             ent["levels"] = c.levels["n"]
+        if getattr(c, "extra", None) and "build_ms" in c.extra:
+            ent["transpose_build_ms"] = round(c.extra["build_ms"], 3)
         if not args.no_cpu:
             try:
                 cpu = benchkit.cpu_sample(c.name, threads)

@@ -356,9 +356,29 @@ def bfs_case(arena, torch, device, log_v: int = 26, deg: int = 8) -> Case:
 
     f = Case("bfs_fused", "bfs_expand_queue", 4 * ne + 12 * nv, ne, "edge", [], host_loop=fused,
              check=fused_check,
-             note="same graph, whole traversal fused on the device (bf_bfs_levels: frontier queues "
-                  "+ L2-resident visited bitmap); levels equal to the per-level launches")
-    return c, f
+             note="same graph, whole traversal fused on the device, top-down only (bf_bfs_levels: frontier "
+                  "queues + L2-resident visited bitmap); levels equal to the per-level launches")
+
+    tg = {}
+
+    def do_step(rt, stream):
+        if "t" not in tg:  # the in-edge CSR is built once per graph, outside the timed steps
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tg["t"] = graph.transpose(rt, row, col, nv)
+            torch.cuda.synchronize()
+            tg["build_ms"] = (time.perf_counter() - t0) * 1e3
+        levels["do_depth"] = graph.bfs_levels(rt, row, col, lvl, nv, 0, transposed=tg["t"])
+        return 1
+
+    d = Case("bfs_do", "bfs_bottom_up", 4 * ne + 12 * nv, ne, "edge", [], host_loop=do_step,
+             check=fused_check,
+             note="same graph, direction-optimizing fused traversal (bf_bfs_levels_do: top-down on small "
+                  "frontiers, bottom-up over the in-edge CSR on large ones, chosen on the device per level); "
+                  "levels equal to the per-level launches; bytes = the same compulsory 4|E| + 12|V|")
+    d.levels = levels
+    d.extra = tg
+    return c, f, d
 
 
 def time_case(case: Case, rt, torch, stream, reps: int, warmup: int) -> dict:
@@ -465,7 +485,7 @@ def sample_instance(name: str, log_n: int):
 # bench-run sample sizes (log2): the C port, all host cores, ~0.5 s each
 PORT_LOG = {"vecadd": 24, "vecadd_pr1": 20, "nn": 22, "hist": 24, "hist_stride": 22, "reduce": 24,
             "wreduce": 24, "fir": 20, "kmeans": 16, "kmeans_loop": 16, "bp_forward": 18,
-            "bp_adjust": 18, "bfs": 22, "bfs_fused": 22, "hotspot": 22}
+            "bp_adjust": 18, "bfs": 22, "bfs_fused": 22, "bfs_do": 22, "hotspot": 22}
 # the reference runtime (pure Python): SURVEY §8d sizes for the study
 # (--workload cpu-runtime), and ~1 s samples for the default bench line
 REF_LOG_SURVEY = {"vecadd_pr1": 20, "vecadd": 20, "hotspot": 16, "kmeans": 10, "bfs": 14, "nn": 20,
@@ -486,7 +506,7 @@ def cpu_sample(name: str, threads: int, budget: float = 0.5) -> Optional[dict]:
     import instances as I
     import oracle
 
-    if name in ("bfs", "bfs_fused"):
+    if name in ("bfs", "bfs_fused", "bfs_do"):
         nv = 1 << PORT_LOG["bfs"]
         row, col = I.random_graph(nv, 8, 1)
         t0 = time.perf_counter()
@@ -510,7 +530,7 @@ def cpu_sample(name: str, threads: int, budget: float = 0.5) -> Optional[dict]:
             "sample": f"{name} {elems} elements, oracle/oracle.c over {nt} thread(s), {reps} run(s) of {dt:.3f} s"}
 
 
-REF_NAME = {"kmeans_loop": "kmeans", "bfs_fused": "bfs"}
+REF_NAME = {"kmeans_loop": "kmeans", "bfs_fused": "bfs", "bfs_do": "bfs"}
 _REF_CACHE: dict = {}
 
 
@@ -577,7 +597,7 @@ def reference_runtime_sample(name: str, pool: int, log_n: int) -> Optional[dict]
     import numpy as np
     import oracle
     A, B, E, H, P, R, S, T = _reference_modules()
-    if name in ("bfs", "bfs_fused"):
+    if name in ("bfs", "bfs_fused", "bfs_do"):
         nv = 1 << log_n
         row, col = I.random_graph(nv, 8, 1)
         want, depth = oracle.bfs_full(row, col, nv, 0)

@@ -260,6 +260,22 @@ int bf_worker_stream(bf_runtime *rt, int32_t worker, void **stream);
 int bf_bfs_levels(bf_runtime *rt, uint32_t row, uint32_t col, uint32_t lvl,
                   int32_t nv, int32_t source, int32_t *depth);
 
+/* In-edge CSR of the graph (row, col) for the bottom-up steps: crow
+ * (nv + 1 entries) and ccol (at least row[nv] entries), i32 arena buffers;
+ * ccol[crow[v] .. crow[v+1]) holds the sources u of the edges u -> v in an
+ * unspecified order.  Built once per graph (a GPU counting sort).  BF_E_FAULT
+ * when row is malformed or a target is out of range.  No reference
+ * counterpart: the bottom-up direction needs the in-edges. */
+int bf_bfs_transpose(bf_runtime *rt, uint32_t row, uint32_t col, int32_t nv,
+                     uint32_t crow, uint32_t ccol);
+/* bf_bfs_levels, direction-optimizing: levels whose frontier is large run
+ * bottom-up over (crow, ccol) from bf_bfs_transpose (each unvisited vertex
+ * looks for a frontier in-neighbour).  Same levels as bf_bfs_levels (BFS
+ * levels are unique); (crow, ccol) must be the transpose of (row, col). */
+int bf_bfs_levels_do(bf_runtime *rt, uint32_t row, uint32_t col, uint32_t crow,
+                     uint32_t ccol, uint32_t lvl, int32_t nv, int32_t source,
+                     int32_t *depth);
+
 /* One pass of Rodinia's kmeans host loop after an assignment launch of
  * kernels/kmeans.kn (kmeans_clustering.c's do/while): cent[c][l] =
  * sums[c][l] / counts[c] in f32 for clusters with members (others keep

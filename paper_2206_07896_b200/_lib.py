@@ -38,7 +38,7 @@ EXPORTS = [
     "bf_synchronize", "bf_hold_new_blocks", "bf_task_get", "bf_task_executed",
     "bf_counters_get", "bf_worker_stream",
     "bf_kernel_count", "bf_kernel_info",
-    "bf_bfs_levels", "bf_hotspot_run", "bf_jit_register",
+    "bf_bfs_levels", "bf_bfs_levels_do", "bf_bfs_transpose", "bf_hotspot_run", "bf_jit_register",
     "bf_bfs_shard_create", "bf_bfs_shard_destroy", "bf_bfs_shard_bitmap", "bf_bfs_shard_begin",
     "bf_bfs_shard_expand", "bf_bfs_shard_merge", "bf_bfs_shard_merge_slice", "bf_bfs_shard_compact", "bf_bfs_shard_finish",
     "bf_kmeans_update",
@@ -129,6 +129,8 @@ def _declare(lib) -> None:
         "bf_worker_stream": (C.c_int, [P, i32, C.POINTER(P)]),
         "bf_kernel_count": (C.c_int, [I32P]),
         "bf_bfs_levels": (C.c_int, [P, u32, u32, u32, i32, i32, I32P]),
+        "bf_bfs_levels_do": (C.c_int, [P, u32, u32, u32, u32, u32, i32, i32, I32P]),
+        "bf_bfs_transpose": (C.c_int, [P, u32, u32, i32, u32, u32]),
         "bf_bfs_shard_create": (C.c_int, [P, i32, C.POINTER(P)]),
         "bf_bfs_shard_destroy": (C.c_int, [P]),
         "bf_bfs_shard_bitmap": (C.c_int, [P, C.POINTER(P), I64P]),

@@ -14,6 +14,8 @@
 #include <climits>
 #include <cstdlib>
 
+#include <cub/device/device_scan.cuh>
+
 #include "bf_internal.h"
 #include "common.cuh"
 
@@ -594,99 +596,32 @@ static int launch_bfs(LaunchCtx& ctx) {
 
 // ===========================================================================
 // Fused traversal (the Rodinia host loop, on the device): bf_bfs_levels.
-// Level-synchronous top-down with two nv-bit bitmaps (8 MB each at 2^26
-// vertices, L2-resident):
-//   expand:  for u in frontier, v in out(u): if v's bit in `now` is clear,
-//            set it (fire-and-forget red.or).
+// Level-synchronous, direction-optimizing (Beamer's top-down / bottom-up
+// switch) over two nv-bit bitmaps (8 MB each at 2^26 vertices, L2-resident):
+//   top-down expand:  for u in frontier, v in out(u): if v's bit in `now` is
+//            clear, set it (fire-and-forget red.or);
 //   compact: next frontier = bits in `now` not in `prev` (a sweep over the
-//            bitmap, not over lvl[]), prev |= now; ids appended with a
-//            warp-aggregated atomic and lvl[id] = d + 1 written in id order
-//            (no random partial-sector writes).
-// The bitmap `now` is pinned in L2 with a persisting access-policy window.
-// Same levels as repeated `bfs` launches.  The per-edge "unvisited?" test is
-// an L2 hit instead of a random DRAM read of lvl[], and no load waits on an
-// atomic.
+//            bitmap, not over lvl[]), prev |= now; ids appended as one
+//            contiguous run per CTA, level bytes merged per 32 B sector;
+//   bottom-up step (bf_bfs_levels_do, with the transposed graph): every
+//            unvisited vertex scans its in-edges until one comes from the
+//            frontier bitmap; the step writes the next frontier's bitmap,
+//            queue and level bytes itself (no separate compaction).
+// BFS levels are unique, so the direction never changes a level: same levels
+// as repeated `bfs` launches.  The choice is made on the device from exact
+// counts (frontier size, visited count) by the first kernel of each level,
+// so the pipelined host loop never waits for it.
 // ===========================================================================
-__global__ void __launch_bounds__(256) bfs_init(int* lvl, unsigned* now, unsigned* prev,
-                                                long long nv, long long words, int src, int* q0,
-                                                int* sizes) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  int4* l4 = reinterpret_cast<int4*>(lvl);
-  for (long long i = t; i < nv / 4; i += stride) l4[i] = make_int4(-1, -1, -1, -1);
-  for (long long i = (nv / 4) * 4 + t; i < nv; i += stride) lvl[i] = -1;
-  for (long long i = t; i < words; i += stride) {
-    now[i] = 0u;
-    prev[i] = 0u;
-  }
-  if (t == 0) {
-    sizes[0] = 1;
-    sizes[1] = 0;
-    sizes[2] = 0;
-    q0[0] = src;
-  }
-}
 
-__global__ void bfs_seed(int* lvl, unsigned* now, unsigned* prev, int src) {
-  lvl[src] = 0;
-  now[src >> 5] = 1u << (src & 31);
-  prev[src >> 5] = 1u << (src & 31);
-}
-
-constexpr int kBfsVPT = 4;  // frontier vertices per thread (independent chains)
-
-__global__ void __launch_bounds__(256) bfs_expand(const int* __restrict__ row,
-                                                  const int* __restrict__ col, long long ne,
-                                                  int* lvl, unsigned* now, long long nv,
-                                                  const int* __restrict__ q, int* sizes, int depth) {
-  const int qn = sizes[0];
-  const long long stride = (long long)gridDim.x * blockDim.x * kBfsVPT;
-  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kBfsVPT; i0 < qn;
-       i0 += stride) {
-    int e0[kBfsVPT], e1[kBfsVPT];
-#pragma unroll
-    for (int a = 0; a < kBfsVPT; a++) {
-      e0[a] = e1[a] = 0;
-      if (i0 + a < qn) {
-        const int u = __ldg(q + i0 + a);
-        e0[a] = __ldg(row + u);
-        e1[a] = __ldg(row + u + 1);
-        if (e0[a] < 0 || e1[a] > ne || e1[a] < e0[a]) {
-          sizes[2] = 1;
-          e1[a] = e0[a];
-        }
-      }
-    }
-    int maxd = 0;
-#pragma unroll
-    for (int a = 0; a < kBfsVPT; a++) maxd = max(maxd, e1[a] - e0[a]);
-    for (int j = 0; j < maxd; j += 4) {
-      int v[kBfsVPT][4];
-      unsigned w[kBfsVPT][4];
-#pragma unroll
-      for (int a = 0; a < kBfsVPT; a++)
-#pragma unroll
-        for (int t = 0; t < 4; t++) v[a][t] = (e0[a] + j + t < e1[a]) ? __ldcs(col + e0[a] + j + t) : -1;
-#pragma unroll
-      for (int a = 0; a < kBfsVPT; a++)
-#pragma unroll
-        for (int t = 0; t < 4; t++) {
-          w[a][t] = 0xffffffffu;
-          if (v[a][t] >= 0) {
-            if (v[a][t] >= nv) sizes[2] = 1;
-            else w[a][t] = __ldcg(now + (v[a][t] >> 5));
-          }
-        }
-#pragma unroll
-      for (int a = 0; a < kBfsVPT; a++)
-#pragma unroll
-        for (int t = 0; t < 4; t++) {
-          const unsigned bit = 1u << (v[a][t] & 31);
-          if (v[a][t] >= 0 && v[a][t] < nv && !(w[a][t] & bit))
-            atomicOr(now + (v[a][t] >> 5), bit);  // result unused: compiled to RED
-        }
-    }
-  }
+// Level-counter block of the pipelined loop (4 ints per level, rotating over
+// three levels): [0] frontier size, [1] frontier bitmap F of this level
+// written (the bottom-up step may run), [2] CSR error flag, [3] direction
+// chosen for this level (1: bottom-up).  Bottom-up when F exists and
+// |F| * alpha16 >= 16 * unvisited.
+__device__ __forceinline__ bool bfs_pick_bottom_up(const int* B, const int* vis, long long nv, int alpha16) {
+  if (!vis || !B[1]) return false;
+  const long long unvisited = nv - 1 - (long long)*vis;
+  return (long long)B[0] * alpha16 >= 16 * unvisited;
 }
 
 // Expansion with whole-adjacency vector loads: two frontier vertices per
@@ -695,16 +630,55 @@ __global__ void __launch_bounds__(256) bfs_expand(const int* __restrict__ row,
 // default caching), anything else edge by edge.  All 16 targets' bitmap
 // words are loaded before any RED is issued.
 constexpr int kBfsV2 = 2;
+
 template <bool TEST, int V = kBfsV2>
 __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
                                                     const int* __restrict__ col, long long ne,
                                                     unsigned* now, long long nv,
                                                     const int* __restrict__ q, int* sizes,
-                                                    int* zero_p, int* hist) {
+                                                    int* zero_p, int* hist, const int* vis = nullptr,
+                                                    int alpha16 = 0, const unsigned* __restrict__ fin = nullptr) {
   const int qn = sizes[0];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // pipelined loop: next-next level's counter, qn record
-    if (zero_p) *zero_p = 0;
+  const bool bottom_up = bfs_pick_bottom_up(sizes, vis, nv, alpha16);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // pipelined loop: next-next level's block, qn record, direction
+    if (zero_p) {
+      zero_p[0] = 0;
+      zero_p[1] = 0;
+      zero_p[3] = 0;
+    }
     if (hist) *(volatile int*)hist = qn;
+    if (vis) sizes[3] = bottom_up;
+  }
+  if (bottom_up) return;  // bfs_bottom_up expands this level
+  if (fin && sizes[1] == 2) {  // a bottom-up level left this frontier as a bitmap only
+    const long long words = (nv + 31) / 32;
+    const long long gstride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += gstride) {
+      for (unsigned f = __ldg(fin + i); f; f &= f - 1) {
+        const int u = (int)(i * 32 + __ffs(f) - 1);
+        int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
+        if (e0 < 0 || e1 > ne || e1 < e0) {
+          sizes[2] = 1;
+          continue;
+        }
+        for (int b = e0; b < e1; b += 8) {
+          int v[8];
+          unsigned wv[8];
+#pragma unroll
+          for (int t = 0; t < 8; t++) v[t] = b + t < e1 ? __ldg(col + b + t) : -1;
+#pragma unroll
+          for (int t = 0; t < 8; t++) {
+            wv[t] = 0xffffffffu;
+            if (v[t] >= nv) sizes[2] = 1;
+            else if (v[t] >= 0) wv[t] = __ldcg(now + (v[t] >> 5));
+          }
+#pragma unroll
+          for (int t = 0; t < 8; t++)
+            if (v[t] >= 0 && v[t] < nv && !(wv[t] & (1u << (v[t] & 31)))) atomicOr(now + (v[t] >> 5), 1u << (v[t] & 31));
+        }
+      }
+    }
+    return;
   }
   const long long stride = (long long)gridDim.x * blockDim.x * V;
   for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * V; i0 < qn; i0 += stride) {
@@ -764,34 +738,6 @@ __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
   }
 }
 
-// Level bytes: while depth + 1 < 255 the compaction records a vertex's level
-// in a byte array (64 MB at 2^26 vertices, L2-resident) instead of scattering
-// 4 B writes over the 256 MB lvl array; bfs_finish converts once, densely.
-__global__ void __launch_bounds__(256) bfs_compact8(unsigned* now, unsigned* prev, long long words,
-                                                    int* nq, int* sizes, unsigned char* lv8, int* lvl,
-                                                    int depth) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const bool bytes = depth + 1 < 255;
-  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < words; i0 += stride) {  // CTA-uniform
-    const long long i = i0 + threadIdx.x;
-    unsigned fresh = 0;
-    if (i < words) {
-      const unsigned nw = __ldcg(now + i);
-      fresh = nw & ~prev[i];
-      if (fresh) prev[i] = nw;
-    }
-    int pos = cta_append(__popc(fresh), sizes + 1);
-    while (fresh) {
-      const int b = __ffs(fresh) - 1;
-      const int v = (int)(i * 32 + b);
-      nq[pos++] = v;
-      if (bytes) lv8[v] = (unsigned char)(depth + 1);
-      else lvl[v] = depth + 1;
-      fresh &= fresh - 1;
-    }
-  }
-}
-
 // Compaction with coalesced writes (depth + 1 < 255): the CTA's new
 // vertices are staged in shared memory and leave as one contiguous queue run,
 // and a word's 32 level bytes (one 32 B sector of lv8) are merged in
@@ -805,11 +751,16 @@ __device__ __forceinline__ unsigned lv8_merge(unsigned x, unsigned fresh, int sh
 
 __global__ void __launch_bounds__(256) bfs_compact8s(unsigned* now, unsigned* prev, long long words,
                                                      int* nq, const int* qn_p, int* out_cnt,
-                                                     unsigned char* lv8, int* lvl, int depth) {
+                                                     unsigned char* lv8, int* lvl, int depth,
+                                                     unsigned* fout = nullptr, int* vis = nullptr) {
+  // qn_p / out_cnt: this and the next level's counter blocks (bfs_pick_bottom_up);
+  // fout: the next level's frontier bitmap, every word written (bottom-up may
+  // expand it); vis: running count of visited vertices
   __shared__ int stage[256 * 32];
   __shared__ int wtot[8];
   __shared__ int cbase, ctot;
-  if (*qn_p == 0) return;  // nothing was expanded: nothing is fresh
+  if (qn_p[0] == 0 || qn_p[3]) return;  // nothing was expanded, or the bottom-up step ran
+  if (fout && blockIdx.x == 0 && threadIdx.x == 0) out_cnt[1] = 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool bytes = depth + 1 < 255;
   const unsigned lb = (unsigned)(depth + 1) * 0x01010101u;
@@ -833,6 +784,7 @@ __global__ void __launch_bounds__(256) bfs_compact8s(unsigned* now, unsigned* pr
       cp = prev[i + stride];
     }
     unsigned fresh = i < words ? nw & ~pw : 0u;
+    if (fout && i < words) fout[i] = fresh;
     if (!__syncthreads_or(fresh != 0)) continue;
     if (i < words) {
       if (fresh && !bytes) {  // levels beyond a byte: lvl written directly
@@ -872,6 +824,7 @@ __global__ void __launch_bounds__(256) bfs_compact8s(unsigned* now, unsigned* pr
       }
       ctot = run;
       cbase = run ? atomicAdd(out_cnt, run) : 0;
+      if (run && vis) atomicAdd(vis, run);
     }
     __syncthreads();
     int pos = wtot[warp] + incl - c;
@@ -880,87 +833,6 @@ __global__ void __launch_bounds__(256) bfs_compact8s(unsigned* now, unsigned* pr
     const int tot = ctot, base = cbase;
     for (int j = threadIdx.x; j < tot; j += blockDim.x) nq[base + j] = stage[j];
     __syncthreads();
-  }
-}
-
-// Small levels: expansion and compaction in one pass.  atomicOr returns the
-// bitmap word, so the one thread that sets a target's bit owns the target: it
-// appends it to the next queue (one atomicAdd per warp and chunk), records its
-// level and sets the bit in prev as well, so a later sweep (bfs_compact8s)
-// sees it as old.  Loops are warp-uniform (warp-wide appends).
-template <int V>
-__global__ void __launch_bounds__(256) bfs_expand_app(const int* __restrict__ row, const int* __restrict__ col,
-                                                      long long ne, unsigned* now, unsigned* prev, long long nv,
-                                                      const int* __restrict__ q, int* sizes, int* nq,
-                                                      unsigned char* lv8, int* lvl, int depth, bool deep) {
-  const int qn = sizes[0];
-  const int lane = threadIdx.x & 31;
-  const long long stride = (long long)gridDim.x * blockDim.x * V;
-  for (long long b0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * V; b0 < qn; b0 += stride) {
-    const long long i0 = b0 + (long long)lane * V;
-    int e0[V], e1[V];
-#pragma unroll
-    for (int a = 0; a < V; a++) {
-      e0[a] = e1[a] = 0;
-      if (i0 + a < qn) {
-        const int u = __ldg(q + i0 + a);
-        e0[a] = __ldg(row + u);
-        e1[a] = __ldg(row + u + 1);
-        if (e0[a] < 0 || e1[a] > ne || e1[a] < e0[a]) {
-          sizes[2] = 1;
-          e1[a] = e0[a];
-        }
-      }
-    }
-    int maxd = 0;
-#pragma unroll
-    for (int a = 0; a < V; a++) maxd = max(maxd, e1[a] - e0[a]);
-    maxd = __reduce_max_sync(0xffffffffu, maxd);
-    for (int j = 0; j < maxd; j += 8) {
-      int v[V][8];
-#pragma unroll
-      for (int a = 0; a < V; a++)
-#pragma unroll
-        for (int t = 0; t < 8; t++) {
-          v[a][t] = e0[a] + j + t < e1[a] ? __ldg(col + e0[a] + j + t) : -1;
-          if (v[a][t] >= nv) {
-            sizes[2] = 1;
-            v[a][t] = -1;
-          }
-        }
-      unsigned mine = 0;
-#pragma unroll
-      for (int a = 0; a < V; a++)
-#pragma unroll
-        for (int t = 0; t < 8; t++)
-          if (v[a][t] >= 0) {
-            const unsigned bit = 1u << (v[a][t] & 31);
-            if (!(__ldcg(now + (v[a][t] >> 5)) & bit) && !(atomicOr(now + (v[a][t] >> 5), bit) & bit))
-              mine |= 1u << (a * 8 + t);
-          }
-      const int c = __popc(mine);
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int base = 0;
-      if (lane == 31 && incl) base = atomicAdd(sizes + 1, incl);
-      base = __shfl_sync(0xffffffffu, base, 31);
-      int pos = base + incl - c;
-#pragma unroll
-      for (int a = 0; a < V; a++)
-#pragma unroll
-        for (int t = 0; t < 8; t++)
-          if (mine & (1u << (a * 8 + t))) {
-            const int x = v[a][t];
-            nq[pos++] = x;
-            if (deep) lvl[x] = depth + 1;
-            else lv8[x] = (unsigned char)(depth + 1);
-            atomicOr(prev + (x >> 5), 1u << (x & 31));
-          }
-    }
   }
 }
 
@@ -1090,251 +962,289 @@ __global__ void __launch_bounds__(256) bfs_compact_sh(unsigned* now, unsigned* p
   }
 }
 
-// ---- bucketed level (large frontiers): targets binned by vertex slice ------
-// A top-down level whose frontier is large probes a random 32 B L2 sector of
-// the visited bitmap per edge.  The bucketed level instead bins the targets
-// by vertex slice (2^18 vertices = a 32 KB bitmap slice) in two streaming
-// passes over the frontier's adjacency (count, then scatter through a
-// shared-memory counting sort so bucket writes are runs, not single words),
-// and one CTA per slice then tests and sets its targets in shared memory,
-// appends the new vertices to the next frontier and writes the slice back:
-// the per-edge random L2 sector becomes ~8 B of streaming DRAM traffic.
-// Status (round 1): bit-exact (tests run it on 2^20 and 2^24 vertex graphs),
-// but this first implementation is 10x slower than the probing level (41.7 vs
-// 4.2 ms per traversal at 2^26 x 8: per-vertex scalar adjacency reads in the
-// count pass, a serial per-round reservation loop in the scatter, one CTA per
-// slice in the apply), so it is opt-in (BF_BFS_BUCKET=1).
-constexpr int kSliceLog = 18;
-constexpr int kSliceWords = 1 << (kSliceLog - 5);
-constexpr int kMaxSlices = 1024;
-
-__global__ void __launch_bounds__(256) bfs_bucket_count(const int* __restrict__ row, const int* __restrict__ col,
-                                                        long long ne, long long nv, const int* __restrict__ q,
-                                                        const int* sizes_in, int* sizes, int* counts, int nslices) {
-  __shared__ int hist[kMaxSlices];
-  for (int i = threadIdx.x; i < nslices; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
-  const int qn = sizes_in[0];
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < qn; i += stride) {
-    const int u = __ldg(q + i);
-    const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
-    if (e0 < 0 || e1 > ne || e1 < e0) {
-      sizes[2] = 1;
-      continue;
-    }
-    for (int e = e0; e < e1; e++) {
-      const int v = __ldg(col + e);
-      if (v < 0 || v >= nv) {
-        sizes[2] = 1;
-        continue;
-      }
-      atomicAdd(&hist[v >> kSliceLog], 1);
-    }
+// ---- bottom-up step (direction-optimizing traversal) ------------------------
+// A warp owns a chunk of 32 bitmap words (1024 vertices) at a time: one
+// coalesced load of the words, a warp scan of their unvisited counts, then
+// the chunk's unvisited vertices are dealt to the lanes by rank (rank ->
+// word by a shuffle binary search, -> bit by __fns), two per lane in flight,
+// each scanning its in-edges four at a time until one comes from the
+// frontier bitmap F.  Hits are OR-ed into the warp's 32 new-bit words in
+// shared memory; then lane j writes word j of the chunk: now/prev, the next
+// frontier bitmap Fn (every word), and the word's 32 level bytes as one
+// merged sector.  No CTA barriers and no queue: a top-down level that
+// follows a bottom-up one reads its frontier from Fn (block flag [1] = 2),
+// and the new-vertex count leaves with one atomic per CTA at the end.
+__device__ __forceinline__ int bu_rank_to_vertex(int r, int T, int incl, int c, unsigned un, long long ch) {
+  // smallest lane j with incl_j > r (all lanes take part in every shuffle)
+  int j = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int x = __shfl_sync(0xffffffffu, incl, j + step - 1);
+    if (x <= r) j += step;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nslices; i += blockDim.x)
-    if (hist[i]) atomicAdd(counts + i, hist[i]);
+  const int ex = __shfl_sync(0xffffffffu, incl - c, j);
+  const unsigned wj = __shfl_sync(0xffffffffu, un, j);
+  if (r >= T) return -1;
+  const int bit = (int)__fns(wj, 0, r - ex + 1);
+  return (int)((ch * 32 + j) * 32 + bit);
 }
 
-// exclusive scan of the bucket counts (one CTA): offsets[b], cursors[b] = offsets[b]
-__global__ void __launch_bounds__(1024) bfs_bucket_scan(const int* counts, long long* offsets, long long* cursors,
-                                                        int nslices) {
-  __shared__ long long part[1024];
-  const int t = threadIdx.x;
-  long long v = t < nslices ? counts[t] : 0;
-  part[t] = v;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const long long y = t >= o ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += y;
-    __syncthreads();
-  }
-  if (t < nslices) {
-    offsets[t] = part[t] - v;
-    cursors[t] = part[t] - v;
-  }
-  if (t == nslices - 1) offsets[nslices] = part[t];
-}
-
-__global__ void __launch_bounds__(256) bfs_bucket_scatter(const int* __restrict__ row, const int* __restrict__ col,
-                                                          long long ne, long long nv, const int* __restrict__ q,
-                                                          const int* sizes_in, long long* cursors, int* buckets,
-                                                          int nslices) {
-  __shared__ int hist[kMaxSlices], loff[kMaxSlices];
-  __shared__ long long gbase[kMaxSlices];
-  __shared__ int stage[256 * 8];
-  __shared__ int total;
-  const int qn = sizes_in[0];
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < qn; i0 += stride) {  // CTA-uniform
-    const long long i = i0 + threadIdx.x;
-    int e0 = 0, e1 = 0;
-    if (i < qn) {
-      const int u = __ldg(q + i);
-      e0 = __ldg(row + u);
-      e1 = __ldg(row + u + 1);
-      if (e0 < 0 || e1 > ne || e1 < e0) e1 = e0;  // reported by bfs_bucket_count
-    }
-    for (int j = 0; __syncthreads_or(e0 + j < e1); j += 8) {
-      for (int b = threadIdx.x; b < nslices; b += blockDim.x) hist[b] = 0;
-      __syncthreads();
-      int v[8];
-#pragma unroll
-      for (int a = 0; a < 8; a++) {
-        v[a] = -1;
-        if (e0 + j + a < e1) {
-          const int x = __ldg(col + e0 + j + a);
-          if (x >= 0 && x < nv) v[a] = x;
-        }
-      }
-      int rank[8];
-#pragma unroll
-      for (int a = 0; a < 8; a++) rank[a] = v[a] >= 0 ? atomicAdd(&hist[v[a] >> kSliceLog], 1) : 0;
-      __syncthreads();
-      if (threadIdx.x == 0) {  // local exclusive offsets + one global reservation per bucket
-        int run = 0;
-        for (int b = 0; b < nslices; b++) {
-          const int c = hist[b];
-          loff[b] = run;
-          run += c;
-          if (c) gbase[b] = atomicAdd((unsigned long long*)(cursors + b), (unsigned long long)c);
-        }
-        total = run;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int a = 0; a < 8; a++)
-        if (v[a] >= 0) stage[loff[v[a] >> kSliceLog] + rank[a]] = v[a];
-      __syncthreads();
-      for (int k = threadIdx.x; k < total; k += blockDim.x) {  // runs per bucket: coalesced writes
-        const int x = stage[k];
-        const int b = x >> kSliceLog;
-        buckets[gbase[b] + (k - loff[b])] = x;
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) bfs_bucket_apply(const int* __restrict__ buckets, const long long* offsets,
-                                                        unsigned* now, unsigned* prev, long long words, int* nq,
-                                                        int* sizes, unsigned char* lv8, int* lvl, int depth,
-                                                        int nslices) {
-  __shared__ unsigned bm[kSliceWords];
+__global__ void __launch_bounds__(256) bfs_bottom_up(const int* __restrict__ crow, const int* __restrict__ ccol,
+                                                     long long ncc, unsigned* now, unsigned* prev, long long words,
+                                                     long long nv, const unsigned* __restrict__ F, unsigned* Fn,
+                                                     int* B, int* Bn, int* vis, unsigned char* lv8, int* lvl,
+                                                     int depth) {
+  __shared__ unsigned fr[8][32];
+  __shared__ int cnt_s[8];
+  if (!B[3]) return;  // top-down level
+  if (blockIdx.x == 0 && threadIdx.x == 0) Bn[1] = 2;  // F written, no queue
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool bytes = depth + 1 < 255;
-  for (int b = blockIdx.x; b < nslices; b += gridDim.x) {
-    const long long w0 = (long long)b * kSliceWords;
-    const int nw = (int)min((long long)kSliceWords, words - w0);
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) bm[i] = now[w0 + i];
-    __syncthreads();
-    const long long lo = offsets[b], hi = offsets[b + 1];
-    for (long long k0 = lo; k0 < hi; k0 += blockDim.x) {  // CTA-uniform
-      const long long k = k0 + threadIdx.x;
-      int v = -1;
-      if (k < hi) {
-        const int x = __ldcs(buckets + k);
-        const int lw = (x >> 5) & (kSliceWords - 1);
-        const unsigned bit = 1u << (x & 31);
-        if (!(bm[lw] & bit) && !(atomicOr(&bm[lw], bit) & bit)) v = x;
-      }
-      int pos = cta_append(v >= 0 ? 1 : 0, sizes + 1);
-      if (v >= 0) {
-        nq[pos] = v;
-        if (bytes) lv8[v] = (unsigned char)(depth + 1);
-        else lvl[v] = depth + 1;
-      }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
-      const unsigned x = bm[i];
-      now[w0 + i] = x;
-      prev[w0 + i] = x;
-    }
-    __syncthreads();
-  }
-}
-
-// next frontier = now & ~prev, prev = now
-__global__ void __launch_bounds__(256) bfs_compact(unsigned* now, unsigned* prev, long long words,
-                                                   int* nq, int* sizes, int* lvl, int depth) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < words; i += stride) {
-    unsigned fresh = 0;
-    if (i < words) {
-      const unsigned nw = __ldcg(now + i);
-      fresh = nw & ~prev[i];
-      if (fresh) prev[i] = nw;
-    }
-    const int c = __popc(fresh);
+  const unsigned lb = (unsigned)(depth + 1) * 0x01010101u;
+  const int tail = (int)(nv & 31);
+  const long long nchunks = (words + 31) / 32;
+  int count = 0;
+  for (long long ch = (long long)blockIdx.x * 8 + warp; ch < nchunks; ch += (long long)gridDim.x * 8) {
+    const long long i = ch * 32 + lane;
+    const unsigned w = i < words ? now[i] : ~0u;
+    unsigned un = ~w;
+    if (i == words - 1 && tail) un &= (1u << tail) - 1u;
+    const int c = __popc(un);
     int incl = c;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int base = 0;
-    if (lane == 31 && total) base = atomicAdd(sizes + 1, total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int pos = base + incl - c;
-    while (fresh) {
-      const int b = __ffs(fresh) - 1;
-      const int v = (int)(i * 32 + b);
-      nq[pos++] = v;
-      lvl[v] = depth + 1;
-      fresh &= fresh - 1;
+    const int T = __shfl_sync(0xffffffffu, incl, 31);
+    if (T == 0) {
+      if (i < words) Fn[i] = 0u;
+      continue;
+    }
+    fr[warp][lane] = 0u;
+    __syncwarp();
+    for (int r0 = 0; r0 < T; r0 += 64) {
+      const int v0 = bu_rank_to_vertex(r0 + lane, T, incl, c, un, ch);
+      const int v1 = bu_rank_to_vertex(r0 + 32 + lane, T, incl, c, un, ch);
+      int a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+      if (v0 >= 0) {
+        a0 = __ldg(crow + v0);
+        a1 = __ldg(crow + v0 + 1);
+      }
+      if (v1 >= 0) {
+        b0 = __ldg(crow + v1);
+        b1 = __ldg(crow + v1 + 1);
+      }
+      if (a0 < 0 || a1 > ncc || a1 < a0) {
+        B[2] = 1;
+        a1 = a0;
+      }
+      if (b0 < 0 || b1 > ncc || b1 < b0) {
+        B[2] = 1;
+        b1 = b0;
+      }
+      bool h0 = false, h1 = false;
+      while (a0 < a1 || b0 < b1) {
+        int u[8];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          u[k] = a0 + k < a1 ? __ldg(ccol + a0 + k) : -1;
+          u[4 + k] = b0 + k < b1 ? __ldg(ccol + b0 + k) : -1;
+        }
+        unsigned fw[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          fw[k] = 0u;
+          if (u[k] >= 0) {
+            if (u[k] >= nv) B[2] = 1;
+            else fw[k] = __ldg(F + (u[k] >> 5)) & (1u << (u[k] & 31));
+          }
+        }
+        const bool x0 = (fw[0] | fw[1] | fw[2] | fw[3]) != 0u;
+        const bool x1 = (fw[4] | fw[5] | fw[6] | fw[7]) != 0u;
+        h0 |= x0;
+        h1 |= x1;
+        a0 = x0 ? a1 : a0 + 4;
+        b0 = x1 ? b1 : b0 + 4;
+      }
+      if (h0) atomicOr(&fr[warp][(v0 >> 5) - (int)(ch * 32)], 1u << (v0 & 31));
+      if (h1) atomicOr(&fr[warp][(v1 >> 5) - (int)(ch * 32)], 1u << (v1 & 31));
+    }
+    __syncwarp();
+    const unsigned fresh = fr[warp][lane];
+    if (i < words) {
+      Fn[i] = fresh;
+      if (fresh) {
+        now[i] = w | fresh;
+        prev[i] = w | fresh;
+        if (bytes) {
+          uint4* p = reinterpret_cast<uint4*>(lv8 + i * 32);
+          uint4 a = p[0], b = p[1];
+          a.x = lv8_merge(a.x, fresh, 0, lb);
+          a.y = lv8_merge(a.y, fresh, 4, lb);
+          a.z = lv8_merge(a.z, fresh, 8, lb);
+          a.w = lv8_merge(a.w, fresh, 12, lb);
+          b.x = lv8_merge(b.x, fresh, 16, lb);
+          b.y = lv8_merge(b.y, fresh, 20, lb);
+          b.z = lv8_merge(b.z, fresh, 24, lb);
+          b.w = lv8_merge(b.w, fresh, 28, lb);
+          p[0] = a;
+          p[1] = b;
+        } else {
+          for (unsigned f = fresh; f; f &= f - 1) lvl[i * 32 + __ffs(f) - 1] = depth + 1;
+        }
+      }
+    }
+    count += __popc(fresh);
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+  if (lane == 0) cnt_s[warp] = count;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int k = 0; k < 8; k++) tot += cnt_s[k];
+    if (tot) {
+      atomicAdd(Bn, tot);
+      atomicAdd(vis, tot);
+    }
+  }
+}
+
+// ---- graph transpose (in-edge CSR for the bottom-up step) --------------------
+// indeg[v] = number of edges u -> v with u < nv (edges outside every
+// [row[u], row[u+1]) are not edges); a malformed row or out-of-range target
+// sets err.
+__global__ void __launch_bounds__(256) bfs_indegree(const int* __restrict__ row, const int* __restrict__ col,
+                                                    long long ncol, long long nv, int* indeg, int* err) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < nv; u += stride) {
+    const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
+    if (e0 < 0 || e1 > ncol || e1 < e0) {
+      *err = 1;
+      continue;
+    }
+    for (int e = e0; e < e1; e++) {
+      const int v = __ldg(col + e);
+      if (v < 0 || v >= nv) *err = 1;
+      else atomicAdd(indeg + v, 1);
+    }
+  }
+}
+
+// ccol[cursor[v]++] = u for every edge u -> v (in-list order is unspecified:
+// the bottom-up step only asks whether any in-neighbour is in the frontier)
+__global__ void __launch_bounds__(256) bfs_fill_in_edges(const int* __restrict__ row, const int* __restrict__ col,
+                                                         long long ncol, long long nv, int* cursor, int* ccol) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < nv; u += stride) {
+    const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
+    if (e0 < 0 || e1 > ncol || e1 < e0) continue;
+    for (int e = e0; e < e1; e++) {
+      const int v = __ldg(col + e);
+      if (v >= 0 && v < nv) ccol[atomicAdd(cursor + v, 1)] = (int)u;
     }
   }
 }
 
 }  // namespace bf
 
-extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, long long lr,
-                                  const int* col, long long lcol, int* lvl, long long ll,
-                                  int nv, int src, int* depth_out, char* err, int errcap) {
+// In-edge CSR (crow: nv + 1, ccol: the edge count) of the CSR graph (row,
+// col); BF_E_FAULT when row is malformed or a target is out of range.
+extern "C" int bf_bfs_transpose_impl(void* stream_v, int num_sms, const int* row, long long lr, const int* col,
+                                     long long lcol, int nv, int* crow, long long lcrow, int* ccol, long long lccol,
+                                     char* err, int errcap) {
   using namespace bf;
   cudaStream_t stream = (cudaStream_t)stream_v;
-  if (nv <= 0 || src < 0 || src >= nv || lr < (long long)nv + 1 || ll < nv) {
-    snprintf(err, errcap, "bfs_levels: bad sizes (nv=%d src=%d len(row)=%lld len(lvl)=%lld)", nv,
-             src, lr, ll);
+  if (nv <= 0 || lr < (long long)nv + 1 || lcrow < (long long)nv + 1) {
+    snprintf(err, errcap, "bfs_transpose: bad sizes (nv=%d len(row)=%lld len(crow)=%lld)", nv, lr, lcrow);
+    return BF_E_INVALID;
+  }
+  int* ws = nullptr;  // [0] error flag, [1] edge count; then the cursor copy of crow
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cudaMalloc((void**)&ws, ((size_t)nv + 3) * 4);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, crow, crow, nv + 1, stream);
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
+  int h[2] = {0, 0};
+  if (e == cudaSuccess) {
+    const int g = stream_grid(nv, 256, num_sms, 8);
+    cudaMemsetAsync(ws, 0, 8, stream);
+    cudaMemsetAsync(crow, 0, ((size_t)nv + 1) * 4, stream);
+    bfs_indegree<<<g, 256, 0, stream>>>(row, col, lcol, nv, crow, ws);
+    e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, crow, crow, nv + 1, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ws + 1, crow + nv, 4, cudaMemcpyDeviceToDevice, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, ws, 8, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e == cudaSuccess && h[0]) {
+      snprintf(err, errcap, "bfs_transpose: CSR index out of range");
+      e = cudaErrorInvalidValue;
+    }
+    if (e == cudaSuccess && h[1] > lccol) {
+      snprintf(err, errcap, "bfs_transpose: %d edges do not fit len(ccol)=%lld", h[1], lccol);
+      e = cudaErrorInvalidValue;
+    }
+    if (e == cudaSuccess) {
+      cudaMemcpyAsync(ws + 2, crow, (size_t)nv * 4, cudaMemcpyDeviceToDevice, stream);
+      bfs_fill_in_edges<<<g, 256, 0, stream>>>(row, col, lcol, nv, ws + 2, ccol);
+      e = cudaStreamSynchronize(stream);
+    }
+  }
+  cudaFree(tmp);
+  cudaFree(ws);
+  if (e != cudaSuccess) {
+    const bool fault = e == cudaErrorInvalidValue && err[0];
+    if (!err[0]) snprintf(err, errcap, "bfs_transpose: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return fault ? BF_E_FAULT : BF_E_CUDA;
+  }
+  return BF_OK;
+}
+
+// crow/ccol null: top-down only (bf_bfs_levels); else direction-optimizing
+// (bf_bfs_levels_do) over the in-edge CSR made by bf_bfs_transpose.
+extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, long long lr, const int* col,
+                                  long long lcol, const int* crow, long long lcrow, const int* ccol, long long lccol,
+                                  int* lvl, long long ll, int nv, int src, int* depth_out, char* err, int errcap) {
+  using namespace bf;
+  cudaStream_t stream = (cudaStream_t)stream_v;
+  if (nv <= 0 || src < 0 || src >= nv || lr < (long long)nv + 1 || ll < nv ||
+      (crow && lcrow < (long long)nv + 1)) {
+    snprintf(err, errcap, "bfs_levels: bad sizes (nv=%d src=%d len(row)=%lld len(lvl)=%lld)", nv, src, lr, ll);
     return BF_E_INVALID;
   }
   const long long words = ((long long)nv + 31) / 32;
-  // scratch (bitmaps, two frontier queues, counters) is kept per device and
-  // only grows: a traversal does no allocation after the first
+  // scratch (bitmaps, frontier queues and bitmaps, counters) per stream, grow-only:
+  // a traversal does no allocation after the first
   struct Scratch : StreamScratch {
     std::mutex busy;  // a traversal is a synchronous host loop: one caller at a time per stream
-    long long cap_words = 0, cap_v = 0;
-    unsigned *now = nullptr, *prev = nullptr;
-    int *qa = nullptr, *qb = nullptr, *sizes = nullptr, *hs = nullptr;
+    long long cap_v = 0;
+    unsigned *now = nullptr, *prev = nullptr, *fb[2] = {nullptr, nullptr};
+    int *qa = nullptr, *qb = nullptr;
     unsigned char* lv8 = nullptr;
-    // bucketed levels (grow-only)
-    int* counts = nullptr;
-    long long *offsets = nullptr, *cursors = nullptr;
-    int* buckets = nullptr;
-    long long cap_buckets = 0;
-    // pipelined loop: rotating level counters, host-mapped qn record, events
-    int* ctr = nullptr;
-    int *hist = nullptr, *hist_d = nullptr;
+    int* ctr = nullptr;  // 3 rotating level blocks of 4 ints, [12] visited count
+    int *hist = nullptr, *hist_d = nullptr;  // host-mapped frontier sizes
     cudaEvent_t evx[4] = {};
-    ~Scratch() override {
+    void release() {
       cudaFree(now);
       cudaFree(prev);
+      cudaFree(fb[0]);
+      cudaFree(fb[1]);
       cudaFree(qa);
       cudaFree(qb);
       cudaFree(lv8);
-      cudaFree(sizes);
-      cudaFree(counts);
-      cudaFree(offsets);
-      cudaFree(cursors);
-      cudaFree(buckets);
+      now = prev = fb[0] = fb[1] = nullptr;
+      qa = qb = nullptr;
+      lv8 = nullptr;
+      cap_v = 0;
+    }
+    ~Scratch() override {
+      release();
       cudaFree(ctr);
-      if (hs) cudaFreeHost(hs);
       if (hist) cudaFreeHost(hist);
-      for (auto& e : evx)
-        if (e) cudaEventDestroy(e);
+      for (auto& ev : evx)
+        if (ev) cudaEventDestroy(ev);
     }
   };
   Scratch& S = scratch_for<Scratch>(stream, SCRATCH_BFS_LEVELS);
@@ -1342,231 +1252,105 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   cudaError_t e = cudaSuccess;
   if (S.cap_v < nv) {
     cudaStreamSynchronize(stream);
-    cudaFree(S.now);
-    cudaFree(S.prev);
-    cudaFree(S.qa);
-    cudaFree(S.qb);
-    cudaFree(S.lv8);
-    S.now = S.prev = nullptr;
-    S.qa = S.qb = nullptr;
-    S.lv8 = nullptr;
-    S.cap_v = S.cap_words = 0;
+    S.release();
     e = cudaMalloc((void**)&S.now, words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.prev, words * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.fb[0], words * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.fb[1], words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.qa, (size_t)nv * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&S.qb, (size_t)nv * 4);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&S.lv8, (size_t)words * 32 + 16);  // whole sectors (bfs_compact8s)
-    if (e == cudaSuccess) {
-      S.cap_v = nv;
-      S.cap_words = words;
-    }
+    if (e == cudaSuccess) e = cudaMalloc((void**)&S.lv8, (size_t)words * 32 + 16);  // whole sectors
+    if (e == cudaSuccess) S.cap_v = nv;
   }
-  if (e == cudaSuccess && !S.sizes) e = cudaMalloc((void**)&S.sizes, 16);
-  if (e == cudaSuccess && !S.hs) e = cudaMallocHost((void**)&S.hs, 16);
-  if (e == cudaSuccess && !S.ctr) e = cudaMalloc((void**)&S.ctr, 12 * sizeof(int));
+  if (e == cudaSuccess && !S.ctr) e = cudaMalloc((void**)&S.ctr, 16 * sizeof(int));
   if (e == cudaSuccess && !S.hist) {
     e = cudaHostAlloc((void**)&S.hist, 64 * sizeof(int), cudaHostAllocMapped);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&S.hist_d, S.hist, 0);
     for (int i = 0; i < 4 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&S.evx[i], cudaEventDisableTiming);
   }
-  unsigned *now = S.now, *prev = S.prev;
-  int *qa = S.qa, *qb = S.qb, *sizes = S.sizes, *hs = S.hs;
-  unsigned char* lv8 = S.lv8;
-  static int variant = -1;  // 1: scalar-edge expansion + direct lvl writes (round-1 path)
-  if (variant < 0) {
-    const char* ve = getenv("BF_BFS_V");
-    variant = ve ? atoi(ve) : 2;
+  // BF_BFS_DO=0 keeps a direction-optimizing call top-down (A/B); BF_BFS_ALPHA16:
+  // bottom-up when 16 * |frontier| * alpha16 / 16 >= unvisited
+  static int do_on = -1, alpha16 = 32;
+  if (do_on < 0) {
+    const char* de = getenv("BF_BFS_DO");
+    do_on = de ? atoi(de) : 1;
+    const char* ae = getenv("BF_BFS_ALPHA16");
+    if (ae) alpha16 = std::max(1, atoi(ae));
   }
-  static int bucket_on = -1;  // bucketed large levels, opt-in (BF_BFS_BUCKET=1): see below
-  if (bucket_on < 0) {
-    const char* be = getenv("BF_BFS_BUCKET");
-    bucket_on = be ? atoi(be) : 0;
-  }
-  // small levels (qn * BF_BFS_APP <= nv) expand and append in one pass; 0: off
-  static int app_div = -1;
-  if (app_div < 0) {
-    const char* ae = getenv("BF_BFS_APP");
-    app_div = ae ? atoi(ae) : 0;
-  }
-  static int cs_on = -1;  // coalesced compaction (bfs_compact8s), BF_BFS_CS
-  if (cs_on < 0) {
-    const char* ce = getenv("BF_BFS_CS");
-    cs_on = ce ? atoi(ce) : 1;
-  }
+  const bool dir = crow && ccol && do_on;
   bool deep = false;
   int depth = 0;
-  // keep the visited bitmap resident in L2 while the graph streams through
-  cudaStreamAttrValue win = {};
-  bool windowed = false;
-  const char* wenv = getenv("BF_BFS_L2WIN");
-  if (e == cudaSuccess && wenv && atoi(wenv) > 0) {
-    int dev = 0, maxwin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    size_t want = (size_t)words * 4;
-    if (maxwin > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
-      win.accessPolicyWindow.base_ptr = now;
-      win.accessPolicyWindow.num_bytes = want < (size_t)maxwin ? want : (size_t)maxwin;
-      win.accessPolicyWindow.hitRatio = 1.0f;
-      win.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      win.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      windowed = cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &win) == cudaSuccess;
-    }
-    cudaGetLastError();
-  }
   if (e == cudaSuccess) {
-    int g = stream_grid(nv, 256 * 4, num_sms, 8);
-    if (variant == 1) {
-      bfs_init<<<g, 256, 0, stream>>>(lvl, now, prev, nv, words, src, qa, sizes);
-      bfs_seed<<<1, 1, 0, stream>>>(lvl, now, prev, src);
-    } else {
-      bfs_init8<<<g, 256, 0, stream>>>(lv8, now, prev, nv, words, src, qa, sizes);
-      bfs_seed8<<<1, 1, 0, stream>>>(lv8, now, prev, src);
-    }
-    int qn = 1;
-    int* q = qa;
-    int* nq = qb;
-    const int cgrid = stream_grid(words, 256, num_sms, 8);
-    // Default path, pipelined: the host enqueues level d + 2 as soon as level
-    // d + 1's expansion has recorded its frontier size (host-mapped), so the
-    // device never waits for a host round trip between levels.  Three
-    // rotating counters: level L expands ctr[4(L%3)] vertices, its compaction
-    // appends into ctr[4((L+1)%3)], and its expansion zeroes ctr[4((L+2)%3)]
-    // (that level's input was consumed by level L - 1); [+2] error flags.
-    const bool piped = variant == 2 && !bucket_on && app_div <= 0 && cs_on;
-    if (piped) {
-      const int xgrid = wave_grid(bfs_expand_v<true>, 256, 0, ((long long)nv + 1) / 2, 256, num_sms, 8);
-      const int sgrid = wave_grid(bfs_compact8s, 256, 0, words, 256, num_sms, 8);
-      auto enqueue = [&](int L) {
-        int* B = S.ctr + 4 * (L % 3);
-        int* Bn = S.ctr + 4 * ((L + 1) % 3);
-        int* Bz = S.ctr + 4 * ((L + 2) % 3);
-        int* qL = (L & 1) ? qb : qa;
-        int* nqL = (L & 1) ? qa : qb;
-        if (L + 1 >= 255 && !deep) {  // levels beyond a byte: lvl written directly from here on
-          bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, nv);
-          deep = true;
-        }
-        bfs_expand_v<true><<<xgrid, 256, 0, stream>>>(row, col, lcol, now, nv, qL, B, Bz, S.hist_d + (L & 63));
-        cudaEventRecord(S.evx[L & 3], stream);
-        bfs_compact8s<<<sgrid, 256, 0, stream>>>(now, prev, words, nqL, B, Bn, lv8, lvl, L);
-      };
-      cudaMemsetAsync(S.ctr, 0, 12 * sizeof(int), stream);
-      bfs_init8<<<g, 256, 0, stream>>>(lv8, now, prev, nv, words, src, qa, S.ctr);
-      bfs_seed8<<<1, 1, 0, stream>>>(lv8, now, prev, src);
-      enqueue(0);
-      enqueue(1);
-      for (int d = 0;; d++) {
-        e = cudaEventSynchronize(S.evx[(d + 1) & 3]);
-        if (e != cudaSuccess) break;
-        const int qn1 = ((volatile int*)S.hist)[(d + 1) & 63];
-        if (qn1 == 0) {
-          depth = d + 1;
-          break;
-        }
-        enqueue(d + 2);
+    unsigned *now = S.now, *prev = S.prev;
+    unsigned char* lv8 = S.lv8;
+    int* vis = S.ctr + 12;
+    const int g = stream_grid(nv, 256 * 4, num_sms, 8);
+    const int xgrid = wave_grid(bfs_expand_v<true>, 256, 0, ((long long)nv + 1) / 2, 256, num_sms, 8);
+    const int sgrid = wave_grid(bfs_compact8s, 256, 0, words, 256, num_sms, 8);
+    const int bgrid = wave_grid(bfs_bottom_up, 256, 0, (words + 31) / 32, 8, num_sms, 8);
+    // Pipelined: the host enqueues level d + 2 as soon as level d + 1's
+    // expansion has recorded its frontier size (host-mapped), so the device
+    // never waits for a host round trip between levels.  Level L uses
+    // counter block ctr[4(L%3)] (its frontier), appends into ctr[4((L+1)%3)],
+    // and its expansion clears ctr[4((L+2)%3)] (consumed by level L - 1).
+    // Bottom-up steps are armed (the previous compaction writes the frontier
+    // bitmap and the step is launched; the device still picks) while the
+    // last known frontier could reach the switch point within two levels.
+    long long seen = 1;  // vertices in the frontiers whose sizes the host has read
+    bool armed = false;
+    auto arm = [&](long long f_last) {
+      const long long unvisited = (long long)nv - seen;
+      return dir && f_last * 256LL * alpha16 >= 16 * unvisited;
+    };
+    bool armed_next = false;  // compaction L wrote F_{L+1}
+    auto enqueue = [&](int L) {
+      int* B = S.ctr + 4 * (L % 3);
+      int* Bn = S.ctr + 4 * ((L + 1) % 3);
+      int* Bz = S.ctr + 4 * ((L + 2) % 3);
+      int* qL = (L & 1) ? S.qb : S.qa;
+      int* nqL = (L & 1) ? S.qa : S.qb;
+      if (L + 1 >= 255 && !deep) {  // levels beyond a byte: lvl written directly from here on
+        bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, nv);
+        deep = true;
       }
-      if (e == cudaSuccess) {
-        int c[12];
-        cudaMemcpyAsync(c, S.ctr, sizeof(c), cudaMemcpyDeviceToHost, stream);
-        e = cudaStreamSynchronize(stream);
-        if (e == cudaSuccess && (c[2] | c[6] | c[10])) {
-          snprintf(err, errcap, "bfs_levels: CSR index out of range");
-          e = cudaErrorInvalidValue;
-        }
-      }
-      qn = 0;
-    }
-    // per-level host loop (other variants)
-    while (qn > 0) {
-      if (variant == 1) {
-        int grid = stream_grid((qn + kBfsVPT - 1) / kBfsVPT, 256, num_sms, 8);
-        bfs_expand<<<grid, 256, 0, stream>>>(row, col, lcol, lvl, now, nv, q, sizes, depth);
-        bfs_compact<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lvl, depth);
-      } else {
-        if (depth + 1 >= 255 && !deep) {  // levels beyond a byte: lvl written directly from here on
-          bfs_fill_m1<<<g, 256, 0, stream>>>(lvl, nv);
-          deep = true;
-        }
-        bool appended = false;
-        const int nslices = (int)((nv + (1 << kSliceLog) - 1) >> kSliceLog);
-        bool bucketed = bucket_on && nslices <= kMaxSlices && (long long)qn * 32 >= nv && nslices >= 2;
-        if (bucketed && (!S.counts || S.cap_buckets < lcol)) {
-          cudaStreamSynchronize(stream);
-          cudaFree(S.counts);
-          cudaFree(S.offsets);
-          cudaFree(S.cursors);
-          cudaFree(S.buckets);
-          S.counts = nullptr;
-          S.offsets = S.cursors = nullptr;
-          S.buckets = nullptr;
-          S.cap_buckets = 0;
-          if (cudaMalloc((void**)&S.counts, kMaxSlices * 4) == cudaSuccess &&
-              cudaMalloc((void**)&S.offsets, (kMaxSlices + 1) * 8) == cudaSuccess &&
-              cudaMalloc((void**)&S.cursors, kMaxSlices * 8) == cudaSuccess &&
-              cudaMalloc((void**)&S.buckets, (size_t)std::max(lcol, 1LL) * 4) == cudaSuccess) {
-            S.cap_buckets = lcol;
-          } else {
-            cudaGetLastError();
-            bucketed = false;  // not enough memory: the probing level below
-          }
-        }
-        if (bucketed) {
-          cudaMemsetAsync(S.counts, 0, nslices * 4, stream);
-          const int g1 = wave_grid(bfs_bucket_count, 256, 0, qn, 256, num_sms, 8);
-          bfs_bucket_count<<<g1, 256, 0, stream>>>(row, col, lcol, nv, q, sizes, sizes, S.counts, nslices);
-          bfs_bucket_scan<<<1, 1024, 0, stream>>>(S.counts, S.offsets, S.cursors, nslices);
-          const int g3 = wave_grid(bfs_bucket_scatter, 256, 0, qn, 256, num_sms, 8);
-          bfs_bucket_scatter<<<g3, 256, 0, stream>>>(row, col, lcol, nv, q, sizes, S.cursors, S.buckets, nslices);
-          bfs_bucket_apply<<<nslices, 256, 0, stream>>>(S.buckets, S.offsets, now, prev, words, nq, sizes, lv8, lvl,
-                                                        depth, nslices);
-        } else if (variant == 4) {  // four frontier vertices per thread (32 probes in flight)
-          int grid = wave_grid(bfs_expand_v<true, 4>, 256, 0, (qn + 3) / 4, 256, num_sms, 8);
-          bfs_expand_v<true, 4><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes, nullptr, nullptr);
-        } else if (variant == 3) {
-          int grid = wave_grid(bfs_expand_v<false>, 256, 0, (qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
-          bfs_expand_v<false><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes, nullptr, nullptr);
-        } else if (app_div > 0 && (long long)qn * app_div <= nv) {  // small level: fused append
-          int grid = wave_grid(bfs_expand_app<2>, 256, 0, (qn + 1) / 2, 256, num_sms, 8);
-          bfs_expand_app<2><<<grid, 256, 0, stream>>>(row, col, lcol, now, prev, nv, q, sizes, nq, lv8, lvl,
-                                                      depth, deep);
-          appended = true;
-        } else {
-          int grid = wave_grid(bfs_expand_v<true>, 256, 0, (qn + kBfsV2 - 1) / kBfsV2, 256, num_sms, 8);
-          bfs_expand_v<true><<<grid, 256, 0, stream>>>(row, col, lcol, now, nv, q, sizes, nullptr, nullptr);
-        }
-        if (appended) {
-        } else if (!bucketed && cs_on && !deep && depth + 1 < 255) {
-          const int sgrid = wave_grid(bfs_compact8s, 256, 0, words, 256, num_sms, 8);
-          bfs_compact8s<<<sgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, sizes + 1, lv8, lvl, depth);
-        } else if (!bucketed) {
-          bfs_compact8<<<cgrid, 256, 0, stream>>>(now, prev, words, nq, sizes, lv8, lvl, depth);
-        }
-      }
-      cudaMemcpyAsync(hs, sizes, 12, cudaMemcpyDeviceToHost, stream);
-      e = cudaStreamSynchronize(stream);
+      const bool bu = armed_next;  // F_L exists: the bottom-up step may run
+      armed_next = armed;
+      bfs_expand_v<true><<<xgrid, 256, 0, stream>>>(row, col, lcol, now, nv, qL, B, Bz, S.hist_d + (L & 63),
+                                                     bu ? vis : nullptr, alpha16, dir ? S.fb[L & 1] : nullptr);
+      cudaEventRecord(S.evx[L & 3], stream);
+      if (bu)
+        bfs_bottom_up<<<bgrid, 256, 0, stream>>>(crow, ccol, lccol, now, prev, words, nv, S.fb[L & 1],
+                                                  S.fb[(L + 1) & 1], B, Bn, vis, lv8, lvl, L);
+      bfs_compact8s<<<sgrid, 256, 0, stream>>>(now, prev, words, nqL, B, Bn, lv8, lvl, L,
+                                               armed_next ? S.fb[(L + 1) & 1] : nullptr, vis);
+    };
+    cudaMemsetAsync(S.ctr, 0, 16 * sizeof(int), stream);
+    bfs_init8<<<g, 256, 0, stream>>>(lv8, now, prev, nv, words, src, S.qa, S.ctr);
+    bfs_seed8<<<1, 1, 0, stream>>>(lv8, now, prev, src);
+    enqueue(0);
+    enqueue(1);
+    for (int d = 0;; d++) {
+      e = cudaEventSynchronize(S.evx[(d + 1) & 3]);
       if (e != cudaSuccess) break;
-      if (hs[2]) {
-        snprintf(err, errcap, "bfs_levels: CSR index out of range");
-        e = cudaErrorInvalidValue;
+      const int qn1 = ((volatile int*)S.hist)[(d + 1) & 63];
+      if (qn1 == 0) {
+        depth = d + 1;
         break;
       }
-      depth++;
-      qn = hs[1];
-      hs[0] = qn;
-      hs[1] = 0;
-      cudaMemcpyAsync(sizes, hs, 8, cudaMemcpyHostToDevice, stream);
-      int* t = q;
-      q = nq;
-      nq = t;
+      seen += qn1;
+      armed = arm(qn1);
+      enqueue(d + 2);
     }
-    if (e == cudaSuccess && variant != 1) bfs_finish<<<g, 256, 0, stream>>>(lv8, lvl, nv, deep);
-  }
-  if (windowed) {
-    win.accessPolicyWindow.num_bytes = 0;
-    cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &win);
-    cudaCtxResetPersistingL2Cache();
-    cudaGetLastError();
+    if (e == cudaSuccess) {
+      int c[12];
+      cudaMemcpyAsync(c, S.ctr, sizeof(c), cudaMemcpyDeviceToHost, stream);
+      e = cudaStreamSynchronize(stream);
+      if (e == cudaSuccess && (c[2] | c[6] | c[10])) {
+        snprintf(err, errcap, "bfs_levels: CSR index out of range");
+        e = cudaErrorInvalidValue;
+      }
+    }
+    if (e == cudaSuccess) bfs_finish<<<g, 256, 0, stream>>>(lv8, lvl, nv, deep);
   }
   cudaStreamSynchronize(stream);
   if (e != cudaSuccess) {
@@ -1577,6 +1361,7 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   *depth_out = depth;
   return BF_OK;
 }
+
 
 // ---- sharded traversal state (bf_bfs_* in include/bfgpu.h) ----------------
 struct BfsShard {

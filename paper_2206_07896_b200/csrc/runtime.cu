@@ -1384,28 +1384,66 @@ int bf_worker_stream(bf_runtime* rt, int32_t worker, void** stream) {
 
 // ---- host-program drivers ---------------------------------------------------
 
-int bf_bfs_levels_impl(void* stream, int num_sms, const int* row, long long lr, const int* col,
-                       long long lcol, int* lvl, long long ll, int nv, int src, int* depth_out,
-                       char* err, int errcap);
+int bf_bfs_levels_impl(void* stream, int num_sms, const int* row, long long lr, const int* col, long long lcol,
+                       const int* crow, long long lcrow, const int* ccol, long long lccol, int* lvl, long long ll,
+                       int nv, int src, int* depth_out, char* err, int errcap);
+int bf_bfs_transpose_impl(void* stream, int num_sms, const int* row, long long lr, const int* col, long long lcol,
+                          int nv, int* crow, long long lcrow, int* ccol, long long lccol, char* err, int errcap);
 
-int bf_bfs_levels(bf_runtime* rt, uint32_t row, uint32_t col, uint32_t lvl, int32_t nv,
-                  int32_t source, int32_t* depth) {
+static int bfs_levels_common(bf_runtime* rt, uint32_t row, uint32_t col, const uint32_t* crow, const uint32_t* ccol,
+                             uint32_t lvl, int32_t nv, int32_t source, int32_t* depth) {
   if (!rt || !depth) return fail(BF_E_INVALID, "null argument");
   if (rt->shut_down) return fail(BF_E_SHUTDOWN, "launch after shutdown");
   Buffer* R = lookup(rt->arena, row);
   Buffer* C = lookup(rt->arena, col);
   Buffer* L = lookup(rt->arena, lvl);
-  if (!R || !C || !L) return fail(BF_E_DANGLING, "dangling buffer handle");
-  if (R->scalar != BF_I32 || C->scalar != BF_I32 || L->scalar != BF_I32)
-    return fail(BF_E_TYPEFAULT, "bfs_levels: row, col and lvl must be i32 buffers");
+  Buffer* CR = crow ? lookup(rt->arena, *crow) : nullptr;
+  Buffer* CC = ccol ? lookup(rt->arena, *ccol) : nullptr;
+  if (!R || !C || !L || (crow && !CR) || (ccol && !CC)) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (R->scalar != BF_I32 || C->scalar != BF_I32 || L->scalar != BF_I32 || (CR && CR->scalar != BF_I32) ||
+      (CC && CC->scalar != BF_I32))
+    return fail(BF_E_TYPEFAULT, "bfs_levels: row, col, lvl (and the transposed graph) must be i32 buffers");
   int rc = set_device(rt->device);
   if (rc) return rc;
   rc = sync_workers(rt);
   if (rc) return rc;
   char err[256] = {0};
-  rc = bf_bfs_levels_impl((void*)rt->streams[0], rt->num_sms, (const int*)R->ptr, R->length,
-                          (const int*)C->ptr, C->length, (int*)L->ptr, L->length, nv, source,
-                          depth, err, sizeof(err));
+  rc = bf_bfs_levels_impl((void*)rt->streams[0], rt->num_sms, (const int*)R->ptr, R->length, (const int*)C->ptr,
+                          C->length, CR ? (const int*)CR->ptr : nullptr, CR ? CR->length : 0,
+                          CC ? (const int*)CC->ptr : nullptr, CC ? CC->length : 0, (int*)L->ptr, L->length, nv,
+                          source, depth, err, sizeof(err));
+  if (rc) return fail(rc, err);
+  return BF_OK;
+}
+
+int bf_bfs_levels(bf_runtime* rt, uint32_t row, uint32_t col, uint32_t lvl, int32_t nv, int32_t source,
+                  int32_t* depth) {
+  return bfs_levels_common(rt, row, col, nullptr, nullptr, lvl, nv, source, depth);
+}
+
+int bf_bfs_levels_do(bf_runtime* rt, uint32_t row, uint32_t col, uint32_t crow, uint32_t ccol, uint32_t lvl,
+                     int32_t nv, int32_t source, int32_t* depth) {
+  return bfs_levels_common(rt, row, col, &crow, &ccol, lvl, nv, source, depth);
+}
+
+int bf_bfs_transpose(bf_runtime* rt, uint32_t row, uint32_t col, int32_t nv, uint32_t crow, uint32_t ccol) {
+  if (!rt) return fail(BF_E_INVALID, "null argument");
+  if (rt->shut_down) return fail(BF_E_SHUTDOWN, "launch after shutdown");
+  Buffer* R = lookup(rt->arena, row);
+  Buffer* C = lookup(rt->arena, col);
+  Buffer* CR = lookup(rt->arena, crow);
+  Buffer* CC = lookup(rt->arena, ccol);
+  if (!R || !C || !CR || !CC) return fail(BF_E_DANGLING, "dangling buffer handle");
+  if (R->scalar != BF_I32 || C->scalar != BF_I32 || CR->scalar != BF_I32 || CC->scalar != BF_I32)
+    return fail(BF_E_TYPEFAULT, "bfs_transpose: row, col, crow and ccol must be i32 buffers");
+  int rc = set_device(rt->device);
+  if (rc) return rc;
+  rc = sync_workers(rt);
+  if (rc) return rc;
+  char err[256] = {0};
+  rc = bf_bfs_transpose_impl((void*)rt->streams[0], rt->num_sms, (const int*)R->ptr, R->length,
+                             (const int*)C->ptr, C->length, nv, (int*)CR->ptr, CR->length, (int*)CC->ptr,
+                             CC->length, err, sizeof(err));
   if (rc) return fail(rc, err);
   return BF_OK;
 }

@@ -10,15 +10,47 @@ produces exactly the levels of the per-level launches of kernels/bfs.kn
 from __future__ import annotations
 
 import ctypes as C
+from typing import NamedTuple, Optional
 
 from . import _lib
 from ._lib import BfError
 
 
-def bfs_levels(rt, row: int, col: int, lvl: int, nv: int, source: int = 0) -> int:
-    """Fill buffer `lvl` with BFS levels from `source`; returns max level + 1."""
+class Transposed(NamedTuple):
+    """In-edge CSR of a graph (arena handles): ccol[crow[v] .. crow[v+1]) are
+    the sources of the edges into v."""
+    crow: int
+    ccol: int
+
+
+def transpose(rt, row: int, col: int, nv: int) -> Transposed:
+    """Build the in-edge CSR of (row, col) on the device (bf_bfs_transpose),
+    allocating its two i32 buffers in rt's arena; done once per graph."""
+    arena = rt.arena
+    crow = arena.alloc("i32", nv + 1)
+    ccol = arena.alloc("i32", max(1, arena.length(col)))
+    try:
+        rc = _lib.lib().bf_bfs_transpose(rt._native, row, col, nv, crow, ccol)
+        if rc != _lib.OK:
+            raise BfError(rc, _lib.last_error())
+    except BaseException:
+        arena.free(crow)
+        arena.free(ccol)
+        raise
+    return Transposed(crow, ccol)
+
+
+def bfs_levels(rt, row: int, col: int, lvl: int, nv: int, source: int = 0,
+               transposed: Optional[Transposed] = None) -> int:
+    """Fill buffer `lvl` with BFS levels from `source`; returns max level + 1.
+    With `transposed` (from `transpose`) the traversal is
+    direction-optimizing: large frontiers are expanded bottom-up."""
     depth = C.c_int32()
-    rc = _lib.lib().bf_bfs_levels(rt._native, row, col, lvl, nv, source, C.byref(depth))
+    if transposed is None:
+        rc = _lib.lib().bf_bfs_levels(rt._native, row, col, lvl, nv, source, C.byref(depth))
+    else:
+        rc = _lib.lib().bf_bfs_levels_do(rt._native, row, col, transposed.crow, transposed.ccol, lvl, nv,
+                                         source, C.byref(depth))
     if rc != _lib.OK:
         raise BfError(rc, _lib.last_error())
     return depth.value

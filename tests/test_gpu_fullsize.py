@@ -102,6 +102,18 @@ def test_bfs_2_26_fused_vs_oracle(graph_2_26):
     assert bit_equal(arena.to_numpy(hl), lv)
 
 
+def test_bfs_2_26_direction_optimizing_vs_oracle(graph_2_26):
+    from paper_2206_07896_b200 import Runtime, graph
+    nv, row, col, lv, depth = graph_2_26
+    arena, hr, hc, hl = _bfs_arena(nv, row, col)
+    with Runtime(arena) as rt:
+        tg = graph.transpose(rt, hr, hc, nv)
+        for _ in range(2):  # the second traversal reuses the scratch
+            arena.fill_value(hl, 3)
+            assert graph.bfs_levels(rt, hr, hc, hl, nv, 0, transposed=tg) == depth
+            assert bit_equal(arena.to_numpy(hl), lv)
+
+
 def test_bfs_2_26_per_level_vs_oracle(graph_2_26):
     """Rodinia's host loop: one `bfs` launch per level, read `changed`."""
     from paper_2206_07896_b200 import ArgSlot, Dim3, PackedArgs, Runtime, routines

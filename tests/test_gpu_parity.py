@@ -283,8 +283,55 @@ def test_bfs_levels_fused_vs_oracle():
         arena.upload_numpy(hc, col)
         with Runtime(arena) as rt:
             got_depth = graph.bfs_levels(rt, hr, hc, hl, nv, src)
-        assert bit_equal(arena.to_numpy(hl), want)
-        assert got_depth == depth
+            assert bit_equal(arena.to_numpy(hl), want)
+            assert got_depth == depth
+            # direction-optimizing (bottom-up on the large levels)
+            arena.fill_value(hl, 7)
+            tg = graph.transpose(rt, hr, hc, nv)
+            assert graph.bfs_levels(rt, hr, hc, hl, nv, src, transposed=tg) == depth
+            assert bit_equal(arena.to_numpy(hl), want)
+
+
+def test_bfs_transpose_vs_numpy():
+    """bf_bfs_transpose: crow is the in-degree prefix sum and each in-list
+    holds exactly the sources of the edges into that vertex (order
+    unspecified); edges outside every row range are not edges; a malformed
+    row or an out-of-range target is BF_E_FAULT."""
+    from paper_2206_07896_b200 import DeviceArena, Runtime, graph
+    from paper_2206_07896_b200._lib import E_FAULT, BfError
+    g = np.random.default_rng(5)
+    for nv, maxdeg in [(1, 3), (1000, 9), (70001, 17)]:
+        degs = g.integers(0, maxdeg, nv)
+        row = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
+        col = g.integers(0, nv, int(row[-1]) + 5).astype(np.int32)  # 5 trailing non-edges
+        arena = DeviceArena()
+        hr, hc = arena.alloc("i32", nv + 1), arena.alloc("i32", col.size)
+        arena.upload_numpy(hr, row)
+        arena.upload_numpy(hc, col)
+        with Runtime(arena) as rt:
+            tg = graph.transpose(rt, hr, hc, nv)
+        crow, ccol = arena.to_numpy(tg.crow), arena.to_numpy(tg.ccol)
+        ne = int(row[-1])
+        src = np.repeat(np.arange(nv), degs)
+        dst = col[:ne].astype(np.int64)
+        assert np.array_equal(crow, np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=nv))]))
+        want = np.lexsort((src, dst))
+        got_pairs = np.stack([np.repeat(np.arange(nv), np.diff(crow)), ccol[:ne]])
+        order = np.lexsort((got_pairs[1], got_pairs[0]))
+        assert np.array_equal(got_pairs[:, order], np.stack([dst[want], src[want]]))
+    arena = DeviceArena()
+    hr, hc = arena.alloc("i32", 4), arena.alloc("i32", 4)
+    arena.upload_numpy(hr, np.array([0, 1, 2, 4], np.int32))
+    arena.upload_numpy(hc, np.array([1, 2, 3, 0], np.int32))  # target 3 >= nv
+    with Runtime(arena) as rt:
+        with pytest.raises(BfError) as ei:
+            graph.transpose(rt, hr, hc, 3)
+        assert ei.value.code == E_FAULT
+        arena.upload_numpy(hc, np.array([1, 2, 0, 0], np.int32))
+        arena.upload_numpy(hr, np.array([0, 2, 1, 4], np.int32))  # row not monotone
+        with pytest.raises(BfError) as ei:
+            graph.transpose(rt, hr, hc, 3)
+        assert ei.value.code == E_FAULT
 
 
 @pytest.mark.parametrize("tsteps", [0, 1, 2, 3, 4, 8, 12, 16])
@@ -748,14 +795,15 @@ def test_benchmark_configs_full_size_vs_oracle():
     assert bit_equal(got["member"], want["member"]) and bit_equal(got["counts"], want["counts"])
 
 
-@pytest.mark.parametrize("switch", [{"BF_BFS_BUCKET": "1"}, {"BF_BFS_CS": "0"}, {"BF_BFS_APP": "256"},
-                                    {"BF_BFS_APP": "1"}, {"BF_BFS_V": "4"}])
+@pytest.mark.parametrize("switch", [{"BF_BFS_ALPHA16": "1000000"}, {"BF_BFS_ALPHA16": "1"},
+                                    {"BF_BFS_DO": "0"}])
 def test_bfs_opt_in_levels_vs_oracle(switch):
-    """The opt-in traversal variants stay bit-exact: bucketed large levels
-    (BF_BFS_BUCKET=1), the per-level host loop with byte-store compaction
-    (BF_BFS_CS=0), fused expand-and-append for small levels (BF_BFS_APP),
-    four vertices per thread (BF_BFS_V=4); a chain graph takes each past 255
-    levels.  Run in a subprocess: the switches are read when the library loads."""
+    """The direction-optimizing traversal under other switch points stays
+    bit-exact: bottom-up on every armed level (BF_BFS_ALPHA16=1000000, from
+    level 3 on, including the tiny ones and a chain graph past 255 levels,
+    where the bottom-up step writes lvl directly), bottom-up only on huge
+    frontiers (1), and top-down only (BF_BFS_DO=0).  Run in a subprocess: the
+    switches are read when the library loads."""
     import os
     import subprocess
     import sys
@@ -789,7 +837,7 @@ for (r, c), src in [((row, col), 7), (I.random_graph(1 << 21, 8, 3), 0), (chain,
     arena.upload_numpy(hr, r)
     arena.upload_numpy(hc, c)
     with Runtime(arena) as rt:
-        assert graph.bfs_levels(rt, hr, hc, hl, n, src) == depth
+        assert graph.bfs_levels(rt, hr, hc, hl, n, src, transposed=graph.transpose(rt, hr, hc, n)) == depth
     assert bit_equal(arena.to_numpy(hl), want)
 print("ok")
 """
