@@ -724,11 +724,12 @@ def run_reorder(args) -> None:
 
 def run_grain(args) -> None:
     """the paper's grain-size study on the GPU runtime.
-    A fetch of `grain` logical blocks is one grid launch on a worker stream,
-    so the grain trades launch count against per-launch parallelism exactly
-    as block_per_fetch trades fetch count against load balance on the CPU
-    pool.  Reports fetches, wall time per launch+sync and
-    device throughput for vecadd and hist at pool sizes 1/4/8."""
+    fetch="device": the CTAs of one persistent grid claim block_per_fetch
+    blocks per atomic on a device counter, so the grain trades claim count
+    (atomic traffic on one address) against load balance as block_per_fetch
+    does on the CPU pool; fetch="host": each fetch is one
+    grid launch (the grain trades launch count instead).  Reports fetches and
+    wall time per launch+sync for vecadd and hist at pool sizes 1/4/8."""
     import torch
 
     from paper_2206_07896_b200 import (ArgSlot, Average, DeviceArena, Dim3, Fixed, PackedArgs,
@@ -752,24 +753,28 @@ def run_grain(args) -> None:
     }
     rows = []
     for name, (routine, pk, nbytes) in cases.items():
-        for pool in (1, 4, 8):
-            for grain in (1, 16, 256, 4096, "average"):
-                policy = Average() if grain == "average" else Fixed(grain)
-                rt = Runtime(arena, pool_size=pool, policy=policy)
-                rt.launch(routine, Dim3(blocks), Dim3(256), 0, pk)
-                rt.device_synchronize()
-                reps = 3
-                t0 = time.perf_counter()
-                for _ in range(reps):
-                    task = rt.launch(routine, Dim3(blocks), Dim3(256), 0, pk)
+        for fetch in ("device", "host"):
+            for pool in (1, 4, 8):
+                for grain in (1, 4, 16, 256, 4096, "average"):
+                    policy = Average() if grain == "average" else Fixed(grain)
+                    rt = Runtime(arena, pool_size=pool, policy=policy, fetch=fetch)
+                    rt.launch(routine, Dim3(blocks), Dim3(256), 0, pk)
                     rt.device_synchronize()
-                wall = (time.perf_counter() - t0) / reps
-                rows.append({"kernel": name, "pool": pool, "grain": grain,
-                             "block_per_fetch": task.block_per_fetch, "fetches": task.fetches,
-                             "wall_ms": round(wall * 1e3, 4), "gbs": round(nbytes / wall / 1e9, 2)})
-                rt.shutdown()
+                    reps = 3 if fetch == "host" and grain in (1, 4) else 20
+                    t0 = time.perf_counter()
+                    for _ in range(reps):
+                        task = rt.launch(routine, Dim3(blocks), Dim3(256), 0, pk)
+                        rt.device_synchronize()
+                    wall = (time.perf_counter() - t0) / reps
+                    rows.append({"kernel": name, "fetch": fetch, "pool": pool, "grain": grain,
+                                 "block_per_fetch": task.block_per_fetch, "fetches": task.fetches,
+                                 "wall_ms": round(wall * 1e3, 4), "gbs": round(nbytes / wall / 1e9, 2)})
+                    rt.shutdown()
     print(json.dumps({"metric": "grain-size study (fetches vs launch+sync wall time)", "value": None,
-                      "unit": "GB/s", "n_gpus": 1, "config": {"workload": "vecadd/hist 2^24, 65536 blocks x 256"},
+                      "unit": "GB/s", "n_gpus": 1,
+                      "config": {"workload": "vecadd/hist 2^24, 65536 blocks x 256",
+                                 "fetch": "device: one persistent grid claims block_per_fetch blocks per atomic "
+                                          "(Runtime(fetch='device')); host: one grid launch per fetched range"},
                       "grain": rows}), flush=True)
 
 

@@ -109,6 +109,13 @@ enum bf_policy { BF_POLICY_AVERAGE = 0, BF_POLICY_FIXED = 1, BF_POLICY_AUTO = 2 
 /* Runtime creation flags. */
 #define BF_FLAG_HOLD_BLOCKS 0x1u  /* gate every block until the next sync (runtime.py:219-222) */
 #define BF_FLAG_INSTRUMENT  0x2u  /* device-side per-block executed[] counters (runtime.py:121,345) */
+/* Device-side block fetching: a launch whose kernel supports it is ONE
+ * persistent grid whose CTAs claim block_per_fetch logical blocks at a time
+ * from a device claim counter (the paper's block fetching, runtime.py:175-201,
+ * 305-350, done by the GPU's own CTAs instead of host-issued launches);
+ * fetch counts, busy blocks and executed[] come from the device.  Other
+ * kernels (and held or delayed launches) keep host-issued fetches. */
+#define BF_FLAG_DEVICE_FETCH 0x4u
 
 typedef struct bf_arena bf_arena;
 typedef struct bf_runtime bf_runtime;

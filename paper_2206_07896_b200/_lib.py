@@ -25,6 +25,7 @@ TRAP_NAMES = {0: None, 1: "OutOfBounds", 2: "DivByZero", 3: "TypeFault", 4: "Non
 POLICY_AVERAGE, POLICY_FIXED, POLICY_AUTO = 0, 1, 2
 FLAG_HOLD_BLOCKS = 0x1
 FLAG_INSTRUMENT = 0x2
+FLAG_DEVICE_FETCH = 0x4
 
 EXPORTS = [
     "bf_abi_version", "bf_last_error", "bf_device_count",

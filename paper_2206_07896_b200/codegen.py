@@ -65,7 +65,27 @@ struct BfJitGeom {
   int* fault;  // {kind, pad, block(lo, hi), task(lo, hi), host flag pointer}
   unsigned long long task;
   int warp_size;
+  // device-side fetching (null dcur: the grid strides over [first, first + count))
+  unsigned long long* dcur;    // the worker's claim counter
+  unsigned long long* dstats;  // per worker slot: claims, blocks executed
+  int* dexec;                  // KernelTask.executed by absolute block (nullable)
+  unsigned long long dbase;
+  long long nfetch, grain;
+  int dslots;
 };
+// CTA-uniform claim of the next fetch (thread 0 issues it, bf_take publishes it)
+__device__ __forceinline__ long long bf_claim(const BfJitGeom& G) {
+  const long long f = (long long)(atomicAdd(G.dcur, 1ull) - G.dbase);
+  if (f < G.nfetch) atomicAdd(G.dstats + 2 * (blockIdx.x %% G.dslots), 1ull);
+  return f;
+}
+__device__ __forceinline__ long long bf_take(long long mine) {
+  __shared__ long long s_claim;
+  __syncthreads();
+  if (threadIdx.x == 0) s_claim = mine;
+  __syncthreads();
+  return s_claim;
+}
 struct BfJitArgs { long long w[%(nw)d]; };
 
 // a trap records the first fault and stops the trapping thread's side
@@ -557,7 +577,20 @@ class _Gen:
         src.append("  const long long wlim = wcount;")
         src.append("  (void)wlane; (void)wlim; (void)B;")
         src.append("  bool bf_t = false;  // this thread trapped")
-        src.append("  for (long long blk = G.first + blockIdx.x; blk < G.first + G.count; blk += gridDim.x) {")
+        # static mode: one pass of the grid over [first, first + count); device
+        # fetching: claims of `grain` blocks until the task is drained (a trap
+        # abandons the rest of its fetch only, runtime.py:335-343)
+        src.append("  const bool bf_dev = G.dcur != nullptr;")
+        src.append("  long long bf_f = bf_dev ? bf_take(tid == 0 ? bf_claim(G) : 0) : 0;")
+        src.append("  const long long bf_nf = bf_dev ? G.nfetch : 1;")
+        src.append("  while (bf_f < bf_nf) {")
+        src.append("  const long long bf_nx = bf_dev && tid == 0 ? bf_claim(G) : 0;")
+        src.append("  const long long bf_b0 = bf_dev ? G.first + bf_f * G.grain : G.first;")
+        src.append("  const long long bf_b1 = bf_dev ? (bf_b0 + G.grain < G.first + G.count ? bf_b0 + G.grain "
+                   ": G.first + G.count) : G.first + G.count;")
+        src.append("  bf_t = false;")
+        src.append("  for (long long blk = bf_b0 + (bf_dev ? 0 : blockIdx.x); blk < bf_b1; "
+                   "blk += (bf_dev ? 1 : gridDim.x)) {")
         src.append("    const int blockIdx_x = (int)(blk % G.gx), blockIdx_y = (int)((blk / G.gx) % G.gy), "
                    "blockIdx_z = (int)(blk / ((long long)G.gx * G.gy));")
         src.append("    (void)blockIdx_x; (void)blockIdx_y; (void)blockIdx_z;")
@@ -571,6 +604,13 @@ class _Gen:
         src.append("    __syncthreads();")
         src.extend(body)
         src.append("    if (__syncthreads_or(bf_t)) break;")
+        src.append("    if (bf_dev && tid == 0) {")
+        src.append("      atomicAdd(G.dstats + 2 * (blockIdx.x % G.dslots) + 1, 1ull);")
+        src.append("      if (G.dexec) atomicAdd(G.dexec + blk, 1);")
+        src.append("    }")
+        src.append("  }")
+        src.append("  if (!bf_dev) break;")
+        src.append("  bf_f = bf_take(bf_nx);")
         src.append("  }")
         src.append("}")
         return "\n".join(src) + "\n"

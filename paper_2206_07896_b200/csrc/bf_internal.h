@@ -36,6 +36,22 @@ struct HostTrap {
   std::string message;
 };
 
+// Device-side block fetching (BF_FLAG_DEVICE_FETCH): one persistent launch
+// per task whose CTAs claim `grain` logical blocks at a time from the
+// worker's claim counter (runtime.py:175-201 on the GPU).  The counter only
+// grows: a launch of G CTAs over F fetches advances it by exactly F + G (each
+// CTA's last claim fails), so the host knows every launch's base without
+// reading it back.
+struct DevFetch {
+  unsigned long long* cursor;  // the worker's claim counter
+  unsigned long long* stats;   // per worker slot: [2w] successful claims, [2w+1] blocks executed
+  int slots;                   // worker slots (pool size): CTA b accounts to slot b % slots
+  unsigned long long base;     // cursor value when this launch starts
+  long long nfetch, grain;     // fetches of the task, blocks per fetch
+  long long first, total;      // the task's logical blocks [first, first + total)
+  int* executed;               // KernelTask.executed indexed by absolute block (nullable)
+};
+
 // Everything a launcher needs to issue one fetched block range.
 struct LaunchCtx {
   const char* name;
@@ -54,6 +70,12 @@ struct LaunchCtx {
   HostTrap* trap;            // host-side trap sink (first wins)
   std::string* error;        // BF_E_UNSUPPORTED / BF_E_CUDA message sink
   const void* user = nullptr;  // KernelEntry::user (JIT kernels)
+  // device-side fetching: the whole task in one persistent launch.  A
+  // launcher that cannot (geometry, a host-detected trap) returns
+  // BF_E_UNSUPPORTED without launching anything, and the runtime falls back
+  // to host-issued fetches; otherwise it sets dfetch_grid to its CTA count.
+  const DevFetch* dfetch = nullptr;
+  int dfetch_grid = 0;
 
   KDesc desc() const;
   // Record a trap detected on the host before launching (e.g. an affine
@@ -85,6 +107,7 @@ struct KernelEntry {
   const void* user = nullptr;
   bool has_fp = false;     // expected MpmdKernel body fingerprint (bf_kernel_set_fingerprint)
   uint8_t fp[32] = {0};
+  bool dev_fetch = false;  // the launcher handles LaunchCtx::dfetch
 };
 
 // Registry (static registrars in each k_*.cu file, plus JIT kernels added at
@@ -93,8 +116,9 @@ std::deque<KernelEntry>& registry();
 const KernelEntry* find_kernel(const char* name);
 
 struct Registrar {
-  Registrar(const char* name, std::vector<ParamSpec> params, LauncherFn fn) {
+  Registrar(const char* name, std::vector<ParamSpec> params, LauncherFn fn, bool dev_fetch = false) {
     registry().push_back(KernelEntry{name, std::move(params), fn, nullptr});
+    registry().back().dev_fetch = dev_fetch;
   }
 };
 
@@ -152,6 +176,10 @@ T& scratch_for(cudaStream_t s, int kind) {
   if (!slot) slot.reset(new T());
   return *static_cast<T*>(slot.get());
 }
+// kmeans assignment on the tcgen05 pipeline (k_kmeans_t5.cu); BF_E_UNSUPPORTED
+// when the shape does not fit it (nothing launched)
+int launch_kmeans_t5(LaunchCtx& ctx, const float* f, const float* cent, int* member, float* sums, int* counts,
+                     int npts, int nf, int k, long long lo, long long hi);
 enum { SCRATCH_BFS_STEP = 1, SCRATCH_BFS_LEVELS = 2, SCRATCH_NN_TOPK = 3 };
 
 // full-grid hotspot step with the streaming band kernel (k_hotspot.cu)

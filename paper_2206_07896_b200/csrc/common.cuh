@@ -54,6 +54,42 @@ __device__ __forceinline__ void mark_executed(const KDesc& d) {
     atomicAdd(d.executed + b, 1);
 }
 
+// ---- device-side block fetching (DevFetch, bf_internal.h) -------------------
+// CTA-uniform claim loop:
+//   long long f = dev_fetch_first(F);
+//   while (f < F.nfetch) { const long long nx = dev_fetch_issue(F); ...blocks of f...;
+//                          dev_fetch_done(F, b0, b1); f = dev_fetch_take(nx); }
+// Thread 0 issues the next claim's atomic before the current fetch's work, so
+// its round trip overlaps the work; dev_fetch_take publishes it to the CTA.
+__device__ __forceinline__ long long dev_fetch_claim(const DevFetch& F) {
+  const long long f = (long long)(atomicAdd(F.cursor, 1ull) - F.base);
+  if (f < F.nfetch) atomicAdd(F.stats + 2 * (blockIdx.x % F.slots), 1ull);
+  return f;
+}
+__device__ __forceinline__ long long dev_fetch_take(long long mine) {
+  __shared__ long long s_claim;
+  __syncthreads();  // every thread is done with the previous fetch
+  if (threadIdx.x == 0) s_claim = mine;
+  __syncthreads();
+  return s_claim;
+}
+__device__ __forceinline__ long long dev_fetch_first(const DevFetch& F) {
+  return dev_fetch_take(threadIdx.x == 0 ? dev_fetch_claim(F) : 0);
+}
+__device__ __forceinline__ long long dev_fetch_issue(const DevFetch& F) {
+  return threadIdx.x == 0 ? dev_fetch_claim(F) : 0;
+}
+__device__ __forceinline__ void dev_fetch_range(const DevFetch& F, long long f, long long& b0, long long& b1) {
+  b0 = F.first + f * F.grain;
+  b1 = b0 + F.grain < F.first + F.total ? b0 + F.grain : F.first + F.total;
+}
+// blocks [b0, b1) of a fetch ran: busy/executed counters (runtime.py:344-348)
+__device__ __forceinline__ void dev_fetch_done(const DevFetch& F, long long b0, long long b1) {
+  if (threadIdx.x == 0) atomicAdd(F.stats + 2 * (blockIdx.x % F.slots) + 1, (unsigned long long)(b1 - b0));
+  if (F.executed)
+    for (long long b = b0 + threadIdx.x; b < b1; b += blockDim.x) atomicAdd(F.executed + b, 1);
+}
+
 // i32 wrapping multiply-add, as `blockIdx.x * blockDim.x + threadIdx.x` is
 // evaluated with wrap_int after every operator (interp.py:89-90, arena.py:39-41).
 __device__ __forceinline__ int wrap_mad(int a, int b, int c) {

@@ -25,6 +25,12 @@ struct BfJitGeom {
   int* fault;
   unsigned long long task;
   int warp_size;
+  unsigned long long* dcur;
+  unsigned long long* dstats;
+  int* dexec;
+  unsigned long long dbase;
+  long long nfetch, grain;
+  int dslots;
 };
 
 struct JitInfo {
@@ -83,7 +89,30 @@ static int jit_launch(LaunchCtx& ctx) {
                          200 * 1024);
     const_cast<JitInfo*>(ji)->max_dyn_set = 200 * 1024;
   }
-  const int grid = (int)std::min<long long>(ctx.count, (long long)ctx.num_sms * 8);
+  g.dcur = nullptr;
+  g.dstats = nullptr;
+  g.dexec = nullptr;
+  g.dbase = 0;
+  g.nfetch = g.grain = 0;
+  g.dslots = 1;
+  int grid = (int)std::min<long long>(ctx.count, (long long)ctx.num_sms * 8);
+  if (ctx.dfetch) {  // persistent grid claiming the task's fetches (codegen.py)
+    const DevFetch& F = *ctx.dfetch;
+    g.dcur = F.cursor;
+    g.dstats = F.stats;
+    g.dexec = F.executed;
+    g.dbase = F.base;
+    g.nfetch = F.nfetch;
+    g.grain = F.grain;
+    g.dslots = F.slots;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)ji->kern, (int)B, smem) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    grid = (int)std::min<long long>(F.nfetch, (long long)per_sm * ctx.num_sms);
+  }
   void* params[2] = {w.data(), &g};
   cudaError_t e = cudaLaunchKernel((const void*)ji->kern, dim3(grid), dim3((unsigned)B), params,
                                    smem, ctx.stream);
@@ -91,6 +120,7 @@ static int jit_launch(LaunchCtx& ctx) {
     *ctx.error = std::string("jit launch failed: ") + cudaGetErrorString(e);
     return BF_E_CUDA;
   }
+  if (ctx.dfetch) ctx.dfetch_grid = grid;
   return BF_OK;
 }
 
@@ -142,5 +172,6 @@ extern "C" int bf_jit_register_impl(const char* key, const char* source, const c
   JitInfo* raw = ji.get();
   jit_infos().push_back(std::move(ji));
   registry().push_back(KernelEntry{raw->key.c_str(), std::move(params), jit_launch, raw});
+  registry().back().dev_fetch = true;
   return BF_OK;
 }

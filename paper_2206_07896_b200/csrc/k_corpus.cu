@@ -439,6 +439,103 @@ static void hist_go(LaunchCtx& ctx, int grid, size_t smem, const ArgVal& P, cons
       (const int*)P.ptr, (int*)Cn.ptr, Cn.len, lo, hi, fm, copies, ctx.desc(), xbase, bx_div);
 }
 
+// Device-side fetching (BF_FLAG_DEVICE_FETCH, 1D geometry): one persistent
+// grid; each CTA claims `grain` logical blocks at a time, counts their pixels
+// [b0*bx, b1*bx) into its private counters, and flushes once at the end.
+template <int MODE, bool POW2, bool SAFE>
+__global__ void __launch_bounds__(256) hist_fetch(const int* __restrict__ pix, int* counts, long long lc,
+                                                  long long n, long long bx, FastMod fm, KDesc k, DevFetch F) {
+  extern __shared__ unsigned sh[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = (int)fm.d;
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < 8 * kHistLaneBins * 32; i += blockDim.x) sh[i] = 0;
+  } else if (MODE == 1) {
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+  }
+  unsigned* mine = sh + warp * (kHistLaneBins * 32) + lane;
+  const int4* p4 = reinterpret_cast<const int4*>(pix);
+  bool bad = false;
+  long long bad_blk = -1;
+  long long f = dev_fetch_first(F);  // (its barrier also orders the counter zeroing)
+  while (f < F.nfetch) {
+    const long long nx = dev_fetch_issue(F);
+    long long b0, b1;
+    dev_fetch_range(F, f, b0, b1);
+    const long long lo = b0 * bx, hi = b1 * bx < n ? b1 * bx : n;
+    const long long vhi = lo + ((hi > lo ? hi - lo : 0) & ~3LL);
+    for (long long g = lo / 4 + threadIdx.x; g < vhi / 4; g += blockDim.x)
+      hist_add4<MODE, POW2, SAFE>(sh, mine, counts, lc, __ldcs(p4 + g), fm, 1u, bad);
+    for (long long i = vhi + threadIdx.x; i < hi; i += blockDim.x)
+      hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(pix[i], fm), 1u, bad);
+    if (bad && bad_blk < 0) bad_blk = b0;
+    dev_fetch_done(F, b0, b1);
+    f = dev_fetch_take(nx);
+  }
+  if (bad) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bad_blk);
+  if (MODE == 2) return;
+  __syncthreads();
+  if (MODE == 0) {
+    for (int b = warp; b < nb && b < kHistLaneBins; b += blockDim.x / 32) {
+      unsigned s = 0;
+      for (int w = 0; w < (int)(blockDim.x / 32); w++) s += sh[w * (kHistLaneBins * 32) + b * 32 + lane];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0 && s && b < lc) atomicAdd((unsigned*)counts + b, s);
+    }
+  } else {
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      if (sh[b] && b < lc) atomicAdd((unsigned*)counts + b, sh[b]);
+  }
+}
+
+template <int MODE, bool POW2, bool SAFE>
+static int hist_fetch_go(LaunchCtx& ctx, size_t smem, const ArgVal& P, const ArgVal& Cn, long long n,
+                         const FastMod& fm) {
+  static bool attr[64] = {};
+  if ((smem > 48 * 1024) && first_on_device(attr)) {
+    cudaFuncSetAttribute(hist_fetch<MODE, POW2, SAFE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaGetLastError();
+  }
+  const DevFetch& F = *ctx.dfetch;
+  const int grid = (int)std::min<long long>(
+      F.nfetch, (long long)resident_ctas((const void*)hist_fetch<MODE, POW2, SAFE>, 256, smem) * ctx.num_sms);
+  hist_fetch<MODE, POW2, SAFE><<<grid, 256, smem, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, n,
+                                                                ctx.block[0], fm, ctx.desc(), F);
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  ctx.dfetch_grid = grid;
+  return BF_OK;
+}
+
+template <int MODE>
+static int hist_fetch_go2(LaunchCtx& ctx, size_t smem, const ArgVal& P, const ArgVal& Cn, long long n,
+                          const FastMod& fm) {
+  const bool pow2 = (fm.d & (fm.d - 1)) == 0;
+  const bool safe = Cn.len >= (long long)fm.d;
+  if (pow2 && safe) return hist_fetch_go<MODE, true, true>(ctx, smem, P, Cn, n, fm);
+  if (pow2) return hist_fetch_go<MODE, true, false>(ctx, smem, P, Cn, n, fm);
+  if (safe) return hist_fetch_go<MODE, false, true>(ctx, smem, P, Cn, n, fm);
+  return hist_fetch_go<MODE, false, false>(ctx, smem, P, Cn, n, fm);
+}
+
+static int launch_hist_fetch(LaunchCtx& ctx) {
+  const DevFetch& F = *ctx.dfetch;
+  const ArgVal& P = ctx.args[0];
+  const ArgVal& Cn = ctx.args[1];
+  const long long n = ctx.args[2].i32;
+  const int nbins = ctx.args[3].i32;
+  const long long bx = ctx.block[0];
+  const long long hi = std::min((F.first + F.total) * bx, n);
+  // 1D geometry, aligned blocks, no host-detected trap (those keep host fetches)
+  if ((long long)ctx.grid[1] * ctx.grid[2] * ctx.block[1] * ctx.block[2] != 1 || bx % 4 != 0 || nbins == 0 ||
+      hi > P.len || hi - 1 > (long long)INT_MAX)
+    return BF_E_UNSUPPORTED;
+  const FastMod fm = make_fastmod(nbins);
+  const long long nb = fm.d;
+  if (nb <= kHistLaneBins) return hist_fetch_go2<0>(ctx, 8 * kHistLaneBins * 32 * sizeof(unsigned), P, Cn, n, fm);
+  if (nb <= kHistSmemBins) return hist_fetch_go2<1>(ctx, nb * sizeof(unsigned), P, Cn, n, fm);
+  return hist_fetch_go2<2>(ctx, 0, P, Cn, n, fm);
+}
+
 template <int MODE>
 static void hist_go2(LaunchCtx& ctx, int grid, size_t smem, const ArgVal& P, const ArgVal& Cn,
                      long long lo, long long hi, const FastMod& fm, unsigned copies,
@@ -470,6 +567,7 @@ static int hist_issue(LaunchCtx& ctx, const ArgVal& P, const ArgVal& Cn, long lo
 }
 
 static int launch_hist(LaunchCtx& ctx) {
+  if (ctx.dfetch) return launch_hist_fetch(ctx);
   const ArgVal& P = ctx.args[0];
   const ArgVal& Cn = ctx.args[1];
   const long long n = ctx.args[2].i32;
@@ -817,7 +915,7 @@ static Registrar reg_hist("hist",
                            {BF_SLOT_HANDLE, BF_I32, "counts"},
                            {BF_SLOT_I32, BF_I32, "n"},
                            {BF_SLOT_I32, BF_I32, "nbins"}},
-                          launch_hist);
+                          launch_hist, /*dev_fetch=*/true);
 static Registrar reg_hist_stride("hist_stride",
                                  {{BF_SLOT_HANDLE, BF_I32, "pix"},
                                   {BF_SLOT_HANDLE, BF_I32, "counts"},

@@ -268,12 +268,18 @@ __global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
   const long long n4 = a.n >> 2;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const float4* d4 = reinterpret_cast<const float4*>(a.d);
-  unsigned thr = 0xffffffffu;  // high word of the list's last key: fast reject
+  // fast reject on the raw float: v > tf (the value of the list's last key)
+  // cannot enter; a NaN tf (list not full, or a NaN last key) rejects nothing
+  float tf = __uint_as_float(0x7fffffffu);
   auto offer = [&](float v, long long i) {
+    if (v > tf) return;
     const unsigned long long key = topk_key(v, (unsigned)i);
-    if ((unsigned)(key >> 32) > thr || key <= lo) return;
+    if (key >= t.l[K - 1] || key <= lo) return;
     t.insert(key);
-    thr = (unsigned)(t.l[K - 1] >> 32);
+    const unsigned hb = (unsigned)(t.l[K - 1] >> 32);
+    // inverse of topk_key's order map (0xffffffff: empty slot or NaN)
+    tf = hb == 0xffffffffu ? __uint_as_float(0x7fffffffu)
+                           : __uint_as_float((hb & 0x80000000u) ? (hb & 0x7fffffffu) : ~hb);
   };
   // four 16 B loads in flight per thread before any key work
   for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < n4; j0 += 4 * stride) {

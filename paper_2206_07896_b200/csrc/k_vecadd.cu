@@ -45,7 +45,53 @@ __global__ void __launch_bounds__(256) vecadd_stream(const float* a, const float
   }
 }
 
+// Device-side fetching (BF_FLAG_DEVICE_FETCH): one persistent grid; each CTA
+// claims `grain` logical blocks at a time and streams their elements
+// [b0*bx, b1*bx) with 16 B vectors (1D grids, bx % 4 == 0).
+__global__ void __launch_bounds__(256) vecadd_fetch(const float* a, const float* b, float* c, long long n,
+                                                    long long bx, DevFetch F) {
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  float4* c4 = reinterpret_cast<float4*>(c);
+  long long f = dev_fetch_first(F);
+  while (f < F.nfetch) {
+    const long long nx = dev_fetch_issue(F);
+    long long b0, b1;
+    dev_fetch_range(F, f, b0, b1);
+    const long long lo = b0 * bx, hi = b1 * bx < n ? b1 * bx : n;
+    const long long vhi = lo + ((hi > lo ? hi - lo : 0) & ~3LL);
+    for (long long i = lo / 4 + threadIdx.x; i < vhi / 4; i += blockDim.x) {
+      const float4 x = __ldcs(a4 + i), y = __ldcs(b4 + i);
+      __stcs(c4 + i, make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w));
+    }
+    for (long long i = vhi + threadIdx.x; i < hi; i += blockDim.x) c[i] = a[i] + b[i];
+    dev_fetch_done(F, b0, b1);
+    f = dev_fetch_take(nx);
+  }
+}
+
+static int launch_vecadd_fetch(LaunchCtx& ctx) {
+  const DevFetch& F = *ctx.dfetch;
+  const ArgVal& A = ctx.args[0];
+  const ArgVal& B = ctx.args[1];
+  const ArgVal& C = ctx.args[2];
+  const long long n = ctx.args[3].i32;
+  const long long bx = ctx.block[0];
+  const long long hi = std::min((F.first + F.total) * bx, n);
+  // 1D geometry, aligned blocks, no host-detected trap (those keep host fetches)
+  if ((long long)ctx.grid[1] * ctx.grid[2] * ctx.block[1] * ctx.block[2] != 1 || bx % 4 != 0 ||
+      hi - 1 > (long long)INT_MAX || hi > std::min(A.len, std::min(B.len, C.len)))
+    return BF_E_UNSUPPORTED;
+  const int grid = (int)std::min<long long>(F.nfetch, (long long)resident_ctas((const void*)vecadd_fetch, 256, 0) *
+                                                          ctx.num_sms);
+  vecadd_fetch<<<grid, 256, 0, ctx.stream>>>((const float*)A.ptr, (const float*)B.ptr, (float*)C.ptr, n, bx, F);
+  BF_CUDA_LAUNCH_CHECK(ctx);
+  ctx.dfetch_grid = grid;
+  return BF_OK;
+}
+
 static int launch_vecadd(LaunchCtx& ctx) {
+  if (ctx.dfetch) return launch_vecadd_fetch(ctx);
   const ArgVal& A = ctx.args[0];
   const ArgVal& B = ctx.args[1];
   const ArgVal& C = ctx.args[2];
@@ -88,6 +134,6 @@ static Registrar reg_vecadd("vecadd",
                              {BF_SLOT_HANDLE, BF_F32, "b"},
                              {BF_SLOT_HANDLE, BF_F32, "c"},
                              {BF_SLOT_I32, BF_I32, "n"}},
-                            launch_vecadd);
+                            launch_vecadd, /*dev_fetch=*/true);
 
 }  // namespace bf

@@ -327,6 +327,7 @@ struct FetchRecord {
   uint64_t task;
   int worker;
   long long first, count;
+  bool device = false;  // a device-fetched task (counters come from the device)
   cudaEvent_t done;  // shared by the fetches a lazy cover event covers (event_refs)
 };
 
@@ -378,6 +379,11 @@ struct bf_runtime {
   std::map<cudaEvent_t, int> event_refs;  // fetch records still pointing at each in-use event
   uint64_t next_task = 1;
   uint64_t rr = 0;               // round-robin worker cursor
+  // device-side fetching (BF_FLAG_DEVICE_FETCH): per worker a claim counter,
+  // per worker slot (claims, blocks executed); host copy of the counters' bases
+  unsigned long long* dfetch_dev = nullptr;  // [pool] cursors, then [pool][2] stats
+  std::vector<unsigned long long> dfetch_base;
+  bool dfetch_used = false;
   // counters
   int64_t blocks_executed = 0;
   int64_t syncs = 0;
@@ -467,8 +473,10 @@ static int retire(bf_runtime* rt, bool wait) {
             TaskRec& t = rt->tasks[it->task];
             t.completed += it->count;
             t.done_ranges.push_back({it->first, it->count});
-            rt->blocks_executed += it->count;
-            rt->busy[it->worker] += it->count;
+            if (!it->device) {  // device-fetched: busy / executed counted on the device
+              rt->blocks_executed += it->count;
+              rt->busy[it->worker] += it->count;
+            }
             drop_event_ref(rt, it->done);
             it = rt->inflight.erase(it);
           } else {
@@ -483,8 +491,10 @@ static int retire(bf_runtime* rt, bool wait) {
     TaskRec& t = rt->tasks[f.task];
     t.completed += f.count;
     t.done_ranges.push_back({f.first, f.count});
-    rt->blocks_executed += f.count;
-    rt->busy[f.worker] += f.count;
+    if (!f.device) {
+      rt->blocks_executed += f.count;
+      rt->busy[f.worker] += f.count;
+    }
     if (f.done) drop_event_ref(rt, f.done);
     rt->inflight.pop_front();
   }
@@ -1012,6 +1022,14 @@ int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double blo
       return fail(BF_E_CUDA, "fault word initialisation failed");
     }
   }
+  if (flags & BF_FLAG_DEVICE_FETCH) {
+    if (cudaMalloc((void**)&rt->dfetch_dev, sizeof(unsigned long long) * 3 * pool_size) != cudaSuccess ||
+        cudaMemset(rt->dfetch_dev, 0, sizeof(unsigned long long) * 3 * pool_size) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(BF_E_CUDA, "device fetch counters allocation failed");
+    }
+    rt->dfetch_base.assign(pool_size, 0ull);
+  }
   a->live_runtimes++;
   *out = rt;
   return BF_OK;
@@ -1040,6 +1058,7 @@ int bf_runtime_destroy(bf_runtime* rt) {
   for (auto& kv : rt->tasks)
     if (kv.second.executed_dev) cudaFree(kv.second.executed_dev);
   if (rt->fault_dev) cudaFree(rt->fault_dev);
+  if (rt->dfetch_dev) cudaFree(rt->dfetch_dev);
   if (rt->fault_host) cudaFreeHost(rt->fault_host);
   if (rt->fault_flag) cudaFreeHost(rt->fault_flag);
   bf_arena* a = rt->arena;
@@ -1215,6 +1234,70 @@ static int launch_impl(bf_runtime* rt, const char* kernel, const int32_t grid[3]
     CK(cudaStreamSynchronize(rt->streams[0]));
   }
 
+  // device-side fetching: the task's fetches are claimed by the CTAs of one
+  // persistent launch on the next worker stream
+  if (rt->dfetch_dev && ke->dev_fetch && !rt->holding && rt->block_delay <= 0.0 && pre.kind == BF_TRAP_NONE) {
+    const int w = (int)(rt->rr % (uint64_t)rt->pool);
+    const int64_t nfetch = (total + grain - 1) / grain;
+    DevFetch df;
+    df.cursor = rt->dfetch_dev + w;
+    df.stats = rt->dfetch_dev + rt->pool;
+    df.slots = rt->pool;
+    df.base = rt->dfetch_base[w];
+    df.nfetch = nfetch;
+    df.grain = grain;
+    df.first = range_first;
+    df.total = total;
+    df.executed = tr.executed_dev ? tr.executed_dev - tr.base : nullptr;
+    LaunchCtx ctx;
+    ctx.name = ke->name;
+    for (int i = 0; i < 3; i++) {
+      ctx.grid[i] = grid[i];
+      ctx.block[i] = block[i];
+    }
+    ctx.first = range_first;
+    ctx.count = total;
+    ctx.shmem = shmem_bytes;
+    ctx.warp_size = warp_size;
+    ctx.args = args.data();
+    ctx.nargs = (int)args.size();
+    ctx.stream = rt->streams[w];
+    ctx.num_sms = rt->num_sms;
+    ctx.executed = tr.executed_dev;
+    ctx.fault = rt->fault_dev;
+    ctx.task = id;
+    HostTrap ht;
+    std::string err;
+    ctx.trap = &ht;
+    ctx.error = &err;
+    ctx.user = ke->user;
+    ctx.dfetch = &df;
+    int lrc = ke->launch(ctx);
+    if (lrc == BF_OK && ctx.dfetch_grid > 0 && ht.kind == BF_TRAP_NONE) {
+      rt->rr++;
+      rt->dfetch_base[w] += (unsigned long long)(nfetch + ctx.dfetch_grid);
+      rt->dfetch_used = true;
+      tr.fetches = nfetch;
+      tr.cursor = total;
+      FetchRecord fr;
+      fr.task = id;
+      fr.worker = w;
+      fr.first = range_first;
+      fr.count = total;
+      fr.device = true;
+      fr.done = nullptr;
+      if (fetch_event_mode() == 1) {
+        fr.done = get_event(rt);
+        CK(cudaEventRecord(fr.done, ctx.stream));
+      }
+      rt->inflight.push_back(fr);
+      return BF_OK;
+    }
+    if (lrc != BF_OK && lrc != BF_E_UNSUPPORTED) return fail(lrc, std::string(ke->name) + ": " + err);
+    if (ctx.dfetch_grid > 0) return fail(BF_E_INVALID, std::string(ke->name) + ": device-fetch launcher trapped after launching");
+    // not this time (geometry, a trap the host detects): host-issued fetches
+  }
+
   // push + dispatch: the host dispatcher plays the pool's fetch loop
   rc = bf_queue_push(&rt->queue, id, total, grain);
   if (rc) return rc;
@@ -1372,6 +1455,24 @@ int bf_counters_get(bf_runtime* rt, bf_counters* out, int64_t* busy, int32_t n) 
   out->pool_size = rt->pool;
   if (busy)
     for (int i = 0; i < n && i < rt->pool; i++) busy[i] = rt->busy[i];
+  if (rt->dfetch_used) {
+    // device-fetched launches: claims and blocks counted by the CTAs (only
+    // their retired launches count, as for host fetches: read once drained)
+    bool drained = true;
+    for (auto& f : rt->inflight)
+      if (f.device) drained = false;
+    if (drained) {
+      std::vector<unsigned long long> st(2 * rt->pool);
+      set_device(rt->device);
+      CK(cudaMemcpy(st.data(), rt->dfetch_dev + rt->pool, st.size() * sizeof(unsigned long long),
+                    cudaMemcpyDeviceToHost));
+      for (int i = 0; i < rt->pool; i++) {
+        out->fetch_count += (int64_t)st[2 * i];
+        out->blocks_executed += (int64_t)st[2 * i + 1];
+        if (busy && i < n) busy[i] += (int64_t)st[2 * i + 1];
+      }
+    }
+  }
   return BF_OK;
 }
 

@@ -399,11 +399,19 @@ class Runtime:
     `hold_blocks=True` gates all block execution until the next
     device_synchronize; `block_delay` inserts a random device-side sleep of up
     to that many seconds before each fetched range (seeded).  `instrument=True`
-    makes every launch count per-block executions on the device."""
+    makes every launch count per-block executions on the device.
+    `fetch="device"` moves block fetching onto the GPU: a launch of a kernel
+    that supports it is one persistent grid whose CTAs claim
+    block_per_fetch blocks at a time from a device counter (the reference's
+    worker fetch loop, runtime.py:175-201, 305-350); "host" (default) issues
+    every fetched range as its own grid launch."""
 
     def __init__(self, arena: DeviceArena, pool_size: Optional[int] = None,
                  policy: FetchPolicy = Average(), hold_blocks: bool = False,
-                 block_delay: float = 0.0, seed: int = 0, instrument: bool = False):
+                 block_delay: float = 0.0, seed: int = 0, instrument: bool = False,
+                 fetch: str = "host"):
+        if fetch not in ("host", "device"):
+            raise ValueError(f"fetch must be 'host' or 'device', got {fetch!r}")
         self.arena = arena
         self.pool_size = pool_size if pool_size is not None else default_pool_size()
         if self.pool_size < 1:
@@ -411,7 +419,9 @@ class Runtime:
         self.policy = policy
         self._native = C.c_void_p()
         flags = (_lib.FLAG_HOLD_BLOCKS if hold_blocks else 0) | \
-                (_lib.FLAG_INSTRUMENT if instrument else 0)
+                (_lib.FLAG_INSTRUMENT if instrument else 0) | \
+                (_lib.FLAG_DEVICE_FETCH if fetch == "device" else 0)
+        self.fetch = fetch
         check(_lib.lib().bf_runtime_create(arena.native, self.pool_size, flags, float(block_delay),
                                            seed & (2**64 - 1), C.byref(self._native)))
         # weak: a task keeps its runtime alive (it reads the native record),

@@ -28,13 +28,14 @@ def materialize(inst, arena):
     return PackedArgs(slots), handles
 
 
-def gpu_run(inst, pool_size: int = 1, policy=None, instrument: bool = False, routine=None):
+def gpu_run(inst, pool_size: int = 1, policy=None, instrument: bool = False, routine=None, fetch: str = "host"):
     arena = DeviceArena()
     packed, handles = materialize(inst, arena)
     if routine is None:
         routine = routines.get(inst.kernel, warp_size=inst.warp_size)
     trap = None
-    with Runtime(arena, pool_size=pool_size, policy=policy or Average(), instrument=instrument) as rt:
+    with Runtime(arena, pool_size=pool_size, policy=policy or Average(), instrument=instrument,
+                 fetch=fetch) as rt:
         task = rt.launch(routine, Dim3(inst.grid.x, inst.grid.y, inst.grid.z),
                          Dim3(inst.block.x, inst.block.y, inst.block.z), inst.shmem, packed)
         try:
