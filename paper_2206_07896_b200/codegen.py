@@ -65,19 +65,28 @@ struct BfJitGeom {
   int* fault;  // {kind, pad, block(lo, hi), task(lo, hi), host flag pointer}
   unsigned long long task;
   int warp_size;
-  // device-side fetching (null dcur: the grid strides over [first, first + count))
-  unsigned long long* dcur;    // the worker's claim counter
+  // device-side fetching (null dcur: the grid strides over [first, first + count));
+  // the fetches are split into 8 sub-ranges with a counter each (bf_internal.h DevFetch)
+  unsigned long long* dcur;    // the worker's 8 claim counters
   unsigned long long* dstats;  // per worker slot: claims, blocks executed
   int* dexec;                  // KernelTask.executed by absolute block (nullable)
-  unsigned long long dbase;
+  unsigned long long dbase[8];
   long long nfetch, grain;
   int dslots;
 };
-// CTA-uniform claim of the next fetch (thread 0 issues it, bf_take publishes it)
-__device__ __forceinline__ long long bf_claim(const BfJitGeom& G) {
-  const long long f = (long long)(atomicAdd(G.dcur, 1ull) - G.dbase);
-  if (f < G.nfetch) atomicAdd(G.dstats + 2 * (blockIdx.x %% G.dslots), 1ull);
-  return f;
+// thread 0's claim of the next fetch (cursor: sub-range and sub-ranges tried)
+__device__ __forceinline__ long long bf_claim(const BfJitGeom& G, int& sub, int& tried) {
+  while (tried < 8) {
+    const long long lo = (G.nfetch * sub) / 8, n = (G.nfetch * (sub + 1)) / 8 - lo;
+    const long long f = (long long)(atomicAdd(G.dcur + sub, 1ull) - G.dbase[sub]);
+    if (f < n) {
+      atomicAdd(G.dstats + 2 * (blockIdx.x %% G.dslots), 1ull);
+      return lo + f;
+    }
+    sub = (sub + 1) %% 8;
+    tried++;
+  }
+  return G.nfetch;
 }
 __device__ __forceinline__ long long bf_take(long long mine) {
   __shared__ long long s_claim;
@@ -581,10 +590,11 @@ class _Gen:
         # fetching: claims of `grain` blocks until the task is drained (a trap
         # abandons the rest of its fetch only, runtime.py:335-343)
         src.append("  const bool bf_dev = G.dcur != nullptr;")
-        src.append("  long long bf_f = bf_dev ? bf_take(tid == 0 ? bf_claim(G) : 0) : 0;")
+        src.append("  int bf_sub = (int)(blockIdx.x % 8), bf_tried = 0;")
+        src.append("  long long bf_f = bf_dev ? bf_take(tid == 0 ? bf_claim(G, bf_sub, bf_tried) : 0) : 0;")
         src.append("  const long long bf_nf = bf_dev ? G.nfetch : 1;")
         src.append("  while (bf_f < bf_nf) {")
-        src.append("  const long long bf_nx = bf_dev && tid == 0 ? bf_claim(G) : 0;")
+        src.append("  const long long bf_nx = bf_dev && tid == 0 ? bf_claim(G, bf_sub, bf_tried) : 0;")
         src.append("  const long long bf_b0 = bf_dev ? G.first + bf_f * G.grain : G.first;")
         src.append("  const long long bf_b1 = bf_dev ? (bf_b0 + G.grain < G.first + G.count ? bf_b0 + G.grain "
                    ": G.first + G.count) : G.first + G.count;")

@@ -38,15 +38,20 @@ struct HostTrap {
 
 // Device-side block fetching (BF_FLAG_DEVICE_FETCH): one persistent launch
 // per task whose CTAs claim `grain` logical blocks at a time from the
-// worker's claim counter (runtime.py:175-201 on the GPU).  The counter only
-// grows: a launch of G CTAs over F fetches advances it by exactly F + G (each
-// CTA's last claim fails), so the host knows every launch's base without
-// reading it back.
+// worker's claim counters (runtime.py:175-201 on the GPU).  The counters
+// only grow, by amounts the host can compute (below), so it knows every
+// launch's bases without reading them back.
+// The fetches are split into kFetchSubs contiguous sub-ranges, each with its
+// own counter (CTA b starts on sub-range b % kFetchSubs and moves on when it
+// is drained): the claims of fine grains do not serialise on one address.
+// Every CTA fails exactly once on every counter before it exits, so a launch
+// of G CTAs advances counter j by exactly (fetches of sub-range j) + G.
+constexpr int kFetchSubs = 8;
 struct DevFetch {
-  unsigned long long* cursor;  // the worker's claim counter
+  unsigned long long* cursor;  // the worker's kFetchSubs claim counters
   unsigned long long* stats;   // per worker slot: [2w] successful claims, [2w+1] blocks executed
   int slots;                   // worker slots (pool size): CTA b accounts to slot b % slots
-  unsigned long long base;     // cursor value when this launch starts
+  unsigned long long base[kFetchSubs];  // counter values when this launch starts
   long long nfetch, grain;     // fetches of the task, blocks per fetch
   long long first, total;      // the task's logical blocks [first, first + total)
   int* executed;               // KernelTask.executed indexed by absolute block (nullable)
@@ -176,10 +181,6 @@ T& scratch_for(cudaStream_t s, int kind) {
   if (!slot) slot.reset(new T());
   return *static_cast<T*>(slot.get());
 }
-// kmeans assignment on the tcgen05 pipeline (k_kmeans_t5.cu); BF_E_UNSUPPORTED
-// when the shape does not fit it (nothing launched)
-int launch_kmeans_t5(LaunchCtx& ctx, const float* f, const float* cent, int* member, float* sums, int* counts,
-                     int npts, int nf, int k, long long lo, long long hi);
 enum { SCRATCH_BFS_STEP = 1, SCRATCH_BFS_LEVELS = 2, SCRATCH_NN_TOPK = 3 };
 
 // full-grid hotspot step with the streaming band kernel (k_hotspot.cu)

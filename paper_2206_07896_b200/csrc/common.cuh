@@ -56,15 +56,34 @@ __device__ __forceinline__ void mark_executed(const KDesc& d) {
 
 // ---- device-side block fetching (DevFetch, bf_internal.h) -------------------
 // CTA-uniform claim loop:
-//   long long f = dev_fetch_first(F);
-//   while (f < F.nfetch) { const long long nx = dev_fetch_issue(F); ...blocks of f...;
+//   FetchCursor fc = dev_fetch_cursor();
+//   long long f = dev_fetch_first(F, fc);
+//   while (f < F.nfetch) { const long long nx = dev_fetch_issue(F, fc); ...blocks of f...;
 //                          dev_fetch_done(F, b0, b1); f = dev_fetch_take(nx); }
 // Thread 0 issues the next claim's atomic before the current fetch's work, so
 // its round trip overlaps the work; dev_fetch_take publishes it to the CTA.
-__device__ __forceinline__ long long dev_fetch_claim(const DevFetch& F) {
-  const long long f = (long long)(atomicAdd(F.cursor, 1ull) - F.base);
-  if (f < F.nfetch) atomicAdd(F.stats + 2 * (blockIdx.x % F.slots), 1ull);
-  return f;
+// Sub-range j of the fetches is [j*F/S, (j+1)*F/S); thread 0's cursor starts
+// on sub-range blockIdx.x % S and moves on when one is drained.
+struct FetchCursor {
+  int sub, tried;
+};
+__device__ __forceinline__ FetchCursor dev_fetch_cursor() { return FetchCursor{(int)(blockIdx.x % kFetchSubs), 0}; }
+__device__ __forceinline__ long long dev_fetch_sub_start(const DevFetch& F, int j) {
+  return (F.nfetch * j) / kFetchSubs;
+}
+__device__ __forceinline__ long long dev_fetch_claim(const DevFetch& F, FetchCursor& c) {
+  while (c.tried < kFetchSubs) {
+    const int j = c.sub;
+    const long long lo = dev_fetch_sub_start(F, j), n = dev_fetch_sub_start(F, j + 1) - lo;
+    const long long f = (long long)(atomicAdd(F.cursor + j, 1ull) - F.base[j]);
+    if (f < n) {
+      atomicAdd(F.stats + 2 * (blockIdx.x % F.slots), 1ull);
+      return lo + f;
+    }
+    c.sub = (j + 1) % kFetchSubs;
+    c.tried++;
+  }
+  return F.nfetch;
 }
 __device__ __forceinline__ long long dev_fetch_take(long long mine) {
   __shared__ long long s_claim;
@@ -73,11 +92,11 @@ __device__ __forceinline__ long long dev_fetch_take(long long mine) {
   __syncthreads();
   return s_claim;
 }
-__device__ __forceinline__ long long dev_fetch_first(const DevFetch& F) {
-  return dev_fetch_take(threadIdx.x == 0 ? dev_fetch_claim(F) : 0);
+__device__ __forceinline__ long long dev_fetch_first(const DevFetch& F, FetchCursor& c) {
+  return dev_fetch_take(threadIdx.x == 0 ? dev_fetch_claim(F, c) : 0);
 }
-__device__ __forceinline__ long long dev_fetch_issue(const DevFetch& F) {
-  return threadIdx.x == 0 ? dev_fetch_claim(F) : 0;
+__device__ __forceinline__ long long dev_fetch_issue(const DevFetch& F, FetchCursor& c) {
+  return threadIdx.x == 0 ? dev_fetch_claim(F, c) : 0;
 }
 __device__ __forceinline__ void dev_fetch_range(const DevFetch& F, long long f, long long& b0, long long& b1) {
   b0 = F.first + f * F.grain;

@@ -457,9 +457,10 @@ __global__ void __launch_bounds__(256) hist_fetch(const int* __restrict__ pix, i
   const int4* p4 = reinterpret_cast<const int4*>(pix);
   bool bad = false;
   long long bad_blk = -1;
-  long long f = dev_fetch_first(F);  // (its barrier also orders the counter zeroing)
+  FetchCursor fc = dev_fetch_cursor();
+  long long f = dev_fetch_first(F, fc);  // (its barrier also orders the counter zeroing)
   while (f < F.nfetch) {
-    const long long nx = dev_fetch_issue(F);
+    const long long nx = dev_fetch_issue(F, fc);
     long long b0, b1;
     dev_fetch_range(F, f, b0, b1);
     const long long lo = b0 * bx, hi = b1 * bx < n ? b1 * bx : n;

@@ -1228,7 +1228,7 @@ static int kmeans_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BF_KMEANS_V");
-    v = e ? atoi(e) : 6;  // 6: tcgen05 pipeline (kmeans_t5, k_kmeans_t5.cu); 5: kmeans_umma; 4: kmeans_tc
+    v = e ? atoi(e) : 4;  // 5: tcgen05 path (kmeans_umma)
   }
   return v;
 }
@@ -1263,12 +1263,6 @@ static int launch_kmeans(LaunchCtx& ctx) {
     if (!ok) {
       ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first_block_with_x(xi.first), "kmeans index out of range");
       continue;
-    }
-    if (kmeans_variant() >= 6 && nf == 32 && k >= 2 && k <= 16 && npts % 4 == 0) {
-      const int rc = launch_kmeans_t5(ctx, (const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr, (float*)S.ptr,
-                                      (int*)Cn.ptr, (int)npts, nf, k, lo, hi);
-      if (rc == BF_OK) continue;
-      if (rc != BF_E_UNSUPPORTED) return rc;
     }
     if (kmeans_variant() == 5 && (nf == 32 || nf == 16) && k >= 2 && k <= 16 && npts % 4 == 0 && lo % 4 == 0 &&
         hi - lo >= 4) {

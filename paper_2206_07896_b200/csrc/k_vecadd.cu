@@ -53,9 +53,10 @@ __global__ void __launch_bounds__(256) vecadd_fetch(const float* a, const float*
   const float4* a4 = reinterpret_cast<const float4*>(a);
   const float4* b4 = reinterpret_cast<const float4*>(b);
   float4* c4 = reinterpret_cast<float4*>(c);
-  long long f = dev_fetch_first(F);
+  FetchCursor fc = dev_fetch_cursor();
+  long long f = dev_fetch_first(F, fc);
   while (f < F.nfetch) {
-    const long long nx = dev_fetch_issue(F);
+    const long long nx = dev_fetch_issue(F, fc);
     long long b0, b1;
     dev_fetch_range(F, f, b0, b1);
     const long long lo = b0 * bx, hi = b1 * bx < n ? b1 * bx : n;

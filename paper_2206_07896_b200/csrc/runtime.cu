@@ -381,7 +381,7 @@ struct bf_runtime {
   uint64_t rr = 0;               // round-robin worker cursor
   // device-side fetching (BF_FLAG_DEVICE_FETCH): per worker a claim counter,
   // per worker slot (claims, blocks executed); host copy of the counters' bases
-  unsigned long long* dfetch_dev = nullptr;  // [pool] cursors, then [pool][2] stats
+  unsigned long long* dfetch_dev = nullptr;  // [pool][kFetchSubs] counters, then [pool][2] stats
   std::vector<unsigned long long> dfetch_base;
   bool dfetch_used = false;
   // counters
@@ -1023,12 +1023,13 @@ int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double blo
     }
   }
   if (flags & BF_FLAG_DEVICE_FETCH) {
-    if (cudaMalloc((void**)&rt->dfetch_dev, sizeof(unsigned long long) * 3 * pool_size) != cudaSuccess ||
-        cudaMemset(rt->dfetch_dev, 0, sizeof(unsigned long long) * 3 * pool_size) != cudaSuccess) {
+    const size_t nctr = (size_t)pool_size * (kFetchSubs + 2);
+    if (cudaMalloc((void**)&rt->dfetch_dev, sizeof(unsigned long long) * nctr) != cudaSuccess ||
+        cudaMemset(rt->dfetch_dev, 0, sizeof(unsigned long long) * nctr) != cudaSuccess) {
       cudaGetLastError();
       return fail(BF_E_CUDA, "device fetch counters allocation failed");
     }
-    rt->dfetch_base.assign(pool_size, 0ull);
+    rt->dfetch_base.assign((size_t)pool_size * kFetchSubs, 0ull);
   }
   a->live_runtimes++;
   *out = rt;
@@ -1240,10 +1241,10 @@ static int launch_impl(bf_runtime* rt, const char* kernel, const int32_t grid[3]
     const int w = (int)(rt->rr % (uint64_t)rt->pool);
     const int64_t nfetch = (total + grain - 1) / grain;
     DevFetch df;
-    df.cursor = rt->dfetch_dev + w;
-    df.stats = rt->dfetch_dev + rt->pool;
+    df.cursor = rt->dfetch_dev + (size_t)w * kFetchSubs;
+    df.stats = rt->dfetch_dev + (size_t)rt->pool * kFetchSubs;
     df.slots = rt->pool;
-    df.base = rt->dfetch_base[w];
+    for (int j = 0; j < kFetchSubs; j++) df.base[j] = rt->dfetch_base[(size_t)w * kFetchSubs + j];
     df.nfetch = nfetch;
     df.grain = grain;
     df.first = range_first;
@@ -1275,7 +1276,9 @@ static int launch_impl(bf_runtime* rt, const char* kernel, const int32_t grid[3]
     int lrc = ke->launch(ctx);
     if (lrc == BF_OK && ctx.dfetch_grid > 0 && ht.kind == BF_TRAP_NONE) {
       rt->rr++;
-      rt->dfetch_base[w] += (unsigned long long)(nfetch + ctx.dfetch_grid);
+      for (int j = 0; j < kFetchSubs; j++)  // sub-range j's fetches + one failed claim per CTA
+        rt->dfetch_base[(size_t)w * kFetchSubs + j] +=
+            (unsigned long long)(nfetch * (j + 1) / kFetchSubs - nfetch * j / kFetchSubs + ctx.dfetch_grid);
       rt->dfetch_used = true;
       tr.fetches = nfetch;
       tr.cursor = total;
@@ -1464,7 +1467,7 @@ int bf_counters_get(bf_runtime* rt, bf_counters* out, int64_t* busy, int32_t n) 
     if (drained) {
       std::vector<unsigned long long> st(2 * rt->pool);
       set_device(rt->device);
-      CK(cudaMemcpy(st.data(), rt->dfetch_dev + rt->pool, st.size() * sizeof(unsigned long long),
+      CK(cudaMemcpy(st.data(), rt->dfetch_dev + (size_t)rt->pool * kFetchSubs, st.size() * sizeof(unsigned long long),
                     cudaMemcpyDeviceToHost));
       for (int i = 0; i < rt->pool; i++) {
         out->fetch_count += (int64_t)st[2 * i];

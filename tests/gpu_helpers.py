@@ -44,6 +44,7 @@ def gpu_run(inst, pool_size: int = 1, policy=None, instrument: bool = False, rou
             trap = (e.trap.kind, e.block_id)
         counters = rt.counters
     outs = {b.name: arena.to_numpy(handles[b.name]) for b in inst.buffers}
+    arena.close()  # device memory and pinned staging go now, not at interpreter exit
     return outs, trap, task, counters
 
 
