@@ -14,7 +14,7 @@
 #include <climits>
 #include <cstdlib>
 
-#include <cub/device/device_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 
 #include "bf_internal.h"
 #include "common.cuh"
@@ -1113,38 +1113,38 @@ __global__ void __launch_bounds__(256) bfs_bottom_up(const int* __restrict__ cro
 }
 
 // ---- graph transpose (in-edge CSR for the bottom-up step) --------------------
-// indeg[v] = number of edges u -> v with u < nv (edges outside every
-// [row[u], row[u+1]) are not edges); a malformed row or out-of-range target
+// A stable radix sort of the (target, source) pairs by target: ccol is the
+// sorted sources (so every in-list is in ascending source order:
+// deterministic), crow[v] the first sorted position with target >= v.
+// Edges are [row[0], row[nv]); a malformed row or an out-of-range target
 // sets err.
-__global__ void __launch_bounds__(256) bfs_indegree(const int* __restrict__ row, const int* __restrict__ col,
-                                                    long long ncol, long long nv, int* indeg, int* err) {
+__global__ void __launch_bounds__(256) bfs_tr_pairs(const int* __restrict__ row, const int* __restrict__ col,
+                                                    long long nv, int e_base, int e_end, unsigned* key, int* srcv,
+                                                    int* err) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < nv; u += stride) {
     const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
-    if (e0 < 0 || e1 > ncol || e1 < e0) {
+    if (e1 < e0 || e0 < e_base || e1 > e_end) {
       *err = 1;
       continue;
     }
     for (int e = e0; e < e1; e++) {
       const int v = __ldg(col + e);
       if (v < 0 || v >= nv) *err = 1;
-      else atomicAdd(indeg + v, 1);
+      key[e - e_base] = (unsigned)v;
+      srcv[e - e_base] = (int)u;
     }
   }
 }
 
-// ccol[cursor[v]++] = u for every edge u -> v (in-list order is unspecified:
-// the bottom-up step only asks whether any in-neighbour is in the frontier)
-__global__ void __launch_bounds__(256) bfs_fill_in_edges(const int* __restrict__ row, const int* __restrict__ col,
-                                                         long long ncol, long long nv, int* cursor, int* ccol) {
+// crow[v] = first i with key[i] >= v (key sorted), crow[nv] = n
+__global__ void __launch_bounds__(256) bfs_tr_offsets(const unsigned* __restrict__ key, long long n, long long nv,
+                                                      int* crow) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < nv; u += stride) {
-    const int e0 = __ldg(row + u), e1 = __ldg(row + u + 1);
-    if (e0 < 0 || e1 > ncol || e1 < e0) continue;
-    for (int e = e0; e < e1; e++) {
-      const int v = __ldg(col + e);
-      if (v >= 0 && v < nv) ccol[atomicAdd(cursor + v, 1)] = (int)u;
-    }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
+    const long long lo = i == 0 ? 0 : (long long)__ldg(key + i - 1) + 1;
+    const long long hi = i == n ? nv : (long long)__ldg(key + i);
+    for (long long v = lo; v <= hi && v <= nv; v++) crow[v] = (int)i;
   }
 }
 
@@ -1161,38 +1161,55 @@ extern "C" int bf_bfs_transpose_impl(void* stream_v, int num_sms, const int* row
     snprintf(err, errcap, "bfs_transpose: bad sizes (nv=%d len(row)=%lld len(crow)=%lld)", nv, lr, lcrow);
     return BF_E_INVALID;
   }
-  int* ws = nullptr;  // [0] error flag, [1] edge count; then the cursor copy of crow
+  int h[2] = {0, 0};
+  cudaError_t e = cudaMemcpyAsync(&h[0], row, 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h[1], row + nv, 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess && (h[0] < 0 || h[1] < h[0] || h[1] > lcol)) {
+    snprintf(err, errcap, "bfs_transpose: CSR index out of range");
+    e = cudaErrorInvalidValue;
+  }
+  const long long n = (long long)h[1] - h[0];
+  if (e == cudaSuccess && n > lccol) {
+    snprintf(err, errcap, "bfs_transpose: %lld edges do not fit len(ccol)=%lld", n, lccol);
+    e = cudaErrorInvalidValue;
+  }
+  int end_bit = 1;
+  while (end_bit < 32 && (1ll << end_bit) < (long long)nv) end_bit++;
+  unsigned *key = nullptr, *key_out = nullptr;
+  int *srcv = nullptr, *flag = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
-  cudaError_t e = cudaMalloc((void**)&ws, ((size_t)nv + 3) * 4);
-  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, crow, crow, nv + 1, stream);
-  if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
-  int h[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMalloc((void**)&flag, 4);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&key, (size_t)std::max(n, 1LL) * 4);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&key_out, (size_t)std::max(n, 1LL) * 4);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&srcv, (size_t)std::max(n, 1LL) * 4);
+  if (e == cudaSuccess)
+    e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_out, srcv, ccol, (int)n, 0, end_bit, stream);
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16));
   if (e == cudaSuccess) {
+    int f = 0;
     const int g = stream_grid(nv, 256, num_sms, 8);
-    cudaMemsetAsync(ws, 0, 8, stream);
-    cudaMemsetAsync(crow, 0, ((size_t)nv + 1) * 4, stream);
-    bfs_indegree<<<g, 256, 0, stream>>>(row, col, lcol, nv, crow, ws);
-    e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, crow, crow, nv + 1, stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(ws + 1, crow + nv, 4, cudaMemcpyDeviceToDevice, stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h, ws, 8, cudaMemcpyDeviceToHost, stream);
+    cudaMemsetAsync(flag, 0, 4, stream);
+    bfs_tr_pairs<<<g, 256, 0, stream>>>(row, col, nv, h[0], h[1], key, srcv, flag);
+    e = cudaMemcpyAsync(&f, flag, 4, cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e == cudaSuccess && h[0]) {
+    if (e == cudaSuccess && f) {
       snprintf(err, errcap, "bfs_transpose: CSR index out of range");
       e = cudaErrorInvalidValue;
     }
-    if (e == cudaSuccess && h[1] > lccol) {
-      snprintf(err, errcap, "bfs_transpose: %d edges do not fit len(ccol)=%lld", h[1], lccol);
-      e = cudaErrorInvalidValue;
-    }
+    if (e == cudaSuccess && n > 0)
+      e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_out, srcv, ccol, (int)n, 0, end_bit, stream);
     if (e == cudaSuccess) {
-      cudaMemcpyAsync(ws + 2, crow, (size_t)nv * 4, cudaMemcpyDeviceToDevice, stream);
-      bfs_fill_in_edges<<<g, 256, 0, stream>>>(row, col, lcol, nv, ws + 2, ccol);
+      bfs_tr_offsets<<<stream_grid(n + 1, 256, num_sms, 8), 256, 0, stream>>>(key_out, n, nv, crow);
       e = cudaStreamSynchronize(stream);
     }
   }
   cudaFree(tmp);
-  cudaFree(ws);
+  cudaFree(key);
+  cudaFree(key_out);
+  cudaFree(srcv);
+  cudaFree(flag);
   if (e != cudaSuccess) {
     const bool fault = e == cudaErrorInvalidValue && err[0];
     if (!err[0]) snprintf(err, errcap, "bfs_transpose: %s", cudaGetErrorString(e));

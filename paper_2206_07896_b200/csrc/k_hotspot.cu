@@ -14,7 +14,7 @@
 // as doubles, so every value is widened to f64 once.  The kernel sits at the
 // HBM roofline only because the f64 arithmetic (14 DP ops per cell) and the
 // f32<->f64 conversions (quarter-rate XU pipe) are kept to one conversion
-// per loaded value; see profiles/r2_hotspot.md.  Algorithmic traffic per
+// per loaded value; see profiles/r2/hotspot.md.  Algorithmic traffic per
 // cell and iteration: 12 B (read src + power, write dst).
 #include <climits>
 #include <cstdlib>
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(288, MINB) hotspot_rows(const float* __restric
 // BF_HOTSPOT_ROWS: 1 (default) = hotspot_rows with 1024-float segments and
 // 6 stages (two CTAs per SM); 2 = 2048-float segments, 4 stages; 0 = the
 // round-1 warp-strip kernel (hotspot_band).  Measured (8192^2, 100 launches,
-// per launch): 125.4 / 126.5 / 139.2 us (profiles/r2_hotspot.md).
+// per launch): 125.4 / 126.5 / 139.2 us (profiles/r2/hotspot.md).
 static int hotspot_rows_variant() {
   static int v = -1;
   if (v < 0) {

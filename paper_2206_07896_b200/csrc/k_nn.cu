@@ -278,25 +278,47 @@ __global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
     t.insert(key);
     const unsigned hb = (unsigned)(t.l[K - 1] >> 32);
     // inverse of topk_key's order map (0xffffffff: empty slot or NaN)
-    tf = hb == 0xffffffffu ? __uint_as_float(0x7fffffffu)
-                           : __uint_as_float((hb & 0x80000000u) ? (hb & 0x7fffffffu) : ~hb);
+    // fminf keeps a tighter (warp) bound; NaN (list not full) never wins
+    tf = fminf(tf, hb == 0xffffffffu ? __uint_as_float(0x7fffffffu)
+                                     : __uint_as_float((hb & 0x80000000u) ? (hb & 0x7fffffffu) : ~hb));
   };
-  // four 16 B loads in flight per thread before any key work
-  for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < n4; j0 += 4 * stride) {
-    float4 v[4];
+  // software-pipelined: the next group's four 16 B loads are in flight while
+  // this group's 16 values are tested; one compare of their minimum against
+  // the threshold rejects the whole group in the common case.  32-bit vector
+  // indices (n < 2^31).
+  const unsigned n4u = (unsigned)n4, su = (unsigned)stride;
+  unsigned j0 = blockIdx.x * blockDim.x + threadIdx.x;
+  float4 v[4];
+#pragma unroll
+  for (int u = 0; u < 4; u++)
+    v[u] = j0 + u * su < n4u ? __ldcs(d4 + j0 + u * su) : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+  for (; __any_sync(0xffffffffu, j0 < n4u); j0 += 4 * su) {  // warp-uniform: the threshold shuffle
+    float4 nx[4];
+    const unsigned j1 = j0 + 4 * su;
 #pragma unroll
     for (int u = 0; u < 4; u++)
-      if (j0 + u * stride < n4) v[u] = __ldcs(d4 + j0 + u * stride);
+      nx[u] = j1 + u * su < n4u ? __ldcs(d4 + j1 + u * su) : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+    float m[4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const long long j = j0 + u * stride;
-      if (j < n4) {
-        offer(v[u].x, 4 * j);
-        offer(v[u].y, 4 * j + 1);
-        offer(v[u].z, 4 * j + 2);
-        offer(v[u].w, 4 * j + 3);
+    for (int u = 0; u < 4; u++) m[u] = fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w));
+    if (!(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])) > tf)) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const unsigned j = j0 + u * su;
+        if (j < n4u && !(m[u] > tf)) {
+          offer(v[u].x, 4ll * j);
+          offer(v[u].y, 4ll * j + 1);
+          offer(v[u].z, 4ll * j + 2);
+          offer(v[u].w, 4ll * j + 3);
+        }
       }
     }
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = nx[u];
+    // the smallest last-value over the warp's lists also bounds every lane:
+    // that lane alone holds K keys at or below it (NaN lanes: lists not full)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tf = fminf(tf, __shfl_xor_sync(0xffffffffu, tf, o));
   }
   if (blockIdx.x == 0 && threadIdx.x < (int)(a.n & 3)) offer(a.d[4 * n4 + threadIdx.x], 4 * n4 + threadIdx.x);
   block_merge<K>(t, a.cnt, a.cand + (long long)blockIdx.x * K);
@@ -380,7 +402,7 @@ static int launch_nn_topk(LaunchCtx& ctx) {
   }
   const bool small = k <= 8;
   const int K = small ? 8 : 32;
-  const int grid = small ? wave_grid(nn_topk_pass<8>, 256, 0, std::max(1LL, n / 4), 256 * 8, ctx.num_sms, 4)
+  const int grid = small ? wave_grid(nn_topk_pass<8>, 256, 0, std::max(1LL, n / 4), 256 * 8, ctx.num_sms, 8)
                          : wave_grid(nn_topk_pass<32>, 256, 0, std::max(1LL, n / 4), 256 * 8, ctx.num_sms, 4);
   TopkScratch& S = scratch_for<TopkScratch>(ctx.stream, SCRATCH_NN_TOPK);
   if (S.cap < (long long)grid * K) {

@@ -9,12 +9,11 @@ from pathlib import Path
 
 out = Path(__file__).resolve().parents[1] / "gpurun_out"
 rows = []
-for rep in sorted(out.glob("full_*.ncu-rep")):
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    r = list(csv.reader(io.StringIO(txt)))
-    if len(r) < 3:
-        continue
-    h, u, v = r[0], r[1], r[2]
+reps = [Path(a) for a in sys.argv[1:]] or sorted(out.glob("full_*.ncu-rep"))
+for rep, h, u, v in ((rep, *hdr, v) for rep in reps
+                     for hdr, vals in [(lambda r: ((r[0], r[1]), r[2:]))(list(csv.reader(io.StringIO(
+                         subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
+                                        text=True).stdout))))] for v in vals):
     m = dict(zip(h, v))
     unit = dict(zip(h, u))
 
