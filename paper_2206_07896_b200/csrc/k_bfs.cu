@@ -637,8 +637,12 @@ __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
                                                     unsigned* now, long long nv,
                                                     const int* __restrict__ q, int* sizes,
                                                     int* zero_p, int* hist, const int* vis = nullptr,
-                                                    int alpha16 = 0, const unsigned* __restrict__ fin = nullptr) {
+                                                    int alpha16 = 0, const unsigned* __restrict__ fin = nullptr,
+                                                    const int* visc = nullptr, int probe_mode = 1) {
   const int qn = sizes[0];
+  // probe the target's bitmap word before the RED: always (1), never (0), or
+  // once more than half of the vertices are visited (2; visc: visited count)
+  const bool probe = TEST && (probe_mode == 1 || (probe_mode == 2 && visc && 2ll * *visc > nv));
   const bool bottom_up = bfs_pick_bottom_up(sizes, vis, nv, alpha16);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // pipelined loop: next-next level's block, qn record, direction
     if (zero_p) {
@@ -724,7 +728,7 @@ __global__ void __launch_bounds__(256) bfs_expand_v(const int* __restrict__ row,
           w[a][t] = 0xffffffffu;
           if (v[a][t] >= 0) {
             if (v[a][t] >= nv) sizes[2] = 1;
-            else w[a][t] = TEST ? __ldcg(now + (v[a][t] >> 5)) : 0u;
+            else w[a][t] = probe ? __ldcg(now + (v[a][t] >> 5)) : 0u;
           }
         }
 #pragma unroll
@@ -1287,8 +1291,10 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
   }
   // BF_BFS_DO=0 keeps a direction-optimizing call top-down (A/B); BF_BFS_ALPHA16:
   // bottom-up when 16 * |frontier| * alpha16 / 16 >= unvisited
-  static int do_on = -1, alpha16 = 32;
+  static int do_on = -1, alpha16 = 32, probe_mode = 2;
   if (do_on < 0) {
+    const char* pe = getenv("BF_BFS_PROBE");
+    if (pe) probe_mode = atoi(pe);
     const char* de = getenv("BF_BFS_DO");
     do_on = de ? atoi(de) : 1;
     const char* ae = getenv("BF_BFS_ALPHA16");
@@ -1333,7 +1339,8 @@ extern "C" int bf_bfs_levels_impl(void* stream_v, int num_sms, const int* row, l
       const bool bu = armed_next;  // F_L exists: the bottom-up step may run
       armed_next = armed;
       bfs_expand_v<true><<<xgrid, 256, 0, stream>>>(row, col, lcol, now, nv, qL, B, Bz, S.hist_d + (L & 63),
-                                                     bu ? vis : nullptr, alpha16, dir ? S.fb[L & 1] : nullptr);
+                                                     bu ? vis : nullptr, alpha16, dir ? S.fb[L & 1] : nullptr,
+                                                     vis, probe_mode);
       cudaEventRecord(S.evx[L & 3], stream);
       if (bu)
         bfs_bottom_up<<<bgrid, 256, 0, stream>>>(crow, ccol, lccol, now, prev, words, nv, S.fb[L & 1],

@@ -197,6 +197,15 @@ __device__ __forceinline__ unsigned long long topk_key(float v, unsigned i) {
   return ((unsigned long long)b << 32) | i;
 }
 
+// high word of topk_key for a non-NaN value, and its inverse
+__device__ __forceinline__ unsigned topk_hi(float v) {
+  unsigned b = v == 0.0f ? 0u : __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float topk_from_hi(unsigned hb) {
+  return __uint_as_float((hb & 0x80000000u) ? (hb & 0x7fffffffu) : ~hb);
+}
+
 template <int K>
 struct TopList {
   unsigned long long l[K];
@@ -271,6 +280,9 @@ __global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
   // fast reject on the raw float: v > tf (the value of the list's last key)
   // cannot enter; a NaN tf (list not full, or a NaN last key) rejects nothing
   float tf = __uint_as_float(0x7fffffffu);
+  __shared__ unsigned s_thr;
+  if (threadIdx.x == 0) s_thr = 0xffffffffu;
+  __syncthreads();
   auto offer = [&](float v, long long i) {
     if (v > tf) return;
     const unsigned long long key = topk_key(v, (unsigned)i);
@@ -279,8 +291,7 @@ __global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
     const unsigned hb = (unsigned)(t.l[K - 1] >> 32);
     // inverse of topk_key's order map (0xffffffff: empty slot or NaN)
     // fminf keeps a tighter (warp) bound; NaN (list not full) never wins
-    tf = fminf(tf, hb == 0xffffffffu ? __uint_as_float(0x7fffffffu)
-                                     : __uint_as_float((hb & 0x80000000u) ? (hb & 0x7fffffffu) : ~hb));
+    tf = fminf(tf, hb == 0xffffffffu ? __uint_as_float(0x7fffffffu) : topk_from_hi(hb));
   };
   // software-pipelined: the next group's four 16 B loads are in flight while
   // this group's 16 values are tested; one compare of their minimum against
@@ -319,6 +330,12 @@ __global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
     // that lane alone holds K keys at or below it (NaN lanes: lists not full)
 #pragma unroll
     for (int o = 16; o; o >>= 1) tf = fminf(tf, __shfl_xor_sync(0xffffffffu, tf, o));
+    // and over the CTA: the order key of the bound, min-combined in shared
+    // memory (0xffffffff: no bound yet)
+    if ((threadIdx.x & 31) == 0 && tf == tf) atomicMin(&s_thr, topk_hi(tf));
+    __syncwarp();
+    const unsigned ct = *(volatile unsigned*)&s_thr;
+    if (ct != 0xffffffffu) tf = fminf(tf, topk_from_hi(ct));
   }
   if (blockIdx.x == 0 && threadIdx.x < (int)(a.n & 3)) offer(a.d[4 * n4 + threadIdx.x], 4 * n4 + threadIdx.x);
   block_merge<K>(t, a.cnt, a.cand + (long long)blockIdx.x * K);
