@@ -107,21 +107,30 @@ class HaloExchange:
         self.view = view
         self.stream = stream
 
+    def transfers(self) -> list:
+        """[(peer, (send lo, hi), (recv lo, hi))] in local element offsets:
+        the first `halo` owned rows go up and the ghost rows above are
+        received from there; the last `halo` owned rows go down and the ghost
+        rows below come back."""
+        b, cols, h = self.b, self.b.cols, self.b.halo
+        o0, o1 = b.own_slice()
+        l0, l1 = 0, b.local_rows[1] - b.local_rows[0]
+        out = []
+        if b.up is not None:
+            out.append((b.up, (o0 * cols, (o0 + h) * cols), (l0 * cols, o0 * cols)))
+        if b.down is not None:
+            out.append((b.down, ((o1 - h) * cols, o1 * cols), (o1 * cols, l1 * cols)))
+        return out
+
     def exchange(self, handle) -> None:
         import torch
         import torch.distributed as dist
 
-        b, cols, h = self.b, self.b.cols, self.b.halo
         t = self.view(handle)
-        o0, o1 = b.own_slice()
-        l0, l1 = 0, b.local_rows[1] - b.local_rows[0]
         ops = []
-        if b.up is not None:
-            ops.append(dist.P2POp(dist.isend, t[o0 * cols:(o0 + h) * cols], b.up))
-            ops.append(dist.P2POp(dist.irecv, t[l0 * cols:o0 * cols], b.up))
-        if b.down is not None:
-            ops.append(dist.P2POp(dist.isend, t[(o1 - h) * cols:o1 * cols], b.down))
-            ops.append(dist.P2POp(dist.irecv, t[o1 * cols:l1 * cols], b.down))
+        for peer, (s0, s1), (r0, r1) in self.transfers():
+            ops.append(dist.P2POp(dist.isend, t[s0:s1], peer))
+            ops.append(dist.P2POp(dist.irecv, t[r0:r1], peer))
         if not ops:
             return
         ctx = torch.cuda.stream(self.stream) if self.stream is not None else _null()

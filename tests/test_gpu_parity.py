@@ -881,3 +881,64 @@ print("ok")
     env = dict(os.environ, **switch)
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world,rows,cols,iters,halo", [(2, 300, 256, 17, 4), (3, 1030, 512, 12, 8),
+                                                        (4, 8192, 1024, 9, 8)])
+def test_hotspot_bands_on_one_device_vs_oracle(world, rows, cols, iters, halo):
+    """The multi-GPU hotspot of bench.py (HotspotBands row bands with ghost
+    zones + HaloExchange every `halo` iterations) with `world` ranks driven in
+    lockstep on one device: each rank's band runs the sm_100a kernel through
+    Runtime.launch, the halo transfers are HaloExchange.transfers() done as
+    device copies; the owned rows equal the single-grid oracle bit for bit."""
+    import torch
+
+    import instances as I
+    from paper_2206_07896_b200 import ArgSlot, DeviceArena, Dim3, PackedArgs, Runtime, routines
+    from paper_2206_07896_b200.parallel import HaloExchange, HotspotBands
+    temp, power = I.hotspot_inputs(rows, cols, 11)
+    params = I.hotspot_params(rows, cols)
+    want = oracle.hotspot_iterate(temp, power, rows, cols, params, iters)
+    arena = DeviceArena()
+    dev = torch.device("cuda", arena.device)
+    ranks = []
+    with Runtime(arena) as rt:
+        for r in range(world):
+            b = HotspotBands(rows, cols, world, r, halo=halo)
+            lo, hi = b.local_rows
+            n = (hi - lo) * cols
+            h = [arena.alloc("f32", n) for _ in range(3)]  # src, power, dst
+            arena.upload_numpy(h[0], temp[lo * cols:hi * cols])
+            arena.upload_numpy(h[1], power[lo * cols:hi * cols])
+
+            def pk(a, c, h=h, lr=hi - lo):
+                return PackedArgs([ArgSlot("handle", a), ArgSlot("handle", h[1]), ArgSlot("handle", c),
+                                   ArgSlot("i32", lr), ArgSlot("i32", cols), ArgSlot("f32", params["sdc"]),
+                                   ArgSlot("f32", params["rx1"]), ArgSlot("f32", params["ry1"]),
+                                   ArgSlot("f32", params["rz1"]), ArgSlot("f32", params["amb"])])
+            ranks.append((b, h, [pk(h[0], h[2]), pk(h[2], h[0])], HaloExchange(b, None)))
+        cur = 0
+        for it in range(iters):
+            for b, h, packs, _ in ranks:
+                lr = b.local_rows[1] - b.local_rows[0]
+                rt.launch(routines.get("hotspot"), Dim3(-(-cols // 16), -(-lr // 16)), Dim3(16, 16), 0,
+                          packs[cur])
+            rt.device_synchronize()
+            cur ^= 1
+            if (it + 1) % halo == 0 and it + 1 < iters:
+                views = [torch.as_tensor(arena.cuda_array(h[2] if cur == 1 else h[0]), device=dev)
+                         for _, h, _, _ in ranks]
+                sends = {}
+                for r, (b, h, _, ex) in enumerate(ranks):
+                    for peer, (s0, s1), _ in ex.transfers():
+                        sends[(r, peer)] = views[r][s0:s1].clone()
+                for r, (b, h, _, ex) in enumerate(ranks):
+                    for peer, _, (r0, r1) in ex.transfers():
+                        views[r][r0:r1] = sends[(peer, r)]
+                torch.cuda.synchronize()
+        got = np.empty(rows * cols, np.float32)
+        for b, h, _, _ in ranks:
+            o0, o1 = b.own_slice()
+            out = arena.to_numpy(h[0] if cur == 0 else h[2])
+            got[b.own[0] * cols:b.own[1] * cols] = out[o0 * cols:o1 * cols]
+    assert bit_equal(got, want)
