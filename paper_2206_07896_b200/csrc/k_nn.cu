@@ -269,19 +269,34 @@ struct TopkArgs {
   unsigned long long* lo;    // keys must exceed *lo (the previous round's last pick)
 };
 
+// Scan: one producer warp streams 16 KB chunks of d into a shared-memory ring
+// with bulk copies (TMA, 1D); eight consumer warps test them (a thread owns
+// four float4 of each chunk).  Many bytes stay in flight with few threads, so
+// the scan runs at the DRAM rate although its per-value work is light.
+constexpr int kTkChunk = 4096;  // floats per chunk
+constexpr int kTkStages = 4;
+constexpr int kTkThreads = 288;  // 8 consumer warps + 1 producer warp
+
 template <int K>
-__global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
+__global__ void __launch_bounds__(kTkThreads) nn_topk_pass(TopkArgs a) {
+  extern __shared__ __align__(128) float tk_ring[];  // kTkStages x kTkChunk
+  __shared__ uint64_t tk_full[kTkStages], tk_empty[kTkStages];
+  __shared__ unsigned s_thr;
   const unsigned long long lo = *a.lo;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   TopList<K> t;
   t.init();
-  const long long n4 = a.n >> 2;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const float4* d4 = reinterpret_cast<const float4*>(a.d);
-  // fast reject on the raw float: v > tf (the value of the list's last key)
-  // cannot enter; a NaN tf (list not full, or a NaN last key) rejects nothing
+  // fast reject on the raw float: v > tf cannot enter (a value such that some
+  // thread of the CTA holds K keys at or below it); NaN tf rejects nothing
   float tf = __uint_as_float(0x7fffffffu);
-  __shared__ unsigned s_thr;
-  if (threadIdx.x == 0) s_thr = 0xffffffffu;
+  if (threadIdx.x == 0) {
+    s_thr = 0xffffffffu;
+    for (int s = 0; s < kTkStages; s++) {
+      mbar_init(&tk_full[s], 1);
+      mbar_init(&tk_empty[s], 8);
+    }
+    fence_barrier_init();
+  }
   __syncthreads();
   auto offer = [&](float v, long long i) {
     if (v > tf) return;
@@ -289,53 +304,85 @@ __global__ void __launch_bounds__(256) nn_topk_pass(TopkArgs a) {
     if (key >= t.l[K - 1] || key <= lo) return;
     t.insert(key);
     const unsigned hb = (unsigned)(t.l[K - 1] >> 32);
-    // inverse of topk_key's order map (0xffffffff: empty slot or NaN)
-    // fminf keeps a tighter (warp) bound; NaN (list not full) never wins
+    // fminf keeps a tighter (shared) bound; NaN (list not full) never wins
     tf = fminf(tf, hb == 0xffffffffu ? __uint_as_float(0x7fffffffu) : topk_from_hi(hb));
   };
-  // software-pipelined: the next group's four 16 B loads are in flight while
-  // this group's 16 values are tested; one compare of their minimum against
-  // the threshold rejects the whole group in the common case.  32-bit vector
-  // indices (n < 2^31).
-  const unsigned n4u = (unsigned)n4, su = (unsigned)stride;
-  unsigned j0 = blockIdx.x * blockDim.x + threadIdx.x;
-  float4 v[4];
-#pragma unroll
-  for (int u = 0; u < 4; u++)
-    v[u] = j0 + u * su < n4u ? __ldcs(d4 + j0 + u * su) : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-  for (; __any_sync(0xffffffffu, j0 < n4u); j0 += 4 * su) {  // warp-uniform: the threshold shuffle
-    float4 nx[4];
-    const unsigned j1 = j0 + 4 * su;
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-      nx[u] = j1 + u * su < n4u ? __ldcs(d4 + j1 + u * su) : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-    float m[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) m[u] = fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w));
-    if (!(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])) > tf)) {
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const unsigned j = j0 + u * su;
-        if (j < n4u && !(m[u] > tf)) {
-          offer(v[u].x, 4ll * j);
-          offer(v[u].y, 4ll * j + 1);
-          offer(v[u].z, 4ll * j + 2);
-          offer(v[u].w, 4ll * j + 3);
-        }
+  const long long n4 = a.n >> 2;            // whole float4 of d; the last n & 3 values below
+  const long long nchunk = (4 * n4 + kTkChunk - 1) / kTkChunk;
+  if (warp == 8) {  // producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int j = 0;
+      for (long long c = blockIdx.x; c < nchunk; c += gridDim.x, j++) {
+        const int st = j % kTkStages;
+        if (j >= kTkStages) mbar_wait(&tk_empty[st], ((j / kTkStages) - 1) & 1);
+        const long long f0 = c * kTkChunk;
+        const uint32_t bytes = (uint32_t)(min((long long)kTkChunk, 4 * n4 - f0) * 4);
+        mbar_arrive_expect_tx(&tk_full[st], bytes);
+        bulk_g2s(tk_ring + st * kTkChunk, a.d + f0, bytes, &tk_full[st], pol);
       }
     }
+  } else {  // consumers
+    int j = 0;
+    for (long long c = blockIdx.x; c < nchunk; c += gridDim.x, j++) {
+      const int st = j % kTkStages;
+      mbar_wait(&tk_full[st], (j / kTkStages) & 1);
+      const long long f0 = c * kTkChunk;
+      const int cnt4 = (int)(min((long long)kTkChunk, 4 * n4 - f0) >> 2);
+      const float4* r4 = reinterpret_cast<const float4*>(tk_ring + st * kTkChunk);
+      float4 v[4];
+      float m[4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) v[u] = nx[u];
-    // the smallest last-value over the warp's lists also bounds every lane:
-    // that lane alone holds K keys at or below it (NaN lanes: lists not full)
+      for (int u = 0; u < 4; u++) {
+        const int q = threadIdx.x + 256 * u;
+        v[u] = q < cnt4 ? r4[q] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+        m[u] = fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tk_empty[st]);  // the values are in registers
+      // warp-uniform branches (votes): the insert code is skipped, not
+      // if-converted into predicated straight-line code
+      if (__any_sync(0xffffffffu, !(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])) > tf))) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) tf = fminf(tf, __shfl_xor_sync(0xffffffffu, tf, o));
-    // and over the CTA: the order key of the bound, min-combined in shared
-    // memory (0xffffffff: no bound yet)
-    if ((threadIdx.x & 31) == 0 && tf == tf) atomicMin(&s_thr, topk_hi(tf));
-    __syncwarp();
-    const unsigned ct = *(volatile unsigned*)&s_thr;
-    if (ct != 0xffffffffu) tf = fminf(tf, topk_from_hi(ct));
+        for (int u = 0; u < 4; u++) {
+          const int q = threadIdx.x + 256 * u;
+          const bool pass = q < cnt4 && !(m[u] > tf);
+          if (__any_sync(0xffffffffu, pass) && pass) {
+            const long long i = f0 + 4ll * q;
+            offer(v[u].x, i);
+            offer(v[u].y, i + 1);
+            offer(v[u].z, i + 2);
+            offer(v[u].w, i + 3);
+          }
+        }
+      }
+      // the smallest bound over the warp, then over the CTA (order keys
+      // min-combined in shared memory; 0xffffffff: none yet)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) tf = fminf(tf, __shfl_xor_sync(0xffffffffu, tf, o));
+      if (K <= 8 && (j & 3) == 3) {
+        // every fourth chunk, a tighter bound: the K-th smallest of the
+        // warp's lane-best values (K lanes each hold a key at or below it),
+        // by K rounds of a warp minimum that retires one lane each
+        const unsigned hb0 = (unsigned)(t.l[0] >> 32);
+        float x = hb0 == 0xffffffffu ? INFINITY : topk_from_hi(hb0);
+        float kth = INFINITY;
+#pragma unroll 1
+        for (int r = 0; r < K; r++) {
+          float m = x;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          kth = m;
+          const unsigned who = __ballot_sync(0xffffffffu, x == m);
+          if (lane == __ffs(who) - 1) x = INFINITY;
+        }
+        if (kth < INFINITY) tf = fminf(tf, kth);
+      }
+      if (lane == 0 && tf == tf) atomicMin(&s_thr, topk_hi(tf));
+      __syncwarp();
+      const unsigned ct = *(volatile unsigned*)&s_thr;
+      if (ct != 0xffffffffu) tf = fminf(tf, topk_from_hi(ct));
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x < (int)(a.n & 3)) offer(a.d[4 * n4 + threadIdx.x], 4 * n4 + threadIdx.x);
   block_merge<K>(t, a.cnt, a.cand + (long long)blockIdx.x * K);
@@ -419,8 +466,17 @@ static int launch_nn_topk(LaunchCtx& ctx) {
   }
   const bool small = k <= 8;
   const int K = small ? 8 : 32;
-  const int grid = small ? wave_grid(nn_topk_pass<8>, 256, 0, std::max(1LL, n / 4), 256 * 8, ctx.num_sms, 8)
-                         : wave_grid(nn_topk_pass<32>, 256, 0, std::max(1LL, n / 4), 256 * 8, ctx.num_sms, 4);
+  const size_t tk_smem = sizeof(float) * kTkStages * kTkChunk;
+  static bool tk_attr[64] = {};
+  if (first_on_device(tk_attr)) {
+    cudaFuncSetAttribute(nn_topk_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tk_smem);
+    cudaFuncSetAttribute(nn_topk_pass<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tk_smem);
+    cudaGetLastError();
+  }
+  const int grid = small ? wave_grid(nn_topk_pass<8>, kTkThreads, tk_smem, std::max(1LL, n / kTkChunk), 1,
+                                     ctx.num_sms, 3)
+                         : wave_grid(nn_topk_pass<32>, kTkThreads, tk_smem, std::max(1LL, n / kTkChunk), 1,
+                                     ctx.num_sms, 2);
   TopkScratch& S = scratch_for<TopkScratch>(ctx.stream, SCRATCH_NN_TOPK);
   if (S.cap < (long long)grid * K) {
     cudaStreamSynchronize(ctx.stream);
@@ -452,8 +508,8 @@ static int launch_nn_topk(LaunchCtx& ctx) {
       BF_CUDA_LAUNCH_CHECK(ctx);
       break;
     }
-    if (small) nn_topk_pass<8><<<grid, 256, 0, ctx.stream>>>(a);
-    else nn_topk_pass<32><<<grid, 256, 0, ctx.stream>>>(a);
+    if (small) nn_topk_pass<8><<<grid, kTkThreads, tk_smem, ctx.stream>>>(a);
+    else nn_topk_pass<32><<<grid, kTkThreads, tk_smem, ctx.stream>>>(a);
     BF_CUDA_LAUNCH_CHECK(ctx);
   }
   return BF_OK;
