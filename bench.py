@@ -355,6 +355,8 @@ def run_ours(args) -> None:
     while len(sets) < 3:
         sets.append(BufferSet())
 
+    trace = os.environ.get("BENCH_E2E_TRACE")
+
     def pipelined(nsteps: int) -> float:
         barrier(world)
         t0 = time.perf_counter()
@@ -362,7 +364,9 @@ def run_ours(args) -> None:
         arena.upload_numpy(sets[0].pow, h_power)
         prev = None
         for k in range(nsteps):
+            ts = [time.perf_counter()]
             res = sets[k % 3].step()
+            ts.append(time.perf_counter())
             pending = None
             if prev is not None:  # D2H of step k-1 on its own stream, from a helper thread
                 pending = copier.submit(arena.download_into, prev, h_outs[(k - 1) % n_outs])
@@ -370,9 +374,15 @@ def run_ours(args) -> None:
                 nxt = sets[(k + 1) % 3]
                 arena.upload_numpy(nxt.src, h_temp)
                 arena.upload_numpy(nxt.pow, h_power)
+            ts.append(time.perf_counter())
             if pending is not None:
                 pending.result()
+            ts.append(time.perf_counter())
             rt.device_synchronize()
+            ts.append(time.perf_counter())
+            if trace:
+                print("e2e step", k, " ".join(f"{(b - a) * 1e3:.2f}" for a, b in zip(ts, ts[1:])),
+                      file=sys.stderr, flush=True)
             prev = res
         arena.download_into(prev, h_outs[(nsteps - 1) % n_outs])
         return max_over_ranks(time.perf_counter() - t0, world)

@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(256, MINB) kmeans_rb(const float* __restrict__
 // read their MMA fragments from the tile (row stride 136 floats: conflict-free
 // A fragments).  HBM is read exactly once.
 #ifndef KM_TC_WARPS
-#define KM_TC_WARPS 4  // consumer warps per CTA (32 points each); kmeans_umma needs 4 (M = 128)
+#define KM_TC_WARPS 4  // consumer warps per CTA (32 points each)
 #endif
 constexpr int kTcPts = 32 * KM_TC_WARPS;
 constexpr int kTcStride = kTcPts + 8;
@@ -872,363 +872,11 @@ static size_t kmeans_tc_smem() {
          sizeof(float) * (16 * NF + 16 + 16 * NF) + sizeof(int) * 16 + sizeof(uint4) * (NF / 8) * 64;
 }
 
-// ---------------------------------------------------------------------------
-// tcgen05 path (nf in {16, 32}, 2 <= k <= 16, npts % 4 == 0): the distance
-// contraction on the 5th-generation tensor cores, accumulators in TMEM.
-//
-// Per 128-point tile (thread p of the four consumer warps <-> point p <->
-// TMEM lane p):
-//   split   thread p reads its point's features from the TMA tile, writes
-//           the TF32 (hi, lo) pair into two 16 KB shared tiles laid out as
-//           UMMA canonical SWIZZLE_NONE K-major operands ([point][feature]
-//           in 8-row x 16 B core matrices);
-//   dist    one thread issues tcgen05.mma kind::tf32 M=128 N=16 K=8 x nf/8:
-//           D_hh = A_hi B_hi, D_lo = A_hi B_lo + A_lo B_hi (centroids as the
-//           K-major B, built once per CTA) and commits to an mbarrier;
-//   screen  tcgen05.ld gives thread p its own 16 cluster values: the screen
-//           (bound and candidate rule of kmeans_tc) runs without shuffles;
-//   sums    per warp, mma.sync m16n8k8 F^T x onehot over its 32 points with
-//           the (hi, lo) operands read straight from the split tiles (no
-//           second split; probes with MN-major / M=64 tcgen05 operands did not
-//           give a usable layout, scripts/micro/umma_dbg.cu).
-// A producer warp streams the feature tiles with bulk copies (as kmeans_tc).
-#ifndef KM_UM_MINB
-#define KM_UM_MINB 2
-#endif
-#ifndef KM_UM_STAGES
-#define KM_UM_STAGES 2
-#endif
-constexpr int kUmStages = KM_UM_STAGES;
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  // SWIZZLE_NONE canonical layout, descriptor version 1 (sm_100), base offset 0
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
-__host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(
-          d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-template <int NF>
-__device__ __forceinline__ void um_split(const float* T, uint32_t* Ah, uint32_t* Al, int arow, int p, bool valid,
-                                         bool& fin, float& fn2) {
-  // thread p: its point's features from the TMA tile -> (hi, residual) words
-  // in the K-major canonical tiles, 4 features per 16 B store.  The residual
-  // x - hi is stored unmasked: the tensor cores read only its TF32 bits
-  // (truncation, probed in scripts/micro/umma_dbg.cu), and hi + residual
-  // reconstructs x exactly for the f64 re-check.
-  fn2 = 0.f;
-#pragma unroll
-  for (int q = 0; q < NF / 4; q++) {
-    float x4[4];
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      x4[j] = valid ? T[(4 * q + j) * kTcStride + p] : 0.f;
-      fn2 = fmaf(x4[j], x4[j], fn2);
-    }
-    uint4 h, lw;
-    h.x = (__float_as_uint(x4[0]) + 0x1000u) & 0xffffe000u;
-    h.y = (__float_as_uint(x4[1]) + 0x1000u) & 0xffffe000u;
-    h.z = (__float_as_uint(x4[2]) + 0x1000u) & 0xffffe000u;
-    h.w = (__float_as_uint(x4[3]) + 0x1000u) & 0xffffe000u;
-    lw.x = __float_as_uint(x4[0] - __uint_as_float(h.x));
-    lw.y = __float_as_uint(x4[1] - __uint_as_float(h.y));
-    lw.z = __float_as_uint(x4[2] - __uint_as_float(h.z));
-    lw.w = __float_as_uint(x4[3] - __uint_as_float(h.w));
-    *reinterpret_cast<uint4*>(Ah + arow + q * 512) = h;
-    *reinterpret_cast<uint4*>(Al + arow + q * 512) = lw;
-  }
-  fin = valid && fn2 <= 3.0e38f;
-  if (!fin) {  // invalid or non-finite / huge point: operand rows must be zero
-#pragma unroll
-    for (int q = 0; q < NF / 4; q++) {
-      *reinterpret_cast<uint4*>(Ah + arow + q * 512) = make_uint4(0u, 0u, 0u, 0u);
-      *reinterpret_cast<uint4*>(Al + arow + q * 512) = make_uint4(0u, 0u, 0u, 0u);
-    }
-  }
-}
-
-// feature l of the point whose row starts at word `arow` (exact: hi + residual)
-__device__ __forceinline__ float um_feat(const uint32_t* Ah, const uint32_t* Al, int arow, int l) {
-  const int w = arow + (l >> 2) * 512 + (l & 3);
-  return __uint_as_float(Ah[w]) + __uint_as_float(Al[w]);
-}
-
-template <int NF>
-__global__ void __launch_bounds__(160, KM_UM_MINB) kmeans_umma(const float* __restrict__ f, const float* __restrict__ cent,
-                                                     int* __restrict__ member, float* sums, int* counts, int npts,
-                                                     int k, long long lo, long long hi) {
-  constexpr int KT = NF / 8;
-  constexpr int MS = NF / 16;  // feature m-tiles of the sums mma.sync
-  extern __shared__ __align__(128) unsigned char smraw[];
-  uint32_t* Abuf = reinterpret_cast<uint32_t*>(smraw);             // 2 x (hi 16 KB, residual 16 KB)
-  uint32_t* Bhi = Abuf + 4 * 4096;                                 // 2 KB centroids hi, K-major
-  uint32_t* Blo = Bhi + 512;                                       // 2 KB
-  float* tiles = reinterpret_cast<float*>(Blo + 512);              // [S][NF][kTcStride]
-  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + kUmStages * NF * kTcStride);
-  uint64_t* empty = full + kUmStages;
-  uint64_t* dist_done = empty + kUmStages;                         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dist_done + 2);
-  float* cf = reinterpret_cast<float*>(tmem_slot + 4);             // [16][NF]
-  float* cn2 = cf + 16 * NF;                                       // [16]
-  float* ssum = cn2 + 16;                                          // [16][NF]
-  int* cnt = reinterpret_cast<int*>(ssum + 16 * NF);               // [16]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-
-  for (int i = tid; i < 16 * NF; i += blockDim.x) {
-    cf[i] = i < k * NF ? cent[i] : 0.f;
-    ssum[i] = 0.f;
-  }
-  if (tid < 16) cnt[tid] = 0;
-  if (tid == 0) {
-    for (int s = 0; s < kUmStages; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 4);
-    }
-    mbar_init(&dist_done[0], 1);
-    mbar_init(&dist_done[1], 1);
-    fence_barrier_init();
-  }
-  if (warp == 4) {  // TMEM: buffer b: D_hh cols [32b, 32b+16), D_lo [32b+16, 32b+32)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  __syncthreads();
-  if (tid < 16) {
-    float n2 = 0.f;
-    for (int l = 0; l < NF; l++) n2 = fmaf(cf[tid * NF + l], cf[tid * NF + l], n2);
-    cn2[tid] = tid < k ? n2 : INFINITY;
-  }
-  // centroid operands, K-major: element (cluster c, feature l) at
-  // (c%8)*16 + (c/8)*128 + (l/4)*256 + (l%4)*4 bytes
-  for (int i = tid; i < 16 * NF; i += blockDim.x) {
-    const int c = i / NF, l = i % NF;
-    uint32_t h, lw;
-    split_tf32(cf[i], h, lw);
-    const int w = ((c & 7) * 16 + (c >> 3) * 128 + (l >> 2) * 256) / 4 + (l & 3);
-    Bhi[w] = h;
-    Blo[w] = lw;
-  }
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-
-  const long long ntile = (hi - lo + kTcPts - 1) / kTcPts;
-  if (warp == 4) {  // producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int n = 0;
-      for (long long i = blockIdx.x; i < ntile; i += gridDim.x, n++) {
-        const int s = n % kUmStages, use = n / kUmStages;
-        if (use > 0) mbar_wait_sleep(&empty[s], (use - 1) & 1);
-        const long long p0 = lo + i * kTcPts;
-        const uint32_t bytes = (uint32_t)min((long long)kTcPts, hi - p0) * 4u;
-        mbar_arrive_expect_tx(&full[s], bytes * NF);
-        float* T = tiles + s * NF * kTcStride;
-#pragma unroll 1
-        for (int l = 0; l < NF; l++) bulk_g2s(T + l * kTcStride, f + (long long)l * npts + p0, bytes, &full[s], pol);
-      }
-    }
-  } else {  // consumers: thread p <-> point p of the tile <-> TMEM lane p
-    const int p = tid;
-    float cmax2 = 0.f;
-    for (int c = 0; c < k; c++) cmax2 = fmaxf(cmax2, cn2[c]);
-    const float cmax = sqrtf(cmax2) * 1.001f;
-    const float eA = 1.52587890625e-05f * 1.03f * 2.f * cmax;
-    const float eB = 1.52587890625e-05f * 1.03f * cmax * cmax + 1e-35f;
-    const uint32_t sBhi = smem_u32(Bhi), sBlo = smem_u32(Blo);
-    const uint32_t id_dist = umma_idesc_tf32(128, 16, false, false);
-    const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
-    const uint32_t one = __float_as_uint(1.0f);
-    const int arow = ((p & 7) * 16 + (p >> 3) * 128) / 4;  // word offset of point p's core-matrix row
-    float acc[MS][2][4];
-#pragma unroll
-    for (int ms = 0; ms < MS; ms++)
-#pragma unroll
-      for (int nt = 0; nt < 2; nt++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) acc[ms][nt][j] = 0.f;
-    // stage: split tile i (n-th of this CTA) into buffer n&1 and issue its distance MMAs
-    bool fin_next = false;
-    float fn2_next = 0.f;
-    auto stage = [&](long long i, int n) {
-      const int s = n % kUmStages, b = n & 1;
-      mbar_wait(&full[s], (n / kUmStages) & 1);
-      const long long p0 = lo + i * kTcPts;
-      const int cntp = (int)min((long long)kTcPts, hi - p0);
-      uint32_t* Ah = Abuf + b * 8192;
-      um_split<NF>(tiles + s * NF * kTcStride, Ah, Ah + 4096, arow, p, p < cntp, fin_next, fn2_next);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // the TMA tile is consumed
-      fence_proxy_async();
-      consumer_bar();
-      if (tid == 0) {
-        tc_fence_after();
-        const uint32_t sA = smem_u32(Ah), sAl = smem_u32(Ah + 4096);
-        const uint32_t dh = tbase + 32 * b, dl = dh + 16;
-#pragma unroll
-        for (int kt = 0; kt < KT; kt++) {
-          const uint64_t ah = umma_desc(sA + kt * 4096, 2048, 128), al = umma_desc(sAl + kt * 4096, 2048, 128);
-          const uint64_t bh = umma_desc(sBhi + kt * 512, 256, 128), bl = umma_desc(sBlo + kt * 512, 256, 128);
-          umma_tf32(dh, ah, bh, id_dist, kt > 0);
-          umma_tf32(dl, ah, bl, id_dist, kt > 0);
-          umma_tf32(dl, al, bh, id_dist, 1u);
-        }
-        umma_commit(&dist_done[b]);
-      }
-    };
-    int n = 0;
-    long long i = blockIdx.x;
-    if (i < ntile) stage(i, 0);
-    for (; i < ntile; i += gridDim.x, n++) {
-      const int b = n & 1;
-      const bool fin0 = fin_next;
-      const float fn2 = fn2_next;
-      const long long p0 = lo + i * kTcPts;
-      const bool valid = p < (int)min((long long)kTcPts, hi - p0);
-      if (i + gridDim.x < ntile) stage(i + gridDim.x, n + 1);  // next tile's MMAs overlap this screen
-      const uint32_t* Ah = Abuf + b * 8192;
-      const uint32_t* Al = Ah + 4096;
-      mbar_wait(&dist_done[b], (n >> 1) & 1);
-      tc_fence_after();
-      float dh[16], dl[16];
-      tmem_ld16(tbase + 32 * b + lane_off, dh);
-      tmem_ld16(tbase + 32 * b + 16 + lane_off, dl);
-      // ---- screen (as kmeans_tc, all 16 clusters in this thread)
-      const float E = fmaf(eA, fn2 * rsqrtf(fn2 + 1e-30f) * 1.01f, eB) + 9.2e-13f * fn2;
-      float tv[16];
-      float m = INFINITY;
-#pragma unroll
-      for (int c = 0; c < 16; c++) {
-        tv[c] = fmaf(-2.f, dh[c] + dl[c], cn2[c]);
-        m = fminf(m, tv[c]);
-      }
-      const float thr = m + 2.f * E;
-      unsigned cm = 0;  // candidate clusters
-#pragma unroll
-      for (int c = 0; c < 16; c++) cm |= (tv[c] <= thr ? 1u : 0u) << c;
-      const int nc = __popc(cm);
-      int best = cm ? __ffs(cm) - 1 : 16;
-      bool fin = fin0 && nc >= 1;
-      if (valid) {
-        if (!fin || nc > 1) {
-          // exact reference recurrence over the candidates (all clusters when
-          // the screen is not finite), features rebuilt exactly from hi + residual;
-          // non-finite points were zeroed in the operand tiles, so re-read them
-          // from global memory
-          double bd = 0.0;
-          int bi = 0;
-          const unsigned cand = fin ? cm : ((1u << k) - 1u);
-          bool first = true;
-          for (unsigned r = cand; r; r &= r - 1) {  // ascending cluster index
-            const int c = __ffs(r) - 1;
-            double dist = 0.0;
-            for (int l = 0; l < NF; l++) {
-              const float xv = fin0 ? um_feat(Ah, Al, arow, l) : f[(long long)l * npts + p0 + p];
-              const double diff = dsub((double)xv, (double)cf[c * NF + l]);
-              dist = dadd(dist, dmul(diff, diff));
-            }
-            if (first || dist < bd) {  // the reference's `c == 0 || dist < bestd` over its scan
-              bd = dist;
-              bi = c;
-              first = false;
-            }
-          }
-          best = bi;
-        }
-        member[p0 + p] = best;
-        atomicAdd(cnt + best, 1);
-        if (!fin0)  // scalar sums path for non-finite / huge points
-          for (int l = 0; l < NF; l++) atomicAdd(ssum + best * NF + l, f[(long long)l * npts + p0 + p]);
-      }
-      // ---- sums: acc[features x clusters] += F^T onehot over this warp's 32 points
-      const int src = (valid && fin0) ? best : -1;
-#pragma unroll
-      for (int ks = 0; ks < 4; ks++) {
-        const int q0 = __shfl_sync(0xffffffffu, src, 8 * ks + t);
-        const int q1 = __shfl_sync(0xffffffffu, src, 8 * ks + t + 4);
-        const int pa = 32 * warp + 8 * ks + t, pb = pa + 4;
-        const int ra = ((pa & 7) * 16 + (pa >> 3) * 128) / 4, rb = ((pb & 7) * 16 + (pb >> 3) * 128) / 4;
-#pragma unroll
-        for (int ms = 0; ms < MS; ms++) {
-          const int f0 = 16 * ms + g, f1 = f0 + 8;
-          const int o0 = (f0 >> 2) * 512 + (f0 & 3), o1 = (f1 >> 2) * 512 + (f1 & 3);
-          const uint32_t yh[4] = {Ah[ra + o0], Ah[ra + o1], Ah[rb + o0], Ah[rb + o1]};
-          const uint32_t yl[4] = {Al[ra + o0] & 0xffffe000u, Al[ra + o1] & 0xffffe000u, Al[rb + o0] & 0xffffe000u,
-                                  Al[rb + o1] & 0xffffe000u};
-#pragma unroll
-          for (int nt = 0; nt < 2; nt++) {
-            const uint32_t b0 = q0 == 8 * nt + g ? one : 0u, b1 = q1 == 8 * nt + g ? one : 0u;
-            mma_tf32(acc[ms][nt], yl, b0, b1);
-            mma_tf32(acc[ms][nt], yh, b0, b1);
-          }
-        }
-      }
-      consumer_bar();  // buffer b is rewritten by the split two tiles ahead
-    }
-    // per-warp sums -> shared
-#pragma unroll
-    for (int ms = 0; ms < MS; ms++)
-#pragma unroll
-      for (int nt = 0; nt < 2; nt++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int feat = 16 * ms + g + (j >= 2 ? 8 : 0), c = 8 * nt + 2 * t + (j & 1);
-          if (c < k && acc[ms][nt][j] != 0.f) atomicAdd(ssum + c * NF + feat, acc[ms][nt][j]);
-        }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 4) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tbase));
-  }
-  for (int i = tid; i < k * NF; i += blockDim.x)
-    if (ssum[i] != 0.f) atomicAdd(sums + i, ssum[i]);
-  for (int i = tid; i < k; i += blockDim.x)
-    if (cnt[i]) atomicAdd(counts + i, cnt[i]);
-}
-
-template <int NF>
-static size_t kmeans_umma_smem() {
-  return 4 * (4096 * 4 + 512 * 2) + sizeof(float) * kUmStages * NF * kTcStride +
-         sizeof(uint64_t) * (2 * kUmStages + 2) + 16 + sizeof(float) * (16 * NF + 16 + 16 * NF) + sizeof(int) * 16;
-}
-
 static int kmeans_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BF_KMEANS_V");
-    v = e ? atoi(e) : 4;  // 5: tcgen05 path (kmeans_umma)
+    v = e ? atoi(e) : 4;  // 4: kmeans_tc; 2/3: kmeans_rb; 1: kmeans_fast
   }
   return v;
 }
@@ -1263,26 +911,6 @@ static int launch_kmeans(LaunchCtx& ctx) {
     if (!ok) {
       ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first_block_with_x(xi.first), "kmeans index out of range");
       continue;
-    }
-    if (kmeans_variant() == 5 && (nf == 32 || nf == 16) && k >= 2 && k <= 16 && npts % 4 == 0 && lo % 4 == 0 &&
-        hi - lo >= 4) {
-      const long long main_hi = lo + (hi - lo) / 4 * 4;
-      auto fn = nf == 32 ? kmeans_umma<32> : kmeans_umma<16>;
-      const size_t smem = nf == 32 ? kmeans_umma_smem<32>() : kmeans_umma_smem<16>();
-      static bool attr[64] = {};
-      if (first_on_device(attr)) {
-        cudaFuncSetAttribute(kmeans_umma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_umma_smem<32>());
-        cudaFuncSetAttribute(kmeans_umma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kmeans_umma_smem<16>());
-        cudaFuncSetAttribute(kmeans_umma<32>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(kmeans_umma<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaGetLastError();
-      }
-      const int grid = stream_grid(main_hi - lo, kTcPts, ctx.num_sms, KM_UM_MINB);  // CTAs per SM (smem, registers)
-      fn<<<grid, 160, smem, ctx.stream>>>((const float*)F.ptr, (const float*)Ce.ptr, (int*)M.ptr, (float*)S.ptr,
-                                          (int*)Cn.ptr, (int)npts, k, lo, main_hi);
-      BF_CUDA_LAUNCH_CHECK(ctx);
-      if (main_hi == hi) continue;
-      lo = main_hi;
     }
     if (kmeans_variant() >= 4 && (nf == 32 || nf == 16 || nf == 24 || nf == 8) && k >= 2 && k <= 16 &&
         npts % 4 == 0 && lo % 4 == 0 && hi - lo >= 4) {
