@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(256) bfs_scan2(const int* __restrict__ lvl, lo
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long quads = ((ll + 31) / 32) * 8;  // whole words
   const long long stride = (long long)gridDim.x * blockDim.x * J;
+  int uc = 0;  // unvisited vertices seen by this thread (qn[1]: the relax's probe choice)
   for (long long t0 = (long long)blockIdx.x * blockDim.x * J; t0 < quads; t0 += stride) {  // CTA-uniform
     int4 x[J];
 #pragma unroll
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(256) bfs_scan2(const int* __restrict__ lvl, lo
       }
       fm[j] = f;
       c += __popc(f);
+      uc += __popc(um);
     }
     int incl = c;
 #pragma unroll
@@ -281,6 +283,9 @@ __global__ void __launch_bounds__(256) bfs_scan2(const int* __restrict__ lvl, lo
     }
     __syncthreads();
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) uc += __shfl_xor_sync(0xffffffffu, uc, o);
+  if (lane == 0 && uc) atomicAdd(qn + 1, uc);
 }
 
 __global__ void __launch_bounds__(256) bfs_relax(const int* __restrict__ row, long long lr,
@@ -353,6 +358,10 @@ __global__ void __launch_bounds__(256) bfs_relax_v(const int* __restrict__ row, 
                                                    KDesc k, int defer_min) {
   const int n = *qn;
   const bool DEFER = n >= defer_min;  // big frontier: bfs_apply writes lvl
+  // with deferred writes a RED on an already visited target changes nothing,
+  // so while most vertices are unvisited (qn[1], counted by bfs_scan2) the
+  // bitmap probe before it is skipped: one L2 operation per edge, not two
+  const bool probe = !DEFER || defer_min == INT_MAX || 2ll * qn[1] <= ll;
   const long long stride = (long long)gridDim.x * blockDim.x * V;
   bool any = false;
   long long bad_u = -1;
@@ -406,7 +415,7 @@ __global__ void __launch_bounds__(256) bfs_relax_v(const int* __restrict__ row, 
             if (v[a][t] < 0 || v[a][t] >= ll) {
               if (bad_u < 0) bad_u = uu[a];
             } else {
-              w[a][t] = __ldcg(unv + (v[a][t] >> 5));
+              w[a][t] = probe ? __ldcg(unv + (v[a][t] >> 5)) : 0xffffffffu;
             }
           }
         }
@@ -500,7 +509,7 @@ static int launch_bfs_two_phase(LaunchCtx& ctx, const ArgVal& R, const ArgVal& C
     S.release();
     if (cudaMalloc((void**)&S.unv, words * 4) != cudaSuccess || cudaMalloc((void**)&S.unv0, words * 4) != cudaSuccess ||
         cudaMalloc((void**)&S.q, nq * 4) != cudaSuccess ||
-        cudaMalloc((void**)&S.qn, 4) != cudaSuccess) {
+        cudaMalloc((void**)&S.qn, 8) != cudaSuccess) {
       *ctx.error = "bfs: scratch allocation failed";
       cudaGetLastError();
       return BF_E_CUDA;
@@ -518,7 +527,7 @@ static int launch_bfs_two_phase(LaunchCtx& ctx, const ArgVal& R, const ArgVal& C
     const char* d = getenv("BF_BFS_DEFER_DIV");  // frontier >= len(lvl) / div: deferred writes
     defer_div = d ? std::max(1, atoi(d)) : 64;
   }
-  cudaMemsetAsync(S.qn, 0, 4, ctx.stream);
+  cudaMemsetAsync(S.qn, 0, 8, ctx.stream);  // [0] frontier, [1] unvisited
   if (relax_v == 3) {
     const int defer_min = (int)std::max(1LL, ll / defer_div);
     const int g1 = wave_grid(bfs_scan2, 256, 0, words * 8, 256 * 8, ctx.num_sms, 8);
