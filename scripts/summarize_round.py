@@ -1,6 +1,11 @@
-"""Regenerate the measured sections of profiles/r1_summary.md from a round
-check (scripts/round_gpu.sh): the bench line and the ncu launch list.  The
-hand-written sections from "## ncu --set full" on are kept."""
+"""Regenerate the measured summary of a round from a round check
+(scripts/round_gpu.sh): the bench line and the ncu launch list.
+
+    python scripts/summarize_round.py [r2]
+
+r1 rewrites profiles/r1_summary.md keeping its hand-written sections from
+"## ncu --set full" on; r2 writes profiles/r2/summary.md (bench line, launch
+list, per-kernel table) and points at the per-kernel notes in profiles/r2/."""
 import collections
 import csv
 import json
@@ -10,10 +15,13 @@ from pathlib import Path
 
 root = Path(__file__).resolve().parents[1]
 out = root / "gpurun_out"
-prof = root / "profiles"
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
+prof = root / "profiles" if rnd == "r1" else root / "profiles" / rnd
+names = {"bench": "r1_bench_line.json", "launches": "r1_launches.csv", "summary": "r1_summary.md"} if rnd == "r1" \
+    else {"bench": "bench_line.json", "launches": "launches.csv", "summary": "summary.md"}
 bench = json.loads((out / "bench.json").read_text().strip().splitlines()[-1])
-shutil.copy(out / "bench.json", prof / "r1_bench_line.json")
-shutil.copy(out / "launches.csv", prof / "r1_launches.csv")
+shutil.copy(out / "bench.json", prof / names["bench"])
+shutil.copy(out / "launches.csv", prof / names["launches"])
 tests = (out / "gputests.log").read_text().strip().splitlines()[-1] if (out / "gputests.log").exists() else "?"
 
 rows = [r for r in csv.reader(open(out / "launches.csv")) if len(r) > 10]
@@ -27,11 +35,12 @@ for r in rows[1:]:
 total = sum(v[1] for v in agg.values())
 
 rf, e2e = bench["roofline"], bench["e2e"]
-L = ["# Round 1 profile summary (B200, sm_100a)", "",
+rel = "profiles/" if rnd == "r1" else f"profiles/{rnd}/"
+L = [f"# Round {rnd[1:]} profile summary (B200, sm_100a)", "",
      "Sources (all N = 1, one B200):",
-     f"* `profiles/r1_bench_line.json` — the default `python bench.py` line of the",
+     f"* `{rel}{names['bench']}` — the default `python bench.py` line of the",
      f"  last round check (`pytest -m gpu` in the same call: {tests}).",
-     "* `profiles/r1_launches.csv` — ncu `--metrics gpu__time_duration.sum",
+     f"* `{rel}{names['launches']}` — ncu `--metrics gpu__time_duration.sum",
      "  --clock-control none` launch list of `python bench.py --no-cpu --steps 2",
      f"  --warmup 1` ({len(rows) - 1} launches; cold-cache and serialised: compare shares).",
      "* per-kernel `ncu --set full` captures (reports in gpurun_out/, metrics",
@@ -45,18 +54,26 @@ L = ["# Round 1 profile summary (B200, sm_100a)", "",
      f"| fused driver (bf_hotspot_run, register-wavefront temporal blocking) | {bench.get('hotspot_fused', {}).get('value', bench.get('hotspot_fused'))} GB/s algorithmic |",
      f"| CPU port (oracle.c, OpenMP, host cores) | {bench['cpu_baseline']['value']} {bench['cpu_baseline']['unit']} |",
      f"| clocks | {bench['clocks']} |", "",
-     f"## Launch list shares (`profiles/r1_launches.csv`)", "",
+     f"## Launch list shares (`{rel}{names['launches']}`)", "",
      "| kernel | launches | avg us (ncu) | share |", "|---|---:|---:|---:|"]
 for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:16]:
     L.append(f"| {name[:90]} | {n} | {t / n / 1e3:.1f} | {100 * t / total:.1f} % |")
-L += ["", "Inside the headline's timed region only hotspot_band runs (100 launches per",
+L += ["", f"Inside the headline's timed region only {rf['kernel']} runs (100 launches per",
       "step, share 100 %).", "",
       "## Per-kernel table (CUDA events, N = 1, fraction of the measured HBM peak)", "",
       "| case | GB/s | frac | elements/s | ms/step | full-size check |", "|---|---:|---:|---|---:|---|"]
 for k, v in bench["kernels"].items():
     eps = next((f"{x:.3g} {key[:-6].replace('_', ' ')}/s" for key, x in v.items() if key.endswith("_per_s")), "")
     L.append(f"| {k} | {v['gbs']} | {v['frac_hbm']} | {eps} | {v['ms_per_step']} | {v['checked']} |")
-old = (prof / "r1_summary.md").read_text()
-keep = old[old.index("## ncu --set full, per kernel"):]
-(prof / "r1_summary.md").write_text("\n".join(L) + "\n\n" + keep)
+if rnd == "r1":
+    old = (prof / "r1_summary.md").read_text()
+    keep = old[old.index("## ncu --set full, per kernel"):]
+else:
+    keep = ("## ncu --set full, per kernel\n\n"
+            "* `hotspot.md` — the headline kernel (hotspot_rows) and its variants.\n"
+            "* `bfs.md`, `bfs_do_launches.txt` — the direction-optimizing traversal level by level.\n"
+            "* `kmeans.md`, `umma_sw128_probe.log` — kmeans_tc and the tcgen05 layout probe.\n"
+            "* `sanitizer_summary.md` — compute-sanitizer memcheck / racecheck / synccheck / initcheck.\n"
+            "* `grain_host_vs_device_fetch.json` — the fetch-grain study with host-issued and device-side fetching.\n")
+(prof / names["summary"]).write_text("\n".join(L) + "\n\n" + keep)
 print("ok")

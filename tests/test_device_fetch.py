@@ -146,3 +146,33 @@ def test_device_fetch_traps(need_gpu):
     want, _ = oracle.run(hs)
     got, trap, task, _ = gpu_run(hs, policy=Fixed(3), fetch="device")
     assert trap is None and bit_equal(got["dst"], want["dst"])
+
+
+@gpu
+def test_device_fetch_launch_range_and_hold(need_gpu):
+    """launch_range with device fetching computes exactly [first, first+count)
+    (executed[] indexed from first); hold_blocks keeps host-issued fetches
+    (nothing runs before the synchronize) and still matches."""
+    n = 1 << 14
+    inst = _vecadd(n)
+    want, _ = oracle.run(inst)
+    arena = DeviceArena()
+    from gpu_helpers import materialize
+    packed, h = materialize(inst, arena)
+    gx = inst.grid.x
+    first, count = 5, gx - 9
+    with Runtime(arena, fetch="device", policy=Fixed(2), instrument=True) as rt:
+        task = rt.launch_range(routines.get("vecadd"), Dim3(gx), Dim3(256), 0, packed, first, count)
+        rt.device_synchronize()
+        assert list(task.executed) == [1] * count and task.fetches == -(-count // 2)
+    got = arena.to_numpy(h["c"])
+    lo, hi = first * 256, (first + count) * 256
+    assert bit_equal(got[lo:hi], want["c"][lo:hi])
+    assert not got[:lo].any() and not got[hi:].any()
+    arena.fill_value(h["c"], 0.0)
+    with Runtime(arena, fetch="device", hold_blocks=True, policy=Fixed(3)) as rt:
+        task = rt.launch(routines.get("vecadd"), Dim3(gx), Dim3(256), 0, packed)
+        assert not arena.to_numpy(h["c"]).any()  # held: nothing ran
+        rt.device_synchronize()
+        assert task.remaining == 0
+    assert bit_equal(arena.to_numpy(h["c"]), want["c"])
