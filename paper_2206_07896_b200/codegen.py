@@ -66,21 +66,22 @@ struct BfJitGeom {
   unsigned long long task;
   int warp_size;
   // device-side fetching (null dcur: the grid strides over [first, first + count));
-  // the fetches are split into 8 sub-ranges with a counter each (bf_internal.h DevFetch)
+  // the fetches are split into 8 sub-ranges with a claim counter each, zeroed
+  // at launch (bf_internal.h DevFetch)
   unsigned long long* dcur;    // the worker's 8 claim counters
   unsigned long long* dstats;  // per worker slot: claims, blocks executed
   int* dexec;                  // KernelTask.executed by absolute block (nullable)
-  unsigned long long dbase[8];
   long long nfetch, grain;
   int dslots;
 };
-// thread 0's claim of the next fetch (cursor: sub-range and sub-ranges tried)
-__device__ __forceinline__ long long bf_claim(const BfJitGeom& G, int& sub, int& tried) {
+// thread 0's claim of the next fetch (cursor: sub-range and sub-ranges tried;
+// the CTA's claims are counted in a register and flushed once at the end)
+__device__ __forceinline__ long long bf_claim(const BfJitGeom& G, int& sub, int& tried, unsigned long long& nclaims) {
   while (tried < 8) {
     const long long lo = (G.nfetch * sub) / 8, n = (G.nfetch * (sub + 1)) / 8 - lo;
-    const long long f = (long long)(atomicAdd(G.dcur + sub, 1ull) - G.dbase[sub]);
+    const long long f = (long long)atomicAdd(G.dcur + sub, 1ull);
     if (f < n) {
-      atomicAdd(G.dstats + 2 * (blockIdx.x %% G.dslots), 1ull);
+      nclaims++;
       return lo + f;
     }
     sub = (sub + 1) %% 8;
@@ -591,10 +592,11 @@ class _Gen:
         # abandons the rest of its fetch only, runtime.py:335-343)
         src.append("  const bool bf_dev = G.dcur != nullptr;")
         src.append("  int bf_sub = (int)(blockIdx.x % 8), bf_tried = 0;")
-        src.append("  long long bf_f = bf_dev ? bf_take(tid == 0 ? bf_claim(G, bf_sub, bf_tried) : 0) : 0;")
+        src.append("  unsigned long long bf_nclaims = 0, bf_nblocks = 0;")
+        src.append("  long long bf_f = bf_dev ? bf_take(tid == 0 ? bf_claim(G, bf_sub, bf_tried, bf_nclaims) : 0) : 0;")
         src.append("  const long long bf_nf = bf_dev ? G.nfetch : 1;")
         src.append("  while (bf_f < bf_nf) {")
-        src.append("  const long long bf_nx = bf_dev && tid == 0 ? bf_claim(G, bf_sub, bf_tried) : 0;")
+        src.append("  const long long bf_nx = bf_dev && tid == 0 ? bf_claim(G, bf_sub, bf_tried, bf_nclaims) : 0;")
         src.append("  const long long bf_b0 = bf_dev ? G.first + bf_f * G.grain : G.first;")
         src.append("  const long long bf_b1 = bf_dev ? (bf_b0 + G.grain < G.first + G.count ? bf_b0 + G.grain "
                    ": G.first + G.count) : G.first + G.count;")
@@ -615,12 +617,16 @@ class _Gen:
         src.extend(body)
         src.append("    if (__syncthreads_or(bf_t)) break;")
         src.append("    if (bf_dev && tid == 0) {")
-        src.append("      atomicAdd(G.dstats + 2 * (blockIdx.x % G.dslots) + 1, 1ull);")
+        src.append("      bf_nblocks++;")
         src.append("      if (G.dexec) atomicAdd(G.dexec + blk, 1);")
         src.append("    }")
         src.append("  }")
         src.append("  if (!bf_dev) break;")
         src.append("  bf_f = bf_take(bf_nx);")
+        src.append("  }")
+        src.append("  if (bf_dev && tid == 0 && bf_nclaims) {")
+        src.append("    atomicAdd(G.dstats + 2 * (blockIdx.x % G.dslots), bf_nclaims);")
+        src.append("    atomicAdd(G.dstats + 2 * (blockIdx.x % G.dslots) + 1, bf_nblocks);")
         src.append("  }")
         src.append("}")
         return "\n".join(src) + "\n"

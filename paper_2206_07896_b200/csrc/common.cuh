@@ -64,10 +64,16 @@ __device__ __forceinline__ void mark_executed(const KDesc& d) {
 // its round trip overlaps the work; dev_fetch_take publishes it to the CTA.
 // Sub-range j of the fetches is [j*F/S, (j+1)*F/S); thread 0's cursor starts
 // on sub-range blockIdx.x % S and moves on when one is drained.
+// thread 0's claim state; the CTA's claim and block counts are flushed once,
+// at the end (dev_fetch_flush), not per claim: per-claim atomics on one
+// statistics word would serialise every CTA of a fine-grained launch
 struct FetchCursor {
   int sub, tried;
+  unsigned long long claims, blocks;
 };
-__device__ __forceinline__ FetchCursor dev_fetch_cursor() { return FetchCursor{(int)(blockIdx.x % kFetchSubs), 0}; }
+__device__ __forceinline__ FetchCursor dev_fetch_cursor() {
+  return FetchCursor{(int)(blockIdx.x % kFetchSubs), 0, 0ull, 0ull};
+}
 __device__ __forceinline__ long long dev_fetch_sub_start(const DevFetch& F, int j) {
   return (F.nfetch * j) / kFetchSubs;
 }
@@ -75,9 +81,9 @@ __device__ __forceinline__ long long dev_fetch_claim(const DevFetch& F, FetchCur
   while (c.tried < kFetchSubs) {
     const int j = c.sub;
     const long long lo = dev_fetch_sub_start(F, j), n = dev_fetch_sub_start(F, j + 1) - lo;
-    const long long f = (long long)(atomicAdd(F.cursor + j, 1ull) - F.base[j]);
+    const long long f = (long long)atomicAdd(F.cursor + j, 1ull);
     if (f < n) {
-      atomicAdd(F.stats + 2 * (blockIdx.x % F.slots), 1ull);
+      c.claims++;
       return lo + f;
     }
     c.sub = (j + 1) % kFetchSubs;
@@ -103,10 +109,17 @@ __device__ __forceinline__ void dev_fetch_range(const DevFetch& F, long long f, 
   b1 = b0 + F.grain < F.first + F.total ? b0 + F.grain : F.first + F.total;
 }
 // blocks [b0, b1) of a fetch ran: busy/executed counters (runtime.py:344-348)
-__device__ __forceinline__ void dev_fetch_done(const DevFetch& F, long long b0, long long b1) {
-  if (threadIdx.x == 0) atomicAdd(F.stats + 2 * (blockIdx.x % F.slots) + 1, (unsigned long long)(b1 - b0));
+__device__ __forceinline__ void dev_fetch_done(const DevFetch& F, FetchCursor& c, long long b0, long long b1) {
+  if (threadIdx.x == 0) c.blocks += (unsigned long long)(b1 - b0);
   if (F.executed)
     for (long long b = b0 + threadIdx.x; b < b1; b += blockDim.x) atomicAdd(F.executed + b, 1);
+}
+// the CTA's totals into its worker slot's statistics (call once, after the loop)
+__device__ __forceinline__ void dev_fetch_flush(const DevFetch& F, const FetchCursor& c) {
+  if (threadIdx.x == 0 && c.claims) {
+    atomicAdd(F.stats + 2 * (blockIdx.x % F.slots), c.claims);
+    atomicAdd(F.stats + 2 * (blockIdx.x % F.slots) + 1, c.blocks);
+  }
 }
 
 // i32 wrapping multiply-add, as `blockIdx.x * blockDim.x + threadIdx.x` is

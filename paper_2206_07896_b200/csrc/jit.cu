@@ -28,7 +28,6 @@ struct BfJitGeom {
   unsigned long long* dcur;
   unsigned long long* dstats;
   int* dexec;
-  unsigned long long dbase[8];
   long long nfetch, grain;
   int dslots;
 };
@@ -92,7 +91,6 @@ static int jit_launch(LaunchCtx& ctx) {
   g.dcur = nullptr;
   g.dstats = nullptr;
   g.dexec = nullptr;
-  for (int j = 0; j < 8; j++) g.dbase[j] = 0;
   g.nfetch = g.grain = 0;
   g.dslots = 1;
   int grid = (int)std::min<long long>(ctx.count, (long long)ctx.num_sms * 8);
@@ -101,8 +99,7 @@ static int jit_launch(LaunchCtx& ctx) {
     g.dcur = F.cursor;
     g.dstats = F.stats;
     g.dexec = F.executed;
-    static_assert(kFetchSubs == 8, "BfJitGeom carries 8 claim counters");
-    for (int j = 0; j < 8; j++) g.dbase[j] = F.base[j];
+    static_assert(kFetchSubs == 8, "codegen.py's bf_claim splits the fetches into 8 sub-ranges");
     g.nfetch = F.nfetch;
     g.grain = F.grain;
     g.dslots = F.slots;

@@ -448,8 +448,9 @@ __global__ void __launch_bounds__(256) hist_fetch(const int* __restrict__ pix, i
   extern __shared__ unsigned sh[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = (int)fm.d;
+  const int nwarps = blockDim.x >> 5;
   if (MODE == 0) {
-    for (int i = threadIdx.x; i < 8 * kHistLaneBins * 32; i += blockDim.x) sh[i] = 0;
+    for (int i = threadIdx.x; i < nwarps * kHistLaneBins * 32; i += blockDim.x) sh[i] = 0;
   } else if (MODE == 1) {
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
   }
@@ -470,9 +471,10 @@ __global__ void __launch_bounds__(256) hist_fetch(const int* __restrict__ pix, i
     for (long long i = vhi + threadIdx.x; i < hi; i += blockDim.x)
       hist_add<MODE, SAFE>(sh, mine, counts, lc, hist_bin<POW2>(pix[i], fm), 1u, bad);
     if (bad && bad_blk < 0) bad_blk = b0;
-    dev_fetch_done(F, b0, b1);
+    dev_fetch_done(F, fc, b0, b1);
     f = dev_fetch_take(nx);
   }
+  dev_fetch_flush(F, fc);
   if (bad) record_fault(k, BF_TRAP_OUT_OF_BOUNDS, bad_blk);
   if (MODE == 2) return;
   __syncthreads();
@@ -493,15 +495,20 @@ template <int MODE, bool POW2, bool SAFE>
 static int hist_fetch_go(LaunchCtx& ctx, size_t smem, const ArgVal& P, const ArgVal& Cn, long long n,
                          const FastMod& fm) {
   static bool attr[64] = {};
-  if ((smem > 48 * 1024) && first_on_device(attr)) {
-    cudaFuncSetAttribute(hist_fetch<MODE, POW2, SAFE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(hist_fetch<MODE, POW2, SAFE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaGetLastError();
   }
   const DevFetch& F = *ctx.dfetch;
+  // a CTA as wide as one fetch's int4 (32..256 threads); MODE 0 keeps one
+  // counter row per warp
+  const int threads =
+      (int)std::min<long long>(256, std::max<long long>(32, (F.grain * ctx.block[0] / 4 + 31) / 32 * 32));
+  if (MODE == 0) smem = (size_t)(threads / 32) * kHistLaneBins * 32 * sizeof(unsigned);
   const int grid = (int)std::min<long long>(
-      F.nfetch, (long long)resident_ctas((const void*)hist_fetch<MODE, POW2, SAFE>, 256, smem) * ctx.num_sms);
-  hist_fetch<MODE, POW2, SAFE><<<grid, 256, smem, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, n,
-                                                                ctx.block[0], fm, ctx.desc(), F);
+      F.nfetch, (long long)resident_ctas((const void*)hist_fetch<MODE, POW2, SAFE>, threads, smem) * ctx.num_sms);
+  hist_fetch<MODE, POW2, SAFE><<<grid, threads, smem, ctx.stream>>>((const int*)P.ptr, (int*)Cn.ptr, Cn.len, n,
+                                                                    ctx.block[0], fm, ctx.desc(), F);
   BF_CUDA_LAUNCH_CHECK(ctx);
   ctx.dfetch_grid = grid;
   return BF_OK;

@@ -66,9 +66,10 @@ __global__ void __launch_bounds__(256) vecadd_fetch(const float* a, const float*
       __stcs(c4 + i, make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w));
     }
     for (long long i = vhi + threadIdx.x; i < hi; i += blockDim.x) c[i] = a[i] + b[i];
-    dev_fetch_done(F, b0, b1);
+    dev_fetch_done(F, fc, b0, b1);
     f = dev_fetch_take(nx);
   }
+  dev_fetch_flush(F, fc);
 }
 
 static int launch_vecadd_fetch(LaunchCtx& ctx) {
@@ -83,9 +84,13 @@ static int launch_vecadd_fetch(LaunchCtx& ctx) {
   if ((long long)ctx.grid[1] * ctx.grid[2] * ctx.block[1] * ctx.block[2] != 1 || bx % 4 != 0 ||
       hi - 1 > (long long)INT_MAX || hi > std::min(A.len, std::min(B.len, C.len)))
     return BF_E_UNSUPPORTED;
-  const int grid = (int)std::min<long long>(F.nfetch, (long long)resident_ctas((const void*)vecadd_fetch, 256, 0) *
-                                                          ctx.num_sms);
-  vecadd_fetch<<<grid, 256, 0, ctx.stream>>>((const float*)A.ptr, (const float*)B.ptr, (float*)C.ptr, n, bx, F);
+  // a CTA as wide as one fetch's float4 (32..256 threads): fine grains get
+  // more, narrower CTAs, i.e. more fetches in flight per SM
+  const int threads = (int)std::min<long long>(256, std::max<long long>(32, (F.grain * bx / 4 + 31) / 32 * 32));
+  const int grid = (int)std::min<long long>(
+      F.nfetch, (long long)resident_ctas((const void*)vecadd_fetch, threads, 0) * ctx.num_sms);
+  vecadd_fetch<<<grid, threads, 0, ctx.stream>>>((const float*)A.ptr, (const float*)B.ptr, (float*)C.ptr, n, bx,
+                                                  F);
   BF_CUDA_LAUNCH_CHECK(ctx);
   ctx.dfetch_grid = grid;
   return BF_OK;

@@ -382,7 +382,6 @@ struct bf_runtime {
   // device-side fetching (BF_FLAG_DEVICE_FETCH): per worker a claim counter,
   // per worker slot (claims, blocks executed); host copy of the counters' bases
   unsigned long long* dfetch_dev = nullptr;  // [pool][kFetchSubs] counters, then [pool][2] stats
-  std::vector<unsigned long long> dfetch_base;
   bool dfetch_used = false;
   // counters
   int64_t blocks_executed = 0;
@@ -1029,7 +1028,6 @@ int bf_runtime_create(bf_arena* a, int32_t pool_size, uint32_t flags, double blo
       cudaGetLastError();
       return fail(BF_E_CUDA, "device fetch counters allocation failed");
     }
-    rt->dfetch_base.assign((size_t)pool_size * kFetchSubs, 0ull);
   }
   a->live_runtimes++;
   *out = rt;
@@ -1244,7 +1242,6 @@ static int launch_impl(bf_runtime* rt, const char* kernel, const int32_t grid[3]
     df.cursor = rt->dfetch_dev + (size_t)w * kFetchSubs;
     df.stats = rt->dfetch_dev + (size_t)rt->pool * kFetchSubs;
     df.slots = rt->pool;
-    for (int j = 0; j < kFetchSubs; j++) df.base[j] = rt->dfetch_base[(size_t)w * kFetchSubs + j];
     df.nfetch = nfetch;
     df.grain = grain;
     df.first = range_first;
@@ -1273,12 +1270,12 @@ static int launch_impl(bf_runtime* rt, const char* kernel, const int32_t grid[3]
     ctx.error = &err;
     ctx.user = ke->user;
     ctx.dfetch = &df;
+    // the worker's claim counters start at zero (ordered before the launch
+    // on its stream; the previous launch on this stream is done with them)
+    CK(cudaMemsetAsync(df.cursor, 0, sizeof(unsigned long long) * kFetchSubs, ctx.stream));
     int lrc = ke->launch(ctx);
     if (lrc == BF_OK && ctx.dfetch_grid > 0 && ht.kind == BF_TRAP_NONE) {
       rt->rr++;
-      for (int j = 0; j < kFetchSubs; j++)  // sub-range j's fetches + one failed claim per CTA
-        rt->dfetch_base[(size_t)w * kFetchSubs + j] +=
-            (unsigned long long)(nfetch * (j + 1) / kFetchSubs - nfetch * j / kFetchSubs + ctx.dfetch_grid);
       rt->dfetch_used = true;
       tr.fetches = nfetch;
       tr.cursor = total;
