@@ -475,6 +475,8 @@ def sample_instance(name: str, log_n: int):
                           [("buf", "x"), ("buf", "y"), ("buf", "w"), ("i32", 8), ("i32", m)], ["y"]), m * 256
     if name in ("kmeans", "kmeans_loop"):
         return I.kmeans(n, 32, 16, 256), n
+    if name == "nn_topk":
+        return I.nn_topk(n, 5, seed=1, d=I.nn_inputs(n, 1)[0::2] + 90.0), n
     if name == "bp_forward":
         return I.backprop_forward(n, seed=1), n
     if name == "bp_adjust":
@@ -485,7 +487,7 @@ def sample_instance(name: str, log_n: int):
 # bench-run sample sizes (log2): the C port, all host cores, ~0.5 s each
 PORT_LOG = {"vecadd": 24, "vecadd_pr1": 20, "nn": 22, "hist": 24, "hist_stride": 22, "reduce": 24,
             "wreduce": 24, "fir": 20, "kmeans": 16, "kmeans_loop": 16, "bp_forward": 18,
-            "bp_adjust": 18, "bfs": 22, "bfs_fused": 22, "bfs_do": 22, "hotspot": 22}
+            "bp_adjust": 18, "bfs": 22, "bfs_fused": 22, "bfs_do": 22, "hotspot": 22, "nn_topk": 22}
 # the reference runtime (pure Python): SURVEY §8d sizes for the study
 # (--workload cpu-runtime), and ~1 s samples for the default bench line
 REF_LOG_SURVEY = {"vecadd_pr1": 20, "vecadd": 20, "hotspot": 16, "kmeans": 10, "bfs": 14, "nn": 20,
@@ -493,7 +495,7 @@ REF_LOG_SURVEY = {"vecadd_pr1": 20, "vecadd": 20, "hotspot": 16, "kmeans": 10, "
                   "bp_forward": 12, "bp_adjust": 12}
 REF_LOG_BENCH = {"vecadd_pr1": 14, "vecadd": 14, "hotspot": 12, "kmeans": 7, "bfs": 11, "nn": 14,
                  "hist": 13, "hist_stride": 13, "reduce": 13, "wreduce": 13, "fir": 13,
-                 "bp_forward": 9, "bp_adjust": 9}
+                 "bp_forward": 9, "bp_adjust": 9, "nn_topk": 12}
 
 
 def cpu_sample(name: str, threads: int, budget: float = 0.5) -> Optional[dict]:
