@@ -59,15 +59,20 @@ struct BpChunk {
   }
 };
 
+// three buffers: the load of chunk n+1 goes into the buffer whose bulk store
+// left two chunks ago, so it waits for at most the older of the two stores
+// in flight (wait_group.read 1) instead of the last one
+constexpr int kBpStages = 3;
+
 __global__ void __launch_bounds__(256) bp_forward(const float* __restrict__ input, float* __restrict__ w,
                                                   float* __restrict__ partial, long long b0, long long b1) {
-  __shared__ __align__(16) float sm[2][kBpChunkF + 8];
-  __shared__ __align__(8) uint64_t full[2];
+  extern __shared__ __align__(16) float bp_dyn[];
+  float (*sm)[kBpChunkF + 8] = reinterpret_cast<float (*)[kBpChunkF + 8]>(bp_dyn);
+  __shared__ __align__(8) uint64_t full[kBpStages];
   const long long cstride = (long long)gridDim.x * kBpChunk;
   const long long first = b0 + (long long)blockIdx.x * kBpChunk;
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int i = 0; i < kBpStages; i++) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -80,11 +85,11 @@ __global__ void __launch_bounds__(256) bp_forward(const float* __restrict__ inpu
   if (threadIdx.x == 0 && first < b1) issue(first, 0);
   int n = 0;
   for (long long c0 = first; c0 < b1; c0 += cstride, n++) {
-    const int buf = n & 1;
+    const int buf = n % kBpStages;
     const BpChunk k(c0, b1);
     if (threadIdx.x == 0 && c0 + cstride < b1) {
-      bulk_wait_read<0>();  // the other buffer's bulk store has left shared memory
-      issue(c0 + cstride, buf ^ 1);
+      bulk_wait_read<1>();  // the store of chunk n-2 (the target buffer) has left shared memory
+      issue(c0 + cstride, (n + 1) % kBpStages);
     }
     float* Sa = sm[buf] + 4;             // a0 -> 16 B aligned
     const int sh = (int)(k.a0 - k.g0);   // 0..3 leading edge floats
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(256) bp_forward(const float* __restrict__ inpu
     const bool on = blk < k.nblk;  // whole warps stay converged for the shuffles
     const long long by = c0 + blk;
     const float node_mine = on ? __ldg(input + 16 * by + col + 1) : 0.f;
-    mbar_wait(&full[buf], (n >> 1) & 1);
+    mbar_wait(&full[buf], (n / kBpStages) & 1);
     __syncthreads();  // edge floats visible
     float* T = Sg + 272 * blk + col + 1;  // row 0 of the block, this column
     float p[16];
@@ -144,16 +149,16 @@ constexpr int kBpChunkAF = 272 * kBpChunkA;
 __global__ void __launch_bounds__(256) bp_adjust(const float* __restrict__ delta, const float* __restrict__ ly,
                                                  float* __restrict__ w, float* __restrict__ oldw, long long b0,
                                                  long long b1, bool bias) {
-  __shared__ __align__(16) float sw[2][kBpChunkAF + 8];
-  __shared__ __align__(16) float so[2][kBpChunkAF + 8];
-  __shared__ __align__(8) uint64_t full[2];
+  extern __shared__ __align__(16) float bp_dyn[];
+  float (*sw)[kBpChunkAF + 8] = reinterpret_cast<float (*)[kBpChunkAF + 8]>(bp_dyn);
+  float (*so)[kBpChunkAF + 8] = sw + kBpStages;
+  __shared__ __align__(8) uint64_t full[kBpStages];
   static_assert(kBpChunkA * 16 * 2 == 256, "two threads per weight row");
   double cx[8];  // 0.3 * delta[col] of this thread's eight columns
 #pragma unroll
   for (int j = 0; j < 8; j++) cx[j] = dmul(0.3, (double)__ldg(delta + 1 + 8 * (threadIdx.x & 1) + j));
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int i = 0; i < kBpStages; i++) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -178,10 +183,10 @@ __global__ void __launch_bounds__(256) bp_adjust(const float* __restrict__ delta
   if (threadIdx.x == 0 && first < b1) issue(first, 0);
   int n = 0;
   for (long long c0 = first; c0 < b1; c0 += cstride, n++) {
-    const int buf = n & 1;
+    const int buf = n % kBpStages;
     if (threadIdx.x == 0 && c0 + cstride < b1) {
-      bulk_wait_read<0>();
-      issue(c0 + cstride, buf ^ 1);
+      bulk_wait_read<1>();
+      issue(c0 + cstride, (n + 1) % kBpStages);
     }
     long long g0, g1, a0, a1;
     region(c0, g0, g1, a0, a1);
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(256) bp_adjust(const float* __restrict__ delta
       W[len - tl + threadIdx.x] = w[a1 + threadIdx.x];
       O[len - tl + threadIdx.x] = oldw[a1 + threadIdx.x];
     }
-    mbar_wait(&full[buf], (n >> 1) & 1);
+    mbar_wait(&full[buf], (n / kBpStages) & 1);
     __syncthreads();
     // two threads per row (columns 1-8 and 9-16): ly[row] is read and
     // converted once per 8 elements, 0.3*delta[col] stays in registers.
@@ -278,9 +283,15 @@ static int launch_bp_forward(LaunchCtx& ctx) {
     b1 = bad;
   }
   if (b0 >= b1) return BF_OK;
-  const int per_sm = resident_ctas((const void*)bp_forward, 256, 0);
+  const size_t smem = sizeof(float) * kBpStages * (kBpChunkF + 8);
+  static bool attr[64] = {};
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(bp_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaGetLastError();
+  }
+  const int per_sm = resident_ctas((const void*)bp_forward, 256, smem);
   const int grid = stream_grid(b1 - b0, kBpChunk, ctx.num_sms, per_sm);
-  bp_forward<<<grid, 256, 0, ctx.stream>>>((const float*)In.ptr, (float*)W.ptr, (float*)P.ptr, b0, b1);
+  bp_forward<<<grid, 256, smem, ctx.stream>>>((const float*)In.ptr, (float*)W.ptr, (float*)P.ptr, b0, b1);
   BF_CUDA_LAUNCH_CHECK(ctx);
   return BF_OK;
 }
@@ -303,10 +314,16 @@ static int launch_bp_adjust(LaunchCtx& ctx) {
   }
   if (b0 >= b1) return BF_OK;
   const bool bias = b0 == 0;
-  const int per_sm = resident_ctas((const void*)bp_adjust, 256, 0);
+  const size_t smem = sizeof(float) * 2 * kBpStages * (kBpChunkAF + 8);
+  static bool attr[64] = {};
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(bp_adjust, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaGetLastError();
+  }
+  const int per_sm = resident_ctas((const void*)bp_adjust, 256, smem);
   const int grid = stream_grid(b1 - b0, kBpChunkA, ctx.num_sms, per_sm);
-  bp_adjust<<<grid, 256, 0, ctx.stream>>>((const float*)D.ptr, (const float*)L.ptr, (float*)W.ptr, (float*)O.ptr,
-                                          b0, b1, bias);
+  bp_adjust<<<grid, 256, smem, ctx.stream>>>((const float*)D.ptr, (const float*)L.ptr, (float*)W.ptr,
+                                             (float*)O.ptr, b0, b1, bias);
   BF_CUDA_LAUNCH_CHECK(ctx);
   return BF_OK;
 }
