@@ -173,7 +173,7 @@ def build_cases(arena, torch, device, scale: int = 28) -> list:
         for i in range(taps):
             acc = acc + tfw[i].double() * tfx[i:i + k].double()
         return bool(torch.equal(tfy[:k], acc.float()))
-    cases.append(Case("fir", "fir_tile", 8 * n + 4 * (taps - 1), n, "output",
+    cases.append(Case("fir", "fir_reg<8>", 8 * n + 4 * (taps - 1), n, "output",
                       [(routines.get("fir"), Dim3(1), Dim3(256), 0, pk)], check=fir_check,
                       note="grid 1 x 256 threads, 8 taps"))
 
@@ -339,7 +339,7 @@ def bfs_case(arena, torch, device, log_v: int = 26, deg: int = 8) -> Case:
         saved["lvl"] = tl.clone()
         return ok
 
-    c = Case("bfs", "bfs_step", 4 * ne + 12 * nv, ne, "edge", [], host_loop=step, reset=reset,
+    c = Case("bfs", "bfs_scan2+bfs_relax_v+bfs_apply", 4 * ne + 12 * nv, ne, "edge", [], host_loop=step, reset=reset,
              check=check_and_save,
              note=f"2^{log_v} vertices x {deg} random out-edges, full traversal by per-level "
                   "launches (Rodinia host loop); bytes = compulsory 4|E| + 12|V|, elem = edges (TEPS)")
@@ -354,7 +354,7 @@ def bfs_case(arena, torch, device, log_v: int = 26, deg: int = 8) -> Case:
     def fused_check():
         return bool(torch.equal(tl, saved["lvl"])) if "lvl" in saved else check()
 
-    f = Case("bfs_fused", "bfs_expand_queue", 4 * ne + 12 * nv, ne, "edge", [], host_loop=fused,
+    f = Case("bfs_fused", "bfs_expand_v+bfs_compact8s", 4 * ne + 12 * nv, ne, "edge", [], host_loop=fused,
              check=fused_check,
              note="same graph, whole traversal fused on the device, top-down only (bf_bfs_levels: frontier "
                   "queues + L2-resident visited bitmap); levels equal to the per-level launches")
@@ -371,7 +371,7 @@ def bfs_case(arena, torch, device, log_v: int = 26, deg: int = 8) -> Case:
         levels["do_depth"] = graph.bfs_levels(rt, row, col, lvl, nv, 0, transposed=tg["t"])
         return 1
 
-    d = Case("bfs_do", "bfs_bottom_up", 4 * ne + 12 * nv, ne, "edge", [], host_loop=do_step,
+    d = Case("bfs_do", "bfs_expand_v+bfs_bottom_up", 4 * ne + 12 * nv, ne, "edge", [], host_loop=do_step,
              check=fused_check,
              note="same graph, direction-optimizing fused traversal (bf_bfs_levels_do: top-down on small "
                   "frontiers, bottom-up over the in-edge CSR on large ones, chosen on the device per level); "
