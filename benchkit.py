@@ -196,7 +196,7 @@ def build_cases(arena, torch, device, scale: int = 28) -> list:
     def km_reset():
         tks.zero_()
         tkn.zero_()
-    cases.append(Case("kmeans", "kmeans_tc<32>", npts * (4 * nf + 4), npts, "point",
+    cases.append(Case("kmeans", "kmeans_tg", npts * (4 * nf + 4), npts, "point",
                       [(routines.get("kmeans"), Dim3(npts // 256), Dim3(256), 0, pk)],
                       check=lambda: int(tkn.long().sum().item()) == npts, reset=km_reset,
                       note="16M x 32 f32, k=16: one assignment + accumulation pass; f64 distances"))
@@ -222,7 +222,7 @@ def build_cases(arena, torch, device, scale: int = 28) -> list:
         tkc2.copy_(tkc)
         if "drv" in state:
             arena.fill_value(state["drv"].prev, -1)
-    cases.append(Case("kmeans_loop", "kmeans_tc<32>+kmeans_update", passes * npts * (4 * nf + 4), passes * npts, "point",
+    cases.append(Case("kmeans_loop", "kmeans_tg+kmeans_update", passes * npts * (4 * nf + 4), passes * npts, "point",
                       [], host_loop=km_loop, reset=km_loop_reset,
                       check=lambda: bool(torch.isfinite(tkc2).all().item()),
                       note=f"Rodinia kmeans host loop, {passes} passes (assignment + centroid update + delta "

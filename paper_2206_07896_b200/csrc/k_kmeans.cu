@@ -14,7 +14,9 @@
 // of one feature are coalesced; each thread keeps its point's <= 32 features
 // in registers; centroids live in shared memory as doubles (broadcast reads).
 // Bound: FP64 (3 DP ops per point x cluster x feature), see DESIGN.md.
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include <climits>
 
@@ -872,11 +874,562 @@ static size_t kmeans_tc_smem() {
          sizeof(float) * (16 * NF + 16 + 16 * NF) + sizeof(int) * 16 + sizeof(uint4) * (NF / 8) * 64;
 }
 
+// ---------------------------------------------------------------------------
+// kmeans_tg: the same screen on the tcgen05 tensor cores (nf = 32, k <= 16).
+//
+// The fp32 tiles cannot feed tcgen05 as they are: kind::tf32 reads K-major
+// operands only (scripts/micro/umma_sw128.cu) and the tiles are feature-major.
+// Split into bf16 hi / lo planes instead (x = hi + lo + r, hi = RN_bf16(x),
+// lo = RN_bf16(x - hi), |r| <= 2^-16 |x|), the planes ARE legal operands in the
+// tiles' own [feature][point] order for both contractions
+// (scripts/micro/umma_bf16.cu checks every layout below on the device):
+//   distance  D[p][c'] = sum_l F[p][l] B[c'][l], M = 128 points, K = 32:
+//             A = the planes read MN-major (SWIZZLE_128B atoms of 8 features x
+//             64 points); B = the centroid rows (hi 0..15, lo 16..31) K-major.
+//             MMA 1: A = F_hi, N = 32 (hi.hi -> cols 0..15, hi.lo -> 16..31);
+//             MMA 2: A = F_lo, B = C_hi, N = 16, accumulated into cols 16..31.
+//   sums      S[r][c] = sum_p P[r][p] onehot[c][p], M = 64 (rows: the 32 hi
+//             features, then the 32 lo), K = 128 points, N = 16: A = the same
+//             planes read K-major, B = the one-hot [cluster][point] tile the
+//             epilogue writes.  S lives in TMEM for the whole kernel.
+// Screen bound with S = sum_l |f_l c_l| <= |f| cmax: the split residue (lo.lo,
+// r_f c, f r_c) <= 3.02 2^-16 S; the tensor-core accumulation of the exact
+// bf16 products (2 MMAs of K = 16 per accumulator) <= 2 x 17 x 2^-23 S; times
+// 2 for s = |c|^2 - 2 f.c: |s(tg) - s| < 2^-13.17 S + 2^-19 |c|^2 (f32 |c|^2)
+// + 2^-23 (S + |c|^2) (epilogue adds).  Used with (>= 2.2x slack)
+//   E = 2^-12 |f| cmax (1.01) + 2^-17 cmax^2 + 2^-40 |f|^2 + 2^-100 cmax + 1e-35
+// (the last two: flushed subnormal bf16 inputs / products).  Points with
+// several candidates get the f32 difference-form distance of each candidate
+// (the warp's lanes over the features, from global memory: L2 hits) and, if
+// that leaves several, the exact f64 recurrence.  Features with |x| > 3e38 or non-finite
+// are zeroed in the planes (0 x NaN would poison every cluster's sums) and
+// added to the sums on the scalar path; their points take the exact scan.
+//
+// Warp roles (448 threads, one CTA per SM, persistent over the tiles):
+//   warps 0-3  split: fp32 tile -> bf16 planes + per-point |f|^2 (features
+//              0-15 in warps 0-1, 16-31 in warps 2-3; two points per thread)
+//   warps 4-11 epilogue, two sets of 4 alternating tiles: TMEM lane = point;
+//              screen, re-check, member, counts, the one-hot tile
+//   warp 12    producer: one 2D tensor copy {128 points x 32 features} per tile
+//   warp 13    MMA issuer (one thread) and TMEM owner
+// Rings: 4 fp32 tiles (released by the split), 6 plane / one-hot stages (3
+// pairs), 6 TMEM accumulators of 32 columns (+ 32 columns of sums): the
+// distances run two tiles ahead of the screen, the split further ahead.
+namespace tg {
+constexpr int kPts = 128;
+constexpr int kNF = 32;
+#ifndef KM_TG_ST
+#define KM_TG_ST 4
+#endif
+constexpr int kST = KM_TG_ST;  // fp32 tiles (released by the split)
+#ifndef KM_TG_SP
+#define KM_TG_SP 6
+#endif
+constexpr int kSP = KM_TG_SP;  // planes / one-hot / accumulators (pairs)
+constexpr int kThreads = 448;  // 4 split + 8 epilogue + producer + MMA warps
+constexpr int kWProd = 12, kWMma = 13;
+constexpr uint32_t kTileB = kNF * kPts * 4;  // 16 KB
+constexpr uint32_t kPlaneB = 16384;          // hi + lo planes of a tile
+constexpr uint32_t kOneHotB = 4096;
+constexpr uint32_t kOffPlanes = kST * kTileB;
+constexpr uint32_t kOffOneHot = kOffPlanes + kSP * kPlaneB;
+constexpr uint32_t kOffCent = kOffOneHot + kSP * kOneHotB;
+constexpr uint32_t kOffNrm = kOffCent + 4096;               // [kSP][2][128] f32
+constexpr uint32_t kOffCf = kOffNrm + kSP * 2 * kPts * 4;   // [16][32] f32 centroids
+constexpr uint32_t kOffSsx = kOffCf + 16 * kNF * 4;         // [16][32] scalar-path sums
+constexpr uint32_t kOffCnt = kOffSsx + 16 * kNF * 4;        // [16] counts
+constexpr uint32_t kOffBar = kOffCnt + 16 * 4;              // mbarriers
+constexpr int kNBar = 2 * kST + 5 * kSP + 1;
+constexpr uint32_t kSmem = kOffBar + kNBar * 8 + 16 + 1024;  // + TMEM slot, + alignment slack
+static_assert(kSmem <= 227 * 1024, "kmeans_tg shared memory");
+static_assert(32 * kSP + 32 <= 256, "kmeans_tg TMEM columns");
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kSumsCol = 32 * kSP;  // 32 columns (M = 128: two stage parities)
+static_assert(kSP % 2 == 0, "stages are used in pairs");
+
+// byte offset of (row r, element q) in a SWIZZLE_128B atom of 8 rows x 64 bf16
+__device__ __forceinline__ uint32_t sw128(int r, int q) {
+  return (uint32_t)(r * 128 + ((((q >> 3) ^ r) & 7) << 4) + (q & 7) * 2);
+}
+// Stages come in pairs (2q, 2q + 1) laid out so that one M = 128 sums MMA
+// reads both tiles' planes: pair buffer = [point half][stage parity][plane
+// P][feature group] of 1 KB atoms; stage_planes(b) is the stage's base.
+// planes of a tile: plane P (0 hi, 1 lo), feature l, point p (from the stage base)
+__device__ __forceinline__ uint32_t plane_off(int P, int l, int p) {
+  return (uint32_t)((p >> 6) * 16384 + (P * 4 + (l >> 3)) * 1024) + sw128(l & 7, p & 63);
+}
+__device__ __forceinline__ uint32_t stage_planes(int b) { return kOffPlanes + (b >> 1) * 32768 + (b & 1) * 8192; }
+__device__ __forceinline__ uint32_t cent_off(int R, int l) { return (uint32_t)((R >> 3) * 1024) + sw128(R & 7, l); }
+// one-hot pair buffer: [point half][cluster row c' = 16 (b & 1) + c] (K-major, 32 rows)
+__device__ __forceinline__ uint32_t onehot_off(int c, int p) {
+  return (uint32_t)((p >> 6) * 4096 + (c >> 3) * 1024) + sw128(c & 7, p & 63);
+}
+__device__ __forceinline__ uint32_t stage_onehot(int b) { return kOffOneHot + (b >> 1) * 8192 + (b & 1) * 2048; }
+__device__ __forceinline__ uint64_t sdesc(uint32_t a, uint32_t lbo, uint32_t sbo) {  // SWIZZLE_128B, sm100
+  return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32
+__host__ __device__ constexpr uint32_t idesc(int M, int N, bool amn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((amn ? 1u : 0u) << 15) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+// issued by the whole (converged) warp: one elected lane executes, so the
+// operands stay warp-uniform (uniform registers, no per-lane issue loop)
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+// 32 lanes x 32 columns of f32 (thread i <- lane base + i)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+}
+
+// the reference recurrences over a point's features in global memory (rare
+// path; the lines were streamed through L2 a few microseconds earlier)
+__device__ __noinline__ int exact_g(const float* fp, long long stride, const float* cf, int k) {
+  double bestd = 0.0;
+  int best = 0;
+  for (int c = 0; c < k; c++) {
+    double dist = 0.0;
+    for (int l = 0; l < kNF; l++) {
+      const double diff = dsub((double)fp[l * stride], (double)cf[c * kNF + l]);
+      dist = dadd(dist, dmul(diff, diff));
+    }
+    if (c == 0 || dist < bestd) {
+      bestd = dist;
+      best = c;
+    }
+  }
+  return best;
+}
+// the exact f64 recurrence over the clusters of `mask`, ascending, first
+// strict minimum (the reference's scan restricted to the survivors)
+__device__ __noinline__ int exact_mask_g(const float* fp, long long stride, const float* cf, unsigned mask) {
+  double bd = 0.0;
+  int bi = -1;
+  for (unsigned r = mask; r; r &= r - 1) {
+    const int c = __ffs(r) - 1;
+    double dist = 0.0;
+    for (int l = 0; l < kNF; l++) {
+      const double diff = dsub((double)fp[l * stride], (double)cf[c * kNF + l]);
+      dist = dadd(dist, dmul(diff, diff));
+    }
+    if (bi < 0 || dist < bd) {
+      bd = dist;
+      bi = c;
+    }
+  }
+  return bi;
+}
+#ifdef KM_TG_TRACE
+// per-tile event times of CTA 0 (ns, %globaltimer): [event][tile]
+__device__ unsigned long long g_trace[12][2048];
+__device__ __forceinline__ void trace(int ev, int n) {
+  if (blockIdx.x == 0 && n < 2048) {
+    unsigned long long t;
+    t = clock64();
+    g_trace[ev][n] = t;
+  }
+}
+#else
+__device__ __forceinline__ void trace(int, int) {}
+#endif
+}  // namespace tg
+
+#ifdef KM_TG_TRACE
+extern "C" int bf_debug_tg_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, tg::g_trace, sizeof(tg::g_trace));
+}
+#endif
+
+__global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_constant__ CUtensorMap tmap,
+                                                            const float* __restrict__ f,
+                                                            const float* __restrict__ cent,
+                                                            int* __restrict__ member, float* sums, int* counts,
+                                                            int npts, int k, long long lo, long long hi) {
+  using namespace tg;
+  extern __shared__ __align__(16) unsigned char tg_raw[];
+  // 1 KB-aligned (SWIZZLE_128B atoms); pointer arithmetic keeps the shared window
+  unsigned char* sm = tg_raw + ((1024u - (smem_u32(tg_raw) & 1023u)) & 1023u);
+  float* nrm = reinterpret_cast<float*>(sm + kOffNrm);
+  float* cf = reinterpret_cast<float*>(sm + kOffCf);
+  float* ssx = reinterpret_cast<float*>(sm + kOffSsx);
+  int* cnt = reinterpret_cast<int*>(sm + kOffCnt);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar);
+  uint64_t* full_t = bars;                  // [kST] producer -> split (tx bytes)
+  uint64_t* empty_t = full_t + kST;         // [kST] epilogue (4 warps) -> producer
+  uint64_t* full_p = empty_t + kST;         // [kSP] split (4 warps) -> MMA
+  uint64_t* empty_p = full_p + kSP;         // [kSP] sums MMA commit -> split
+  uint64_t* oh_full = empty_p + kSP;        // [kSP] epilogue (4 warps) -> MMA
+  uint64_t* acc_full = oh_full + kSP;       // [kSP] distance MMA commit -> epilogue
+  uint64_t* acc_empty = acc_full + kSP;     // [kSP] epilogue (4 warps) -> MMA
+  uint64_t* fin = acc_empty + kSP;          // last sums MMA commit -> epilogue
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(fin + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- setup: barriers, TMEM, centroids (f32, and the bf16 hi / lo rows)
+  if (tid == 0) {
+    for (int s = 0; s < kST; s++) {
+      mbar_init(&full_t[s], 1);
+      mbar_init(&empty_t[s], 4);
+    }
+    for (int b = 0; b < kSP; b++) {
+      mbar_init(&full_p[b], 4);
+      mbar_init(&empty_p[b], 1);
+      mbar_init(&oh_full[b], 4);
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == kWMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = tid; i < 16 * kNF; i += blockDim.x) {
+    cf[i] = i < k * kNF ? cent[i] : 0.f;
+    ssx[i] = 0.f;
+  }
+  if (tid < 16) cnt[tid] = 0;
+  for (int i = tid; i < 32 * 64; i += blockDim.x) {  // 32 rows x 64 bf16 (features 32..63 zero)
+    const int R = i >> 6, q = i & 63, c = R & 15;
+    float v = 0.f;
+    if (q < kNF && c < k) {
+      const float x = cent[c * kNF + q];
+      const float h = __bfloat162float(__float2bfloat16_rn(x));
+      v = R < 16 ? h : x - h;
+    }
+    *reinterpret_cast<__nv_bfloat16*>(sm + kOffCent + cent_off(R, q)) = __float2bfloat16_rn(v);
+  }
+  fence_proxy_async();
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const long long ntile = (hi - lo + kPts - 1) / kPts;
+  const int nmine = ntile > blockIdx.x ? (int)((ntile - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+
+  if (warp == kWProd) {  // ---- producer: one 2D tensor copy {128 points x 32 features} per tile
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+      for (int n = 0; n < nmine; n++) {
+        const int s = n % kST;
+        if (n >= kST) mbar_wait_sleep(&empty_t[s], ((n / kST) - 1) & 1);
+        const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
+        trace(0, n);
+        // the box is always written in full (zeros past npts; columns past hi
+        // are zeroed by the split)
+        mbar_arrive_expect_tx(&full_t[s], kTileB);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(sm + s * kTileB)),
+            "l"(&tmap), "r"((int)p0), "r"(0), "r"(smem_u32(&full_t[s]))
+            : "memory");
+      }
+    }
+  } else if (warp == kWMma) {  // ---- MMA issuer (the whole warp; one elected lane issues)
+    {
+      const uint32_t sCent = smem_u32(sm + kOffCent);
+      const uint32_t idD32 = idesc(128, 32, true), idD16 = idesc(128, 16, true);
+      const uint32_t idS2 = idesc(128, 32, false), idS1 = idesc(128, 16, false);
+      // distances of tile n, then the sums of tile n - kLag: the distances run
+      // kLag tiles ahead of the epilogue (blocking waits wake on the phase flip)
+      constexpr int kLag = 2;
+      for (int n = 0; n < nmine + kLag; n++) {
+        if (n < nmine) {
+          const int b = n % kSP;
+          mbar_wait(&full_p[b], (n / kSP) & 1);
+          if (lane == 0) trace(8, n);
+          if (n >= kSP) mbar_wait(&acc_empty[b], ((n / kSP) - 1) & 1);
+          if (lane == 0) trace(9, n);
+          __syncwarp();  // elect.sync below needs the converged warp
+          tc_after();
+          const uint32_t sP = smem_u32(sm + stage_planes(b)), d = tmem + b * 32;
+#pragma unroll
+          for (int kk = 0; kk < 2; kk++)
+            umma(d, sdesc(sP + kk * 2048, 16384, 1024), sdesc(sCent + kk * 32, 16, 1024), idD32, kk);
+#pragma unroll
+          for (int kk = 0; kk < 2; kk++)
+            umma(d + 16, sdesc(sP + 4096 + kk * 2048, 16384, 1024), sdesc(sCent + kk * 32, 16, 1024), idD16, 1);
+          umma_commit(&acc_full[b]);
+          if (lane == 0) trace(4, n);
+          __syncwarp();
+        }
+        // centroid sums of the tile pair (ms - 1, ms) (ms odd), or of a last
+        // lone even tile: M = 128 rows = both tiles' hi / lo feature rows,
+        // N = 32 = both one-hots (the cross blocks of D are never read)
+        const int ms = n - kLag;
+        if (ms >= 0 && ms < nmine && ((ms & 1) || ms == nmine - 1)) {
+          const int m0 = ms & ~1, b0 = m0 % kSP;
+          const bool pair = ms & 1;
+          mbar_wait(&oh_full[b0], (m0 / kSP) & 1);
+          if (pair) mbar_wait(&oh_full[b0 + 1], (ms / kSP) & 1);
+          if (lane == 0) trace(10, ms);
+          __syncwarp();
+          tc_after();
+          const uint32_t sP = smem_u32(sm + stage_planes(b0)), sO = smem_u32(sm + stage_onehot(b0));
+#pragma unroll
+          for (int ph = 0; ph < 2; ph++)
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++)
+              umma(tmem + kSumsCol, sdesc(sP + ph * 16384 + kk * 32, 16, 1024), sdesc(sO + ph * 4096 + kk * 32, 16, 1024),
+                   pair ? idS2 : idS1, (m0 > 0 || ph > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty_p[b0]);
+          if (pair) umma_commit(&empty_p[b0 + 1]);
+          if (lane == 0) trace(7, ms);
+          __syncwarp();
+          if (ms == nmine - 1) umma_commit(fin);
+        }
+      }
+    }
+  } else if (warp < 4) {  // ---- split: fp32 tile -> bf16 planes, |f|^2 partials
+    const int st = tid, half = st >> 6, pr = st & 63, p = 2 * pr;
+    for (int n = 0; n < nmine; n++) {
+      const int s = n % kST, b = n % kSP;
+      mbar_wait(&full_t[s], (n / kST) & 1);
+      if (st == 0) trace(1, n);
+      if (n >= kSP) mbar_wait(&empty_p[b], ((n / kSP) - 1) & 1);
+      if (st == 0) trace(2, n);
+      const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
+      const int cntp = (int)min((long long)kPts, hi - p0);
+      const float* T = reinterpret_cast<const float*>(sm + s * kTileB);
+      unsigned char* P = sm + stage_planes(b);
+      const bool v0 = p < cntp, v1 = p + 1 < cntp;
+      float n0 = 0.f, n1 = 0.f;
+      float2 xs[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) xs[j] = *reinterpret_cast<const float2*>(T + (16 * half + j) * kPts + p);
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        xs[j].x = v0 ? xs[j].x : 0.f;  // columns past hi: other ranges' points (or zeros)
+        xs[j].y = v1 ? xs[j].y : 0.f;
+        n0 = fmaf(xs[j].x, xs[j].x, n0);
+        n1 = fmaf(xs[j].y, xs[j].y, n1);
+      }
+      // finite norms <= 3e38: every |x| <= 2e19, nothing to drop (the common case)
+      if (!__all_sync(0xffffffffu, n0 <= 3.0e38f && n1 <= 3.0e38f)) {
+#pragma unroll
+        for (int j = 0; j < 16; j++) {  // scalar path (and the exact scan: the norm is not finite)
+          if (!(fabsf(xs[j].x) <= 3.0e38f)) xs[j].x = 0.f;
+          if (!(fabsf(xs[j].y) <= 3.0e38f)) xs[j].y = 0.f;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const int l = 16 * half + j;
+        const float2 x = xs[j];
+        const __nv_bfloat162 h = __floats2bfloat162_rn(x.x, x.y);
+        const __nv_bfloat162 r = __floats2bfloat162_rn(x.x - __low2float(h), x.y - __high2float(h));
+        *reinterpret_cast<__nv_bfloat162*>(P + plane_off(0, l, p)) = h;
+        *reinterpret_cast<__nv_bfloat162*>(P + plane_off(1, l, p)) = r;
+      }
+      *reinterpret_cast<float2*>(nrm + (b * 2 + half) * kPts + p) = make_float2(n0, n1);
+      fence_proxy_async();  // the planes are read by the tensor cores (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&full_p[b]);
+        mbar_arrive(&empty_t[s]);
+      }
+      if (st == 0) trace(3, n);
+    }
+  } else {  // ---- epilogue: two sets of 4 warps (even / odd tiles); TMEM lanes 32 (warp % 4) + lane
+    const int ew = warp & 3, m = 32 * ew + lane, set = (warp - 4) >> 2;
+    float cn[16];
+    float cmax2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      float n2 = 0.f;
+      for (int l = 0; l < kNF; l++) n2 = fmaf(cf[c * kNF + l], cf[c * kNF + l], n2);
+      cn[c] = c < k ? n2 : __int_as_float(0x7fffffff);  // NaN: never a candidate, ignored by fminf
+      if (c < k) cmax2 = fmaxf(cmax2, n2);
+    }
+    const float cmax = sqrtf(cmax2) * 1.001f;
+    const float eA = 2.44140625e-4f * 1.01f * cmax;  // 2^-12 x |f| (rsqrt approximation + 1 %)
+    const float eB = 7.62939453125e-06f * cmax * cmax + 7.8886e-31f * cmax + 1e-35f;  // 2^-17 cmax^2, 2^-100 cmax
+    for (int n = set; n < nmine; n += 2) {
+      const int b = n % kSP;
+      const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
+      const int cntp = (int)min((long long)kPts, hi - p0);
+      // full_p as well: orders the split's |f|^2 stores before the loads below
+      // (the split cannot complete tile n + kSP before this tile's one-hot exists)
+      mbar_wait(&full_p[b], (n / kSP) & 1);
+      mbar_wait(&acc_full[b], (n / kSP) & 1);
+      if (m == 0) trace(5, n);
+      tc_after();
+      float d[32];
+      tmem_ld32(tmem + b * 32 + ((uint32_t)(32 * ew) << 16), d);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      const float nr = nrm[(b * 2) * kPts + m] + nrm[(b * 2 + 1) * kPts + m];
+      const float E = fmaf(eA, nr * rsqrtf(nr + 1e-30f), eB) + 9.2e-13f * nr;
+      float tv[16];
+      float mn = INFINITY;
+#pragma unroll
+      for (int c = 0; c < 16; c++) {
+        tv[c] = fmaf(-2.f, d[c] + d[16 + c], cn[c]);
+        mn = fminf(mn, tv[c]);
+      }
+      const float thr = mn + 2.f * E;
+      unsigned cand = 0;
+#pragma unroll
+      for (int c = 0; c < 16; c++) cand |= (tv[c] <= thr ? 1u : 0u) << c;
+      const bool ok = m < cntp;
+      const bool fin_ = nr <= 3.0e38f && cand != 0;
+      int best = __ffs(cand) - 1;
+      const float* fg = f + p0 + 32 * ew;  // the warp's points in global memory
+      // near-ties: the candidates' f32 distances in the difference form, one
+      // point at a time with the warp's lanes over the features (a tree sum:
+      // |d32 - d| <= (nf + 4) 2^-24 d in any order); one survivor decides,
+      // several (true ties) take the f64 recurrence on the point's lane
+      unsigned tie = __ballot_sync(0xffffffffu, ok && fin_ && (cand & (cand - 1)));
+      while (tie) {
+        // up to 4 tie points per round: their features are loaded together
+        int srcs[4];
+        float xs[4];
+        int nq = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (tie) {
+            srcs[q] = __ffs(tie) - 1;
+            tie &= tie - 1;
+            xs[q] = __ldg(fg + (long long)lane * npts + srcs[q]);
+            nq = q + 1;
+          }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+        if (q >= nq) break;
+        const int src = srcs[q];
+        const float x = xs[q];
+        const unsigned cs = __shfl_sync(0xffffffffu, cand, src);
+        const float e2 = (float)(kNF + 4) * 5.9604645e-08f * 1.01f;
+        float myd = INFINITY, u2 = INFINITY;
+        for (unsigned r = cs; r; r &= r - 1) {
+          const int c = __ffs(r) - 1;
+          const float dl = __fsub_rn(x, cf[c * kNF + lane]);
+          float v = __fmul_rn(dl, dl);
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+          if (lane == c) myd = v;
+          u2 = fminf(u2, fmaf(v, e2, v) + 1e-40f);
+        }
+        const unsigned sv = __ballot_sync(0xffffffffu, ((cs >> lane) & 1) && !(fmaf(-myd, e2, myd) - 1e-40f > u2));
+        if (lane == src) best = (sv & (sv - 1)) ? exact_mask_g(fg + lane, npts, cf, sv) : __ffs(sv) - 1;
+        }
+      }
+      if (ok && !fin_) best = exact_g(fg + lane, npts, cf, k);
+      unsigned char* O = sm + stage_onehot(b);
+      {  // zero this warp's 32 one-hot columns (16 rows x 64 B), then set the ones
+        const int i0 = 2 * lane;
+#pragma unroll
+        for (int i = i0; i < i0 + 2; i++) {
+          const int c = i >> 2, jj = i & 3;
+          *reinterpret_cast<uint4*>(O + onehot_off(c, 32 * ew + 8 * jj)) = make_uint4(0, 0, 0, 0);
+        }
+      }
+      __syncwarp();
+      if (ok) {
+        member[p0 + m] = best;
+        atomicAdd(cnt + best, 1);
+        *reinterpret_cast<unsigned short*>(O + onehot_off(best, m)) = 0x3F80;  // bf16 1.0
+        if (!(nr <= 3.0e38f)) {  // features the planes dropped
+          for (int l = 0; l < kNF; l++) {
+            const float x = fg[(long long)l * npts + lane];
+            if (!(fabsf(x) <= 3.0e38f)) atomicAdd(ssx + best * kNF + l, x);
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&oh_full[b]);
+      if (m == 0) trace(6, n);
+        }
+    if (nmine > 0 && set == 0) {  // the sums accumulator: lane r = 64 parity + 32 P + feature
+      mbar_wait(fin, 0);
+      tc_after();
+      float v[16];
+      // rows 0..63 (even stages) x cols 0..15, rows 64..127 (odd stages) x cols 16..31
+      tmem_ld16(tmem + kSumsCol + (ew >= 2 ? 16u : 0u) + ((uint32_t)(32 * ew) << 16), v);
+      if (ew < 2 || nmine >= 2) {  // odd-stage rows exist (and were initialised) only with two tiles
+#pragma unroll
+        for (int c = 0; c < 16; c++)
+          if (c < k && v[c] != 0.f) atomicAdd(sums + c * kNF + lane, v[c]);
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  for (int i = tid; i < k * kNF; i += blockDim.x)
+    if (ssx[i] != 0.f) atomicAdd(sums + i, ssx[i]);
+  for (int i = tid; i < k; i += blockDim.x)
+    if (cnt[i]) atomicAdd(counts + i, cnt[i]);
+  if (warp == kWMma) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// 2D tensor map over the feature-major points: dims {npts, 32}, box {128, 32}
+static bool kmeans_tile_map(CUtensorMap* m, const void* f, long long npts) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  if (!enc || npts > INT_MAX || ((uintptr_t)f & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)npts, (cuuint64_t)tg::kNF};
+  cuuint64_t strides[1] = {(cuuint64_t)npts * 4};
+  cuuint32_t box[2] = {(cuuint32_t)tg::kPts, (cuuint32_t)tg::kNF}, es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(f), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int kmeans_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BF_KMEANS_V");
-    v = e ? atoi(e) : 4;  // 4: kmeans_tc; 2/3: kmeans_rb; 1: kmeans_fast
+    v = e ? atoi(e) : 5;  // 5: kmeans_tg (nf = 32, else as 4); 4: kmeans_tc; 2/3: kmeans_rb; 1: kmeans_fast
   }
   return v;
 }
@@ -911,6 +1464,23 @@ static int launch_kmeans(LaunchCtx& ctx) {
     if (!ok) {
       ctx.host_trap(BF_TRAP_OUT_OF_BOUNDS, ctx.first_block_with_x(xi.first), "kmeans index out of range");
       continue;
+    }
+    CUtensorMap tmap;
+    if (kmeans_variant() >= 5 && nf == 32 && k >= 2 && k <= 16 && npts % 4 == 0 && lo % 4 == 0 && hi - lo >= 4 &&
+        kmeans_tile_map(&tmap, F.ptr, npts)) {
+      const long long main_hi = lo + (hi - lo) / 4 * 4;
+      static bool attr[64] = {};
+      if (first_on_device(attr)) {
+        cudaFuncSetAttribute(kmeans_tg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tg::kSmem);
+        cudaGetLastError();
+      }
+      const int grid = stream_grid(main_hi - lo, tg::kPts, ctx.num_sms, 1);
+      kmeans_tg<<<grid, tg::kThreads, tg::kSmem, ctx.stream>>>(tmap, (const float*)F.ptr, (const float*)Ce.ptr,
+                                                               (int*)M.ptr, (float*)S.ptr, (int*)Cn.ptr, (int)npts,
+                                                               k, lo, main_hi);
+      BF_CUDA_LAUNCH_CHECK(ctx);
+      if (main_hi == hi) continue;
+      lo = main_hi;  // < 4 trailing points: register-blocked path below
     }
     if (kmeans_variant() >= 4 && (nf == 32 || nf == 16 || nf == 24 || nf == 8) && k >= 2 && k <= 16 &&
         npts % 4 == 0 && lo % 4 == 0 && hi - lo >= 4) {

@@ -605,12 +605,22 @@ cases = [I.kmeans(3000, 32, 16, 256, seed=11), I.kmeans(999, 16, 16, 96, seed=14
          I.kmeans(4096, 32, 16, 256, seed=16, dup=True), I.kmeans(3001, 32, 7, 256, seed=19, dup=True),
          I.kmeans(20000, 32, 16, 256, seed=21), I.kmeans(1024, 16, 5, 128, seed=22)]
 edge = I.kmeans(2048, 32, 16, 256, seed=20)
+c = np.asarray(edge.buffer("cent").values).copy()
+c[2 * 32:3 * 32] = c[:32]
+c[2 * 32 + 5] = np.nextafter(c[5], np.float32(2))
+c[3 * 32:4 * 32] = c[32:64]
+c[3 * 32 + 31] = np.nextafter(c[32 + 31], np.float32(-2))
+edge.buffer("cent").values = c
 fe = np.asarray(edge.buffer("f").values).copy().reshape(32, 2048)
 fe[3, 7] = np.nan
+fe[0, 9] = np.inf
 fe[:, 11] = np.float32(3e38)
+fe[:, 13] = c[:32]
 fe[:, 100:140] *= np.float32(1e-30)
 edge.buffer("f").values = fe.reshape(-1)
 cases.append(edge)
+for nf in (8, 16, 24):
+    cases.append(I.kmeans(2052, nf, 9, 128, seed=30 + nf, dup=True))
 for k, inst in enumerate(cases):
     want, _ = oracle.run(inst)
     got, trap, _, _ = gpu_run(inst)
@@ -625,12 +635,13 @@ print("ok", len(cases))
 """
 
 
-@pytest.mark.parametrize("variant", [2, 3])
-def test_kmeans_opt_in_variants_vs_oracle(variant):
-    """The register-blocked FFMA screen (kmeans_rb, the fallback for shapes
-    kmeans_tc does not take; BF_KMEANS_V=2/3 forces it with two / one CTAs per
-    SM) stays bit-exact in membership; run in a subprocess because the variant
-    is read once when the library loads."""
+@pytest.mark.parametrize("variant", [2, 3, 4, 5])
+def test_kmeans_variants_vs_oracle(variant):
+    """Every kmeans screen stays bit-exact in membership: the register-blocked
+    FFMA screen (kmeans_rb, the fallback for shapes the tensor-core kernel does
+    not take; BF_KMEANS_V=2/3 with two / one CTAs per SM) and kmeans_tc (4);
+    run in a subprocess because the variant is read once when the library
+    loads."""
     import os
     import subprocess
     import sys
