@@ -888,10 +888,16 @@ static size_t kmeans_tc_smem() {
 //             64 points); B = the centroid rows (hi 0..15, lo 16..31) K-major.
 //             MMA 1: A = F_hi, N = 32 (hi.hi -> cols 0..15, hi.lo -> 16..31);
 //             MMA 2: A = F_lo, B = C_hi, N = 16, accumulated into cols 16..31.
-//   sums      S[r][c] = sum_p P[r][p] onehot[c][p], M = 64 (rows: the 32 hi
-//             features, then the 32 lo), K = 128 points, N = 16: A = the same
-//             planes read K-major, B = the one-hot [cluster][point] tile the
-//             epilogue writes.  S lives in TMEM for the whole kernel.
+//   sums      S[r][c] = sum_p P[r][p] onehot[c][p] over a PAIR of tiles:
+//             M = 128 rows (tile 2q: 32 hi + 32 lo feature rows, tile 2q+1
+//             the same), K = 128 points, N = 32 (the two tiles' one-hots,
+//             [cluster][point] K-major, written by the epilogue); A = the
+//             same planes read K-major.  The cross blocks (tile 2q rows x tile
+//             2q+1 one-hot) are never read.  S lives in TMEM for the whole
+//             kernel: 8 MMAs per pair instead of 8 per tile (a tcgen05.mma
+//             costs ~45 cycles whatever N <= 64: scripts/micro/umma_rate.cu).
+//   Distance and sums MMAs are issued by two warps, so the distances never
+//   wait for a screen.
 // Screen bound with S = sum_l |f_l c_l| <= |f| cmax: the split residue (lo.lo,
 // r_f c, f r_c) <= 3.02 2^-16 S; the tensor-core accumulation of the exact
 // bf16 products (2 MMAs of K = 16 per accumulator) <= 2 x 17 x 2^-23 S; times
@@ -899,19 +905,22 @@ static size_t kmeans_tc_smem() {
 // + 2^-23 (S + |c|^2) (epilogue adds).  Used with (>= 2.2x slack)
 //   E = 2^-12 |f| cmax (1.01) + 2^-17 cmax^2 + 2^-40 |f|^2 + 2^-100 cmax + 1e-35
 // (the last two: flushed subnormal bf16 inputs / products).  Points with
-// several candidates get the f32 difference-form distance of each candidate
-// (the warp's lanes over the features, from global memory: L2 hits) and, if
-// that leaves several, the exact f64 recurrence.  Features with |x| > 3e38 or non-finite
-// are zeroed in the planes (0 x NaN would poison every cluster's sums) and
-// added to the sums on the scalar path; their points take the exact scan.
+// several candidates are deferred: no one-hot entry (their tile's planes are
+// released without waiting), then the f32 difference-form distance of each
+// candidate (the warp's lanes over the features, from global memory: L2
+// hits), the exact f64 recurrence if that leaves several, and their features
+// added to the sums on the scalar path.  Features with |x| > 3e38 or
+// non-finite are zeroed in the planes (0 x NaN would poison every cluster's
+// sums); their points (norm not finite) are deferred to the exact scan.
 //
-// Warp roles (448 threads, one CTA per SM, persistent over the tiles):
+// Warp roles (480 threads, one CTA per SM, persistent over the tiles):
 //   warps 0-3  split: fp32 tile -> bf16 planes + per-point |f|^2 (features
-//              0-15 in warps 0-1, 16-31 in warps 2-3; two points per thread)
+//              0-15 in warps 0-1, 16-31 in 2-3; two points per thread)
 //   warps 4-11 epilogue, two sets of 4 alternating tiles: TMEM lane = point;
-//              screen, re-check, member, counts, the one-hot tile
+//              screen, member, counts, the one-hot tile, deferred re-checks
 //   warp 12    producer: one 2D tensor copy {128 points x 32 features} per tile
-//   warp 13    MMA issuer (one thread) and TMEM owner
+//   warp 13    distance MMA issuer (one elected lane) and TMEM owner
+//   warp 14    sums MMA issuer
 // Rings: 4 fp32 tiles (released by the split), 6 plane / one-hot stages (3
 // pairs), 6 TMEM accumulators of 32 columns (+ 32 columns of sums): the
 // distances run two tiles ahead of the screen, the split further ahead.
@@ -926,8 +935,10 @@ constexpr int kST = KM_TG_ST;  // fp32 tiles (released by the split)
 #define KM_TG_SP 6
 #endif
 constexpr int kSP = KM_TG_SP;  // planes / one-hot / accumulators (pairs)
-constexpr int kThreads = 448;  // 4 split + 8 epilogue + producer + MMA warps
-constexpr int kWProd = 12, kWMma = 13;
+constexpr int kSplitSets = 1;  // split warp sets of 4 (2 sets: register spills in the epilogue, slower)
+constexpr int kWEpi = 4 * kSplitSets;         // first of the 8 epilogue warps
+constexpr int kWProd = kWEpi + 8, kWMma = kWProd + 1, kWSum = kWProd + 2;
+constexpr int kThreads = 32 * (kWSum + 1);
 constexpr uint32_t kTileB = kNF * kPts * 4;  // 16 KB
 constexpr uint32_t kPlaneB = 16384;          // hi + lo planes of a tile
 constexpr uint32_t kOneHotB = 4096;
@@ -947,6 +958,12 @@ constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kSumsCol = 32 * kSP;  // 32 columns (M = 128: two stage parities)
 static_assert(kSP % 2 == 0, "stages are used in pairs");
 
+// (lo, hi) -> bf16x2 {lo in bits 0..15, hi in 16..31}, both rounded to nearest even
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 // byte offset of (row r, element q) in a SWIZZLE_128B atom of 8 rows x 64 bf16
 __device__ __forceinline__ uint32_t sw128(int r, int q) {
   return (uint32_t)(r * 128 + ((((q >> 3) ^ r) & 7) << 4) + (q & 7) * 2);
@@ -974,13 +991,48 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N, bool amn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((amn ? 1u : 0u) << 15) | ((uint32_t)(N >> 3) << 17) |
          ((uint32_t)(M >> 4) << 24);
 }
-// issued by the whole (converged) warp: one elected lane executes, so the
-// operands stay warp-uniform (uniform registers, no per-lane issue loop)
-__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+// MMA helpers are issued by the whole (converged) warp: one elected lane
+// executes, so the operands stay warp-uniform (no per-lane issue loop)
+// the 4 distance MMAs of a tile + the commit on `bar`, one elected lane, one
+// asm block (no per-MMA descriptor arithmetic on the issuing warp):
+//   D[0..31]  = F_hi . [C_hi | C_lo]   (K = 32: feature groups 0-1, 2-3)
+//   D[16..31] += F_lo . C_hi
+// aH = the stage's hi-plane descriptor (lo plane +4096 B, second K step
+// +2048 B), bC = the centroid descriptor (second K step +32 B)
+__device__ __forceinline__ void umma_dist(uint32_t d, uint64_t aH, uint64_t bC, uint32_t id32, uint32_t id16,
+                                          uint64_t* bar) {
   asm volatile(
-      "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d),
-      "l"(a), "l"(b), "r"(id), "r"(acc)
+      "{\n .reg .pred e, f, t;\n .reg .b64 a1, a2, a3, b1;\n"
+      " elect.sync _|e, 0xffffffff;\n setp.eq.u32 f, 1, 0;\n setp.eq.u32 t, 0, 0;\n"
+      " add.s64 a1, %1, 128;\n add.s64 a2, %1, 256;\n add.s64 a3, %1, 384;\n add.s64 b1, %2, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a2, %2, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a3, b1, %5, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n}" ::"r"(d),
+      "l"(aH), "l"(bC), "r"(id32), "r"(d + 16), "r"(id16), "r"(smem_u32(bar))
+      : "memory");
+}
+// the 8 sums MMAs of a tile pair (two point halves x 4 K steps of 16 points):
+// A = the pair's planes (+16384 B per half, +32 B per K step), B = the pair's
+// one-hot rows (+4096 B per half, +32 B per K step); `first` clears D
+__device__ __forceinline__ void umma_sums(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t first) {
+  asm volatile(
+      "{\n .reg .pred e, p, t;\n .reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      " elect.sync _|e, 0xffffffff;\n setp.eq.u32 p, %4, 0;\n setp.eq.u32 t, 0, 0;\n"
+      " add.s64 a1, %1, 2;\n add.s64 a2, %1, 4;\n add.s64 a3, %1, 6;\n"
+      " add.s64 a4, %1, 1024;\n add.s64 a5, %1, 1026;\n add.s64 a6, %1, 1028;\n add.s64 a7, %1, 1030;\n"
+      " add.s64 b1, %2, 2;\n add.s64 b2, %2, 4;\n add.s64 b3, %2, 6;\n"
+      " add.s64 b4, %2, 256;\n add.s64 b5, %2, 258;\n add.s64 b6, %2, 260;\n add.s64 b7, %2, 262;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, t;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(first)
       : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -1163,64 +1215,48 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
             : "memory");
       }
     }
-  } else if (warp == kWMma) {  // ---- MMA issuer (the whole warp; one elected lane issues)
-    {
-      const uint32_t sCent = smem_u32(sm + kOffCent);
-      const uint32_t idD32 = idesc(128, 32, true), idD16 = idesc(128, 16, true);
-      const uint32_t idS2 = idesc(128, 32, false), idS1 = idesc(128, 16, false);
-      // distances of tile n, then the sums of tile n - kLag: the distances run
-      // kLag tiles ahead of the epilogue (blocking waits wake on the phase flip)
-      constexpr int kLag = 2;
-      for (int n = 0; n < nmine + kLag; n++) {
-        if (n < nmine) {
-          const int b = n % kSP;
-          mbar_wait(&full_p[b], (n / kSP) & 1);
-          if (lane == 0) trace(8, n);
-          if (n >= kSP) mbar_wait(&acc_empty[b], ((n / kSP) - 1) & 1);
-          if (lane == 0) trace(9, n);
-          __syncwarp();  // elect.sync below needs the converged warp
-          tc_after();
-          const uint32_t sP = smem_u32(sm + stage_planes(b)), d = tmem + b * 32;
-#pragma unroll
-          for (int kk = 0; kk < 2; kk++)
-            umma(d, sdesc(sP + kk * 2048, 16384, 1024), sdesc(sCent + kk * 32, 16, 1024), idD32, kk);
-#pragma unroll
-          for (int kk = 0; kk < 2; kk++)
-            umma(d + 16, sdesc(sP + 4096 + kk * 2048, 16384, 1024), sdesc(sCent + kk * 32, 16, 1024), idD16, 1);
-          umma_commit(&acc_full[b]);
-          if (lane == 0) trace(4, n);
-          __syncwarp();
-        }
-        // centroid sums of the tile pair (ms - 1, ms) (ms odd), or of a last
-        // lone even tile: M = 128 rows = both tiles' hi / lo feature rows,
-        // N = 32 = both one-hots (the cross blocks of D are never read)
-        const int ms = n - kLag;
-        if (ms >= 0 && ms < nmine && ((ms & 1) || ms == nmine - 1)) {
-          const int m0 = ms & ~1, b0 = m0 % kSP;
-          const bool pair = ms & 1;
-          mbar_wait(&oh_full[b0], (m0 / kSP) & 1);
-          if (pair) mbar_wait(&oh_full[b0 + 1], (ms / kSP) & 1);
-          if (lane == 0) trace(10, ms);
-          __syncwarp();
-          tc_after();
-          const uint32_t sP = smem_u32(sm + stage_planes(b0)), sO = smem_u32(sm + stage_onehot(b0));
-#pragma unroll
-          for (int ph = 0; ph < 2; ph++)
-#pragma unroll
-            for (int kk = 0; kk < 4; kk++)
-              umma(tmem + kSumsCol, sdesc(sP + ph * 16384 + kk * 32, 16, 1024), sdesc(sO + ph * 4096 + kk * 32, 16, 1024),
-                   pair ? idS2 : idS1, (m0 > 0 || ph > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&empty_p[b0]);
-          if (pair) umma_commit(&empty_p[b0 + 1]);
-          if (lane == 0) trace(7, ms);
-          __syncwarp();
-          if (ms == nmine - 1) umma_commit(fin);
-        }
-      }
-    }
-  } else if (warp < 4) {  // ---- split: fp32 tile -> bf16 planes, |f|^2 partials
-    const int st = tid, half = st >> 6, pr = st & 63, p = 2 * pr;
+  } else if (warp == kWMma) {  // ---- distance MMAs (the whole warp; one elected lane issues)
+    const uint64_t dC = sdesc(smem_u32(sm + kOffCent), 16, 1024);
+    const uint32_t idD32 = idesc(128, 32, true), idD16 = idesc(128, 16, true);
     for (int n = 0; n < nmine; n++) {
+      const int b = n % kSP;
+      mbar_wait(&full_p[b], (n / kSP) & 1);
+      if (lane == 0) trace(8, n);
+      if (n >= kSP) mbar_wait(&acc_empty[b], ((n / kSP) - 1) & 1);
+      if (lane == 0) trace(9, n);
+      __syncwarp();  // elect.sync below needs the converged warp
+      tc_after();
+      umma_dist(tmem + b * 32, sdesc(smem_u32(sm + stage_planes(b)), 16384, 1024), dC, idD32, idD16, &acc_full[b]);
+      if (lane == 0) trace(4, n);
+      __syncwarp();
+    }
+  } else if (warp == kWSum) {
+    // ---- centroid sums, issued by a second thread so that the distances
+    // never wait for a screen: the tile pair (m0, m0 + 1), or a last lone
+    // even tile; M = 128 rows = both tiles' hi / lo feature rows, N = 32 =
+    // both one-hots (the cross blocks of D are never read).  A pair's
+    // distance MMAs completed before its screens began, so the commit on
+    // empty_p covers every tensor-core read of the stages.
+    const uint32_t idS2 = idesc(128, 32, false), idS1 = idesc(128, 16, false);
+    for (int m0 = 0; m0 < nmine; m0 += 2) {
+      const int b0 = m0 % kSP;
+      const bool pair = m0 + 1 < nmine;
+      mbar_wait(&oh_full[b0], (m0 / kSP) & 1);
+      if (pair) mbar_wait(&oh_full[b0 + 1], ((m0 + 1) / kSP) & 1);
+      if (lane == 0) trace(10, m0 + pair);
+      __syncwarp();
+      tc_after();
+      umma_sums(tmem + kSumsCol, sdesc(smem_u32(sm + stage_planes(b0)), 16, 1024),
+                sdesc(smem_u32(sm + stage_onehot(b0)), 16, 1024), pair ? idS2 : idS1, m0 == 0 ? 1u : 0u);
+      umma_commit(&empty_p[b0]);
+      if (pair) umma_commit(&empty_p[b0 + 1]);
+      if (lane == 0) trace(7, m0 + pair);
+      __syncwarp();
+      if (m0 + 2 >= nmine) umma_commit(fin);
+    }
+  } else if (warp < kWEpi) {  // ---- split: fp32 tile -> bf16 planes, |f|^2 partials
+    const int st = tid & 127, half = st >> 6, pr = st & 63, p = 2 * pr, sset = warp >> 2;
+    for (int n = sset; n < nmine; n += kSplitSets) {
       const int s = n % kST, b = n % kSP;
       mbar_wait(&full_t[s], (n / kST) & 1);
       if (st == 0) trace(1, n);
@@ -1230,15 +1266,20 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       const int cntp = (int)min((long long)kPts, hi - p0);
       const float* T = reinterpret_cast<const float*>(sm + s * kTileB);
       unsigned char* P = sm + stage_planes(b);
-      const bool v0 = p < cntp, v1 = p + 1 < cntp;
       float n0 = 0.f, n1 = 0.f;
       float2 xs[16];
 #pragma unroll
       for (int j = 0; j < 16; j++) xs[j] = *reinterpret_cast<const float2*>(T + (16 * half + j) * kPts + p);
+      if (cntp < kPts) {  // columns past hi: other ranges' points (or zeros)
+        const bool v0 = p < cntp, v1 = p + 1 < cntp;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          xs[j].x = v0 ? xs[j].x : 0.f;
+          xs[j].y = v1 ? xs[j].y : 0.f;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 16; j++) {
-        xs[j].x = v0 ? xs[j].x : 0.f;  // columns past hi: other ranges' points (or zeros)
-        xs[j].y = v1 ? xs[j].y : 0.f;
         n0 = fmaf(xs[j].x, xs[j].x, n0);
         n1 = fmaf(xs[j].y, xs[j].y, n1);
       }
@@ -1254,10 +1295,10 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       for (int j = 0; j < 16; j++) {
         const int l = 16 * half + j;
         const float2 x = xs[j];
-        const __nv_bfloat162 h = __floats2bfloat162_rn(x.x, x.y);
-        const __nv_bfloat162 r = __floats2bfloat162_rn(x.x - __low2float(h), x.y - __high2float(h));
-        *reinterpret_cast<__nv_bfloat162*>(P + plane_off(0, l, p)) = h;
-        *reinterpret_cast<__nv_bfloat162*>(P + plane_off(1, l, p)) = r;
+        const uint32_t h = bf16x2_rn(x.x, x.y);
+        const uint32_t r = bf16x2_rn(x.x - __uint_as_float(h << 16), x.y - __uint_as_float(h & 0xffff0000u));
+        *reinterpret_cast<uint32_t*>(P + plane_off(0, l, p)) = h;
+        *reinterpret_cast<uint32_t*>(P + plane_off(1, l, p)) = r;
       }
       *reinterpret_cast<float2*>(nrm + (b * 2 + half) * kPts + p) = make_float2(n0, n1);
       fence_proxy_async();  // the planes are read by the tensor cores (async proxy)
@@ -1269,7 +1310,7 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       if (st == 0) trace(3, n);
     }
   } else {  // ---- epilogue: two sets of 4 warps (even / odd tiles); TMEM lanes 32 (warp % 4) + lane
-    const int ew = warp & 3, m = 32 * ew + lane, set = (warp - 4) >> 2;
+    const int ew = warp & 3, m = 32 * ew + lane, set = (warp - kWEpi) >> 2;
     float cn[16];
     float cmax2 = 0.f;
 #pragma unroll
@@ -1312,48 +1353,12 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       for (int c = 0; c < 16; c++) cand |= (tv[c] <= thr ? 1u : 0u) << c;
       const bool ok = m < cntp;
       const bool fin_ = nr <= 3.0e38f && cand != 0;
-      int best = __ffs(cand) - 1;
-      const float* fg = f + p0 + 32 * ew;  // the warp's points in global memory
-      // near-ties: the candidates' f32 distances in the difference form, one
-      // point at a time with the warp's lanes over the features (a tree sum:
-      // |d32 - d| <= (nf + 4) 2^-24 d in any order); one survivor decides,
-      // several (true ties) take the f64 recurrence on the point's lane
-      unsigned tie = __ballot_sync(0xffffffffu, ok && fin_ && (cand & (cand - 1)));
-      while (tie) {
-        // up to 4 tie points per round: their features are loaded together
-        int srcs[4];
-        float xs[4];
-        int nq = 0;
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-          if (tie) {
-            srcs[q] = __ffs(tie) - 1;
-            tie &= tie - 1;
-            xs[q] = __ldg(fg + (long long)lane * npts + srcs[q]);
-            nq = q + 1;
-          }
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-        if (q >= nq) break;
-        const int src = srcs[q];
-        const float x = xs[q];
-        const unsigned cs = __shfl_sync(0xffffffffu, cand, src);
-        const float e2 = (float)(kNF + 4) * 5.9604645e-08f * 1.01f;
-        float myd = INFINITY, u2 = INFINITY;
-        for (unsigned r = cs; r; r &= r - 1) {
-          const int c = __ffs(r) - 1;
-          const float dl = __fsub_rn(x, cf[c * kNF + lane]);
-          float v = __fmul_rn(dl, dl);
-#pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-          if (lane == c) myd = v;
-          u2 = fminf(u2, fmaf(v, e2, v) + 1e-40f);
-        }
-        const unsigned sv = __ballot_sync(0xffffffffu, ((cs >> lane) & 1) && !(fmaf(-myd, e2, myd) - 1e-40f > u2));
-        if (lane == src) best = (sv & (sv - 1)) ? exact_mask_g(fg + lane, npts, cf, sv) : __ffs(sv) - 1;
-        }
-      }
-      if (ok && !fin_) best = exact_g(fg + lane, npts, cf, k);
+      const int best = __ffs(cand) - 1;
+      // points whose screen does not decide (several candidates, or a norm
+      // that is not finite) are deferred: they get no one-hot entry, so the
+      // tile's planes are released before their re-check, and all their
+      // features go to the sums on the scalar path
+      const bool defer = ok && (!fin_ || (cand & (cand - 1)));
       unsigned char* O = sm + stage_onehot(b);
       {  // zero this warp's 32 one-hot columns (16 rows x 64 B), then set the ones
         const int i0 = 2 * lane;
@@ -1364,20 +1369,68 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
         }
       }
       __syncwarp();
-      if (ok) {
+      if (ok && !defer) {
         member[p0 + m] = best;
         atomicAdd(cnt + best, 1);
         *reinterpret_cast<unsigned short*>(O + onehot_off(best, m)) = 0x3F80;  // bf16 1.0
-        if (!(nr <= 3.0e38f)) {  // features the planes dropped
-          for (int l = 0; l < kNF; l++) {
-            const float x = fg[(long long)l * npts + lane];
-            if (!(fabsf(x) <= 3.0e38f)) atomicAdd(ssx + best * kNF + l, x);
-          }
-        }
       }
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&oh_full[b]);
+      // deferred points, up to 4 per round, lanes over the features (their
+      // loads issued together; the lines went through L2 microseconds ago):
+      // the candidates' f32 distances in the difference form (a tree sum,
+      // |d32 - d| <= (nf + 4) 2^-24 d in any order); one survivor decides,
+      // several (true ties) take the f64 recurrence on the point's lane, as
+      // does the full reference scan of a point whose norm is not finite
+      const float* fg = f + p0 + 32 * ew;  // the warp's points in global memory
+      unsigned dm = __ballot_sync(0xffffffffu, defer);
+      while (dm) {
+        int srcs[4];
+        float xs[4];
+        int nq = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (dm) {
+            srcs[q] = __ffs(dm) - 1;
+            dm &= dm - 1;
+            xs[q] = __ldg(fg + (long long)lane * npts + srcs[q]);
+            nq = q + 1;
+          }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          if (q >= nq) break;
+          const int src = srcs[q];
+          const float x = xs[q];
+          const unsigned cs = __shfl_sync(0xffffffffu, cand, src);
+          const bool sfin = __shfl_sync(0xffffffffu, fin_ ? 1 : 0, src) != 0;
+          int pick = 0;
+          if (sfin) {
+            const float e2 = (float)(kNF + 4) * 5.9604645e-08f * 1.01f;
+            float myd = INFINITY, u2 = INFINITY;
+            for (unsigned r = cs; r; r &= r - 1) {
+              const int c = __ffs(r) - 1;
+              const float dl = __fsub_rn(x, cf[c * kNF + lane]);
+              float v = __fmul_rn(dl, dl);
+#pragma unroll
+              for (int o = 16; o >= 1; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+              if (lane == c) myd = v;
+              u2 = fminf(u2, fmaf(v, e2, v) + 1e-40f);
+            }
+            const unsigned sv =
+                __ballot_sync(0xffffffffu, ((cs >> lane) & 1) && !(fmaf(-myd, e2, myd) - 1e-40f > u2));
+            if (lane == src) pick = (sv & (sv - 1)) ? exact_mask_g(fg + lane, npts, cf, sv) : __ffs(sv) - 1;
+          } else if (lane == src) {
+            pick = exact_g(fg + lane, npts, cf, k);
+          }
+          pick = __shfl_sync(0xffffffffu, pick, src);
+          if (lane == src) {
+            member[p0 + 32 * ew + src] = pick;
+            atomicAdd(cnt + pick, 1);
+          }
+          atomicAdd(ssx + pick * kNF + lane, x);  // feature `lane` of the point (NaN / inf included)
+        }
+      }
       if (m == 0) trace(6, n);
         }
     if (nmine > 0 && set == 0) {  // the sums accumulator: lane r = 64 parity + 32 P + feature

@@ -7,3 +7,6 @@ for v in 4 5 5 5; do
   BF_KMEANS_V=$v timeout 300 python bench.py --no-cpu --no-fused --no-bfs --cases kmeans,kmeans_loop --steps 10 --warmup 3 > gpurun_out/tg_$v.json 2>gpurun_out/tg_$v.err
   python -c "import json;d=json.load(open('gpurun_out/tg_$v.json'));k=d['kernels'];print('$v', k['kmeans']['ms_per_step'], k['kmeans'].get('checked'), k['kmeans_loop']['ms_per_step'])" 2>/dev/null || tail -2 gpurun_out/tg_$v.err
 done
+cp alt_libs/trace.so paper_2206_07896_b200/libbfgpu.so
+timeout 200 python scripts/micro/tg_trace.py 2>&1 | tail -12
+cp alt_libs/base.so paper_2206_07896_b200/libbfgpu.so
