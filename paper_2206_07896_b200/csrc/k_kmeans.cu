@@ -921,14 +921,14 @@ static size_t kmeans_tc_smem() {
 //   warp 12    producer: one 2D tensor copy {128 points x 32 features} per tile
 //   warp 13    distance MMA issuer (one elected lane) and TMEM owner
 //   warp 14    sums MMA issuer
-// Rings: 4 fp32 tiles (released by the split), 6 plane / one-hot stages (3
+// Rings: 5 fp32 tiles (released by the split), 6 plane / one-hot stages (3
 // pairs), 6 TMEM accumulators of 32 columns (+ 32 columns of sums): the
 // distances run two tiles ahead of the screen, the split further ahead.
 namespace tg {
 constexpr int kPts = 128;
 constexpr int kNF = 32;
 #ifndef KM_TG_ST
-#define KM_TG_ST 4
+#define KM_TG_ST 5
 #endif
 constexpr int kST = KM_TG_ST;  // fp32 tiles (released by the split)
 #ifndef KM_TG_SP
@@ -958,6 +958,19 @@ constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kSumsCol = 32 * kSP;  // 32 columns (M = 128: two stage parities)
 static_assert(kSP % 2 == 0, "stages are used in pairs");
 
+// packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a): two points per instruction
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)), "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
 // (lo, hi) -> bf16x2 {lo in bits 0..15, hi in 16..31}, both rounded to nearest even
 __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
   uint32_t r;
@@ -1278,11 +1291,11 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
           xs[j].y = v1 ? xs[j].y : 0.f;
         }
       }
+      float2 nn = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 16; j++) {
-        n0 = fmaf(xs[j].x, xs[j].x, n0);
-        n1 = fmaf(xs[j].y, xs[j].y, n1);
-      }
+      for (int j = 0; j < 16; j++) nn = fma2(xs[j], xs[j], nn);  // = the two scalar fmaf chains
+      n0 = nn.x;
+      n1 = nn.y;
       // finite norms <= 3e38: every |x| <= 2e19, nothing to drop (the common case)
       if (!__all_sync(0xffffffffu, n0 <= 3.0e38f && n1 <= 3.0e38f)) {
 #pragma unroll
@@ -1296,7 +1309,8 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
         const int l = 16 * half + j;
         const float2 x = xs[j];
         const uint32_t h = bf16x2_rn(x.x, x.y);
-        const uint32_t r = bf16x2_rn(x.x - __uint_as_float(h << 16), x.y - __uint_as_float(h & 0xffff0000u));
+        const float2 rr = sub2(x, make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u)));
+        const uint32_t r = bf16x2_rn(rr.x, rr.y);
         *reinterpret_cast<uint32_t*>(P + plane_off(0, l, p)) = h;
         *reinterpret_cast<uint32_t*>(P + plane_off(1, l, p)) = r;
       }

@@ -72,7 +72,7 @@ else:
     keep = ("## ncu --set full, per kernel\n\n"
             "* `hotspot.md` — the headline kernel (hotspot_rows) and its variants.\n"
             "* `bfs.md`, `bfs_do_launches.txt` — the direction-optimizing traversal level by level.\n"
-            "* `kmeans.md`, `umma_sw128_probe.log` — kmeans_tc and the tcgen05 layout probe.\n"
+            "* `kmeans.md`, `kmeans_tg_sass.txt`, `umma_sw128_probe.log`, `umma_bf16_probe.log`, `umma_rate.log` — kmeans_tg (tcgen05) and its probes.\n"
             "* `sanitizer_summary.md` — compute-sanitizer memcheck / racecheck / synccheck / initcheck.\n"
             "* `grain_host_vs_device_fetch.json` — the fetch-grain study with host-issued and device-side fetching.\n")
 (prof / names["summary"]).write_text("\n".join(L) + "\n\n" + keep)
