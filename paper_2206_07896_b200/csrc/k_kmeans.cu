@@ -934,10 +934,21 @@ constexpr int kST = KM_TG_ST;  // fp32 tiles (released by the split)
 #ifndef KM_TG_SP
 #define KM_TG_SP 6
 #endif
-constexpr int kSP = KM_TG_SP;  // planes / one-hot / accumulators (pairs)
-constexpr int kSplitSets = 1;  // split warp sets of 4 (2 sets: register spills in the epilogue, slower)
-constexpr int kWEpi = 4 * kSplitSets;         // first of the 8 epilogue warps
-constexpr int kWProd = kWEpi + 8, kWMma = kWProd + 1, kWSum = kWProd + 2;
+constexpr int kSP = KM_TG_SP;  // planes / one-hot stages (pairs)
+#ifndef KM_TG_SA
+#define KM_TG_SA 6
+#endif
+constexpr int kSA = KM_TG_SA;  // TMEM distance accumulators (32 columns each)
+#ifndef KM_TG_SPLIT_SETS
+#define KM_TG_SPLIT_SETS 1
+#endif
+#ifndef KM_TG_EPI_SETS
+#define KM_TG_EPI_SETS 2
+#endif
+constexpr int kSplitSets = KM_TG_SPLIT_SETS;  // split warp sets of 4 (alternating tiles)
+constexpr int kEpiSets = KM_TG_EPI_SETS;      // epilogue warp sets of 4 (alternating tiles)
+constexpr int kWEpi = 4 * kSplitSets;         // first epilogue warp
+constexpr int kWProd = kWEpi + 4 * kEpiSets, kWMma = kWProd + 1, kWSum = kWProd + 2;
 constexpr int kThreads = 32 * (kWSum + 1);
 constexpr uint32_t kTileB = kNF * kPts * 4;  // 16 KB
 constexpr uint32_t kPlaneB = 16384;          // hi + lo planes of a tile
@@ -950,12 +961,12 @@ constexpr uint32_t kOffCf = kOffNrm + kSP * 2 * kPts * 4;   // [16][32] f32 cent
 constexpr uint32_t kOffSsx = kOffCf + 16 * kNF * 4;         // [16][32] scalar-path sums
 constexpr uint32_t kOffCnt = kOffSsx + 16 * kNF * 4;        // [16] counts
 constexpr uint32_t kOffBar = kOffCnt + 16 * 4;              // mbarriers
-constexpr int kNBar = 2 * kST + 5 * kSP + 1;
+constexpr int kNBar = 2 * kST + 3 * kSP + 2 * kSA + 1;
 constexpr uint32_t kSmem = kOffBar + kNBar * 8 + 16 + 1024;  // + TMEM slot, + alignment slack
 static_assert(kSmem <= 227 * 1024, "kmeans_tg shared memory");
-static_assert(32 * kSP + 32 <= 256, "kmeans_tg TMEM columns");
+static_assert(32 * kSA + 32 <= 256, "kmeans_tg TMEM columns");
 constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kSumsCol = 32 * kSP;  // 32 columns (M = 128: two stage parities)
+constexpr uint32_t kSumsCol = 32 * kSA;  // 32 columns (M = 128: two stage parities)
 static_assert(kSP % 2 == 0, "stages are used in pairs");
 
 // packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a): two points per instruction
@@ -1160,9 +1171,9 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
   uint64_t* full_p = empty_t + kST;         // [kSP] split (4 warps) -> MMA
   uint64_t* empty_p = full_p + kSP;         // [kSP] sums MMA commit -> split
   uint64_t* oh_full = empty_p + kSP;        // [kSP] epilogue (4 warps) -> MMA
-  uint64_t* acc_full = oh_full + kSP;       // [kSP] distance MMA commit -> epilogue
-  uint64_t* acc_empty = acc_full + kSP;     // [kSP] epilogue (4 warps) -> MMA
-  uint64_t* fin = acc_empty + kSP;          // last sums MMA commit -> epilogue
+  uint64_t* acc_full = oh_full + kSP;       // [kSA] distance MMA commit -> epilogue
+  uint64_t* acc_empty = acc_full + kSA;     // [kSA] epilogue (4 warps) -> MMA
+  uint64_t* fin = acc_empty + kSA;          // last sums MMA commit -> epilogue
   uint32_t* tslot = reinterpret_cast<uint32_t*>(fin + 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -1176,8 +1187,10 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       mbar_init(&full_p[b], 4);
       mbar_init(&empty_p[b], 1);
       mbar_init(&oh_full[b], 4);
-      mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4);
+    }
+    for (int a = 0; a < kSA; a++) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
     }
     mbar_init(fin, 1);
     fence_barrier_init();
@@ -1215,7 +1228,7 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
       for (int n = 0; n < nmine; n++) {
         const int s = n % kST;
-        if (n >= kST) mbar_wait_sleep(&empty_t[s], ((n / kST) - 1) & 1);
+        if (n >= kST) mbar_wait(&empty_t[s], ((n / kST) - 1) & 1);  // wakes on the phase flip (a nanosleep back-off added ~1200 cycles per slot)
         const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
         trace(0, n);
         // the box is always written in full (zeros past npts; columns past hi
@@ -1235,11 +1248,12 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       const int b = n % kSP;
       mbar_wait(&full_p[b], (n / kSP) & 1);
       if (lane == 0) trace(8, n);
-      if (n >= kSP) mbar_wait(&acc_empty[b], ((n / kSP) - 1) & 1);
+      const int a = n % kSA;
+      if (n >= kSA) mbar_wait(&acc_empty[a], ((n / kSA) - 1) & 1);
       if (lane == 0) trace(9, n);
       __syncwarp();  // elect.sync below needs the converged warp
       tc_after();
-      umma_dist(tmem + b * 32, sdesc(smem_u32(sm + stage_planes(b)), 16384, 1024), dC, idD32, idD16, &acc_full[b]);
+      umma_dist(tmem + a * 32, sdesc(smem_u32(sm + stage_planes(b)), 16384, 1024), dC, idD32, idD16, &acc_full[a]);
       if (lane == 0) trace(4, n);
       __syncwarp();
     }
@@ -1337,21 +1351,22 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
     const float cmax = sqrtf(cmax2) * 1.001f;
     const float eA = 2.44140625e-4f * 1.01f * cmax;  // 2^-12 x |f| (rsqrt approximation + 1 %)
     const float eB = 7.62939453125e-06f * cmax * cmax + 7.8886e-31f * cmax + 1e-35f;  // 2^-17 cmax^2, 2^-100 cmax
-    for (int n = set; n < nmine; n += 2) {
+    for (int n = set; n < nmine; n += kEpiSets) {
       const int b = n % kSP;
       const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
       const int cntp = (int)min((long long)kPts, hi - p0);
       // full_p as well: orders the split's |f|^2 stores before the loads below
       // (the split cannot complete tile n + kSP before this tile's one-hot exists)
       mbar_wait(&full_p[b], (n / kSP) & 1);
-      mbar_wait(&acc_full[b], (n / kSP) & 1);
+      const int a = n % kSA;
+      mbar_wait(&acc_full[a], (n / kSA) & 1);
       if (m == 0) trace(5, n);
       tc_after();
       float d[32];
-      tmem_ld32(tmem + b * 32 + ((uint32_t)(32 * ew) << 16), d);
+      tmem_ld32(tmem + a * 32 + ((uint32_t)(32 * ew) << 16), d);
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      if (lane == 0) mbar_arrive(&acc_empty[a]);
       const float nr = nrm[(b * 2) * kPts + m] + nrm[(b * 2 + 1) * kPts + m];
       const float E = fmaf(eA, nr * rsqrtf(nr + 1e-30f), eB) + 9.2e-13f * nr;
       float tv[16];

@@ -74,11 +74,20 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensor
   }
 }
 
+__global__ void fill(float* f, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned x = (unsigned)i * 2654435761u;
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    f[i] = (float)(x >> 8) * (1.0f / 16777216.0f);
+  }
+}
+
 int main() {
   const long long npts = 1 << 24;
   float *f, *sink;
   cudaMalloc(&f, npts * 32 * 4);
-  cudaMemset(f, 0, npts * 32 * 4);
+  fill<<<148 * 8, 256>>>(f, npts * 32);  // non-zero data (a zero-filled buffer reads faster than the copy peak)
   cudaMalloc(&sink, 4096 * 4);
   PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   cudaDriverEntryPointQueryResult q;
