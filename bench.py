@@ -614,8 +614,36 @@ def run_kmeans(args) -> None:
     barrier(world)
     ms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
     cent_sum = float(tc.double().sum().item())
+    # e2e: the same step through the public API from pinned host memory: the
+    # points are uploaded every step, the memberships and centroids read back
+    # and compared with the resident run's (every rank holds all points)
+    import numpy as np
+    expect_member, expect_cent = arena.to_numpy(member), arena.to_numpy(cent)
+    h_f = torch.empty(npts * nf, dtype=torch.float32).pin_memory().numpy()
+    arena.download_into(f, h_f)
+    h_member = torch.empty(npts, dtype=torch.int32).pin_memory().numpy()
+    h_cent = torch.empty(k * nf, dtype=torch.float32).pin_memory().numpy()
+    e2e_s = []
+    for i in range(args.warmup + args.steps):
+        barrier(world)
+        t0 = time.perf_counter()
+        arena.upload_numpy(f, h_f)
+        step()
+        rt.device_synchronize()
+        torch.cuda.synchronize()
+        arena.download_into(member, h_member)
+        arena.download_into(cent, h_cent)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_s.append(max_over_ranks(dt, world))
+    # the centroid sums are f32 atomics (order-dependent, as in the reference),
+    # so a later pass may differ in the last bits: centroids within 1e-4, and
+    # memberships equal up to the points the rounding moves across a tie
+    mismatch = float(np.mean(h_member != expect_member))
+    e2e_checked = bool(np.allclose(h_cent, expect_cent, rtol=1e-4, atol=1e-6) and mismatch <= 1e-3)
     if rank == 0:
         pts = npts * passes
+        e2e_t = statistics.median(e2e_s)
         print(json.dumps({
             "metric": METRIC, "value": round(pts * (4 * nf + 4) / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -625,6 +653,10 @@ def run_kmeans(args) -> None:
                        "parallelism": f"point ranges x{world}, per-pass all-reduce of sums/counts",
                        "bytes_per_point_pass": 4 * nf + 4},
             "elem_per_s": pts / (ms * 1e-3), "centroid_checksum": cent_sum,
+            "e2e": {"value": round(pts * (4 * nf + 4) / e2e_t / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": npts * nf * 4, "d2h_bytes_per_step": npts * 4 + k * nf * 4,
+                    "ms_per_step": round(e2e_t * 1e3, 3), "checked": e2e_checked,
+                    "member_mismatch": mismatch},
             "clocks": clocks.summary()}), flush=True)
     rt.shutdown()
     if world > 1:

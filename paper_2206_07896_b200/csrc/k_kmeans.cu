@@ -1310,6 +1310,10 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       for (int j = 0; j < 16; j++) nn = fma2(xs[j], xs[j], nn);  // = the two scalar fmaf chains
       n0 = nn.x;
       n1 = nn.y;
+      // every value of the slot is in registers (the norms consumed them):
+      // hand the fp32 slot back to the producer before the conversions
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_t[s]);
       // finite norms <= 3e38: every |x| <= 2e19, nothing to drop (the common case)
       if (!__all_sync(0xffffffffu, n0 <= 3.0e38f && n1 <= 3.0e38f)) {
 #pragma unroll
@@ -1331,10 +1335,7 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       *reinterpret_cast<float2*>(nrm + (b * 2 + half) * kPts + p) = make_float2(n0, n1);
       fence_proxy_async();  // the planes are read by the tensor cores (async proxy)
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&full_p[b]);
-        mbar_arrive(&empty_t[s]);
-      }
+      if (lane == 0) mbar_arrive(&full_p[b]);
       if (st == 0) trace(3, n);
     }
   } else {  // ---- epilogue: two sets of 4 warps (even / odd tiles); TMEM lanes 32 (warp % 4) + lane
