@@ -621,6 +621,11 @@ edge.buffer("f").values = fe.reshape(-1)
 cases.append(edge)
 for nf in (8, 16, 24):
     cases.append(I.kmeans(2052, nf, 9, 128, seed=30 + nf, dup=True))
+# kmeans_tg tile bookkeeping: an odd number of 128-point tiles per CTA (a lone
+# last tile), a partial last tile, few clusters (padding rows), 2 tiles per CTA
+cases.append(I.kmeans(128 * 148 * 3 + 36, 32, 3, 256, seed=41))
+cases.append(I.kmeans(128 * 148 * 2, 32, 16, 256, seed=42, dup=True))
+cases.append(I.kmeans(128 * 150 + 4, 32, 2, 256, seed=43))
 for k, inst in enumerate(cases):
     want, _ = oracle.run(inst)
     got, trap, _, _ = gpu_run(inst)
