@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cfloat>
 #include <climits>
 
 #include "bf_internal.h"
@@ -885,9 +886,10 @@ static size_t kmeans_tc_smem() {
 // (scripts/micro/umma_bf16.cu checks every layout below on the device):
 //   distance  D[p][c'] = sum_l F[p][l] B[c'][l], M = 128 points, K = 32:
 //             A = the planes read MN-major (SWIZZLE_128B atoms of 8 features x
-//             64 points); B = the centroid rows (hi 0..15, lo 16..31) K-major.
+//             64 points); B = the centroid rows (hi 0..15, lo 16..31, lo2 32..47) K-major.
 //             MMA 1: A = F_hi, N = 32 (hi.hi -> cols 0..15, hi.lo -> 16..31);
-//             MMA 2: A = F_lo, B = C_hi, N = 16, accumulated into cols 16..31.
+//             MMAs 2-4: F_lo.C_hi, F_hi.C_lo2, F_lo.C_lo, N = 16, accumulated
+//             into cols 16..31 (B rows 32..47 = C_lo2).
 //   sums      S[r][c] = sum_p P[r][p] onehot[c][p] over a PAIR of tiles:
 //             M = 128 rows (tile 2q: 32 hi + 32 lo feature rows, tile 2q+1
 //             the same), K = 128 points, N = 32 (the two tiles' one-hots,
@@ -898,12 +900,21 @@ static size_t kmeans_tc_smem() {
 //             costs ~45 cycles whatever N <= 64: scripts/micro/umma_rate.cu).
 //   Distance and sums MMAs are issued by two warps, so the distances never
 //   wait for a screen.
-// Screen bound with S = sum_l |f_l c_l| <= |f| cmax: the split residue (lo.lo,
-// r_f c, f r_c) <= 3.02 2^-16 S; the tensor-core accumulation of the exact
-// bf16 products (2 MMAs of K = 16 per accumulator) <= 2 x 17 x 2^-23 S; times
-// 2 for s = |c|^2 - 2 f.c: |s(tg) - s| < 2^-13.17 S + 2^-19 |c|^2 (f32 |c|^2)
-// + 2^-23 (S + |c|^2) (epilogue adds).  Used with (>= 2.2x slack)
-//   E = 2^-12 |f| cmax (1.01) + 2^-17 cmax^2 + 2^-40 |f|^2 + 2^-100 cmax + 1e-35
+// Screen bound with S = sum_l |f_l c_l| <= |f| cmax.  The centroids are
+// split into THREE planes, c = C_hi + C_lo + C_lo2 + r_c (r_c = 0 unless a
+// plane is subnormal, measured per launch), the points into two (the split
+// is the pipeline's slowest stage), and the distance sums F_hi.C_hi in its own
+// columns and F_lo.C_hi + F_hi.C_lo + F_hi.C_lo2 + F_lo.C_lo in the other.
+// Dropped: r_f.c <= 2^-16 S, F_lo.(C_lo2 + r_c) <= 2^-24 S + |f||r_c|; the
+// tensor-core accumulation of the exact bf16 products: 2 MMAs of K = 16 into
+// the hi.hi columns <= 2 x 17 x 2^-23 S, 8 into the small ones (terms <=
+// 2^-7 S) <= 2^-22.9 S; times 2 for s = |c|^2 - 2 f.c, plus 2^-24 |c|^2 (f64
+// |c|^2 rounded once) and 2^-22.4 S + 2^-24 |c|^2 (epilogue adds):
+// |s(tg) - s| < 2^-14.63 S + 2 |f||r_c| + 2^-23 |c|^2.  Used with (>= 1.5x
+// slack; round 2 had 2^-13.17 S with two centroid planes and E = 2^-12 ...,
+// which deferred 1.2-2.7 % of the points of the 16M x 32 bench data)
+//   E = 2^-14 |f| cmax (1.01) + 2.02 |f| max|r_c| + 2^-21 cmax^2 + 2^-40 |f|^2
+//       + 2^-100 cmax + 1e-35
 // (the last two: flushed subnormal bf16 inputs / products).  Points with
 // several candidates are deferred: no one-hot entry (their tile's planes are
 // released without waiting), then the f32 difference-form distance of each
@@ -956,11 +967,12 @@ constexpr uint32_t kOneHotB = 4096;
 constexpr uint32_t kOffPlanes = kST * kTileB;
 constexpr uint32_t kOffOneHot = kOffPlanes + kSP * kPlaneB;
 constexpr uint32_t kOffCent = kOffOneHot + kSP * kOneHotB;
-constexpr uint32_t kOffNrm = kOffCent + 4096;               // [kSP][2][128] f32
+constexpr uint32_t kOffNrm = kOffCent + 6144;               // [kSP][2][128] f32
 constexpr uint32_t kOffCf = kOffNrm + kSP * 2 * kPts * 4;   // [16][32] f32 centroids
 constexpr uint32_t kOffSsx = kOffCf + 16 * kNF * 4;         // [16][32] scalar-path sums
 constexpr uint32_t kOffCnt = kOffSsx + 16 * kNF * 4;        // [16] counts
-constexpr uint32_t kOffBar = kOffCnt + 16 * 4;              // mbarriers
+constexpr uint32_t kOffCn = kOffCnt + 16 * 4;               // [16] |c|^2 (f64 sums rounded), [16] |r_c|
+constexpr uint32_t kOffBar = kOffCn + 32 * 4;               // mbarriers
 constexpr int kNBar = 2 * kST + 3 * kSP + 2 * kSA + 1;
 constexpr uint32_t kSmem = kOffBar + kNBar * 8 + 16 + 1024;  // + TMEM slot, + alignment slack
 static_assert(kSmem <= 227 * 1024, "kmeans_tg shared memory");
@@ -1017,22 +1029,28 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N, bool amn) {
 }
 // MMA helpers are issued by the whole (converged) warp: one elected lane
 // executes, so the operands stay warp-uniform (no per-lane issue loop)
-// the 4 distance MMAs of a tile + the commit on `bar`, one elected lane, one
+// the 8 distance MMAs of a tile + the commit on `bar`, one elected lane, one
 // asm block (no per-MMA descriptor arithmetic on the issuing warp):
 //   D[0..31]  = F_hi . [C_hi | C_lo]   (K = 32: feature groups 0-1, 2-3)
-//   D[16..31] += F_lo . C_hi
+//   D[16..31] += F_lo . C_hi + F_hi . C_lo2 + F_lo . C_lo
 // aH = the stage's hi-plane descriptor (lo plane +4096 B, second K step
-// +2048 B), bC = the centroid descriptor (second K step +32 B)
+// +2048 B), bC = the centroid descriptor (rows 16.. +2048 B, rows 32..
+// +4096 B, second K step +32 B)
 __device__ __forceinline__ void umma_dist(uint32_t d, uint64_t aH, uint64_t bC, uint32_t id32, uint32_t id16,
                                           uint64_t* bar) {
   asm volatile(
-      "{\n .reg .pred e, f, t;\n .reg .b64 a1, a2, a3, b1;\n"
+      "{\n .reg .pred e, f, t;\n .reg .b64 a1, a2, a3, b1, b2, b3, b4, b5;\n"
       " elect.sync _|e, 0xffffffff;\n setp.eq.u32 f, 1, 0;\n setp.eq.u32 t, 0, 0;\n"
       " add.s64 a1, %1, 128;\n add.s64 a2, %1, 256;\n add.s64 a3, %1, 384;\n add.s64 b1, %2, 2;\n"
+      " add.s64 b2, %2, 256;\n add.s64 b3, %2, 258;\n add.s64 b4, %2, 128;\n add.s64 b5, %2, 130;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a2, %2, %5, t;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a3, b1, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], %1, b2, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a1, b3, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a2, b4, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a3, b5, %5, t;\n"
       " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n}" ::"r"(d),
       "l"(aH), "l"(bC), "r"(id32), "r"(d + 16), "r"(id16), "r"(smem_u32(bar))
       : "memory");
@@ -1204,14 +1222,37 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
     cf[i] = i < k * kNF ? cent[i] : 0.f;
     ssx[i] = 0.f;
   }
-  if (tid < 16) cnt[tid] = 0;
-  for (int i = tid; i < 32 * 64; i += blockDim.x) {  // 32 rows x 64 bf16 (features 32..63 zero)
+  if (tid < 16) {
+    cnt[tid] = 0;
+    // |c|^2 as an f64 sum rounded once (error 2^-24 |c|^2), and the norm of
+    // the centroid's split residue c - hi - lo - lo2 (exact f32 differences;
+    // zero unless a plane is subnormal or overflows), rounded up
+    float* cnrm = reinterpret_cast<float*>(sm + kOffCn);
+    // (planes below FLT_MIN count as residue: the tensor cores may flush them)
+    double n2 = 0.0, r2 = 0.0;
+    if (tid < k) {
+      for (int l = 0; l < kNF; l++) {
+        const float x = cent[tid * kNF + l];
+        n2 = fma((double)x, (double)x, n2);
+        const float h = __bfloat162float(__float2bfloat16_rn(x));
+        const float u = x - h, l1 = __bfloat162float(__float2bfloat16_rn(u));
+        const float l2 = __bfloat162float(__float2bfloat16_rn(u - l1));
+        const double r = (double)x - (fabsf(h) < FLT_MIN ? 0.0 : (double)h) -
+                         (fabsf(l1) < FLT_MIN ? 0.0 : (double)l1) - (fabsf(l2) < FLT_MIN ? 0.0 : (double)l2);
+        r2 = fma(r, r, r2);
+      }
+    }
+    cnrm[tid] = tid < k ? (float)n2 : __int_as_float(0x7fffffff);  // NaN: never a candidate
+    cnrm[16 + tid] = tid < k ? (r2 == r2 ? (float)sqrt(r2) * 1.001f : INFINITY) : 0.f;  // NaN: screen off
+  }
+  for (int i = tid; i < 48 * 64; i += blockDim.x) {  // 48 rows x 64 bf16 (features 32..63 zero)
     const int R = i >> 6, q = i & 63, c = R & 15;
     float v = 0.f;
-    if (q < kNF && c < k) {
+    if (q < kNF && c < k) {  // rows 0..15 hi, 16..31 lo, 32..47 lo2: c = hi + lo + lo2 (+ r_c)
       const float x = cent[c * kNF + q];
       const float h = __bfloat162float(__float2bfloat16_rn(x));
-      v = R < 16 ? h : x - h;
+      const float u = x - h;
+      v = R < 16 ? h : R < 32 ? u : u - __bfloat162float(__float2bfloat16_rn(u));
     }
     *reinterpret_cast<__nv_bfloat16*>(sm + kOffCent + cent_off(R, q)) = __float2bfloat16_rn(v);
   }
@@ -1341,17 +1382,20 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
   } else {  // ---- epilogue: two sets of 4 warps (even / odd tiles); TMEM lanes 32 (warp % 4) + lane
     const int ew = warp & 3, m = 32 * ew + lane, set = (warp - kWEpi) >> 2;
     float cn[16];
-    float cmax2 = 0.f;
+    float cmax2 = 0.f, rcmax = 0.f;
+    const float* cnrm = reinterpret_cast<const float*>(sm + kOffCn);
 #pragma unroll
     for (int c = 0; c < 16; c++) {
-      float n2 = 0.f;
-      for (int l = 0; l < kNF; l++) n2 = fmaf(cf[c * kNF + l], cf[c * kNF + l], n2);
-      cn[c] = c < k ? n2 : __int_as_float(0x7fffffff);  // NaN: never a candidate, ignored by fminf
-      if (c < k) cmax2 = fmaxf(cmax2, n2);
+      cn[c] = cnrm[c];  // NaN past k: never a candidate, ignored by fminf
+      if (c < k) {
+        cmax2 = fmaxf(cmax2, cn[c]);
+        rcmax = fmaxf(rcmax, cnrm[16 + c]);
+      }
     }
     const float cmax = sqrtf(cmax2) * 1.001f;
-    const float eA = 2.44140625e-4f * 1.01f * cmax;  // 2^-12 x |f| (rsqrt approximation + 1 %)
-    const float eB = 7.62939453125e-06f * cmax * cmax + 7.8886e-31f * cmax + 1e-35f;  // 2^-17 cmax^2, 2^-100 cmax
+    // x |f|: 2^-14 cmax (rsqrt approximation + 1 %) + 2 |r_c|
+    const float eA = 6.103515625e-05f * 1.01f * cmax + 2.02f * rcmax;
+    const float eB = 4.76837158203125e-07f * cmax * cmax + 7.8886e-31f * cmax + 1e-35f;  // 2^-21 cmax^2, 2^-100 cmax
     for (int n = set; n < nmine; n += kEpiSets) {
       const int b = n % kSP;
       const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
