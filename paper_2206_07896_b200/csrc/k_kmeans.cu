@@ -887,9 +887,9 @@ static size_t kmeans_tc_smem() {
 //   distance  D[p][c'] = sum_l F[p][l] B[c'][l], M = 128 points, K = 32:
 //             A = the planes read MN-major (SWIZZLE_128B atoms of 8 features x
 //             64 points); B = the centroid rows (hi 0..15, lo 16..31, lo2 32..47) K-major.
-//             MMA 1: A = F_hi, N = 32 (hi.hi -> cols 0..15, hi.lo -> 16..31);
-//             MMAs 2-4: F_lo.C_hi, F_hi.C_lo2, F_lo.C_lo, N = 16, accumulated
-//             into cols 16..31 (B rows 32..47 = C_lo2).
+//             MMA 1: A = F_hi, N = 48 (hi.hi -> cols 0..15, hi.lo -> 16..31,
+//             hi.lo2 -> 32..47); MMA 2: A = F_lo, B = [C_hi | C_lo], N = 32,
+//             accumulated into cols 16..47.
 //   sums      S[r][c] = sum_p P[r][p] onehot[c][p] over a PAIR of tiles:
 //             M = 128 rows (tile 2q: 32 hi + 32 lo feature rows, tile 2q+1
 //             the same), K = 128 points, N = 32 (the two tiles' one-hots,
@@ -903,8 +903,9 @@ static size_t kmeans_tc_smem() {
 // Screen bound with S = sum_l |f_l c_l| <= |f| cmax.  The centroids are
 // split into THREE planes, c = C_hi + C_lo + C_lo2 + r_c (r_c = 0 unless a
 // plane is subnormal, measured per launch), the points into two (the split
-// is the pipeline's slowest stage), and the distance sums F_hi.C_hi in its own
-// columns and F_lo.C_hi + F_hi.C_lo + F_hi.C_lo2 + F_lo.C_lo in the other.
+// is the pipeline's slowest stage), and the distance accumulates F_hi.C_hi,
+// F_hi.C_lo + F_lo.C_hi and F_hi.C_lo2 + F_lo.C_lo in three column groups
+// (N = 48: 4 MMAs per tile, as with two centroid planes), summed small first.
 // Dropped: r_f.c <= 2^-16 S, F_lo.(C_lo2 + r_c) <= 2^-24 S + |f||r_c|; the
 // tensor-core accumulation of the exact bf16 products: 2 MMAs of K = 16 into
 // the hi.hi columns <= 2 x 17 x 2^-23 S, 8 into the small ones (terms <=
@@ -933,7 +934,7 @@ static size_t kmeans_tc_smem() {
 //   warp 13    distance MMA issuer (one elected lane) and TMEM owner
 //   warp 14    sums MMA issuer
 // Rings: 5 fp32 tiles (released by the split), 6 plane / one-hot stages (3
-// pairs), 6 TMEM accumulators of 32 columns (+ 32 columns of sums): the
+// pairs), 6 TMEM accumulators of 48 columns (+ 32 columns of sums): the
 // distances run two tiles ahead of the screen, the split further ahead.
 namespace tg {
 constexpr int kPts = 128;
@@ -976,9 +977,10 @@ constexpr uint32_t kOffBar = kOffCn + 32 * 4;               // mbarriers
 constexpr int kNBar = 2 * kST + 3 * kSP + 2 * kSA + 1;
 constexpr uint32_t kSmem = kOffBar + kNBar * 8 + 16 + 1024;  // + TMEM slot, + alignment slack
 static_assert(kSmem <= 227 * 1024, "kmeans_tg shared memory");
-static_assert(32 * kSA + 32 <= 256, "kmeans_tg TMEM columns");
-constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kSumsCol = 32 * kSA;  // 32 columns (M = 128: two stage parities)
+constexpr uint32_t kAccCols = 48;  // hi.hi | hi.lo + lo.hi | hi.lo2 + lo.lo
+static_assert(kAccCols * kSA + 32 <= 512, "kmeans_tg TMEM columns");
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kSumsCol = kAccCols * kSA;  // 32 columns (M = 128: two stage parities)
 static_assert(kSP % 2 == 0, "stages are used in pairs");
 
 // packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a): two points per instruction
@@ -1029,30 +1031,26 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N, bool amn) {
 }
 // MMA helpers are issued by the whole (converged) warp: one elected lane
 // executes, so the operands stay warp-uniform (no per-lane issue loop)
-// the 8 distance MMAs of a tile + the commit on `bar`, one elected lane, one
+// the 4 distance MMAs of a tile + the commit on `bar`, one elected lane, one
 // asm block (no per-MMA descriptor arithmetic on the issuing warp):
-//   D[0..31]  = F_hi . [C_hi | C_lo]   (K = 32: feature groups 0-1, 2-3)
-//   D[16..31] += F_lo . C_hi + F_hi . C_lo2 + F_lo . C_lo
+//   D[0..47]  = F_hi . [C_hi | C_lo | C_lo2]   (K = 32: feature groups 0-1, 2-3)
+//   D[16..47] += F_lo . [C_hi | C_lo]
+// (each plane is read once per K step: the tile's MMAs are smem-read bound
+// together with the TMA writes, the split and the sums)
 // aH = the stage's hi-plane descriptor (lo plane +4096 B, second K step
-// +2048 B), bC = the centroid descriptor (rows 16.. +2048 B, rows 32..
-// +4096 B, second K step +32 B)
-__device__ __forceinline__ void umma_dist(uint32_t d, uint64_t aH, uint64_t bC, uint32_t id32, uint32_t id16,
+// +2048 B), bC = the centroid descriptor (second K step +32 B)
+__device__ __forceinline__ void umma_dist(uint32_t d, uint64_t aH, uint64_t bC, uint32_t id48, uint32_t id32,
                                           uint64_t* bar) {
   asm volatile(
-      "{\n .reg .pred e, f, t;\n .reg .b64 a1, a2, a3, b1, b2, b3, b4, b5;\n"
+      "{\n .reg .pred e, f, t;\n .reg .b64 a1, a2, a3, b1;\n"
       " elect.sync _|e, 0xffffffff;\n setp.eq.u32 f, 1, 0;\n setp.eq.u32 t, 0, 0;\n"
       " add.s64 a1, %1, 128;\n add.s64 a2, %1, 256;\n add.s64 a3, %1, 384;\n add.s64 b1, %2, 2;\n"
-      " add.s64 b2, %2, 256;\n add.s64 b3, %2, 258;\n add.s64 b4, %2, 128;\n add.s64 b5, %2, 130;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a2, %2, %5, t;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a3, b1, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], %1, b2, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a1, b3, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a2, b4, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%4], a3, b5, %5, t;\n"
       " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n}" ::"r"(d),
-      "l"(aH), "l"(bC), "r"(id32), "r"(d + 16), "r"(id16), "r"(smem_u32(bar))
+      "l"(aH), "l"(bC), "r"(id48), "r"(d + 16), "r"(id32), "r"(smem_u32(bar))
       : "memory");
 }
 // the 8 sums MMAs of a tile pair (two point halves x 4 K steps of 16 points):
@@ -1099,6 +1097,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+// columns 16..47 into d, 0..15 into h, one wait
+__device__ __forceinline__ void tmem_ld32_16(uint32_t taddr, float (&d)[32], float (&h)[16]) {
+  uint32_t r[32], q[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr + 16));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]), "=r"(q[8]),
+        "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; i++) d[i] = __uint_as_float(r[i]);
+#pragma unroll
+  for (int i = 0; i < 16; i++) h[i] = __uint_as_float(q[i]);
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -1284,7 +1304,7 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
     }
   } else if (warp == kWMma) {  // ---- distance MMAs (the whole warp; one elected lane issues)
     const uint64_t dC = sdesc(smem_u32(sm + kOffCent), 16, 1024);
-    const uint32_t idD32 = idesc(128, 32, true), idD16 = idesc(128, 16, true);
+    const uint32_t idD48 = idesc(128, 48, true), idD32 = idesc(128, 32, true);
     for (int n = 0; n < nmine; n++) {
       const int b = n % kSP;
       mbar_wait(&full_p[b], (n / kSP) & 1);
@@ -1294,7 +1314,8 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       if (lane == 0) trace(9, n);
       __syncwarp();  // elect.sync below needs the converged warp
       tc_after();
-      umma_dist(tmem + a * 32, sdesc(smem_u32(sm + stage_planes(b)), 16384, 1024), dC, idD32, idD16, &acc_full[a]);
+      umma_dist(tmem + a * kAccCols, sdesc(smem_u32(sm + stage_planes(b)), 16384, 1024), dC, idD48, idD32,
+                &acc_full[a]);
       if (lane == 0) trace(4, n);
       __syncwarp();
     }
@@ -1407,8 +1428,8 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       mbar_wait(&acc_full[a], (n / kSA) & 1);
       if (m == 0) trace(5, n);
       tc_after();
-      float d[32];
-      tmem_ld32(tmem + a * 32 + ((uint32_t)(32 * ew) << 16), d);
+      float d[32], h[16];  // cols 16..47 (the small terms), 0..15 (hi.hi)
+      tmem_ld32_16(tmem + a * kAccCols + ((uint32_t)(32 * ew) << 16), d, h);
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
@@ -1418,7 +1439,7 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       float mn = INFINITY;
 #pragma unroll
       for (int c = 0; c < 16; c++) {
-        tv[c] = fmaf(-2.f, d[c] + d[16 + c], cn[c]);
+        tv[c] = fmaf(-2.f, h[c] + (d[c] + d[16 + c]), cn[c]);
         mn = fminf(mn, tv[c]);
       }
       const float thr = mn + 2.f * E;
