@@ -1169,6 +1169,43 @@ __device__ __noinline__ int exact_mask_g(const float* fp, long long stride, cons
   }
   return bi;
 }
+// mbarrier waits of the pipeline roles (default 1: 0.533 -> 0.529 ms,
+// scripts/ab/km_tg_wait.sh).  KM_TG_WAIT: 0 = try_wait with a
+// 1 ms suspend-time hint everywhere; 1 = the single-thread issuers (producer,
+// MMA warps) poll with test_wait; 2 = every role uses try_wait without a
+// hint; 3 = the issuers use try_wait without a hint
+#ifndef KM_TG_WAIT
+#define KM_TG_WAIT 1
+#endif
+__device__ __forceinline__ void wait_poll(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void wait_nohint(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tg_wait_issuer(uint64_t* bar, uint32_t parity) {
+  if (KM_TG_WAIT == 1) wait_poll(bar, parity);
+  else if (KM_TG_WAIT >= 2) wait_nohint(bar, parity);
+  else mbar_wait(bar, parity);
+}
+__device__ __forceinline__ void tg_wait_worker(uint64_t* bar, uint32_t parity) {
+  if (KM_TG_WAIT == 2) wait_nohint(bar, parity);
+  else mbar_wait(bar, parity);
+}
 #ifdef KM_TG_TRACE
 // per-tile event times of CTA 0 (ns, %globaltimer): [event][tile]
 __device__ unsigned long long g_trace[12][2048];
@@ -1289,7 +1326,7 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
       for (int n = 0; n < nmine; n++) {
         const int s = n % kST;
-        if (n >= kST) mbar_wait(&empty_t[s], ((n / kST) - 1) & 1);  // wakes on the phase flip (a nanosleep back-off added ~1200 cycles per slot)
+        if (n >= kST) tg_wait_issuer(&empty_t[s], ((n / kST) - 1) & 1);  // wakes on the phase flip (a nanosleep back-off added ~1200 cycles per slot)
         const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
         trace(0, n);
         // the box is always written in full (zeros past npts; columns past hi
@@ -1307,10 +1344,10 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
     const uint32_t idD48 = idesc(128, 48, true), idD32 = idesc(128, 32, true);
     for (int n = 0; n < nmine; n++) {
       const int b = n % kSP;
-      mbar_wait(&full_p[b], (n / kSP) & 1);
+      tg_wait_issuer(&full_p[b], (n / kSP) & 1);
       if (lane == 0) trace(8, n);
       const int a = n % kSA;
-      if (n >= kSA) mbar_wait(&acc_empty[a], ((n / kSA) - 1) & 1);
+      if (n >= kSA) tg_wait_issuer(&acc_empty[a], ((n / kSA) - 1) & 1);
       if (lane == 0) trace(9, n);
       __syncwarp();  // elect.sync below needs the converged warp
       tc_after();
@@ -1330,8 +1367,8 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
     for (int m0 = 0; m0 < nmine; m0 += 2) {
       const int b0 = m0 % kSP;
       const bool pair = m0 + 1 < nmine;
-      mbar_wait(&oh_full[b0], (m0 / kSP) & 1);
-      if (pair) mbar_wait(&oh_full[b0 + 1], ((m0 + 1) / kSP) & 1);
+      tg_wait_issuer(&oh_full[b0], (m0 / kSP) & 1);
+      if (pair) tg_wait_issuer(&oh_full[b0 + 1], ((m0 + 1) / kSP) & 1);
       if (lane == 0) trace(10, m0 + pair);
       __syncwarp();
       tc_after();
@@ -1347,9 +1384,9 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
     const int st = tid & 127, half = st >> 6, pr = st & 63, p = 2 * pr, sset = warp >> 2;
     for (int n = sset; n < nmine; n += kSplitSets) {
       const int s = n % kST, b = n % kSP;
-      mbar_wait(&full_t[s], (n / kST) & 1);
+      tg_wait_worker(&full_t[s], (n / kST) & 1);
       if (st == 0) trace(1, n);
-      if (n >= kSP) mbar_wait(&empty_p[b], ((n / kSP) - 1) & 1);
+      if (n >= kSP) tg_wait_worker(&empty_p[b], ((n / kSP) - 1) & 1);
       if (st == 0) trace(2, n);
       const long long p0 = lo + (blockIdx.x + (long long)n * gridDim.x) * kPts;
       const int cntp = (int)min((long long)kPts, hi - p0);
@@ -1376,6 +1413,7 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       // hand the fp32 slot back to the producer before the conversions
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_t[s]);
+      if (st == 0) trace(11, n);
       // finite norms <= 3e38: every |x| <= 2e19, nothing to drop (the common case)
       if (!__all_sync(0xffffffffu, n0 <= 3.0e38f && n1 <= 3.0e38f)) {
 #pragma unroll
@@ -1423,9 +1461,9 @@ __global__ void __launch_bounds__(tg::kThreads, 1) kmeans_tg(const __grid_consta
       const int cntp = (int)min((long long)kPts, hi - p0);
       // full_p as well: orders the split's |f|^2 stores before the loads below
       // (the split cannot complete tile n + kSP before this tile's one-hot exists)
-      mbar_wait(&full_p[b], (n / kSP) & 1);
+      tg_wait_worker(&full_p[b], (n / kSP) & 1);
       const int a = n % kSA;
-      mbar_wait(&acc_full[a], (n / kSA) & 1);
+      tg_wait_worker(&acc_full[a], (n / kSA) & 1);
       if (m == 0) trace(5, n);
       tc_after();
       float d[32], h[16];  // cols 16..47 (the small terms), 0..15 (hi.hi)
