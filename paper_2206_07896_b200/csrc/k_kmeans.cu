@@ -959,6 +959,10 @@ constexpr int kSA = KM_TG_SA;  // TMEM distance accumulators (32 columns each)
 #endif
 constexpr int kSplitSets = KM_TG_SPLIT_SETS;  // split warp sets of 4 (alternating tiles)
 constexpr int kEpiSets = KM_TG_EPI_SETS;      // epilogue warp sets of 4 (alternating tiles)
+// the measured balance (scripts/ab/km_tg_sets.sh): 2 split sets + 1 epilogue
+// set ran 0.60 ms and faulted once in four runs, 2 + 2 spills registers at
+// 608 threads (0.70 ms); only 1 + 2 is built and tested
+static_assert(kSplitSets == 1 && kEpiSets == 2, "kmeans_tg: untested warp-role balance");
 constexpr int kWEpi = 4 * kSplitSets;         // first epilogue warp
 constexpr int kWProd = kWEpi + 4 * kEpiSets, kWMma = kWProd + 1, kWSum = kWProd + 2;
 constexpr int kThreads = 32 * (kWSum + 1);
