@@ -180,7 +180,7 @@ T& scratch_for(cudaStream_t s, int kind) {
   if (!slot) slot.reset(new T());
   return *static_cast<T*>(slot.get());
 }
-enum { SCRATCH_BFS_STEP = 1, SCRATCH_BFS_LEVELS = 2, SCRATCH_NN_TOPK = 3 };
+enum { SCRATCH_BFS_STEP = 1, SCRATCH_BFS_LEVELS = 2, SCRATCH_NN_TOPK = 3, SCRATCH_KM_UPDATE = 4 };
 
 // full-grid hotspot step with the streaming band kernel (k_hotspot.cu)
 int hotspot_step_full(cudaStream_t stream, int num_sms, const float* src, const float* power,

@@ -1834,25 +1834,37 @@ __global__ void __launch_bounds__(256) kmeans_delta(const int* __restrict__ memb
 }
 }  // namespace bf
 
+namespace bf {
+struct KmUpdateScratch : StreamScratch {
+  unsigned long long* d = nullptr;  // device delta counter
+  unsigned long long* h = nullptr;  // pinned read-back
+  void release() {
+    if (d) cudaFree(d);
+    if (h) cudaFreeHost(h);
+    d = h = nullptr;
+  }
+  ~KmUpdateScratch() override { release(); }
+};
+}  // namespace bf
+
 extern "C" int bf_kmeans_update_impl(void* stream_v, int num_sms, float* cent, float* sums, int* counts, int nf,
                                      int k, const int* member, int* prev, long long p_lo, long long p_hi,
                                      long long* delta, char* err, int errcap) {
   using namespace bf;
   cudaStream_t stream = (cudaStream_t)stream_v;
-  static unsigned long long* dd[64] = {};  // per-device scratch counter + pinned read-back
-  static unsigned long long* hh[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  unsigned long long*& d = dd[dev & 63];
-  unsigned long long*& h = hh[dev & 63];
-  if (!d) {
-    if (cudaMalloc((void**)&d, 8) != cudaSuccess || cudaMallocHost((void**)&h, 8) != cudaSuccess) {
+  // the delta counter and its pinned read-back, keyed by the stream (several
+  // runtimes or host threads never share them)
+  KmUpdateScratch& S = scratch_for<KmUpdateScratch>(stream, SCRATCH_KM_UPDATE);
+  if (!S.d) {
+    if (cudaMalloc((void**)&S.d, 8) != cudaSuccess || cudaMallocHost((void**)&S.h, 8) != cudaSuccess) {
       snprintf(err, errcap, "kmeans_update: scratch allocation failed");
       cudaGetLastError();
-      d = nullptr;
+      S.release();
       return BF_E_CUDA;
     }
   }
+  unsigned long long* d = S.d;
+  unsigned long long* h = S.h;
   kmeans_centroids<<<1, 512, 0, stream>>>(cent, sums, counts, nf, k);
   cudaMemsetAsync(d, 0, 8, stream);
   if (p_hi > p_lo) {
