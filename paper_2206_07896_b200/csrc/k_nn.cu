@@ -332,12 +332,18 @@ __global__ void __launch_bounds__(kTkThreads) nn_topk_pass(TopkArgs a) {
       const float4* r4 = reinterpret_cast<const float4*>(tk_ring + st * kTkChunk);
       float4 v[4];
       float m[4];
+      if (cnt4 == kTkChunk / 4) {  // every chunk but the last: no bounds, no padding values
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int q = threadIdx.x + 256 * u;
-        v[u] = q < cnt4 ? r4[q] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-        m[u] = fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w));
+        for (int u = 0; u < 4; u++) v[u] = r4[threadIdx.x + 256 * u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int q = threadIdx.x + 256 * u;
+          v[u] = q < cnt4 ? r4[q] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+        }
       }
+#pragma unroll
+      for (int u = 0; u < 4; u++) m[u] = fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w));
       __syncwarp();
       if (lane == 0) mbar_arrive(&tk_empty[st]);  // the values are in registers
       // warp-uniform branches (votes): the insert code is skipped, not
